@@ -1,0 +1,162 @@
+/*
+ * flexshm.h - C ABI of libflexshm.so, the B200-native one-to-many data path
+ * of Flex-MIG (arxiv 2511.09143): a data-parallel job spread over many 1g
+ * instances (MIG slices, or SM-partitioned stand-ins) joined by a
+ * host-shared-memory allreduce / broadcast.
+ *
+ * Plain C types only (no torch / CUDA types in the signatures): device
+ * buffers are `void*` device pointers, the stream is a `void*` that holds a
+ * cudaStream_t.  Every call returns an int status, 0 = FMX_OK.
+ *
+ * What each entry point replaces (reference file:line, /root/reference):
+ *
+ *   fmx_validate_peers  <- migsim.commsim.discover_peers
+ *                          (pkg/src/migsim/commsim.py:67-88) and
+ *                          PeerInfo.__post_init__ (commsim.py:35-42)
+ *   fmx_topology        <- migsim.commsim.build_topology (commsim.py:91-116)
+ *   fmx_restore_bus_id  <- migsim.commsim.restore_bus_id (commsim.py:119-123)
+ *   fmx_comm_init       <- the paper's patched ncclCommInitRank: bootstrap
+ *                          allgather of peer info incl. mig_id, duplicate
+ *                          check, synthetic bus-id labels;
+ *                          shaped like ncclCommInitRank (nccl.h:160)
+ *   fmx_allreduce       <- ncclAllReduce over the SHM transport, reached from
+ *                          DDP (nccl.h:379)
+ *   fmx_broadcast       <- ncclBroadcast (ZeRO shard / DDP init broadcast,
+ *                          PAPER.md:485; nccl.h:392)
+ *   fmx_comm_destroy / fmx_comm_abort <- ncclCommDestroy / ncclCommAbort
+ *
+ * Status codes map 1:1 to Python exceptions (paper_2511_09143_b200/_lib.py):
+ * DUPLICATE_DEVICE -> DuplicateDeviceError(rank_a, rank_b) with the same
+ * (earlier, later) pair as commsim.py:85-86; MALFORMED_LABEL ->
+ * MalformedLabelError; BAD_RANKS / EMPTY_MIG_ID / INVALID_ARG -> ValueError.
+ *
+ * Threading: one communicator per rank process (several per process are
+ * allowed for in-process testing); calls on one communicator must be
+ * serialised by the caller (the NCCL rule).  Collectives are asynchronous on
+ * the given stream; init and destroy are blocking.
+ */
+#ifndef FLEXSHM_H
+#define FLEXSHM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMX_ABI_VERSION 1
+#define FMX_BUS_ID_LEN 16   /* "XX:XX:XX.0" + NUL, padded */
+#define FMX_MIG_ID_LEN 128
+#define FMX_MAX_RANKS 64
+#define FMX_MAX_RANKS_PER_BUS 10
+
+enum fmx_status {
+  FMX_OK = 0,
+  FMX_ERR_DUPLICATE_DEVICE = 1, /* two ranks bound to one device (commsim.py:85-86) */
+  FMX_ERR_MALFORMED_LABEL = 2,  /* non-canonical bus id, or > 10 ranks per bus */
+  FMX_ERR_BAD_RANKS = 3,        /* ranks not exactly 0..n-1 (commsim.py:76-77) */
+  FMX_ERR_EMPTY_MIG_ID = 4,     /* PeerInfo with empty mig_id (commsim.py:41-42) */
+  FMX_ERR_INVALID_ARG = 5,
+  FMX_ERR_CUDA = 6,
+  FMX_ERR_SHM = 7,
+  FMX_ERR_TIMEOUT = 8,
+  FMX_ERR_ABORTED = 9,
+  FMX_ERR_UNSUPPORTED = 10
+};
+
+enum fmx_dtype { FMX_FLOAT32 = 0, FMX_BFLOAT16 = 1 };
+
+/* Scale conventions; the arithmetic is the fixed ascending-rank fp32 sum. */
+enum fmx_op {
+  FMX_OP_SUM = 0,           /* out = x0 + x1 + ... (left to right)            */
+  FMX_OP_SUM_POSTSCALE = 1, /* out = (sum) * factor                           */
+  FMX_OP_PREDIV_SUM = 2     /* out = x0/factor + x1/factor + ... (DDP default  */
+                            /* hook: bucket.div_(world) then SUM)              */
+};
+
+/* How host-link bytes move.  ZC: SM kernels store to / load from the mapped
+ * SHM segment (128-bit, zero-copy).  CE: copy engines move the bytes, SM
+ * kernels reduce out of HBM.  AUTO picks CE (measured faster across processes
+ * on one GPU). */
+enum fmx_transport { FMX_TRANSPORT_AUTO = 0, FMX_TRANSPORT_ZC = 1, FMX_TRANSPORT_CE = 2 };
+
+/* One rank's identity (commsim.PeerInfo, commsim.py:27-42). */
+typedef struct fmx_peer_info {
+  int32_t rank;
+  char pcie_bus_id[FMX_BUS_ID_LEN]; /* canonical "XX:XX:XX.0" (upper case)   */
+  char mig_id[FMX_MIG_ID_LEN];      /* MIG UUID or "GC-<gpu uuid>-<slot>"   */
+  int64_t host_hash;
+  int64_t pid_hash;
+} fmx_peer_info;
+
+typedef struct fmx_comm* fmx_comm_t;
+
+/* ---- host-only bootstrap rules (no GPU needed) ---------------------------- */
+
+/* Normalise + validate one PeerInfo in place (upper-cases the bus id). */
+int fmx_check_peer(fmx_peer_info* peer);
+
+/* discover_peers: ranks must be 0..n-1; duplicate key (host, bus, mig_id),
+ * or (host, bus) when mig_aware == 0.  On FMX_ERR_DUPLICATE_DEVICE,
+ * *rank_a / *rank_b receive the (earlier, later) pair. */
+int fmx_validate_peers(const fmx_peer_info* peers, int n, int mig_aware,
+                       int* rank_a, int* rank_b);
+
+/* build_topology over peers in rank order: labels[i] (FMX_BUS_ID_LEN chars)
+ * is rank i's label; mig_buses / mig_counts (n entries) receive the mig_list
+ * in first-seen order, *n_buses its length. */
+int fmx_topology(const fmx_peer_info* peers, int n, char* labels, char* mig_buses,
+                 int* mig_counts, int* n_buses);
+
+/* restore_bus_id: "00:4B:00.3" -> "00:4B:00.0"; out has FMX_BUS_ID_LEN bytes. */
+int fmx_restore_bus_id(const char* label, char* out);
+
+/* ---- communicator ---------------------------------------------------------- */
+
+/* Collective over all `nranks` processes calling it with the same job_key.
+ * Rank 0 creates POSIX SHM "/fmx-<job_key>", every rank publishes `self`,
+ * the table is validated with the rules above (mig_aware), the segment is
+ * pinned and device-mapped (cudaHostRegister Mapped|Portable) in the calling
+ * thread's current CUDA context.  slice_bytes = bytes per (owner,
+ * contributor) pipeline slot, 0 = default; nslots must be 2 (double
+ * buffering) or 0 = default.  timeout_s bounds every bootstrap wait. */
+int fmx_comm_init(fmx_comm_t* comm, const char* job_key, int nranks, int rank,
+                  const fmx_peer_info* self, int mig_aware, size_t slice_bytes, int nslots,
+                  int transport, double timeout_s);
+
+/* In-place allowed (send == recv).  count elements of dtype; op/factor per
+ * enum fmx_op.  Enqueued on `stream` (a cudaStream_t); returns immediately. */
+int fmx_allreduce(fmx_comm_t comm, const void* send, void* recv, size_t count, int dtype,
+                  int op, float factor, void* stream);
+
+/* Root's send buffer -> every rank's recv buffer (bit copy). */
+int fmx_broadcast(fmx_comm_t comm, const void* send, void* recv, size_t count, int dtype,
+                  int root, void* stream);
+
+/* Host-side barrier over the communicator (SHM counter; no GPU work). */
+int fmx_barrier(fmx_comm_t comm, double timeout_s);
+
+int fmx_comm_destroy(fmx_comm_t comm);
+/* Marks the communicator aborted and releases every stream wait of every
+ * rank on it (results of in-flight collectives are undefined). */
+int fmx_comm_abort(fmx_comm_t comm);
+
+int fmx_comm_rank(fmx_comm_t comm, int* rank);
+int fmx_comm_count(fmx_comm_t comm, int* nranks);
+int fmx_comm_peer(fmx_comm_t comm, int rank, fmx_peer_info* out);
+/* Effective configuration: slice bytes, transport, segment bytes. */
+int fmx_comm_config(fmx_comm_t comm, size_t* slice_bytes, int* transport, size_t* shm_bytes);
+/* Number of device kernels this communicator has launched so far. */
+int fmx_comm_kernel_launches(fmx_comm_t comm, uint64_t* launches);
+
+/* ---- diagnostics ----------------------------------------------------------- */
+
+const char* fmx_last_error(void);           /* thread-local message          */
+int fmx_dup_ranks(int* rank_a, int* rank_b); /* pair of the last DUPLICATE    */
+int fmx_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLEXSHM_H */

@@ -1,0 +1,179 @@
+"""Process-group init over a set of instances, and the collectives.
+
+New Python surface (the reference has none; shaped like torch / NCCL):
+
+    comm = init_process_group(decision, rank, job_key, instance=inst)
+    comm.allreduce(flat_grad)                 # fixed rank-order fp32 sum
+    comm.allreduce(flat_grad, op="avg")       # DDP's divide-then-sum
+    comm.broadcast(flat_params, root=0)
+    comm.destroy()
+
+`decision` is the `AllocationDecision` from `fm_select`; its `instances`
+order is the rank order (reference scheduler.py:117-136), which is also the
+summation order of every allreduce.  Bootstrap runs natively inside
+`fmx_comm_init` (MIG-aware duplicate check and topology labels, reference
+commsim.py:67-116 / PAPER.md:386-399); the Python side then rebuilds the
+reference's `Communicator` and `TopologyGraph` from the exchanged peer table
+so callers see the same objects `discover_peers` / `build_topology` return.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+from . import _lib
+from .commsim import Communicator, PeerInfo, TopologyGraph, build_topology, discover_peers
+from .scheduler import AllocationDecision
+
+OPS = {
+    "sum": _lib.OP_SUM,
+    "postscale": _lib.OP_SUM_POSTSCALE,
+    "prediv": _lib.OP_PREDIV_SUM,
+}
+
+
+def _dtype_code(tensor) -> int:
+    import torch
+    if tensor.dtype == torch.float32:
+        return _lib.FLOAT32
+    if tensor.dtype == torch.bfloat16:
+        return _lib.BFLOAT16
+    raise TypeError(f"unsupported dtype {tensor.dtype} (float32 or bfloat16)")
+
+
+def _check_tensor(t, what: str):
+    if not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous (flat gradient buffer)")
+
+
+class ShmCommunicator:
+    """Handle of one rank's membership in a host-SHM communicator."""
+
+    def __init__(self, handle: int, rank: int, peers: list[PeerInfo], instance=None):
+        self._h = ctypes.c_void_p(handle)
+        self.rank = rank
+        self.size = len(peers)
+        self.comm: Communicator = Communicator(tuple(peers))
+        self.topology: TopologyGraph = build_topology(self.comm)
+        self.instance = instance
+        sb, tr, shm = ctypes.c_size_t(), ctypes.c_int(), ctypes.c_size_t()
+        _lib.check(_lib.lib().fmx_comm_config(self._h, ctypes.byref(sb), ctypes.byref(tr),
+                                              ctypes.byref(shm)))
+        self.slice_bytes, self.transport, self.shm_bytes = sb.value, tr.value, shm.value
+
+    # -- helpers -------------------------------------------------------------
+    def _stream(self, stream) -> int:
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+    def _alive(self):
+        if self._h is None or not self._h.value:
+            raise RuntimeError("communicator was destroyed")
+
+    # -- collectives -----------------------------------------------------------
+    def allreduce(self, tensor, op: str = "sum", factor: float | None = None, out=None,
+                  stream=None):
+        """In-place (or into `out`) allreduce of a flat float32/bf16 buffer.
+
+        op: "sum"; "avg" (= "prediv" by world size, the DDP default hook);
+        "prediv" (each contribution / factor); "postscale" (sum * factor).
+        """
+        self._alive()
+        _check_tensor(tensor, "tensor")
+        if op == "avg":
+            op, factor = "prediv", float(self.size)
+        if op not in OPS:
+            raise ValueError(f"unknown op {op!r}")
+        if factor is None:
+            factor = 1.0
+        if op != "sum" and not math.isfinite(factor):
+            raise ValueError("factor must be finite")
+        dst = tensor if out is None else out
+        if dst is not tensor:
+            _check_tensor(dst, "out")
+            if dst.dtype != tensor.dtype or dst.numel() != tensor.numel():
+                raise ValueError("out must match tensor dtype and size")
+        rc = _lib.lib().fmx_allreduce(self._h, tensor.data_ptr(), dst.data_ptr(),
+                                      tensor.numel(), _dtype_code(tensor), OPS[op],
+                                      ctypes.c_float(factor), self._stream(stream))
+        _lib.check(rc, "fmx_allreduce")
+        return dst
+
+    def broadcast(self, tensor, root: int = 0, stream=None):
+        self._alive()
+        _check_tensor(tensor, "tensor")
+        rc = _lib.lib().fmx_broadcast(self._h, tensor.data_ptr(), tensor.data_ptr(),
+                                      tensor.numel(), _dtype_code(tensor), int(root),
+                                      self._stream(stream))
+        _lib.check(rc, "fmx_broadcast")
+        return tensor
+
+    def barrier(self, timeout_s: float = 120.0) -> None:
+        self._alive()
+        _lib.check(_lib.lib().fmx_barrier(self._h, timeout_s), "fmx_barrier")
+
+    def kernel_launches(self) -> int:
+        v = ctypes.c_uint64()
+        _lib.check(_lib.lib().fmx_comm_kernel_launches(self._h, ctypes.byref(v)))
+        return v.value
+
+    def abort(self) -> None:
+        if self._h is not None and self._h.value:
+            _lib.lib().fmx_comm_abort(self._h)
+
+    def destroy(self) -> None:
+        if self._h is not None and self._h.value:
+            h, self._h = self._h, None
+            _lib.check(_lib.lib().fmx_comm_destroy(h), "fmx_comm_destroy")
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.destroy()
+
+
+def init_process_group(decision: AllocationDecision | None, rank: int, job_key: str, *,
+                       instance=None, peer: PeerInfo | None = None, nranks: int | None = None,
+                       mig_aware: bool = True, slice_bytes: int = 0, transport: str = "auto",
+                       timeout_s: float = 120.0) -> ShmCommunicator:
+    """Join the communicator of `decision` as `rank` (collective, blocking).
+
+    The published identity is `peer` if given, else `instance.peer_info`.
+    Raises DuplicateDeviceError / MalformedLabelError / ValueError exactly
+    where the reference's discover_peers / build_topology would.
+    """
+    from .instance import peer_info as _peer_info
+
+    n = nranks if nranks is not None else len(decision.instances)
+    if decision is not None and nranks is not None and nranks != len(decision.instances):
+        raise ValueError("nranks disagrees with the decision")
+    if peer is None:
+        if instance is None:
+            raise ValueError("need an instance binding or an explicit PeerInfo")
+        peer = _peer_info(instance, rank)
+    if peer.rank != rank:
+        raise ValueError(f"peer rank {peer.rank} != rank {rank}")
+    if transport not in _lib.TRANSPORTS:
+        raise ValueError(f"unknown transport {transport!r}")
+    me = _lib.peer_to_c(peer.rank, peer.pcie_bus_id, peer.mig_id, peer.host_hash, peer.pid_hash)
+    h = ctypes.c_void_p()
+    rc = _lib.lib().fmx_comm_init(ctypes.byref(h), job_key.encode(), n, rank, ctypes.byref(me),
+                                  1 if mig_aware else 0, slice_bytes, 0,
+                                  _lib.TRANSPORTS[transport], timeout_s)
+    _lib.check(rc, "fmx_comm_init")
+    peers = []
+    for r in range(n):
+        pc = _lib.PeerInfoC()
+        _lib.check(_lib.lib().fmx_comm_peer(h, r, ctypes.byref(pc)))
+        peers.append(PeerInfo(pc.rank, pc.pcie_bus_id.decode(), pc.mig_id.decode(),
+                              pc.host_hash, pc.pid_hash))
+    # Same checks, reference semantics, on the exchanged table (cannot fail
+    # where the native check passed; kept as the drop-in object model).
+    comm = discover_peers(peers, mig_aware=mig_aware)
+    return ShmCommunicator(h.value, rank, list(comm.peers), instance)

@@ -1,0 +1,697 @@
+// Communicator, SHM segment manager and the chunk pipeline of libflexshm.
+//
+// Design:
+//  * One POSIX SHM segment per communicator, "/fmx-<job_key>", created by rank
+//    0, pinned + device-mapped by every rank (cudaHostRegister Mapped |
+//    Portable).  MIG forbids cross-instance P2P/NVLink (reference
+//    PAPER.md:262), so host memory is the only shared medium - the same
+//    transport NCCL's SHM path gives the paper's ranks.
+//  * Bootstrap = the paper's patched ncclCommInitRank:
+//    every rank publishes its fmx_peer_info into the segment's peer table,
+//    then every rank applies discover_peers / build_topology rules
+//    (flexshm_host.cpp) to the full table, so all ranks agree on failure.
+//  * Allreduce = reduce-scatter + all-gather through the segment.  Rank r owns
+//    chunk r of the flat buffer (16-byte aligned chunk boundaries).  Each
+//    chunk is pipelined in rounds of `slice` elements; round R uses slot
+//    R % 2 of every region (double buffering).  Per round a rank (1) stages
+//    its pieces of the other owners' chunks into in-slot[owner][r], (2) after
+//    every peer signalled STAGED, reduces its own chunk in ascending rank
+//    order (own contribution read from HBM at its own rank position) into
+//    its HBM result and out-slot[r], (3) after every peer signalled REDUCED,
+//    gathers the other owners' results.
+//  * Flags are monotone 32-bit round counters in the segment, one 64-byte
+//    line each, written with cuStreamWriteValue-class stream memory ops
+//    (system-scope fence before the write) and waited on with stream
+//    memory-op waits.  No SM ever spins: a wait parks the stream in the GPU
+//    front end, which matters because rank processes sharing one GPU without
+//    MPS are time-sliced.  Slot reuse needs no credit messages: the waits of
+//    round R already imply every peer finished round R-1.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <errno.h>
+#include <fcntl.h>
+#include <signal.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "fmx_internal.h"
+#include "flexshm_kernels.cuh"
+
+using namespace fmx;
+
+namespace {
+
+typedef CUresult (*PFN_batchMemOp)(CUstream, unsigned int, CUstreamBatchMemOpParams*,
+                                   unsigned int);
+PFN_batchMemOp g_batch = nullptr;
+std::once_flag g_driver_once;
+int g_driver_status = FMX_OK;
+
+int load_driver() {
+  std::call_once(g_driver_once, [] {
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPointByVersion("cuStreamBatchMemOp", (void**)&g_batch,
+                                                     12000, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !g_batch)
+      g_driver_status = FMX_ERR_UNSUPPORTED;
+  });
+  if (g_driver_status != FMX_OK)
+    return fail(FMX_ERR_UNSUPPORTED, "cuStreamBatchMemOp entry point unavailable");
+  return FMX_OK;
+}
+
+#define FMX_CUDA(call)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(FMX_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+constexpr size_t kDefaultSliceCap = 4u << 20;   // bytes per (owner, contributor) slot
+constexpr size_t kSegmentBudget = 1ull << 30;   // default cap on data-slot bytes
+constexpr int kBatchMax = 128;                  // memops per cuStreamBatchMemOp call
+
+bool pid_alive(int pid) { return pid > 0 && (kill(pid, 0) == 0 || errno == EPERM); }
+
+}  // namespace
+
+struct fmx_comm {
+  int rank = -1, nranks = 0, nslots = 2, transport = FMX_TRANSPORT_CE, mig_aware = 1;
+  size_t slice_bytes = 0, total_bytes = 0;
+  Layout L{};
+  char* base = nullptr;   // host VA of the mapping
+  char* dbase = nullptr;  // device VA of the same bytes
+  Header* hdr = nullptr;
+  bool registered = false;
+  uint32_t ar_round = 0, bc_round = 0;
+  int64_t barrier_gen = 0;
+  char* scratch = nullptr;  // CE transport: n * slice_bytes of HBM
+  cudaEvent_t done = nullptr;
+  bool has_done = false;
+  uint64_t launches = 0;
+  std::vector<fmx_peer_info> peers;
+  std::vector<CUstreamBatchMemOpParams> ops;
+
+  char* in_slot(bool dev, uint32_t R, int owner, int contrib) const {
+    size_t s = R % nslots;
+    return (dev ? dbase : base) + L.ar_in_off +
+           ((s * nranks + owner) * nranks + contrib) * slice_bytes;
+  }
+  char* out_slot(bool dev, uint32_t R, int owner) const {
+    size_t s = R % nslots;
+    return (dev ? dbase : base) + L.ar_out_off + (s * nranks + owner) * slice_bytes;
+  }
+  char* bc_slot(bool dev, uint32_t R) const {
+    size_t s = R % nslots;
+    return (dev ? dbase : base) + L.bc_off + s * nranks * slice_bytes;
+  }
+  CUdeviceptr flag_dev(int r, int f) const {
+    return (CUdeviceptr)(dbase + L.flags_off + ((size_t)r * kFlagsPerRank + f) * 64);
+  }
+  volatile uint32_t* flag_host(int r, int f) const {
+    return (volatile uint32_t*)(base + L.flags_off + ((size_t)r * kFlagsPerRank + f) * 64);
+  }
+};
+
+namespace {
+
+void unmap(fmx_comm* c) {
+  if (c->base) munmap(c->base, c->total_bytes);
+  c->base = nullptr;
+  c->hdr = nullptr;
+}
+
+// ---- stream memory operations ------------------------------------------------
+
+int signal(fmx_comm* c, cudaStream_t s, int flag, uint32_t value) {
+  CUstreamBatchMemOpParams op;
+  memset(&op, 0, sizeof op);
+  op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+  op.writeValue.address = c->flag_dev(c->rank, flag);
+  op.writeValue.value = value;
+  op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;  // fence before the write
+  CUresult r = g_batch((CUstream)s, 1, &op, 0);
+  if (r != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "stream write-value failed (%d)", (int)r);
+  return FMX_OK;
+}
+
+int signal2(fmx_comm* c, cudaStream_t s, int f0, uint32_t v0, int f1, uint32_t v1) {
+  CUstreamBatchMemOpParams op[2];
+  memset(op, 0, sizeof op);
+  op[0].writeValue.operation = op[1].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+  op[0].writeValue.address = c->flag_dev(c->rank, f0);
+  op[0].writeValue.value = v0;
+  op[1].writeValue.address = c->flag_dev(c->rank, f1);
+  op[1].writeValue.value = v1;
+  CUresult r = g_batch((CUstream)s, 2, op, 0);
+  if (r != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "stream write-value failed (%d)", (int)r);
+  return FMX_OK;
+}
+
+// Wait until flag `flag` of every rank in [0, n) except `skip` is >= value (cyclic).
+int wait_peers(fmx_comm* c, cudaStream_t s, int flag, uint32_t value, int skip) {
+  c->ops.clear();
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == skip) continue;
+    CUstreamBatchMemOpParams op;
+    memset(&op, 0, sizeof op);
+    op.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+    op.waitValue.address = c->flag_dev(q, flag);
+    op.waitValue.value = value;
+    op.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+    c->ops.push_back(op);
+  }
+  for (size_t i = 0; i < c->ops.size(); i += kBatchMax) {
+    unsigned cnt = (unsigned)std::min<size_t>(kBatchMax, c->ops.size() - i);
+    CUresult r = g_batch((CUstream)s, cnt, c->ops.data() + i, 0);
+    if (r != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "stream wait-value failed (%d)", (int)r);
+  }
+  return FMX_OK;
+}
+
+int wait_rank(fmx_comm* c, cudaStream_t s, int q, int flag, uint32_t value) {
+  CUstreamBatchMemOpParams op;
+  memset(&op, 0, sizeof op);
+  op.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+  op.waitValue.address = c->flag_dev(q, flag);
+  op.waitValue.value = value;
+  op.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+  CUresult r = g_batch((CUstream)s, 1, &op, 0);
+  if (r != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "stream wait-value failed (%d)", (int)r);
+  return FMX_OK;
+}
+
+// ---- data movement ------------------------------------------------------------
+
+int grid_for(size_t work_items, int threads, int cap) {
+  size_t g = (work_items + threads - 1) / threads;
+  return (int)std::max<size_t>(1, std::min<size_t>(g, (size_t)cap));
+}
+
+// Batched copy: kernel (ZC) or copy engine (CE).
+int copy_segments(fmx_comm* c, cudaStream_t s, const std::vector<CopySeg>& segs, bool src_sys,
+                  bool use_kernel) {
+  if (segs.empty()) return FMX_OK;
+  if (!use_kernel) {
+    for (const CopySeg& g : segs)
+      FMX_CUDA(cudaMemcpyAsync(g.dst, g.src, g.bytes, cudaMemcpyDefault, s));
+    return FMX_OK;
+  }
+  for (size_t i0 = 0; i0 < segs.size(); i0 += kMaxSegs) {
+    CopyArgs a;
+    memset(&a, 0, sizeof a);
+    a.nseg = (int)std::min<size_t>(kMaxSegs, segs.size() - i0);
+    a.src_sys = src_sys ? 1 : 0;
+    size_t maxb = 0;
+    for (int k = 0; k < a.nseg; ++k) {
+      a.seg[k] = segs[i0 + k];
+      maxb = std::max(maxb, a.seg[k].bytes);
+    }
+    constexpr int kThreads = 512, kU = 4;
+    int gx = grid_for((maxb / 16 + kU - 1) / kU, kThreads, std::max(1, 1184 / a.nseg));
+    dim3 grid(gx, a.nseg);
+    fmx_copy_kernel<kU><<<grid, kThreads, 0, s>>>(a);
+    FMX_CUDA(cudaGetLastError());
+    c->launches++;
+  }
+  return FMX_OK;
+}
+
+int launch_reduce(fmx_comm* c, cudaStream_t s, const ReduceArgs& a, int dtype, bool aligned) {
+  if (a.len == 0) return FMX_OK;
+  constexpr int kThreads = 256, kU = 2;
+  const int V = dtype == FMX_FLOAT32 ? 4 : 8;
+  if (aligned) {
+    int g = grid_for((a.len / V + kU - 1) / kU + 1, kThreads, 1184);
+    if (dtype == FMX_FLOAT32)
+      fmx_reduce_kernel<float, kU><<<g, kThreads, 0, s>>>(a);
+    else
+      fmx_reduce_kernel<__nv_bfloat16, kU><<<g, kThreads, 0, s>>>(a);
+  } else {
+    int g = grid_for(a.len, kThreads, 1184);
+    if (dtype == FMX_FLOAT32)
+      fmx_reduce_scalar_kernel<float><<<g, kThreads, 0, s>>>(a);
+    else
+      fmx_reduce_scalar_kernel<__nv_bfloat16><<<g, kThreads, 0, s>>>(a);
+  }
+  FMX_CUDA(cudaGetLastError());
+  c->launches++;
+  return FMX_OK;
+}
+
+struct Geometry {
+  size_t count, esz, chunk, slice;
+  uint32_t rounds;
+  size_t lo(int owner, uint32_t j) const { return (size_t)owner * chunk + (size_t)j * slice; }
+  size_t len(int owner, uint32_t j) const {
+    size_t a = lo(owner, j);
+    size_t end = std::min((size_t)(owner + 1) * chunk, count);
+    if (a >= end) return 0;
+    return std::min(slice, end - a);
+  }
+};
+
+int check_comm(fmx_comm* c) {
+  if (!c || !c->hdr) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
+  if (c->hdr->aborted.load(std::memory_order_acquire))
+    return fail(FMX_ERR_ABORTED, "communicator was aborted");
+  return FMX_OK;
+}
+
+int record_done(fmx_comm* c, cudaStream_t s) {
+  FMX_CUDA(cudaEventRecord(c->done, s));
+  c->has_done = true;
+  return FMX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
+                  const fmx_peer_info* self, int mig_aware, size_t slice_bytes, int nslots,
+                  int transport, double timeout_s) {
+  if (!out || !job_key || !self) return fail(FMX_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (nranks < 1 || nranks > FMX_MAX_RANKS)
+    return fail(FMX_ERR_INVALID_ARG, "nranks %d outside 1..%d", nranks, FMX_MAX_RANKS);
+  if (rank < 0 || rank >= nranks || self->rank != rank)
+    return fail(FMX_ERR_BAD_RANKS, "ranks must be 0..%d and distinct", nranks - 1);
+  size_t klen = strlen(job_key);
+  if (klen == 0 || klen > 100 || strchr(job_key, '/'))
+    return fail(FMX_ERR_INVALID_ARG, "job_key must be 1..100 chars without '/'");
+  if (nslots != 0 && nslots != 2) return fail(FMX_ERR_INVALID_ARG, "nslots must be 2");
+  if (transport < FMX_TRANSPORT_AUTO || transport > FMX_TRANSPORT_CE)
+    return fail(FMX_ERR_INVALID_ARG, "bad transport %d", transport);
+  if (timeout_s <= 0) timeout_s = 120.0;
+  fmx_peer_info me = *self;
+  int rc = fmx_check_peer(&me);
+  if (rc) return rc;
+  if ((rc = load_driver())) return rc;
+
+  auto* c = new fmx_comm();
+  c->rank = rank;
+  c->nranks = nranks;
+  c->nslots = 2;
+  const std::string name = std::string("/fmx-") + job_key;
+  const double t_end = now_s() + timeout_s;
+
+  if (rank == 0) {
+    size_t sb = slice_bytes;
+    if (sb == 0) {
+      size_t per = (size_t)c->nslots * ((size_t)nranks * nranks + 2 * nranks);
+      sb = std::min(kDefaultSliceCap, kSegmentBudget / per);
+    }
+    sb = std::max<size_t>(4096, sb / 4096 * 4096);
+    Layout L = compute_layout(nranks, c->nslots, sb);
+    shm_unlink(name.c_str());  // stale segment of a crashed job with the same key
+    int fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+    if (fd < 0) {
+      delete c;
+      return fail(FMX_ERR_SHM, "shm_open(%s) failed: %s", name.c_str(), strerror(errno));
+    }
+    if (ftruncate(fd, (off_t)L.total) != 0) {
+      close(fd);
+      shm_unlink(name.c_str());
+      delete c;
+      return fail(FMX_ERR_SHM, "ftruncate(%zu) failed: %s", L.total, strerror(errno));
+    }
+    void* p = mmap(nullptr, L.total, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) {
+      shm_unlink(name.c_str());
+      delete c;
+      return fail(FMX_ERR_SHM, "mmap(%zu) failed: %s", L.total, strerror(errno));
+    }
+    c->base = (char*)p;
+    c->total_bytes = L.total;
+    Header* h = (Header*)p;
+    h->version = kVersion;
+    h->nranks = nranks;
+    h->nslots = c->nslots;
+    h->slice_bytes = sb;
+    h->total_bytes = L.total;
+    h->peers_off = L.peers_off;
+    h->flags_off = L.flags_off;
+    h->ar_in_off = L.ar_in_off;
+    h->ar_out_off = L.ar_out_off;
+    h->bc_off = L.bc_off;
+    h->creator_pid = (int32_t)getpid();
+    h->mig_aware = mig_aware ? 1 : 0;
+    snprintf(h->job_key, sizeof h->job_key, "%s", job_key);
+    h->magic.store(kMagicReady, std::memory_order_release);
+  } else {
+    for (;;) {
+      if (now_s() > t_end) {
+        delete c;
+        return fail(FMX_ERR_TIMEOUT, "timed out waiting for rank 0 to create %s", name.c_str());
+      }
+      int fd = shm_open(name.c_str(), O_RDWR, 0600);
+      if (fd < 0) {
+        usleep(1000);
+        continue;
+      }
+      struct stat st;
+      if (fstat(fd, &st) != 0 || (size_t)st.st_size < 4096) {
+        close(fd);
+        usleep(1000);
+        continue;
+      }
+      void* p = mmap(nullptr, (size_t)st.st_size, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+      close(fd);
+      if (p == MAP_FAILED) {
+        usleep(1000);
+        continue;
+      }
+      Header* h = (Header*)p;
+      if (h->magic.load(std::memory_order_acquire) != kMagicReady || !pid_alive(h->creator_pid) ||
+          h->total_bytes != (uint64_t)st.st_size) {
+        munmap(p, (size_t)st.st_size);
+        usleep(1000);
+        continue;
+      }
+      if (h->nranks != nranks) {
+        munmap(p, (size_t)st.st_size);
+        delete c;
+        return fail(FMX_ERR_BAD_RANKS, "segment %s has %d ranks, caller says %d", name.c_str(),
+                    h->nranks, nranks);
+      }
+      c->base = (char*)p;
+      c->total_bytes = (size_t)st.st_size;
+      break;
+    }
+  }
+  Header* h = c->hdr = (Header*)c->base;
+  c->slice_bytes = h->slice_bytes;
+  c->L = Layout{h->peers_off, h->flags_off, h->ar_in_off, h->ar_out_off, h->bc_off, h->total_bytes};
+  c->mig_aware = h->mig_aware;
+
+  // publish this rank's PeerInfo
+  PeerSlot* slots = (PeerSlot*)(c->base + c->L.peers_off);
+  int expected = 0;
+  slots[rank].info = me;
+  slots[rank].pid = (int32_t)getpid();
+  if (!slots[rank].state.compare_exchange_strong(expected, 1, std::memory_order_acq_rel)) {
+    unmap(c);
+    delete c;
+    return fail(FMX_ERR_BAD_RANKS, "rank %d joined twice", rank);
+  }
+  h->arrived.fetch_add(1, std::memory_order_acq_rel);
+  while (h->arrived.load(std::memory_order_acquire) < nranks) {
+    if (h->aborted.load() || now_s() > t_end) {
+      int code = h->aborted.load() ? FMX_ERR_ABORTED : FMX_ERR_TIMEOUT;
+      int got = h->arrived.load();
+      if (rank == 0) shm_unlink(name.c_str());
+      unmap(c);
+      delete c;
+      return fail(code, "bootstrap: %d of %d ranks arrived", got, nranks);
+    }
+    usleep(200);
+  }
+  if (rank == 0) shm_unlink(name.c_str());  // everyone has it mapped: no stale name on crash
+
+  c->peers.resize(nranks);
+  for (int r = 0; r < nranks; ++r) c->peers[r] = slots[r].info;
+  int a = -1, b = -1;
+  rc = fmx_validate_peers(c->peers.data(), nranks, c->mig_aware, &a, &b);
+  if (rc == FMX_OK) {
+    std::vector<char> labels((size_t)nranks * FMX_BUS_ID_LEN);
+    rc = fmx_topology(c->peers.data(), nranks, labels.data(), nullptr, nullptr, nullptr);
+  }
+  if (rc != FMX_OK) {
+    unmap(c);
+    delete c;
+    return rc;  // message / dup pair already set
+  }
+
+  // device mapping
+  cudaError_t e = cudaHostRegister(c->base, c->total_bytes,
+                                   cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e == cudaSuccess) {
+    c->registered = true;
+    e = cudaHostGetDevicePointer((void**)&c->dbase, c->base, 0);
+  }
+  c->transport = transport == FMX_TRANSPORT_AUTO ? FMX_TRANSPORT_CE : transport;
+  if (e == cudaSuccess && c->transport == FMX_TRANSPORT_CE)
+    e = cudaMalloc((void**)&c->scratch, (size_t)nranks * c->slice_bytes);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    h->aborted.store(1);
+    fail(FMX_ERR_CUDA, "device mapping of %zu-byte segment failed: %s", c->total_bytes,
+         cudaGetErrorString(e));
+    if (c->registered) cudaHostUnregister(c->base);
+    if (c->scratch) cudaFree(c->scratch);
+    unmap(c);
+    delete c;
+    return FMX_ERR_CUDA;
+  }
+  h->mapped.fetch_add(1, std::memory_order_acq_rel);
+  while (h->mapped.load(std::memory_order_acquire) < nranks) {
+    if (h->aborted.load() || now_s() > t_end) {
+      int code = h->aborted.load() ? FMX_ERR_ABORTED : FMX_ERR_TIMEOUT;
+      fmx_comm_destroy(c);
+      return fail(code, "bootstrap: a rank failed to map the segment");
+    }
+    usleep(200);
+  }
+  *out = c;
+  return FMX_OK;
+}
+
+int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int dtype, int op,
+                  float factor, void* stream) {
+  int rc = check_comm(c);
+  if (rc) return rc;
+  if (dtype != FMX_FLOAT32 && dtype != FMX_BFLOAT16)
+    return fail(FMX_ERR_INVALID_ARG, "bad dtype %d", dtype);
+  if (op < FMX_OP_SUM || op > FMX_OP_PREDIV_SUM) return fail(FMX_ERR_INVALID_ARG, "bad op %d", op);
+  if (op != FMX_OP_SUM && !std::isfinite(factor))
+    return fail(FMX_ERR_INVALID_ARG, "factor must be finite");
+  if (count == 0) return FMX_OK;
+  if (!send || !recv) return fail(FMX_ERR_INVALID_ARG, "null buffer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int n = c->nranks, me = c->rank;
+  const bool zc = c->transport == FMX_TRANSPORT_ZC;
+  Geometry g;
+  g.count = count;
+  g.esz = dtype == FMX_FLOAT32 ? 4 : 2;
+  const size_t vec = 16 / g.esz;
+  g.chunk = ((count + n - 1) / n + vec - 1) / vec * vec;
+  g.slice = c->slice_bytes / g.esz;
+  g.rounds = (uint32_t)((g.chunk + g.slice - 1) / g.slice);
+  const bool aligned = (((uintptr_t)send | (uintptr_t)recv) & 15) == 0;
+  const char* src = (const char*)send;
+  char* dst = (char*)recv;
+
+  if (n == 1) {  // nothing to exchange: apply the scale convention locally
+    ReduceArgs a;
+    memset(&a, 0, sizeof a);
+    a.src[0] = src;
+    a.nsrc = 1;
+    a.out_dev = dst;
+    a.len = count;
+    a.op = op;
+    a.factor = factor;
+    if (op == FMX_OP_SUM) {
+      if (send != recv) FMX_CUDA(cudaMemcpyAsync(recv, send, count * g.esz, cudaMemcpyDeviceToDevice, s));
+    } else if ((rc = launch_reduce(c, s, a, dtype, aligned))) {
+      return rc;
+    }
+    return record_done(c, s);
+  }
+
+  std::vector<CopySeg> segs;
+  auto stage = [&](uint32_t j) -> int {
+    const uint32_t R = c->ar_round + j;
+    segs.clear();
+    for (int o = 0; o < n; ++o) {
+      if (o == me) continue;
+      size_t len = g.len(o, j);
+      if (len) segs.push_back({src + g.lo(o, j) * g.esz, c->in_slot(zc, R, o, me), len * g.esz});
+    }
+    int r = copy_segments(c, s, segs, false, zc);
+    return r ? r : signal(c, s, kStaged, R + 1);
+  };
+
+  if ((rc = stage(0))) return rc;
+  for (uint32_t j = 0; j < g.rounds; ++j) {
+    const uint32_t R = c->ar_round + j;
+    if (j + 1 < g.rounds && (rc = stage(j + 1))) return rc;
+    // reduce-scatter: my chunk, rank order
+    if ((rc = wait_peers(c, s, kStaged, R + 1, me))) return rc;
+    const size_t mylen = g.len(me, j);
+    if (mylen) {
+      ReduceArgs a;
+      memset(&a, 0, sizeof a);
+      a.nsrc = n;
+      a.len = mylen;
+      a.op = op;
+      a.factor = factor;
+      a.out_dev = dst + g.lo(me, j) * g.esz;
+      a.out_sys = c->out_slot(true, R, me);
+      if (!zc) {  // copy engine pulls the n-1 contributions into HBM scratch
+        segs.clear();
+        for (int q = 0; q < n; ++q)
+          if (q != me)
+            segs.push_back({c->in_slot(false, R, me, q), c->scratch + (size_t)q * c->slice_bytes,
+                            mylen * g.esz});
+        if ((rc = copy_segments(c, s, segs, true, false))) return rc;
+      }
+      for (int q = 0; q < n; ++q) {
+        if (q == me) {
+          a.src[q] = src + g.lo(me, j) * g.esz;
+        } else if (zc) {
+          a.src[q] = c->in_slot(true, R, me, q);
+          a.sys_mask |= 1ull << q;
+        } else {
+          a.src[q] = c->scratch + (size_t)q * c->slice_bytes;
+        }
+      }
+      if ((rc = launch_reduce(c, s, a, dtype, aligned))) return rc;
+    }
+    if ((rc = signal(c, s, kReduced, R + 1))) return rc;
+    // all-gather: the other owners' results
+    if ((rc = wait_peers(c, s, kReduced, R + 1, me))) return rc;
+    segs.clear();
+    for (int q = 0; q < n; ++q) {
+      if (q == me) continue;
+      size_t len = g.len(q, j);
+      if (len) segs.push_back({c->out_slot(zc, R, q), dst + g.lo(q, j) * g.esz, len * g.esz});
+    }
+    if ((rc = copy_segments(c, s, segs, true, zc))) return rc;
+  }
+  c->ar_round += g.rounds;
+  return record_done(c, s);
+}
+
+int fmx_broadcast(fmx_comm_t c, const void* send, void* recv, size_t count, int dtype, int root,
+                  void* stream) {
+  int rc = check_comm(c);
+  if (rc) return rc;
+  if (dtype != FMX_FLOAT32 && dtype != FMX_BFLOAT16)
+    return fail(FMX_ERR_INVALID_ARG, "bad dtype %d", dtype);
+  if (root < 0 || root >= c->nranks) return fail(FMX_ERR_INVALID_ARG, "bad root %d", root);
+  if (count == 0) return FMX_OK;
+  const int n = c->nranks, me = c->rank;
+  const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;
+  if (!recv || (me == root && !send)) return fail(FMX_ERR_INVALID_ARG, "null buffer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool zc = c->transport == FMX_TRANSPORT_ZC;
+  if (n == 1) {
+    if (send != recv) FMX_CUDA(cudaMemcpyAsync(recv, send, count * esz, cudaMemcpyDeviceToDevice, s));
+    return record_done(c, s);
+  }
+  const size_t bslice = (size_t)n * c->slice_bytes / esz;
+  const uint32_t rounds = (uint32_t)((count + bslice - 1) / bslice);
+  std::vector<CopySeg> segs(1);
+  for (uint32_t j = 0; j < rounds; ++j) {
+    const uint32_t R = c->bc_round + j;
+    const size_t lo = (size_t)j * bslice, len = std::min(bslice, count - lo);
+    if (me == root) {
+      if (R + 1 > (uint32_t)c->nslots && (rc = wait_peers(c, s, kBcDone, R + 1 - c->nslots, me)))
+        return rc;
+      segs[0] = {(const char*)send + lo * esz, c->bc_slot(zc, R), len * esz};
+      if ((rc = copy_segments(c, s, segs, false, zc))) return rc;
+      if ((rc = signal2(c, s, kBcStaged, R + 1, kBcDone, R + 1))) return rc;
+      if (send != recv)
+        FMX_CUDA(cudaMemcpyAsync((char*)recv + lo * esz, (const char*)send + lo * esz, len * esz,
+                                 cudaMemcpyDeviceToDevice, s));
+    } else {
+      if ((rc = wait_rank(c, s, root, kBcStaged, R + 1))) return rc;
+      segs[0] = {c->bc_slot(zc, R), (char*)recv + lo * esz, len * esz};
+      if ((rc = copy_segments(c, s, segs, true, zc))) return rc;
+      if ((rc = signal(c, s, kBcDone, R + 1))) return rc;
+    }
+  }
+  c->bc_round += rounds;
+  return record_done(c, s);
+}
+
+int fmx_barrier(fmx_comm_t c, double timeout_s) {
+  int rc = check_comm(c);
+  if (rc) return rc;
+  if (timeout_s <= 0) timeout_s = 120.0;
+  const double t_end = now_s() + timeout_s;
+  c->barrier_gen++;
+  const int64_t target = c->barrier_gen * c->nranks;
+  c->hdr->barrier_count.fetch_add(1, std::memory_order_acq_rel);
+  while (c->hdr->barrier_count.load(std::memory_order_acquire) < target) {
+    if (c->hdr->aborted.load()) return fail(FMX_ERR_ABORTED, "communicator was aborted");
+    if (now_s() > t_end) return fail(FMX_ERR_TIMEOUT, "barrier timed out");
+    std::this_thread::yield();
+  }
+  return FMX_OK;
+}
+
+int fmx_comm_destroy(fmx_comm_t c) {
+  if (!c) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
+  int rc = FMX_OK;
+  if (c->has_done && cudaEventSynchronize(c->done) != cudaSuccess)
+    rc = fail(FMX_ERR_CUDA, "pending collective failed: %s", cudaGetErrorString(cudaGetLastError()));
+  if (c->done) cudaEventDestroy(c->done);
+  if (c->scratch) cudaFree(c->scratch);
+  if (c->registered) cudaHostUnregister(c->base);
+  if (c->hdr) c->hdr->departed.fetch_add(1);
+  unmap(c);
+  delete c;
+  return rc;
+}
+
+int fmx_comm_abort(fmx_comm_t c) {
+  if (!c || !c->hdr) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
+  c->hdr->aborted.store(1, std::memory_order_release);
+  // Release every pending stream wait on every rank: push all counters far
+  // ahead (cyclic >= compares, so +2^29 satisfies any outstanding target).
+  for (int r = 0; r < c->nranks; ++r)
+    for (int f = 0; f < kFlagsPerRank; ++f) {
+      volatile uint32_t* p = c->flag_host(r, f);
+      *p = *p + (1u << 29);
+    }
+  __sync_synchronize();
+  return FMX_OK;
+}
+
+int fmx_comm_rank(fmx_comm_t c, int* rank) {
+  if (!c || !rank) return fail(FMX_ERR_INVALID_ARG, "null argument");
+  *rank = c->rank;
+  return FMX_OK;
+}
+
+int fmx_comm_count(fmx_comm_t c, int* nranks) {
+  if (!c || !nranks) return fail(FMX_ERR_INVALID_ARG, "null argument");
+  *nranks = c->nranks;
+  return FMX_OK;
+}
+
+int fmx_comm_peer(fmx_comm_t c, int rank, fmx_peer_info* out) {
+  if (!c || !out || rank < 0 || rank >= c->nranks) return fail(FMX_ERR_INVALID_ARG, "bad rank");
+  *out = c->peers[rank];
+  return FMX_OK;
+}
+
+int fmx_comm_config(fmx_comm_t c, size_t* slice_bytes, int* transport, size_t* shm_bytes) {
+  if (!c) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
+  if (slice_bytes) *slice_bytes = c->slice_bytes;
+  if (transport) *transport = c->transport;
+  if (shm_bytes) *shm_bytes = c->total_bytes;
+  return FMX_OK;
+}
+
+int fmx_comm_kernel_launches(fmx_comm_t c, uint64_t* launches) {
+  if (!c || !launches) return fail(FMX_ERR_INVALID_ARG, "null argument");
+  *launches = c->launches;
+  return FMX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,249 @@
+// sm_100a kernels of the SHM data path.
+//
+//   fmx_copy_kernel    - batched segment copy (stage: HBM -> SHM with 128-bit
+//                        stores; gather / broadcast: SHM -> HBM with 128-bit
+//                        cache-volatile loads).  One blockIdx.y per segment.
+//   fmx_reduce_kernel  - owner-chunk reduction: n sources (peer slots in SHM or
+//                        HBM scratch, own chunk in HBM), fixed ascending-rank
+//                        fp32 sum (__fadd_rn, no contraction), fused
+//                        pre-divide / post-scale and bf16 RNE cast, written to
+//                        the rank's HBM result and its SHM result slot.
+//
+// All host-link traffic is streaming (each byte touched once), so the kernels
+// are memory-level-parallelism bound: 128-bit accesses, several independent
+// vectors in flight per thread, grid-stride over the piece.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/flexshm.h"
+
+namespace fmx {
+
+constexpr int kMaxSegs = 64;
+
+struct CopySeg {
+  const char* src;
+  char* dst;
+  size_t bytes;
+};
+
+struct CopyArgs {
+  CopySeg seg[kMaxSegs];
+  int nseg;
+  int src_sys;  // 1: sources live in mapped host memory -> ld.cv
+};
+
+struct ReduceArgs {
+  const char* src[FMX_MAX_RANKS];  // rank-ordered sources
+  uint64_t sys_mask;               // bit q set: src[q] is mapped host memory
+  char* out_dev;                   // HBM result (may alias src[own])
+  char* out_sys;                   // SHM result slot (may be null)
+  size_t len;                      // elements
+  int nsrc;
+  int op;
+  float factor;
+};
+
+__device__ __forceinline__ uint4 ld_cv_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.cv.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ uint4 ld_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// ---------------------------------------------------------------- copy
+
+template <int U>
+__global__ void __launch_bounds__(512) fmx_copy_kernel(const __grid_constant__ CopyArgs a) {
+  const CopySeg s = a.seg[blockIdx.y];
+  const size_t nvec = s.bytes / 16;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((((uintptr_t)s.src | (uintptr_t)s.dst) & 15) == 0) {
+    for (; i + (U - 1) * stride < nvec; i += U * stride) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        v[u] = a.src_sys ? ld_cv_v4(s.src + (i + u * stride) * 16)
+                         : ld_v4(s.src + (i + u * stride) * 16);
+#pragma unroll
+      for (int u = 0; u < U; ++u) st_v4(s.dst + (i + u * stride) * 16, v[u]);
+    }
+    for (; i < nvec; i += stride)
+      st_v4(s.dst + i * 16, a.src_sys ? ld_cv_v4(s.src + i * 16) : ld_v4(s.src + i * 16));
+    // byte tail
+    size_t t = nvec * 16 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; t < s.bytes; t += stride) s.dst[t] = ((volatile const char*)s.src)[t];
+  } else {
+    for (; i < s.bytes; i += stride) s.dst[i] = ((volatile const char*)s.src)[i];
+  }
+}
+
+// ---------------------------------------------------------------- reduce
+
+template <typename T>
+struct Elem;
+
+template <>
+struct Elem<float> {
+  static constexpr int kVec = 4;
+  __device__ static __forceinline__ void widen(const uint4& v, float* f) {
+    f[0] = __uint_as_float(v.x);
+    f[1] = __uint_as_float(v.y);
+    f[2] = __uint_as_float(v.z);
+    f[3] = __uint_as_float(v.w);
+  }
+  __device__ static __forceinline__ uint4 narrow(const float* f) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                      __float_as_uint(f[3]));
+  }
+  __device__ static __forceinline__ float prediv(float x, float d) { return __fdiv_rn(x, d); }
+  __device__ static __forceinline__ float load1(const char* p) {
+    return *(volatile const float*)p;
+  }
+  __device__ static __forceinline__ void store1(char* p, float v) { *(float*)p = v; }
+};
+
+__device__ __forceinline__ float bf16_bits_to_f32(uint32_t b) { return __uint_as_float(b << 16); }
+__device__ __forceinline__ uint32_t f32_to_bf16_bits(float f) {
+  return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+template <>
+struct Elem<__nv_bfloat16> {
+  static constexpr int kVec = 8;
+  __device__ static __forceinline__ void widen(const uint4& v, float* f) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      f[2 * k] = bf16_bits_to_f32(w[k] & 0xFFFFu);
+      f[2 * k + 1] = bf16_bits_to_f32(w[k] >> 16);
+    }
+  }
+  __device__ static __forceinline__ uint4 narrow(const float* f) {
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = f32_to_bf16_bits(f[2 * k]) | (f32_to_bf16_bits(f[2 * k + 1]) << 16);
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  // A bf16 bucket divided in place is rounded back to bf16 before the sum.
+  __device__ static __forceinline__ float prediv(float x, float d) {
+    return bf16_bits_to_f32(f32_to_bf16_bits(__fdiv_rn(x, d)));
+  }
+  __device__ static __forceinline__ float load1(const char* p) {
+    return bf16_bits_to_f32(*(volatile const unsigned short*)p);
+  }
+  __device__ static __forceinline__ void store1(char* p, float v) {
+    *(unsigned short*)p = (unsigned short)f32_to_bf16_bits(v);
+  }
+};
+
+// Sum of one 16-byte vector position across all sources, rank order.
+template <typename T>
+__device__ __forceinline__ void reduce_vec(const ReduceArgs& a, size_t off, float* acc) {
+  using E = Elem<T>;
+  constexpr int V = E::kVec;
+  constexpr int B = 8;  // sources loaded per batch (independent loads in flight)
+  const bool prediv = a.op == FMX_OP_PREDIV_SUM;
+  for (int q0 = 0; q0 < a.nsrc; q0 += B) {
+    uint4 raw[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int q = q0 + b;
+      if (q < a.nsrc)
+        raw[b] = ((a.sys_mask >> q) & 1) ? ld_cv_v4(a.src[q] + off) : ld_v4(a.src[q] + off);
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int q = q0 + b;
+      if (q < a.nsrc) {
+        float x[V];
+        E::widen(raw[b], x);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          float c = prediv ? E::prediv(x[k], a.factor) : x[k];
+          acc[k] = q == 0 ? c : __fadd_rn(acc[k], c);
+        }
+      }
+    }
+  }
+  if (a.op == FMX_OP_SUM_POSTSCALE) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] = __fmul_rn(acc[k], a.factor);
+  }
+}
+
+template <typename T, int U>
+__global__ void __launch_bounds__(256) fmx_reduce_kernel(const __grid_constant__ ReduceArgs a) {
+  using E = Elem<T>;
+  constexpr int V = E::kVec;
+  const size_t nvec = a.len / V;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (size_t i = tid; i < nvec; i += U * stride) {
+    float acc[U][V];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i + u * stride < nvec) reduce_vec<T>(a, (i + u * stride) * 16, acc[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (i + u * stride < nvec) {
+        uint4 o = E::narrow(acc[u]);
+        st_v4(a.out_dev + (i + u * stride) * 16, o);
+        if (a.out_sys) st_v4(a.out_sys + (i + u * stride) * 16, o);
+      }
+    }
+  }
+  // element tail (len not a multiple of the vector width)
+  const size_t esz = sizeof(T);
+  for (size_t e = nvec * V + tid; e < a.len; e += stride) {
+    float acc = 0.f;
+    for (int q = 0; q < a.nsrc; ++q) {
+      float c = E::load1(a.src[q] + e * esz);
+      if (a.op == FMX_OP_PREDIV_SUM) c = E::prediv(c, a.factor);
+      acc = q == 0 ? c : __fadd_rn(acc, c);
+    }
+    if (a.op == FMX_OP_SUM_POSTSCALE) acc = __fmul_rn(acc, a.factor);
+    E::store1(a.out_dev + e * esz, acc);
+    if (a.out_sys) E::store1(a.out_sys + e * esz, acc);
+  }
+}
+
+// Unaligned fallback: one element per thread iteration.
+template <typename T>
+__global__ void __launch_bounds__(256) fmx_reduce_scalar_kernel(const __grid_constant__ ReduceArgs a) {
+  using E = Elem<T>;
+  const size_t esz = sizeof(T);
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.len; e += stride) {
+    float acc = 0.f;
+    for (int q = 0; q < a.nsrc; ++q) {
+      float c = E::load1(a.src[q] + e * esz);
+      if (a.op == FMX_OP_PREDIV_SUM) c = E::prediv(c, a.factor);
+      acc = q == 0 ? c : __fadd_rn(acc, c);
+    }
+    if (a.op == FMX_OP_SUM_POSTSCALE) acc = __fmul_rn(acc, a.factor);
+    E::store1(a.out_dev + e * esz, acc);
+    if (a.out_sys) E::store1(a.out_sys + e * esz, acc);
+  }
+}
+
+}  // namespace fmx

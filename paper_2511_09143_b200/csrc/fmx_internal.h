@@ -1,0 +1,58 @@
+// Internal declarations shared by the host and device halves of libflexshm.
+#pragma once
+
+#include <atomic>
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include "../../include/flexshm.h"
+
+namespace fmx {
+
+// ---- error state (thread-local, fmx_last_error / fmx_dup_ranks) ------------
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+void set_dup(int a, int b);
+
+// ---- SHM segment layout ----------------------------------------------------
+// [header 4 KiB][peer table][flag lines][AR in-slots][AR out-slots][BC slots]
+// Every region starts on a 4 KiB boundary; every flag owns a 64-byte line.
+constexpr uint32_t kMagicReady = 0x464D5831u;  // "FMX1"
+constexpr uint32_t kVersion = 1;
+constexpr int kFlagsPerRank = 4;
+enum Flag { kStaged = 0, kReduced = 1, kBcStaged = 2, kBcDone = 3 };
+
+struct alignas(64) PeerSlot {
+  std::atomic<int32_t> state;  // 0 empty, 1 published
+  int32_t pid;
+  fmx_peer_info info;
+};
+
+struct Header {
+  std::atomic<uint32_t> magic;
+  uint32_t version;
+  int32_t nranks;
+  int32_t nslots;
+  uint64_t slice_bytes;
+  uint64_t total_bytes;
+  uint64_t peers_off, flags_off, ar_in_off, ar_out_off, bc_off;
+  int32_t creator_pid;
+  int32_t mig_aware;
+  alignas(64) std::atomic<int32_t> arrived;
+  alignas(64) std::atomic<int32_t> mapped;
+  alignas(64) std::atomic<int32_t> aborted;
+  alignas(64) std::atomic<int64_t> barrier_count;
+  alignas(64) std::atomic<int32_t> departed;
+  char job_key[128];
+};
+
+struct Layout {
+  size_t peers_off, flags_off, ar_in_off, ar_out_off, bc_off, total;
+};
+Layout compute_layout(int nranks, int nslots, size_t slice_bytes);
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+double now_s();
+
+}  // namespace fmx

@@ -1,0 +1,71 @@
+"""Rank-process bodies for the multi-process GPU tests (spawned by
+paper_2511_09143_b200.launcher.launch).  Inputs are drawn with the oracle's
+seeded generators so the parent can recompute the expected result."""
+
+from __future__ import annotations
+
+import hashlib
+import os
+
+import numpy as np
+
+
+def make_input(rank: int, sc: dict) -> np.ndarray:
+    from oracle import oracle as orc
+    dt = orc.F32 if sc["dtype"] == "f32" else orc.BF16
+    if sc.get("inputs", "normal") == "adversarial":
+        return orc.adversarial(rank, sc["count"], dt)
+    return orc.synthetic_gradient(rank, sc["count"], dt, seed=sc.get("seed", 1234))
+
+
+def digest(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).view(np.uint8)).hexdigest()
+
+
+def suite_worker(rank: int, job_key: str, n: int, transport: str, mode: str, scenarios: list,
+                 slice_bytes: int = 0, peer_override: dict | None = None):
+    import torch
+
+    from paper_2511_09143_b200 import instance as inst_mod
+    from paper_2511_09143_b200.comm import init_process_group
+    from paper_2511_09143_b200.commsim import PeerInfo
+
+    inst = inst_mod.bind(0, rank + 1, mode=mode)
+    peer = inst_mod.peer_info(inst, rank)
+    if peer_override and rank in peer_override:
+        peer = PeerInfo(rank, peer.pcie_bus_id, peer_override[rank], peer.host_hash, peer.pid_hash)
+    try:
+        comm = init_process_group(None, rank, job_key, instance=inst, peer=peer, nranks=n,
+                                  slice_bytes=slice_bytes, transport=transport, timeout_s=120)
+    except Exception as exc:  # bootstrap failures are part of what we test
+        return {"init_error": type(exc).__name__, "args": getattr(exc, "rank_a", None),
+                "args_b": getattr(exc, "rank_b", None)}
+    out = []
+    stream = inst.stream
+    for sc in scenarios:
+        x = make_input(rank, sc)
+        tdtype = torch.float32 if sc["dtype"] == "f32" else torch.bfloat16
+        host = torch.from_numpy(x.view(np.float32) if sc["dtype"] == "f32" else x.view(np.int16))
+        off = sc.get("offset", 0)
+        buf = torch.empty(sc["count"] + off, dtype=tdtype, device="cuda")
+        t = buf[off:]
+        t.copy_(host.view(tdtype) if sc["dtype"] != "f32" else host, non_blocking=False)
+        if sc["kind"] == "allreduce":
+            if sc.get("inplace", True):
+                comm.allreduce(t, op=sc.get("op", "sum"), factor=sc.get("factor"), stream=stream)
+                res = t
+            else:
+                res = torch.empty_like(t)
+                comm.allreduce(t, op=sc.get("op", "sum"), factor=sc.get("factor"), out=res,
+                               stream=stream)
+        else:
+            comm.broadcast(t, root=sc["root"], stream=stream)
+            res = t
+        torch.cuda.synchronize()
+        r = res.cpu()
+        arr = r.numpy() if sc["dtype"] == "f32" else r.view(torch.int16).numpy().view(np.uint16)
+        out.append(digest(arr) if sc.get("ret") == "sha" else arr.copy())
+    launches = comm.kernel_launches()
+    comm.barrier()
+    comm.destroy()
+    return {"results": out, "launches": launches, "pid": os.getpid()}

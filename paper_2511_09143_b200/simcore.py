@@ -1,0 +1,67 @@
+"""Cost model of a multi-leaf job (adjacent to the path).
+
+The reference's only stand-in for the SHM allreduce is a constant factor:
+`PerfModel.multi_overhead` x `placement_penalty(imbalance)` x
+`net_transport_factor` (reference `pkg/src/migsim/simcore.py:37-100`).
+`estimate_jct` reproduces that arithmetic exactly so the reference's
+`estimate_jct` tests run unchanged; `PerfModel.from_measurement` is the hook
+for recalibrating `multi_overhead` from measured B200 step times (a
+one-to-many step time over the one-to-one step time).  The discrete-event
+engine (`Simulation`, simcore.py:213-419) is out of scope.
+"""
+
+from __future__ import annotations
+
+from dataclasses import asdict, dataclass
+
+from .errors import InvalidDecisionError
+from .scheduler import AllocationDecision
+from .workload import Job
+
+
+@dataclass
+class PerfModel:
+    speedup_1g10: float = 0.8
+    multi_overhead: float = 1.07
+    placement_penalty_slope: float = 0.03
+    placement_penalty_cap: float = 1.15
+    contention_factor: float = 1.06
+    net_transport_factor: float = 1.0
+
+    def placement_penalty(self, imbalance: int) -> float:
+        return min(1.0 + self.placement_penalty_slope * imbalance, self.placement_penalty_cap)
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+    @classmethod
+    def from_dict(cls, doc: dict) -> "PerfModel":
+        return cls(**doc)
+
+    @classmethod
+    def from_measurement(cls, one_to_many_step_s: float, one_to_one_step_s: float,
+                         **overrides) -> "PerfModel":
+        """Calibrate `multi_overhead` as measured step-time ratio."""
+        if one_to_one_step_s <= 0 or one_to_many_step_s <= 0:
+            raise ValueError("step times must be positive")
+        return cls(multi_overhead=one_to_many_step_s / one_to_one_step_s, **overrides)
+
+
+def estimate_jct(job: Job, decision: AllocationDecision, model: PerfModel,
+                 num_gpus: int = 2) -> float:
+    """Uncontended duration of `job` under `decision` (simcore.py:72-100)."""
+    insts = decision.instances
+    if not insts or len(decision.profiles) != len(insts):
+        raise InvalidDecisionError(f"malformed decision for job {job.job_id}")
+    if len(insts) == 1:
+        lone_double = job.size == 1 and decision.profiles[0] == "1g.10gb"
+        return job.base_duration_s * (model.speedup_1g10 if lone_double else 1.0)
+    per_gpu = dict.fromkeys(range(num_gpus), 0)
+    for gpu_id, _ in insts:
+        if gpu_id not in per_gpu:
+            raise InvalidDecisionError(f"decision references unknown gpu {gpu_id}")
+        per_gpu[gpu_id] += 1
+    imbalance = max(per_gpu.values()) - min(per_gpu.values())
+    return job.base_duration_s * (model.multi_overhead
+                                  * model.placement_penalty(imbalance)
+                                  * model.net_transport_factor)
