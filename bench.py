@@ -1,0 +1,435 @@
+"""Benchmark of the one-to-many SHM allreduce (BASELINE.json metric:
+"SHM allreduce GB/s vs host-link peak; ResNet-50 img/s on 1g slices").
+
+Workload (N=1): BASELINE configs[1]'s communication step - the ResNet-50
+gradient (25,557,032 fp32 = 102,228,128 B, the size torchvision's resnet50
+has) allreduced across the 7 1g instances of one B200 (rank order from
+fm_select, one process per instance).  N>1 (torchrun, one process per GPU):
+7 instances per GPU, 7N ranks in one communicator, rank order from fm_select
+over N GPUs (weak scaling: the per-rank gradient is fixed).
+
+A step = one allreduce of every rank's gradient.  `value` = algbw = gradient
+bytes / step time (device time, CUDA events on each rank's stream, max over
+ranks).  Inputs are device-resident and 7 x 102 MB per GPU of gradients plus
+the SHM slots exceed the 126 MB L2.  `e2e` = the same metric through the
+public API with host buffers: each step copies every rank's gradient from
+pinned host memory to the device, allreduces, and copies the result back.
+
+`--impl reference` times the CPU restatement of the same algorithm
+(oracle/flexshm_oracle.c: multi-threaded SHM reduce-scatter/all-gather,
+bit-identical results) on the box's host cores - the reference itself has no
+runnable allreduce (its data path is NCCL).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+RESNET50_PARAMS = 25_557_032
+RANKS_PER_GPU = 7
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# Host-link peaks measured on this pool's B200 box (profiles/r01_probe/bw.jsonl):
+# copy-engine pinned H2D / D2H / bidirectional, PCIe Gen5 x16.
+LINK_PEAK_FALLBACK = {"h2d": 55.61, "d2h": 56.77, "bidir": 100.21}
+
+
+def parse_args(argv=None):
+    p = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--ranks-per-gpu", type=int, default=RANKS_PER_GPU)
+    p.add_argument("--count", type=int, default=RESNET50_PARAMS)
+    p.add_argument("--dtype", choices=["f32", "bf16"], default="f32")
+    p.add_argument("--transport", choices=["auto", "ce", "zc"], default="auto")
+    p.add_argument("--mode", choices=["green", "mps", "full"], default="green")
+    p.add_argument("--slice-bytes", type=int, default=0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--inproc", action="store_true",
+                   help="ranks as threads of one process (for ncu); not the headline layout")
+    p.add_argument("--out", default=None, help="also write the JSON line here")
+    return p.parse_args(argv)
+
+
+# ----------------------------------------------------------------------------- helpers
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return int(os.environ.get("RANK", "0")), ws, int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def decision_for(gpus: int, ranks_per_gpu: int):
+    from paper_2511_09143_b200.scheduler import fm_select, make_cluster
+    from paper_2511_09143_b200.workload import Job
+    d = fm_select(Job(0, "train", gpus * ranks_per_gpu, 0.0, 0.0), make_cluster("FM", gpus))
+    assert d is not None and len(d.instances) == gpus * ranks_per_gpu
+    return d
+
+
+def link_bytes(n: int, per_gpu: list[int], s_bytes: int):
+    """Algorithmic host-link bytes per allreduce for each GPU:
+    D2H_g = k_g * S, H2D_g = 2 k_g (n-1)/n * S."""
+    return [(k * s_bytes, 2 * k * (n - 1) * s_bytes / n) for k in per_gpu]
+
+
+def step_roofline(n, per_gpu, s_bytes, t_s, peaks):
+    """T* = max_g max(D2H/B_d2h, H2D/B_h2d, (D2H+H2D)/B_bidir)."""
+    tstar = 0.0
+    for d2h, h2d in link_bytes(n, per_gpu, s_bytes):
+        tstar = max(tstar, d2h / (peaks["d2h"] * 1e9), h2d / (peaks["h2d"] * 1e9),
+                    (d2h + h2d) / (peaks["bidir"] * 1e9))
+    d2h0, h2d0 = link_bytes(n, per_gpu, s_bytes)[0]
+    return {"bound": "host_link", "t_star_ms": tstar * 1e3, "frac": tstar / t_s,
+            "achieved": (d2h0 + h2d0) / t_s / 1e9, "unit": "GB/s",
+            "peak_bidir": peaks["bidir"], "peak_h2d": peaks["h2d"], "peak_d2h": peaks["d2h"],
+            "link_bytes_per_gpu": {"d2h": d2h0, "h2d": h2d0},
+            "peak_source": "profiles/r01_probe/bw.jsonl (cudaMemcpyAsync pinned, best of 5)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- rank body
+
+
+def rank_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_local: int,
+              barrier_comm=None):
+    """One instance rank: bind, join, warm up, time K device-resident
+    allreduces, then K end-to-end (host buffer) allreduces."""
+    import torch
+
+    from paper_2511_09143_b200 import instance as inst_mod
+    from paper_2511_09143_b200.comm import init_process_group
+
+    gpu_id, inst_id = cfg["instances"][rank]
+    inst = inst_mod.bind(gpu_id, inst_id, cfg["profiles"][rank], mode=inst_mode, device=gpu_local)
+    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n,
+                              transport=cfg["transport"], slice_bytes=cfg["slice_bytes"],
+                              timeout_s=300)
+    stream = inst.stream
+    tdt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
+    count = cfg["count"]
+    gen = torch.Generator(device="cpu").manual_seed(1234 + rank)
+    host = (torch.randn(count, generator=gen) * (1e-3 if cfg["dtype"] == "f32" else 1e-2)).to(tdt)
+    with torch.cuda.stream(stream):
+        buf = host.to(f"cuda:{gpu_local}")
+        base = buf.clone()
+    out = {"rank": rank}
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed(k: int, e2e: bool, pinned_in=None, pinned_out=None):
+        comm.barrier(300)
+        torch.cuda.synchronize()
+        comm.barrier(300)
+        l0 = comm.kernel_launches()
+        ev0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(k):
+                if e2e:
+                    buf.copy_(pinned_in, non_blocking=True)
+                    comm.allreduce(buf, stream=stream)
+                    pinned_out.copy_(buf, non_blocking=True)
+                else:
+                    comm.allreduce(buf, stream=stream)
+        ev1.record(stream)
+        ev1.synchronize()
+        comm.barrier(300)
+        return ev0.elapsed_time(ev1), comm.kernel_launches() - l0
+
+    # warm-up (untimed)
+    with torch.cuda.stream(stream):
+        for _ in range(cfg["warmup"]):
+            comm.allreduce(buf, stream=stream)
+    torch.cuda.synchronize()
+    ms, launches = timed(cfg["steps"], False)
+    out["ms_total"], out["launches"] = ms, launches
+    if cfg["e2e"]:
+        pin_in = host.pin_memory()
+        pin_out = torch.empty_like(pin_in).pin_memory()
+        with torch.cuda.stream(stream):
+            buf.copy_(pin_in, non_blocking=True)
+            comm.allreduce(buf, stream=stream)
+            pin_out.copy_(buf, non_blocking=True)
+        torch.cuda.synchronize()
+        ms_e2e, l_e2e = timed(cfg["steps"], True, pin_in, pin_out)
+        out["ms_total_e2e"], out["launches_e2e"] = ms_e2e, l_e2e
+        # parity spot check of the e2e result against the device path: every
+        # rank must hold the same bytes
+        out["e2e_digest"] = int(pin_out.view(torch.int32 if tdt == torch.float32 else torch.int16)
+                                .to(torch.int64).sum().item())
+    del base
+    comm.destroy()
+    return out
+
+
+def _spawned_rank(rank, job_key, n, cfg, inst_mode, gpu_local):
+    return rank_body(rank, job_key, n, cfg, inst_mode, gpu_local)
+
+
+# ----------------------------------------------------------------------------- arms
+
+
+def run_ours(args) -> dict | None:
+    import multiprocessing as mp
+
+    import torch
+
+    grank, world, local = dist_env()
+    gpus = args.gpus if world == 1 else world
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    d = decision_for(gpus, args.ranks_per_gpu)
+    n = len(d.instances)
+    cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
+           "slice_bytes": args.slice_bytes, "dtype": args.dtype, "count": args.count,
+           "warmup": args.warmup, "steps": args.steps, "e2e": not args.no_e2e}
+    # one job key for all processes of all GPUs
+    job_key = os.environ.get("FMX_BENCH_KEY") or f"bench-{os.environ.get('MASTER_PORT', '0')}-" \
+        f"{os.environ.get('TORCHELASTIC_RUN_ID', str(os.getppid()))}"
+    if world > 1:
+        import torch.distributed as dist
+        obj = [job_key if grank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        job_key = obj[0]
+    my_gpu = grank if world > 1 else 0
+    mine = [r for r, (g, _) in enumerate(d.instances) if g == my_gpu] if world > 1 else list(range(n))
+    gpu_local = local if world > 1 else 0
+    if world > 1:
+        os.environ["CUDA_VISIBLE_DEVICES"] = os.environ.get("CUDA_VISIBLE_DEVICES", str(local))
+    inst_mode = args.mode
+    sampler = ClockSampler()
+    results = {}
+    errors = []
+
+    if args.inproc:
+        # all ranks of this GPU as threads (ncu-friendly); primary context
+        def th(r):
+            try:
+                results[r] = rank_body(r, job_key, n, cfg, "full", gpu_local)
+            except BaseException as exc:  # noqa: BLE001
+                errors.append((r, exc))
+        ts = [threading.Thread(target=th, args=(r,)) for r in mine]
+        sampler.start()
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    else:
+        ctx = mp.get_context("spawn")
+        mps = None
+        if inst_mode == "mps":
+            from paper_2511_09143_b200.launcher import MPS_PERCENT, MpsDaemon
+            mps = MpsDaemon(job_key)
+            if not mps.start():
+                raise RuntimeError("MPS daemon failed to start")
+            os.environ.update(mps.env)
+            os.environ["CUDA_MPS_ACTIVE_THREAD_PERCENTAGE"] = str(MPS_PERCENT)
+        try:
+            with ctx.Pool(len(mine) - 1) as pool:
+                async_res = [pool.apply_async(_spawned_rank, (r, job_key, n, cfg, inst_mode, gpu_local))
+                             for r in mine[1:]]
+                sampler.start()
+                try:
+                    results[mine[0]] = rank_body(mine[0], job_key, n, cfg, inst_mode, gpu_local)
+                except BaseException as exc:  # noqa: BLE001
+                    errors.append((mine[0], exc))
+                for r, a in zip(mine[1:], async_res):
+                    try:
+                        results[r] = a.get(timeout=900)
+                    except BaseException as exc:  # noqa: BLE001
+                        errors.append((r, exc))
+        finally:
+            if mps is not None:
+                mps.stop()
+    clocks = sampler.stop()
+    if errors:
+        raise RuntimeError(f"rank {errors[0][0]} failed: {errors[0][1]!r}") from errors[0][1]
+    local_max = max(r["ms_total"] for r in results.values())
+    local_max_e2e = max(r.get("ms_total_e2e", 0.0) for r in results.values())
+    launches = sum(r["launches"] for r in results.values())
+    digests = {r.get("e2e_digest") for r in results.values()}
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([local_max, local_max_e2e, float(launches)], dtype=torch.float64)
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        local_max, local_max_e2e, launches = mx[0].item(), mx[1].item(), int(sm[2].item())
+        if grank != 0:
+            dist.destroy_process_group()
+            return None
+        dist.destroy_process_group()
+    esz = 4 if args.dtype == "f32" else 2
+    s_bytes = args.count * esz
+    t_step = local_max / 1e3 / args.steps
+    per_gpu = [sum(1 for g, _ in d.instances if g == gg) for gg in range(gpus)]
+    peaks = dict(LINK_PEAK_FALLBACK)
+    line = {
+        "metric": "SHM allreduce GB/s vs host-link peak; ResNet-50 img/s on 1g slices",
+        "value": s_bytes / t_step / 1e9,
+        "unit": "GB/s (algbw: ResNet-50 gradient bytes allreduced per second)",
+        "n_gpus": gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "float32" if args.dtype == "f32" else "bfloat16",
+        "data": "synthetic (seeded N(0,1)*1e-3 gradient per rank)",
+        "config": {"workload": f"ResNet-50-sized gradient allreduce ({args.count} "
+                               f"{args.dtype}) across {args.ranks_per_gpu} 1g instances per "
+                               f"B200 x {gpus} (BASELINE configs[1] comm step)",
+                   "ranks": n, "ranks_per_gpu": per_gpu, "bytes": s_bytes,
+                   "instance_mode": "threads" if args.inproc else inst_mode,
+                   "transport": args.transport, "l2": "inputs > L2 (7 x 102 MB per GPU)",
+                   "rank_order": "fm_select round-robin"},
+        "busbw_gbs": s_bytes / t_step / 1e9 * 2 * (n - 1) / n,
+        "step_roofline": step_roofline(n, per_gpu, s_bytes, t_step, peaks),
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if not args.no_e2e:
+        t_e2e = local_max_e2e / 1e3 / args.steps
+        line["e2e"] = {"value": s_bytes / t_e2e / 1e9, "unit": line["unit"],
+                       "ms_per_step": t_e2e * 1e3,
+                       "h2d_bytes_per_step": n * s_bytes, "d2h_bytes_per_step": n * s_bytes,
+                       "ranks_agree": len(digests) == 1}
+    return line
+
+
+def run_cpu_reference(count: int, n: int, dtype: str, steps: int, warmup: int,
+                      nthreads: int | None = None, seconds: float | None = None) -> dict:
+    """CPU restatement of the same algorithm (oracle/), all host threads."""
+    import numpy as np
+
+    from oracle import oracle as orc
+    dt = orc.F32 if dtype == "f32" else orc.BF16
+    nthreads = nthreads or os.cpu_count() or 1
+    bufs = [orc.synthetic_gradient(r, count, dt) for r in range(n)]
+    shm = orc.ShmAllreduce(n, count, dt, nthreads)
+    for _ in range(warmup):
+        shm(bufs)
+    times = []
+    t_end = time.perf_counter() + (seconds or 0)
+    k = 0
+    while k < steps or (seconds and time.perf_counter() < t_end):
+        t0 = time.perf_counter()
+        shm(bufs)
+        times.append(time.perf_counter() - t0)
+        k += 1
+    t = sum(times) / len(times)
+    esz = 4 if dtype == "f32" else 2
+    del np
+    return {"value": count * esz / t / 1e9, "ms_per_step": t * 1e3, "iters": k,
+            "cores": nthreads}
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    grank, world, _ = dist_env()
+    n = (args.gpus if world == 1 else world) * args.ranks_per_gpu
+    unit = "GB/s (algbw: ResNet-50 gradient bytes allreduced per second)"
+    if args.impl == "reference":
+        if grank != 0:
+            return 0
+        r = run_cpu_reference(args.count, n, args.dtype, args.steps, args.warmup)
+        sample = (f"{n} rank buffers of {args.count} {args.dtype} in one process; "
+                  f"{r['iters']} full allreduces, {r['cores']} threads")
+        line = {"impl": "reference", "metric": "SHM allreduce GB/s vs host-link peak; ResNet-50 "
+                "img/s on 1g slices", "value": r["value"], "unit": unit,
+                "n_gpus": args.gpus if world == 1 else world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None,
+                "dtype": "float32" if args.dtype == "f32" else "bfloat16", "data": "synthetic",
+                "config": {"workload": f"ResNet-50-sized gradient allreduce ({args.count} "
+                                       f"{args.dtype}) across {n} ranks", "ranks": n},
+                "cpu_baseline": {"value": r["value"], "unit": unit, "cores": r["cores"],
+                                 "kind": "port", "sample": sample},
+                "e2e": {"value": r["value"], "unit": unit, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0},
+                "note": "reference has no runnable allreduce (NCCL in the paper); CPU port of "
+                        "the same SHM RS/AG algorithm, oracle/flexshm_oracle.c"}
+        print(json.dumps(line))
+        return 0
+    line = run_ours(args)
+    if line is None:
+        return 0
+    if not args.no_cpu_baseline:
+        r = run_cpu_reference(args.count, n, args.dtype, 1, 1, seconds=args.cpu_seconds)
+        line["cpu_baseline"] = {"value": r["value"], "unit": line["unit"], "cores": r["cores"],
+                                "kind": "port",
+                                "sample": f"full workload ({n} ranks x {args.count} {args.dtype}), "
+                                          f"{r['iters']} allreduces in ~{args.cpu_seconds:.0f} s, "
+                                          f"oracle/flexshm_oracle.c threads"}
+    print(json.dumps(line))
+    if args.out:
+        with open(args.out, "w") as f:
+            f.write(json.dumps(line) + "\n")
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

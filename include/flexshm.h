@@ -78,8 +78,15 @@ enum fmx_op {
 /* How host-link bytes move.  ZC: SM kernels store to / load from the mapped
  * SHM segment (128-bit, zero-copy).  CE: copy engines move the bytes, SM
  * kernels reduce out of HBM.  AUTO picks CE (measured faster across processes
- * on one GPU). */
-enum fmx_transport { FMX_TRANSPORT_AUTO = 0, FMX_TRANSPORT_ZC = 1, FMX_TRANSPORT_CE = 2 };
+ * on one GPU).  HOST joins the bootstrap and host barrier without
+ * touching CUDA (collectives then return FMX_ERR_UNSUPPORTED); it is how the
+ * multi-process bootstrap is exercised on GPU-less machines. */
+enum fmx_transport {
+  FMX_TRANSPORT_AUTO = 0,
+  FMX_TRANSPORT_ZC = 1,
+  FMX_TRANSPORT_CE = 2,
+  FMX_TRANSPORT_HOST = 3 /* bootstrap + barrier only, no CUDA calls at all */
+};
 
 /* One rank's identity (commsim.PeerInfo, commsim.py:27-42). */
 typedef struct fmx_peer_info {
@@ -147,8 +154,23 @@ int fmx_comm_count(fmx_comm_t comm, int* nranks);
 int fmx_comm_peer(fmx_comm_t comm, int rank, fmx_peer_info* out);
 /* Effective configuration: slice bytes, transport, segment bytes. */
 int fmx_comm_config(fmx_comm_t comm, size_t* slice_bytes, int* transport, size_t* shm_bytes);
+/* Snapshot of every rank's flag counters (nranks x 4: STAGED, REDUCED,
+ * BC_STAGED, BC_DONE), read from host memory - for hang diagnosis. */
+int fmx_comm_flags(fmx_comm_t comm, uint32_t* out, int cap);
 /* Number of device kernels this communicator has launched so far. */
 int fmx_comm_kernel_launches(fmx_comm_t comm, uint64_t* launches);
+
+/* ---- schedule introspection (no GPU, no segment) ---------------------------- */
+
+/* Write the schedule `rank` of an `nranks` communicator would enqueue for a
+ * sequence of `nops` collectives (kinds[i]: 0 allreduce, 1 broadcast with
+ * roots[i]) as text: one line per SHM access ("W off bytes round", "R off
+ * bytes writer round") or flag op ("S flag value", "A rank flag value"),
+ * "#" between collectives.  Used to model-check the protocol for any world
+ * size on a CPU (tests/test_protocol_model.py).  *used = bytes needed. */
+int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int nops,
+                   const int* kinds, const size_t* counts, const int* dtypes, const int* roots,
+                   char* buf, size_t cap, size_t* used);
 
 /* ---- diagnostics ----------------------------------------------------------- */
 

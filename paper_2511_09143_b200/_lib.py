@@ -34,8 +34,9 @@ FMX_ERR_UNSUPPORTED = 10
 
 FLOAT32, BFLOAT16 = 0, 1
 OP_SUM, OP_SUM_POSTSCALE, OP_PREDIV_SUM = 0, 1, 2
-TRANSPORT_AUTO, TRANSPORT_ZC, TRANSPORT_CE = 0, 1, 2
-TRANSPORTS = {"auto": TRANSPORT_AUTO, "zc": TRANSPORT_ZC, "ce": TRANSPORT_CE}
+TRANSPORT_AUTO, TRANSPORT_ZC, TRANSPORT_CE, TRANSPORT_HOST = 0, 1, 2, 3
+TRANSPORTS = {"auto": TRANSPORT_AUTO, "zc": TRANSPORT_ZC, "ce": TRANSPORT_CE,
+              "host": TRANSPORT_HOST}
 
 BUS_ID_LEN = 16
 MIG_ID_LEN = 128
@@ -46,7 +47,8 @@ EXPORTS = (
     "fmx_check_peer", "fmx_validate_peers", "fmx_topology", "fmx_restore_bus_id",
     "fmx_comm_init", "fmx_allreduce", "fmx_broadcast", "fmx_barrier", "fmx_comm_destroy",
     "fmx_comm_abort", "fmx_comm_rank", "fmx_comm_count", "fmx_comm_peer", "fmx_comm_config",
-    "fmx_comm_kernel_launches", "fmx_last_error", "fmx_dup_ranks", "fmx_abi_version",
+    "fmx_comm_kernel_launches", "fmx_comm_flags", "fmx_trace_plan", "fmx_last_error", "fmx_dup_ranks",
+    "fmx_abi_version",
 )
 
 
@@ -107,6 +109,9 @@ def lib() -> ctypes.CDLL:
         "fmx_comm_peer": [c_void, c_int, P(PeerInfoC)],
         "fmx_comm_config": [c_void, P(c_size), P(c_int), P(c_size)],
         "fmx_comm_kernel_launches": [c_void, P(ctypes.c_uint64)],
+        "fmx_comm_flags": [c_void, P(ctypes.c_uint32), c_int],
+        "fmx_trace_plan": [c_int, c_int, c_int, c_size, c_int, P(c_int), P(c_size), P(c_int),
+                           P(c_int), ctypes.c_char_p, c_size, P(c_size)],
         "fmx_dup_ranks": [P(c_int), P(c_int)],
         "fmx_abi_version": [],
     }
@@ -120,6 +125,25 @@ def lib() -> ctypes.CDLL:
         raise ImportError("libflexshm ABI version mismatch")
     _lib = L
     return L
+
+
+def trace_plan(nranks: int, rank: int, ops: list[tuple], slice_bytes: int = 4096,
+               transport: str = "ce") -> str:
+    """Schedule text of `rank` for ops = [("allreduce", count, dtype) |
+    ("broadcast", count, dtype, root)] (see fmx_trace_plan)."""
+    n = len(ops)
+    kinds = (ctypes.c_int * max(1, n))(*[0 if o[0] == "allreduce" else 1 for o in ops])
+    counts = (ctypes.c_size_t * max(1, n))(*[o[1] for o in ops])
+    dtypes = (ctypes.c_int * max(1, n))(*[o[2] for o in ops])
+    roots = (ctypes.c_int * max(1, n))(*[o[3] if len(o) > 3 else 0 for o in ops])
+    used = ctypes.c_size_t()
+    L = lib()
+    L.fmx_trace_plan(nranks, rank, TRANSPORTS[transport], slice_bytes, n, kinds, counts, dtypes,
+                     roots, None, 0, ctypes.byref(used))
+    buf = ctypes.create_string_buffer(used.value)
+    check(L.fmx_trace_plan(nranks, rank, TRANSPORTS[transport], slice_bytes, n, kinds, counts,
+                           dtypes, roots, buf, used.value, ctypes.byref(used)), "fmx_trace_plan")
+    return buf.value.decode()
 
 
 def last_error() -> str:

@@ -122,6 +122,12 @@ class ShmCommunicator:
         _lib.check(_lib.lib().fmx_comm_kernel_launches(self._h, ctypes.byref(v)))
         return v.value
 
+    def flags(self) -> list[list[int]]:
+        """Every rank's [STAGED, REDUCED, BC_STAGED, BC_DONE] counters."""
+        buf = (ctypes.c_uint32 * (4 * self.size))()
+        _lib.check(_lib.lib().fmx_comm_flags(self._h, buf, 4 * self.size))
+        return [list(buf[4 * r:4 * r + 4]) for r in range(self.size)]
+
     def abort(self) -> None:
         if self._h is not None and self._h.value:
             _lib.lib().fmx_comm_abort(self._h)

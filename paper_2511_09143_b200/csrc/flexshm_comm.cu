@@ -37,6 +37,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -103,19 +104,18 @@ struct fmx_comm {
   std::vector<fmx_peer_info> peers;
   std::vector<CUstreamBatchMemOpParams> ops;
 
-  char* in_slot(bool dev, uint32_t R, int owner, int contrib) const {
-    size_t s = R % nslots;
-    return (dev ? dbase : base) + L.ar_in_off +
-           ((s * nranks + owner) * nranks + contrib) * slice_bytes;
+  // byte offsets of the pipeline slots inside the segment
+  size_t in_off(uint32_t R, int owner, int contrib) const {
+    return L.ar_in_off + (((size_t)(R % nslots) * nranks + owner) * nranks + contrib) * slice_bytes;
   }
-  char* out_slot(bool dev, uint32_t R, int owner) const {
-    size_t s = R % nslots;
-    return (dev ? dbase : base) + L.ar_out_off + (s * nranks + owner) * slice_bytes;
+  size_t out_off(uint32_t R, int owner) const {
+    return L.ar_out_off + ((size_t)(R % nslots) * nranks + owner) * slice_bytes;
   }
-  char* bc_slot(bool dev, uint32_t R) const {
-    size_t s = R % nslots;
-    return (dev ? dbase : base) + L.bc_off + s * nranks * slice_bytes;
+  size_t bc_slot_off(uint32_t R) const {
+    return L.bc_off + (size_t)(R % nslots) * nranks * slice_bytes;
   }
+  // host (dev=false) or device (dev=true) address of a segment offset
+  char* at(bool dev, size_t off) const { return (dev ? dbase : base) + off; }
   CUdeviceptr flag_dev(int r, int f) const {
     return (CUdeviceptr)(dbase + L.flags_off + ((size_t)r * kFlagsPerRank + f) * 64);
   }
@@ -132,123 +132,221 @@ void unmap(fmx_comm* c) {
   c->hdr = nullptr;
 }
 
-// ---- stream memory operations ------------------------------------------------
+// ---- the plan: what one rank enqueues for one collective -----------------------
+//
+// plan_allreduce / plan_broadcast describe the schedule once, against a Sink.
+// CudaSink turns it into stream operations; TraceSink records the SHM bytes
+// each step reads / writes and the flags it signals / waits on, so the
+// schedule of every rank of any world size can be model-checked on a CPU
+// (fmx_trace_plan, tests/test_protocol_model.py).
 
-int signal(fmx_comm* c, cudaStream_t s, int flag, uint32_t value) {
-  CUstreamBatchMemOpParams op;
-  memset(&op, 0, sizeof op);
-  op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
-  op.writeValue.address = c->flag_dev(c->rank, flag);
-  op.writeValue.value = value;
-  op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;  // fence before the write
-  CUresult r = g_batch((CUstream)s, 1, &op, 0);
-  if (r != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "stream write-value failed (%d)", (int)r);
-  return FMX_OK;
-}
+// SHM side of a data movement, for the trace: byte range relative to the
+// segment base, the rank that (should have) written it and in which round.
+struct Annot {
+  int64_t off = -1;
+  size_t bytes = 0;
+  int writer = -1;
+  uint32_t round = 0;
+};
 
-int signal2(fmx_comm* c, cudaStream_t s, int f0, uint32_t v0, int f1, uint32_t v1) {
-  CUstreamBatchMemOpParams op[2];
-  memset(op, 0, sizeof op);
-  op[0].writeValue.operation = op[1].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
-  op[0].writeValue.address = c->flag_dev(c->rank, f0);
-  op[0].writeValue.value = v0;
-  op[1].writeValue.address = c->flag_dev(c->rank, f1);
-  op[1].writeValue.value = v1;
-  CUresult r = g_batch((CUstream)s, 2, op, 0);
-  if (r != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "stream write-value failed (%d)", (int)r);
-  return FMX_OK;
-}
+struct PlanSeg {
+  const char* src;
+  char* dst;
+  size_t bytes;
+  Annot shm;          // the SHM end of this segment
+  bool shm_is_dst;    // true: this step writes SHM; false: reads it
+};
 
-// Wait until flag `flag` of every rank in [0, n) except `skip` is >= value (cyclic).
-int wait_peers(fmx_comm* c, cudaStream_t s, int flag, uint32_t value, int skip) {
-  c->ops.clear();
-  for (int q = 0; q < c->nranks; ++q) {
-    if (q == skip) continue;
-    CUstreamBatchMemOpParams op;
-    memset(&op, 0, sizeof op);
-    op.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
-    op.waitValue.address = c->flag_dev(q, flag);
-    op.waitValue.value = value;
-    op.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
-    c->ops.push_back(op);
-  }
-  for (size_t i = 0; i < c->ops.size(); i += kBatchMax) {
-    unsigned cnt = (unsigned)std::min<size_t>(kBatchMax, c->ops.size() - i);
-    CUresult r = g_batch((CUstream)s, cnt, c->ops.data() + i, 0);
-    if (r != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "stream wait-value failed (%d)", (int)r);
-  }
-  return FMX_OK;
-}
+struct PlanReduce {
+  ReduceArgs args;
+  std::vector<Annot> reads;  // SHM inputs (ZC transport)
+  Annot write;               // SHM result slot
+  int dtype;
+  bool aligned;
+};
 
-int wait_rank(fmx_comm* c, cudaStream_t s, int q, int flag, uint32_t value) {
-  CUstreamBatchMemOpParams op;
-  memset(&op, 0, sizeof op);
-  op.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
-  op.waitValue.address = c->flag_dev(q, flag);
-  op.waitValue.value = value;
-  op.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
-  CUresult r = g_batch((CUstream)s, 1, &op, 0);
-  if (r != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "stream wait-value failed (%d)", (int)r);
-  return FMX_OK;
-}
-
-// ---- data movement ------------------------------------------------------------
+struct Sink {
+  virtual ~Sink() {}
+  virtual int copy(const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel) = 0;
+  virtual int reduce(const PlanReduce& r) = 0;
+  virtual int signal(int flag, uint32_t v) = 0;
+  virtual int signal2(int f0, uint32_t v0, int f1, uint32_t v1) = 0;
+  virtual int wait_peers(int flag, uint32_t v, int skip) = 0;
+  virtual int wait_rank(int q, int flag, uint32_t v) = 0;
+  virtual int d2d(void* dst, const void* src, size_t bytes) = 0;
+};
 
 int grid_for(size_t work_items, int threads, int cap) {
   size_t g = (work_items + threads - 1) / threads;
   return (int)std::max<size_t>(1, std::min<size_t>(g, (size_t)cap));
 }
 
-// Batched copy: kernel (ZC) or copy engine (CE).
-int copy_segments(fmx_comm* c, cudaStream_t s, const std::vector<CopySeg>& segs, bool src_sys,
-                  bool use_kernel) {
-  if (segs.empty()) return FMX_OK;
-  if (!use_kernel) {
-    for (const CopySeg& g : segs)
-      FMX_CUDA(cudaMemcpyAsync(g.dst, g.src, g.bytes, cudaMemcpyDefault, s));
+class CudaSink final : public Sink {
+ public:
+  CudaSink(fmx_comm* c, cudaStream_t s) : c_(c), s_(s) {}
+
+  int copy(const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel) override {
+    if (segs.empty()) return FMX_OK;
+    if (!use_kernel) {
+      for (const PlanSeg& g : segs)
+        FMX_CUDA(cudaMemcpyAsync(g.dst, g.src, g.bytes, cudaMemcpyDefault, s_));
+      return FMX_OK;
+    }
+    for (size_t i0 = 0; i0 < segs.size(); i0 += kMaxSegs) {
+      CopyArgs a;
+      memset(&a, 0, sizeof a);
+      a.nseg = (int)std::min<size_t>(kMaxSegs, segs.size() - i0);
+      a.src_sys = src_sys ? 1 : 0;
+      size_t maxb = 0;
+      for (int k = 0; k < a.nseg; ++k) {
+        a.seg[k] = CopySeg{segs[i0 + k].src, segs[i0 + k].dst, segs[i0 + k].bytes};
+        maxb = std::max(maxb, a.seg[k].bytes);
+      }
+      constexpr int kThreads = 512, kU = 4;
+      int gx = grid_for((maxb / 16 + kU - 1) / kU, kThreads, std::max(1, 1184 / a.nseg));
+      dim3 grid(gx, a.nseg);
+      fmx_copy_kernel<kU><<<grid, kThreads, 0, s_>>>(a);
+      FMX_CUDA(cudaGetLastError());
+      c_->launches++;
+    }
     return FMX_OK;
   }
-  for (size_t i0 = 0; i0 < segs.size(); i0 += kMaxSegs) {
-    CopyArgs a;
-    memset(&a, 0, sizeof a);
-    a.nseg = (int)std::min<size_t>(kMaxSegs, segs.size() - i0);
-    a.src_sys = src_sys ? 1 : 0;
-    size_t maxb = 0;
-    for (int k = 0; k < a.nseg; ++k) {
-      a.seg[k] = segs[i0 + k];
-      maxb = std::max(maxb, a.seg[k].bytes);
-    }
-    constexpr int kThreads = 512, kU = 4;
-    int gx = grid_for((maxb / 16 + kU - 1) / kU, kThreads, std::max(1, 1184 / a.nseg));
-    dim3 grid(gx, a.nseg);
-    fmx_copy_kernel<kU><<<grid, kThreads, 0, s>>>(a);
-    FMX_CUDA(cudaGetLastError());
-    c->launches++;
-  }
-  return FMX_OK;
-}
 
-int launch_reduce(fmx_comm* c, cudaStream_t s, const ReduceArgs& a, int dtype, bool aligned) {
-  if (a.len == 0) return FMX_OK;
-  constexpr int kThreads = 256, kU = 2;
-  const int V = dtype == FMX_FLOAT32 ? 4 : 8;
-  if (aligned) {
-    int g = grid_for((a.len / V + kU - 1) / kU + 1, kThreads, 1184);
-    if (dtype == FMX_FLOAT32)
-      fmx_reduce_kernel<float, kU><<<g, kThreads, 0, s>>>(a);
-    else
-      fmx_reduce_kernel<__nv_bfloat16, kU><<<g, kThreads, 0, s>>>(a);
-  } else {
-    int g = grid_for(a.len, kThreads, 1184);
-    if (dtype == FMX_FLOAT32)
-      fmx_reduce_scalar_kernel<float><<<g, kThreads, 0, s>>>(a);
-    else
-      fmx_reduce_scalar_kernel<__nv_bfloat16><<<g, kThreads, 0, s>>>(a);
+  int reduce(const PlanReduce& r) override {
+    const ReduceArgs& a = r.args;
+    if (a.len == 0) return FMX_OK;
+    constexpr int kThreads = 256, kU = 2;
+    const int V = r.dtype == FMX_FLOAT32 ? 4 : 8;
+    if (r.aligned) {
+      int g = grid_for((a.len / V + kU - 1) / kU + 1, kThreads, 1184);
+      if (r.dtype == FMX_FLOAT32)
+        fmx_reduce_kernel<float, kU><<<g, kThreads, 0, s_>>>(a);
+      else
+        fmx_reduce_kernel<__nv_bfloat16, kU><<<g, kThreads, 0, s_>>>(a);
+    } else {
+      int g = grid_for(a.len, kThreads, 1184);
+      if (r.dtype == FMX_FLOAT32)
+        fmx_reduce_scalar_kernel<float><<<g, kThreads, 0, s_>>>(a);
+      else
+        fmx_reduce_scalar_kernel<__nv_bfloat16><<<g, kThreads, 0, s_>>>(a);
+    }
+    FMX_CUDA(cudaGetLastError());
+    c_->launches++;
+    return FMX_OK;
   }
-  FMX_CUDA(cudaGetLastError());
-  c->launches++;
-  return FMX_OK;
-}
+
+  int signal(int flag, uint32_t v) override {
+    CUstreamBatchMemOpParams op;
+    memset(&op, 0, sizeof op);
+    op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+    op.writeValue.address = c_->flag_dev(c_->rank, flag);
+    op.writeValue.value = v;
+    op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;  // fence before the write
+    return batch(&op, 1);
+  }
+
+  int signal2(int f0, uint32_t v0, int f1, uint32_t v1) override {
+    CUstreamBatchMemOpParams op[2];
+    memset(op, 0, sizeof op);
+    op[0].writeValue.operation = op[1].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+    op[0].writeValue.address = c_->flag_dev(c_->rank, f0);
+    op[0].writeValue.value = v0;
+    op[1].writeValue.address = c_->flag_dev(c_->rank, f1);
+    op[1].writeValue.value = v1;
+    return batch(op, 2);
+  }
+
+  int wait_peers(int flag, uint32_t v, int skip) override {
+    ops_.clear();
+    for (int q = 0; q < c_->nranks; ++q)
+      if (q != skip) ops_.push_back(wait_op(q, flag, v));
+    for (size_t i = 0; i < ops_.size(); i += kBatchMax) {
+      int rc = batch(ops_.data() + i, (unsigned)std::min<size_t>(kBatchMax, ops_.size() - i));
+      if (rc) return rc;
+    }
+    return FMX_OK;
+  }
+
+  int wait_rank(int q, int flag, uint32_t v) override {
+    CUstreamBatchMemOpParams op = wait_op(q, flag, v);
+    return batch(&op, 1);
+  }
+
+  int d2d(void* dst, const void* src, size_t bytes) override {
+    FMX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s_));
+    return FMX_OK;
+  }
+
+ private:
+  CUstreamBatchMemOpParams wait_op(int q, int flag, uint32_t v) {
+    CUstreamBatchMemOpParams op;
+    memset(&op, 0, sizeof op);
+    op.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+    op.waitValue.address = c_->flag_dev(q, flag);
+    op.waitValue.value = v;
+    op.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;  // cyclic >=
+    return op;
+  }
+  int batch(CUstreamBatchMemOpParams* ops, unsigned n) {
+    CUresult r = g_batch((CUstream)s_, n, ops, 0);
+    if (r != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "cuStreamBatchMemOp failed (%d)", (int)r);
+    return FMX_OK;
+  }
+  fmx_comm* c_;
+  cudaStream_t s_;
+  std::vector<CUstreamBatchMemOpParams> ops_;
+};
+
+// Text trace, one line per SHM access / flag operation:
+//   W <off> <bytes> <round>            this rank writes SHM bytes of `round`
+//   R <off> <bytes> <writer> <round>   reads bytes `writer` wrote in `round`
+//   S <flag> <value>                   signal own flag
+//   A <rank> <flag> <value>            wait until rank's flag >= value
+class TraceSink final : public Sink {
+ public:
+  explicit TraceSink(std::string* out) : out_(out) {}
+  int copy(const std::vector<PlanSeg>& segs, bool, bool) override {
+    for (const PlanSeg& g : segs) access(g.shm, g.shm_is_dst);
+    return FMX_OK;
+  }
+  int reduce(const PlanReduce& r) override {
+    for (const Annot& a : r.reads) access(a, false);
+    access(r.write, true);
+    return FMX_OK;
+  }
+  int signal(int flag, uint32_t v) override { return line("S %d %u\n", flag, v); }
+  int signal2(int f0, uint32_t v0, int f1, uint32_t v1) override {
+    line("S %d %u\n", f0, v0);
+    return line("S %d %u\n", f1, v1);
+  }
+  int wait_peers(int flag, uint32_t v, int skip) override {
+    for (int q = 0; q < nranks; ++q)
+      if (q != skip) line("A %d %d %u\n", q, flag, v);
+    return FMX_OK;
+  }
+  int wait_rank(int q, int flag, uint32_t v) override { return line("A %d %d %u\n", q, flag, v); }
+  int d2d(void*, const void*, size_t) override { return FMX_OK; }
+  int nranks = 0;
+
+ private:
+  void access(const Annot& a, bool write) {
+    if (a.off < 0 || a.bytes == 0) return;
+    if (write)
+      line("W %lld %zu %u\n", (long long)a.off, a.bytes, a.round);
+    else
+      line("R %lld %zu %d %u\n", (long long)a.off, a.bytes, a.writer, a.round);
+  }
+  int line(const char* fmt, ...) __attribute__((format(printf, 2, 3))) {
+    char buf[128];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    out_->append(buf);
+    return FMX_OK;
+  }
+  std::string* out_;
+};
 
 struct Geometry {
   size_t count, esz, chunk, slice;
@@ -262,10 +360,145 @@ struct Geometry {
   }
 };
 
-int check_comm(fmx_comm* c) {
+Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype) {
+  Geometry g;
+  const int n = c->nranks;
+  g.count = count;
+  g.esz = dtype == FMX_FLOAT32 ? 4 : 2;
+  const size_t vec = 16 / g.esz;
+  g.chunk = ((count + n - 1) / n + vec - 1) / vec * vec;  // 16-byte aligned chunk starts
+  g.slice = c->slice_bytes / g.esz;
+  g.rounds = (uint32_t)((g.chunk + g.slice - 1) / g.slice);
+  return g;
+}
+
+// Reduce-scatter + all-gather through the segment, pipelined in rounds
+// (schedule and its hazard argument: DESIGN.md §3.3).
+int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
+                   int op, float factor, bool aligned) {
+  const int n = c->nranks, me = c->rank;
+  const bool zc = c->transport == FMX_TRANSPORT_ZC;
+  const Geometry g = allreduce_geometry(c, count, dtype);
+  std::vector<PlanSeg> segs;
+  int rc;
+
+  auto stage = [&](uint32_t j) -> int {
+    const uint32_t R = c->ar_round + j;
+    segs.clear();
+    for (int o = 0; o < n; ++o) {
+      const size_t len = o == me ? 0 : g.len(o, j);
+      if (!len) continue;
+      const size_t off = c->in_off(R, o, me);
+      segs.push_back({src + g.lo(o, j) * g.esz, c->at(zc, off), len * g.esz,
+                      Annot{(int64_t)off, len * g.esz, me, R}, true});
+    }
+    int r = k.copy(segs, false, zc);
+    return r ? r : k.signal(kStaged, R + 1);
+  };
+
+  if ((rc = stage(0))) return rc;
+  for (uint32_t j = 0; j < g.rounds; ++j) {
+    const uint32_t R = c->ar_round + j;
+    if (j + 1 < g.rounds && (rc = stage(j + 1))) return rc;  // prefetch next round
+    // reduce-scatter of my chunk, ascending rank order
+    if ((rc = k.wait_peers(kStaged, R + 1, me))) return rc;
+    const size_t mylen = g.len(me, j);
+    if (mylen) {
+      PlanReduce pr;
+      memset(&pr.args, 0, sizeof pr.args);
+      pr.dtype = dtype;
+      pr.aligned = aligned;
+      ReduceArgs& a = pr.args;
+      a.nsrc = n;
+      a.len = mylen;
+      a.op = op;
+      a.factor = factor;
+      a.out_dev = dst + g.lo(me, j) * g.esz;
+      const size_t out_off = c->out_off(R, me);
+      a.out_sys = c->at(true, out_off);
+      pr.write = Annot{(int64_t)out_off, mylen * g.esz, me, R};
+      if (!zc) {  // copy engine pulls the n-1 contributions into HBM scratch first
+        segs.clear();
+        for (int q = 0; q < n; ++q) {
+          if (q == me) continue;
+          const size_t off = c->in_off(R, me, q);
+          segs.push_back({c->at(false, off), c->scratch + (size_t)q * c->slice_bytes,
+                          mylen * g.esz, Annot{(int64_t)off, mylen * g.esz, q, R}, false});
+        }
+        if ((rc = k.copy(segs, true, false))) return rc;
+      }
+      for (int q = 0; q < n; ++q) {
+        if (q == me) {
+          a.src[q] = src + g.lo(me, j) * g.esz;
+        } else if (zc) {
+          const size_t off = c->in_off(R, me, q);
+          a.src[q] = c->at(true, off);
+          a.sys_mask |= 1ull << q;
+          pr.reads.push_back(Annot{(int64_t)off, mylen * g.esz, q, R});
+        } else {
+          a.src[q] = c->scratch + (size_t)q * c->slice_bytes;
+        }
+      }
+      if ((rc = k.reduce(pr))) return rc;
+    }
+    if ((rc = k.signal(kReduced, R + 1))) return rc;
+    // all-gather of the other owners' results
+    if ((rc = k.wait_peers(kReduced, R + 1, me))) return rc;
+    segs.clear();
+    for (int q = 0; q < n; ++q) {
+      const size_t len = q == me ? 0 : g.len(q, j);
+      if (!len) continue;
+      const size_t off = c->out_off(R, q);
+      segs.push_back({c->at(zc, off), dst + g.lo(q, j) * g.esz, len * g.esz,
+                      Annot{(int64_t)off, len * g.esz, q, R}, false});
+    }
+    if ((rc = k.copy(segs, true, zc))) return rc;
+  }
+  c->ar_round += g.rounds;
+  return FMX_OK;
+}
+
+// Root stages rounds of n*slice bytes into the broadcast slot; every other
+// rank copies them out and signals BC_DONE, which the root waits on before
+// reusing a slot (two rounds later).
+int plan_broadcast(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
+                   int root) {
+  const int me = c->rank;
+  const bool zc = c->transport == FMX_TRANSPORT_ZC;
+  const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;
+  const size_t bslice = (size_t)c->nranks * c->slice_bytes / esz;
+  const uint32_t rounds = (uint32_t)((count + bslice - 1) / bslice);
+  std::vector<PlanSeg> segs(1);
+  int rc;
+  for (uint32_t j = 0; j < rounds; ++j) {
+    const uint32_t R = c->bc_round + j;
+    const size_t lo = (size_t)j * bslice, len = std::min(bslice, count - lo);
+    const size_t off = c->bc_slot_off(R);
+    const Annot an{(int64_t)off, len * esz, root, R};
+    if (me == root) {
+      if (R + 1 > (uint32_t)c->nslots && (rc = k.wait_peers(kBcDone, R + 1 - c->nslots, me)))
+        return rc;
+      segs[0] = {src + lo * esz, c->at(zc, off), len * esz, an, true};
+      if ((rc = k.copy(segs, false, zc))) return rc;
+      if ((rc = k.signal2(kBcStaged, R + 1, kBcDone, R + 1))) return rc;
+      if (src != dst && (rc = k.d2d(dst + lo * esz, src + lo * esz, len * esz))) return rc;
+    } else {
+      if ((rc = k.wait_rank(root, kBcStaged, R + 1))) return rc;
+      segs[0] = {c->at(zc, off), dst + lo * esz, len * esz, an, false};
+      if ((rc = k.copy(segs, true, zc))) return rc;
+      if ((rc = k.signal(kBcDone, R + 1))) return rc;
+    }
+  }
+  c->bc_round += rounds;
+  return FMX_OK;
+}
+
+int check_comm(fmx_comm* c, bool needs_device = true) {
   if (!c || !c->hdr) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
   if (c->hdr->aborted.load(std::memory_order_acquire))
     return fail(FMX_ERR_ABORTED, "communicator was aborted");
+  if (needs_device && c->transport == FMX_TRANSPORT_HOST)
+    return fail(FMX_ERR_UNSUPPORTED, "host-only communicator has no device path");
   return FMX_OK;
 }
 
@@ -292,13 +525,14 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (klen == 0 || klen > 100 || strchr(job_key, '/'))
     return fail(FMX_ERR_INVALID_ARG, "job_key must be 1..100 chars without '/'");
   if (nslots != 0 && nslots != 2) return fail(FMX_ERR_INVALID_ARG, "nslots must be 2");
-  if (transport < FMX_TRANSPORT_AUTO || transport > FMX_TRANSPORT_CE)
+  if (transport < FMX_TRANSPORT_AUTO || transport > FMX_TRANSPORT_HOST)
     return fail(FMX_ERR_INVALID_ARG, "bad transport %d", transport);
   if (timeout_s <= 0) timeout_s = 120.0;
   fmx_peer_info me = *self;
   int rc = fmx_check_peer(&me);
   if (rc) return rc;
-  if ((rc = load_driver())) return rc;
+  const bool host_only = transport == FMX_TRANSPORT_HOST;
+  if (!host_only && (rc = load_driver())) return rc;
 
   auto* c = new fmx_comm();
   c->rank = rank;
@@ -435,6 +669,11 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
     return rc;  // message / dup pair already set
   }
 
+  c->transport = transport == FMX_TRANSPORT_AUTO ? FMX_TRANSPORT_CE : transport;
+  if (host_only) {
+    *out = c;
+    return FMX_OK;
+  }
   // device mapping
   cudaError_t e = cudaHostRegister(c->base, c->total_bytes,
                                    cudaHostRegisterMapped | cudaHostRegisterPortable);
@@ -442,7 +681,6 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
     c->registered = true;
     e = cudaHostGetDevicePointer((void**)&c->dbase, c->base, 0);
   }
-  c->transport = transport == FMX_TRANSPORT_AUTO ? FMX_TRANSPORT_CE : transport;
   if (e == cudaSuccess && c->transport == FMX_TRANSPORT_CE)
     e = cudaMalloc((void**)&c->scratch, (size_t)nranks * c->slice_bytes);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming);
@@ -481,97 +719,30 @@ int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int 
   if (count == 0) return FMX_OK;
   if (!send || !recv) return fail(FMX_ERR_INVALID_ARG, "null buffer");
   cudaStream_t s = (cudaStream_t)stream;
-  const int n = c->nranks, me = c->rank;
-  const bool zc = c->transport == FMX_TRANSPORT_ZC;
-  Geometry g;
-  g.count = count;
-  g.esz = dtype == FMX_FLOAT32 ? 4 : 2;
-  const size_t vec = 16 / g.esz;
-  g.chunk = ((count + n - 1) / n + vec - 1) / vec * vec;
-  g.slice = c->slice_bytes / g.esz;
-  g.rounds = (uint32_t)((g.chunk + g.slice - 1) / g.slice);
+  const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;
   const bool aligned = (((uintptr_t)send | (uintptr_t)recv) & 15) == 0;
-  const char* src = (const char*)send;
-  char* dst = (char*)recv;
-
-  if (n == 1) {  // nothing to exchange: apply the scale convention locally
-    ReduceArgs a;
-    memset(&a, 0, sizeof a);
-    a.src[0] = src;
-    a.nsrc = 1;
-    a.out_dev = dst;
-    a.len = count;
-    a.op = op;
-    a.factor = factor;
+  CudaSink sink(c, s);
+  if (c->nranks == 1) {  // nothing to exchange: apply the scale convention locally
     if (op == FMX_OP_SUM) {
-      if (send != recv) FMX_CUDA(cudaMemcpyAsync(recv, send, count * g.esz, cudaMemcpyDeviceToDevice, s));
-    } else if ((rc = launch_reduce(c, s, a, dtype, aligned))) {
-      return rc;
+      if (send != recv) FMX_CUDA(cudaMemcpyAsync(recv, send, count * esz, cudaMemcpyDeviceToDevice, s));
+    } else {
+      PlanReduce pr;
+      memset(&pr.args, 0, sizeof pr.args);
+      pr.args.src[0] = (const char*)send;
+      pr.args.nsrc = 1;
+      pr.args.out_dev = (char*)recv;
+      pr.args.len = count;
+      pr.args.op = op;
+      pr.args.factor = factor;
+      pr.dtype = dtype;
+      pr.aligned = aligned;
+      if ((rc = sink.reduce(pr))) return rc;
     }
     return record_done(c, s);
   }
-
-  std::vector<CopySeg> segs;
-  auto stage = [&](uint32_t j) -> int {
-    const uint32_t R = c->ar_round + j;
-    segs.clear();
-    for (int o = 0; o < n; ++o) {
-      if (o == me) continue;
-      size_t len = g.len(o, j);
-      if (len) segs.push_back({src + g.lo(o, j) * g.esz, c->in_slot(zc, R, o, me), len * g.esz});
-    }
-    int r = copy_segments(c, s, segs, false, zc);
-    return r ? r : signal(c, s, kStaged, R + 1);
-  };
-
-  if ((rc = stage(0))) return rc;
-  for (uint32_t j = 0; j < g.rounds; ++j) {
-    const uint32_t R = c->ar_round + j;
-    if (j + 1 < g.rounds && (rc = stage(j + 1))) return rc;
-    // reduce-scatter: my chunk, rank order
-    if ((rc = wait_peers(c, s, kStaged, R + 1, me))) return rc;
-    const size_t mylen = g.len(me, j);
-    if (mylen) {
-      ReduceArgs a;
-      memset(&a, 0, sizeof a);
-      a.nsrc = n;
-      a.len = mylen;
-      a.op = op;
-      a.factor = factor;
-      a.out_dev = dst + g.lo(me, j) * g.esz;
-      a.out_sys = c->out_slot(true, R, me);
-      if (!zc) {  // copy engine pulls the n-1 contributions into HBM scratch
-        segs.clear();
-        for (int q = 0; q < n; ++q)
-          if (q != me)
-            segs.push_back({c->in_slot(false, R, me, q), c->scratch + (size_t)q * c->slice_bytes,
-                            mylen * g.esz});
-        if ((rc = copy_segments(c, s, segs, true, false))) return rc;
-      }
-      for (int q = 0; q < n; ++q) {
-        if (q == me) {
-          a.src[q] = src + g.lo(me, j) * g.esz;
-        } else if (zc) {
-          a.src[q] = c->in_slot(true, R, me, q);
-          a.sys_mask |= 1ull << q;
-        } else {
-          a.src[q] = c->scratch + (size_t)q * c->slice_bytes;
-        }
-      }
-      if ((rc = launch_reduce(c, s, a, dtype, aligned))) return rc;
-    }
-    if ((rc = signal(c, s, kReduced, R + 1))) return rc;
-    // all-gather: the other owners' results
-    if ((rc = wait_peers(c, s, kReduced, R + 1, me))) return rc;
-    segs.clear();
-    for (int q = 0; q < n; ++q) {
-      if (q == me) continue;
-      size_t len = g.len(q, j);
-      if (len) segs.push_back({c->out_slot(zc, R, q), dst + g.lo(q, j) * g.esz, len * g.esz});
-    }
-    if ((rc = copy_segments(c, s, segs, true, zc))) return rc;
-  }
-  c->ar_round += g.rounds;
+  if ((rc = plan_allreduce(c, sink, (const char*)send, (char*)recv, count, dtype, op, factor,
+                           aligned)))
+    return rc;
   return record_done(c, s);
 }
 
@@ -583,43 +754,56 @@ int fmx_broadcast(fmx_comm_t c, const void* send, void* recv, size_t count, int 
     return fail(FMX_ERR_INVALID_ARG, "bad dtype %d", dtype);
   if (root < 0 || root >= c->nranks) return fail(FMX_ERR_INVALID_ARG, "bad root %d", root);
   if (count == 0) return FMX_OK;
-  const int n = c->nranks, me = c->rank;
   const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;
-  if (!recv || (me == root && !send)) return fail(FMX_ERR_INVALID_ARG, "null buffer");
+  if (!recv || (c->rank == root && !send)) return fail(FMX_ERR_INVALID_ARG, "null buffer");
   cudaStream_t s = (cudaStream_t)stream;
-  const bool zc = c->transport == FMX_TRANSPORT_ZC;
-  if (n == 1) {
+  if (c->nranks == 1) {
     if (send != recv) FMX_CUDA(cudaMemcpyAsync(recv, send, count * esz, cudaMemcpyDeviceToDevice, s));
     return record_done(c, s);
   }
-  const size_t bslice = (size_t)n * c->slice_bytes / esz;
-  const uint32_t rounds = (uint32_t)((count + bslice - 1) / bslice);
-  std::vector<CopySeg> segs(1);
-  for (uint32_t j = 0; j < rounds; ++j) {
-    const uint32_t R = c->bc_round + j;
-    const size_t lo = (size_t)j * bslice, len = std::min(bslice, count - lo);
-    if (me == root) {
-      if (R + 1 > (uint32_t)c->nslots && (rc = wait_peers(c, s, kBcDone, R + 1 - c->nslots, me)))
-        return rc;
-      segs[0] = {(const char*)send + lo * esz, c->bc_slot(zc, R), len * esz};
-      if ((rc = copy_segments(c, s, segs, false, zc))) return rc;
-      if ((rc = signal2(c, s, kBcStaged, R + 1, kBcDone, R + 1))) return rc;
-      if (send != recv)
-        FMX_CUDA(cudaMemcpyAsync((char*)recv + lo * esz, (const char*)send + lo * esz, len * esz,
-                                 cudaMemcpyDeviceToDevice, s));
-    } else {
-      if ((rc = wait_rank(c, s, root, kBcStaged, R + 1))) return rc;
-      segs[0] = {c->bc_slot(zc, R), (char*)recv + lo * esz, len * esz};
-      if ((rc = copy_segments(c, s, segs, true, zc))) return rc;
-      if ((rc = signal(c, s, kBcDone, R + 1))) return rc;
-    }
-  }
-  c->bc_round += rounds;
+  CudaSink sink(c, s);
+  if ((rc = plan_broadcast(c, sink, (const char*)send, (char*)recv, count, dtype, root))) return rc;
   return record_done(c, s);
 }
 
+int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int nops,
+                   const int* kinds, const size_t* counts, const int* dtypes, const int* roots,
+                   char* buf, size_t cap, size_t* used) {
+  if (nranks < 2 || nranks > FMX_MAX_RANKS || rank < 0 || rank >= nranks || nops < 0 ||
+      slice_bytes < 4096 || slice_bytes % 4096 || !kinds || !counts || !dtypes)
+    return fail(FMX_ERR_INVALID_ARG, "bad trace arguments");
+  fmx_comm c;  // geometry only: no segment, no CUDA
+  c.rank = rank;
+  c.nranks = nranks;
+  c.nslots = 2;
+  c.transport = transport == FMX_TRANSPORT_ZC ? FMX_TRANSPORT_ZC : FMX_TRANSPORT_CE;
+  c.slice_bytes = slice_bytes;
+  c.L = compute_layout(nranks, 2, slice_bytes);
+  c.total_bytes = c.L.total;
+  std::string out;
+  TraceSink sink(&out);
+  sink.nranks = nranks;
+  // fake user buffers: only their offsets matter and they never reach SHM
+  static char dummy[16] __attribute__((aligned(16)));
+  for (int i = 0; i < nops; ++i) {
+    int rc;
+    out.append("#\n");
+    if (kinds[i] != 0 && (!roots || roots[i] < 0 || roots[i] >= nranks))
+      return fail(FMX_ERR_INVALID_ARG, "bad broadcast root");
+    if (kinds[i] == 0)
+      rc = plan_allreduce(&c, sink, dummy, dummy, counts[i], dtypes[i], FMX_OP_SUM, 1.0f, true);
+    else
+      rc = plan_broadcast(&c, sink, dummy, dummy, counts[i], dtypes[i], roots ? roots[i] : 0);
+    if (rc) return rc;
+  }
+  if (used) *used = out.size() + 1;
+  if (!buf || cap < out.size() + 1) return fail(FMX_ERR_INVALID_ARG, "trace buffer too small");
+  memcpy(buf, out.c_str(), out.size() + 1);
+  return FMX_OK;
+}
+
 int fmx_barrier(fmx_comm_t c, double timeout_s) {
-  int rc = check_comm(c);
+  int rc = check_comm(c, false);
   if (rc) return rc;
   if (timeout_s <= 0) timeout_s = 120.0;
   const double t_end = now_s() + timeout_s;
@@ -685,6 +869,14 @@ int fmx_comm_config(fmx_comm_t c, size_t* slice_bytes, int* transport, size_t* s
   if (slice_bytes) *slice_bytes = c->slice_bytes;
   if (transport) *transport = c->transport;
   if (shm_bytes) *shm_bytes = c->total_bytes;
+  return FMX_OK;
+}
+
+int fmx_comm_flags(fmx_comm_t c, uint32_t* out, int cap) {
+  if (!c || !c->base || !out || cap < c->nranks * kFlagsPerRank)
+    return fail(FMX_ERR_INVALID_ARG, "bad arguments");
+  for (int r = 0; r < c->nranks; ++r)
+    for (int f = 0; f < kFlagsPerRank; ++f) out[r * kFlagsPerRank + f] = *c->flag_host(r, f);
   return FMX_OK;
 }
 

@@ -105,10 +105,12 @@ class MpsDaemon:
 
 def launch(fn, decision: AllocationDecision, args: tuple = (), *, job_key: str | None = None,
            mode: str = "green", timeout_s: float = 900.0, gpu_map=None, mig_uuids=None,
-           env_extra: dict | None = None) -> list:
+           env_extra: dict | None = None, inline_rank0: bool = False) -> list:
     """Run fn(rank, *args) in one spawned process per rank; return the
     results in rank order.  Raises RuntimeError with the first failing
-    rank's traceback."""
+    rank's traceback.  inline_rank0 runs rank 0 in the calling process (its
+    GPU must then be the caller's current device; CUDA_VISIBLE_DEVICES of
+    the caller is left alone)."""
     job_key = job_key or new_job_key()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -122,15 +124,25 @@ def launch(fn, decision: AllocationDecision, args: tuple = (), *, job_key: str |
         extra["CUDA_MPS_ACTIVE_THREAD_PERCENTAGE"] = str(MPS_PERCENT)
     procs = []
     try:
-        for r in range(len(decision.instances)):
+        first = 1 if inline_rank0 else 0
+        for r in range(first, len(decision.instances)):
             env = rank_env(decision, r, job_key, mode, gpu_map, mig_uuids)
             env.update(extra)
             p = ctx.Process(target=_child, args=(fn, r, env, args, q), daemon=False)
             p.start()
             procs.append(p)
         results, errors = {}, []
+        if inline_rank0:
+            env = rank_env(decision, 0, job_key, mode, gpu_map, mig_uuids)
+            env.pop("CUDA_VISIBLE_DEVICES", None)
+            env.update({k: v for k, v in extra.items() if k != "CUDA_VISIBLE_DEVICES"})
+            os.environ.update(env)
+            try:
+                results[0] = fn(0, *args)
+            except BaseException:  # noqa: BLE001
+                errors.append((0, traceback.format_exc()))
         deadline = time.time() + timeout_s
-        while len(results) + len(errors) < len(procs):
+        while not errors and len(results) < len(decision.instances):
             left = deadline - time.time()
             if left <= 0:
                 raise RuntimeError(f"launch timed out after {timeout_s}s "
@@ -154,7 +166,7 @@ def launch(fn, decision: AllocationDecision, args: tuple = (), *, job_key: str |
             raise RuntimeError(f"rank {rank} failed:\n{tb}")
         for p in procs:
             p.join(timeout=60)
-        return [results[r] for r in range(len(procs))]
+        return [results[r] for r in range(len(decision.instances))]
     finally:
         for p in procs:
             if p.is_alive():

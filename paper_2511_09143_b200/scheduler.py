@@ -15,9 +15,11 @@ Semantics follow the reference `pkg/src/migsim/scheduler.py`:
 * `schedule_step` FIFO / bounded backfill (scheduler.py:409-446).
 
 The returned `AllocationDecision.instances` list is the communicator's rank
-order: rank r is bound to `instances[r]` (see `launcher.py`).  DM/SM policies
-(scheduler.py:180-366) are outside the one-to-many path; the names exist for
-import compatibility and raise NotImplementedError.
+order: rank r is bound to `instances[r]` (see `launcher.py`).  The Dynamic-MIG
+policy (scheduler.py:180-330) is outside the one-to-many path: `dm_select`
+exists for import compatibility and raises NotImplementedError.  The small
+Static-MIG `sm_select` (scheduler.py:336-366) is kept so the shared queue
+discipline can be tested on SM clusters too.
 """
 
 from __future__ import annotations
@@ -25,7 +27,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import Mapping, Union
 
-from .errors import WrongModeError
+from .errors import OversizedJobError, WrongModeError
 from .mig import (
     DOUBLE_LEAF,
     LEAF,
@@ -36,6 +38,7 @@ from .mig import (
     ReconfigCosts,
     ReconfigPlan,
     flexmig_layout,
+    profile_by_name,
     static_layout,
 )
 from .workload import Job
@@ -175,7 +178,36 @@ def _out_of_scope(name: str):
 
 
 dm_select = _out_of_scope("dm_select")
-sm_select = _out_of_scope("sm_select")
+
+# Static MIG (one-to-one baseline, scheduler.py:336-366): small enough to keep,
+# so queue-discipline tests that run on SM clusters stay runnable.
+_SM_LADDER = ("1g.10gb", "2g.10gb", "4g.20gb")
+
+
+def sm_rounded_profile(size: int) -> MigProfile:
+    for name in _SM_LADDER:
+        p = profile_by_name(name)
+        if p.compute_slices >= size:
+            return p
+    raise OversizedJobError(f"size {size} exceeds the static partitioning")
+
+
+def sm_select(job: Job, cluster: ClusterState) -> AllocationDecision | None:
+    if cluster.mode != "SM":
+        raise WrongModeError(f"sm_select on a {cluster.mode} cluster")
+    if job.size > 4:
+        raise OversizedJobError(f"job {job.job_id} has size {job.size} > 4")
+    need = sm_rounded_profile(job.size)
+    for name in _SM_LADDER:
+        p = profile_by_name(name)
+        if (p.compute_slices, p.memory_gb) < (need.compute_slices, need.memory_gb):
+            continue
+        for g in cluster.schedulable_gpus():
+            for inst in g.idle_instances():
+                if inst.profile.name == name:
+                    return AllocationDecision(job.job_id, [(g.gpu_id, inst.instance_id)],
+                                              "LOCAL", [name])
+    return None
 
 
 def select_for(job: Job, cluster: ClusterState, cost_params: ReconfigCosts,
@@ -203,7 +235,7 @@ class StepResult:
 
 def _apply(outcome, cluster: ClusterState):
     if not isinstance(outcome, AllocationDecision):
-        raise NotImplementedError("only FM allocation decisions are applied here")
+        raise NotImplementedError("reconfiguration plans (DM) are out of scope")
     for gpu_id, inst_id in outcome.instances:
         cluster.layout(gpu_id).assign(inst_id, outcome.job_id)
     return outcome

@@ -65,3 +65,22 @@ def estimate_jct(job: Job, decision: AllocationDecision, model: PerfModel,
     return job.base_duration_s * (model.multi_overhead
                                   * model.placement_penalty(imbalance)
                                   * model.net_transport_factor)
+
+
+# --------------------------------------------------------------------------
+# The discrete-event engine (simcore.py:103-419) is a simulator, not part of
+# the data path; the names exist so reference imports resolve.
+
+def _out_of_scope(name: str):
+    def fn(*args, **kwargs):
+        raise NotImplementedError(
+            f"{name} belongs to the trace-driven cluster simulator, outside the "
+            "one-to-many SHM data path this package implements (DESIGN.md §6)")
+    fn.__name__ = name
+    return fn
+
+
+MetricsReport = _out_of_scope("MetricsReport")
+Simulation = _out_of_scope("Simulation")
+compute_metrics = _out_of_scope("compute_metrics")
+run_simulation = _out_of_scope("run_simulation")

@@ -18,3 +18,17 @@ class Job:
     base_duration_s: float
     arrival_s: float
     model_tag: str = ""
+
+
+def _out_of_scope(name: str):
+    def fn(*args, **kwargs):
+        raise NotImplementedError(
+            f"{name} belongs to trace synthesis, outside the one-to-many SHM data "
+            "path this package implements (DESIGN.md §6)")
+    fn.__name__ = name
+    return fn
+
+
+Trace = _out_of_scope("Trace")
+TraceConfig = _out_of_scope("TraceConfig")
+generate_trace = _out_of_scope("generate_trace")

@@ -6,6 +6,7 @@ from __future__ import annotations
 
 import hashlib
 import os
+import time
 
 import numpy as np
 
@@ -61,7 +62,13 @@ def suite_worker(rank: int, job_key: str, n: int, transport: str, mode: str, sce
         else:
             comm.broadcast(t, root=sc["root"], stream=stream)
             res = t
-        torch.cuda.synchronize()
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        t0 = time.time()
+        while not ev.query():
+            if time.time() - t0 > 60:
+                return {"stuck": sc, "index": len(out), "flags": comm.flags(), "rank": rank}
+            time.sleep(0.002)
         r = res.cpu()
         arr = r.numpy() if sc["dtype"] == "f32" else r.view(torch.int16).numpy().view(np.uint16)
         out.append(digest(arr) if sc.get("ret") == "sha" else arr.copy())

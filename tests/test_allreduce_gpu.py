@@ -59,11 +59,12 @@ def run(n: int, scenarios: list, transport: str = "auto", mode: str = "green",
     key = new_job_key("t")
     return launch(_workers.suite_worker, decision,
                   args=(key, n, transport, mode, scenarios, slice_bytes, peer_override),
-                  job_key=key, mode=mode, timeout_s=600, gpu_map={0: "0", 1: "0"})
+                  job_key=key, mode=mode, timeout_s=300, gpu_map={0: "0", 1: "0"})
 
 
 def check_all(n, scenarios, results):
     for r, res in enumerate(results):
+        assert "stuck" not in res, f"rank {r} hung: {res}"
         assert "results" in res, f"rank {r}: {res}"
         assert res["launches"] > 0, "no CUDA kernel launched"
     for i, sc in enumerate(scenarios):

@@ -1,0 +1,151 @@
+"""The native bootstrap rules of libflexshm (fmx_check_peer,
+fmx_validate_peers, fmx_topology, fmx_restore_bus_id) against the golden
+vectors produced by the REFERENCE (tests/golden/control_golden.json), and
+the multi-process SHM bootstrap (host-only transport: no GPU needed) with
+world sizes 2 and 7, including a MIG-aware duplicate across processes."""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import multiprocessing as mp
+import os
+import uuid
+
+import pytest
+
+from paper_2511_09143_b200 import _lib
+from paper_2511_09143_b200.errors import DuplicateDeviceError, MalformedLabelError
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "control_golden.json")))
+
+
+def c_peers(recs):
+    arr = (_lib.PeerInfoC * max(1, len(recs)))()
+    for i, p in enumerate(recs):
+        arr[i] = _lib.peer_to_c(p["rank"], p["pcie_bus_id"].upper(), p["mig_id"], p["host_hash"],
+                                p["pid_hash"])
+    return arr
+
+
+def native_outcome(recs, mig_aware):
+    L = _lib.lib()
+    arr = c_peers(recs)
+    a, b = ctypes.c_int(-1), ctypes.c_int(-1)
+    rc = L.fmx_validate_peers(arr, len(recs), int(mig_aware), ctypes.byref(a), ctypes.byref(b))
+    if rc == _lib.FMX_ERR_DUPLICATE_DEVICE:
+        return {"error": "DuplicateDeviceError", "rank_a": a.value, "rank_b": b.value}, None
+    if rc == _lib.FMX_ERR_BAD_RANKS:
+        return {"error": "ValueError"}, None
+    assert rc == 0, _lib.last_error()
+    n = len(recs)
+    labels = ctypes.create_string_buffer(_lib.BUS_ID_LEN * max(1, n))
+    buses = ctypes.create_string_buffer(_lib.BUS_ID_LEN * max(1, n))
+    counts = (ctypes.c_int * max(1, n))()
+    nb = ctypes.c_int()
+    rc = L.fmx_topology(arr, n, labels, buses, counts, ctypes.byref(nb))
+    discover = {"ranks": list(range(n))}
+    if rc == _lib.FMX_ERR_MALFORMED_LABEL:
+        return discover, {"error": "MalformedLabelError"}
+    assert rc == 0
+    by_rank = sorted(recs, key=lambda p: p["rank"])
+
+    def s(buf, i):
+        return buf.raw[i * _lib.BUS_ID_LEN:(i + 1) * _lib.BUS_ID_LEN].split(b"\0")[0].decode()
+
+    topo = {"labels": [[s(labels, i), by_rank[i]["pcie_bus_id"].upper(), by_rank[i]["rank"]]
+                       for i in range(n)],
+            "mig_list": [[s(buses, i), counts[i]] for i in range(nb.value)]}
+    return discover, topo
+
+
+def test_native_validation_and_topology_match_reference_golden():
+    checked = 0
+    for case in GOLDEN["discover_topology"]:
+        disc, topo = native_outcome(case["peers"], case["mig_aware"])
+        assert disc == case["discover"], case
+        if topo is not None:
+            assert topo == case["topology"], case
+        checked += 1
+    assert checked > 400
+
+
+def test_native_check_peer_matches_reference_golden():
+    L = _lib.lib()
+    for case in GOLDEN["peerinfo"]:
+        try:
+            p = _lib.peer_to_c(0, case["bus"], case["mig"], 1, 1)
+        except MalformedLabelError:
+            assert case.get("error") == "MalformedLabelError"
+            continue
+        rc = L.fmx_check_peer(ctypes.byref(p))
+        if "ok" in case:
+            assert rc == 0, (case, _lib.last_error())
+            assert p.pcie_bus_id.decode() == case["ok"]
+        elif case["error"] == "MalformedLabelError":
+            assert rc == _lib.FMX_ERR_MALFORMED_LABEL, case
+        else:
+            assert rc == _lib.FMX_ERR_EMPTY_MIG_ID, case
+
+
+def test_native_restore_bus_id_matches_reference_golden():
+    L = _lib.lib()
+    for case in GOLDEN["restore_bus_id"]:
+        out = ctypes.create_string_buffer(_lib.BUS_ID_LEN)
+        rc = L.fmx_restore_bus_id(case["label"].encode(), out)
+        if "ok" in case:
+            assert rc == 0 and out.value.decode() == case["ok"], case
+        else:
+            assert rc == _lib.FMX_ERR_MALFORMED_LABEL, case
+
+
+# ---------------------------------------------------------------- multi-process
+
+
+def _host_rank(rank, n, key, mig_ids, q):
+    from paper_2511_09143_b200.comm import init_process_group
+    from paper_2511_09143_b200.commsim import PeerInfo
+    try:
+        peer = PeerInfo(rank, "00:C0:00.0", mig_ids[rank], 7, 100 + rank)
+        comm = init_process_group(None, rank, key, peer=peer, nranks=n, transport="host",
+                                  timeout_s=30)
+        for _ in range(3):
+            comm.barrier(30)
+        labels = [nd.label for nd in comm.topology.nodes]
+        comm.destroy()
+        q.put((rank, "ok", labels))
+    except DuplicateDeviceError as exc:
+        q.put((rank, "dup", (exc.rank_a, exc.rank_b)))
+    except Exception as exc:  # noqa: BLE001
+        q.put((rank, "err", repr(exc)))
+
+
+def run_host_world(n, mig_ids):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    key = f"cpu-{uuid.uuid4().hex[:10]}"
+    ps = [ctx.Process(target=_host_rank, args=(r, n, key, mig_ids, q)) for r in range(n)]
+    for p in ps:
+        p.start()
+    out = {}
+    for _ in range(n):
+        r, status, payload = q.get(timeout=120)
+        out[r] = (status, payload)
+    for p in ps:
+        p.join(timeout=30)
+    assert not os.path.exists(f"/dev/shm/fmx-{key}"), "segment name must be unlinked"
+    return out
+
+
+@pytest.mark.parametrize("n", [2, 7])
+def test_multiprocess_bootstrap_labels(n):
+    out = run_host_world(n, [f"GC-gpu0-{r + 1}" for r in range(n)])
+    want = ["00:C0:00.0"] + [f"00:C0:00.{k}" for k in range(1, n)]
+    for r in range(n):
+        assert out[r] == ("ok", want)
+
+
+def test_multiprocess_bootstrap_rejects_double_binding():
+    out = run_host_world(3, ["MIG-a", "MIG-b", "MIG-a"])
+    for r in range(3):
+        assert out[r] == ("dup", (0, 2))
