@@ -62,6 +62,12 @@ def parse_args(argv=None):
     p.add_argument("--inproc", action="store_true",
                    help="ranks as threads of one process (for ncu); not the headline layout")
     p.add_argument("--out", default=None, help="also write the JSON line here")
+    p.add_argument("--train", action="store_true", help="also measure ResNet-50 DP img/s")
+    p.add_argument("--train-only", action="store_true")
+    p.add_argument("--train-mode", choices=["green", "mps", "full"], default="mps")
+    p.add_argument("--batch", type=int, default=32)
+    p.add_argument("--train-steps", type=int, default=10)
+    p.add_argument("--train-warmup", type=int, default=5)
     return p.parse_args(argv)
 
 
@@ -231,12 +237,136 @@ def _spawned_rank(rank, job_key, n, cfg, inst_mode, gpu_local):
     return rank_body(rank, job_key, n, cfg, inst_mode, gpu_local)
 
 
+def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_local: int):
+    """One instance rank of ResNet-50 data-parallel training (BASELINE
+    configs[1]): batch 32 per instance, synthetic ImageNet-shaped inputs,
+    random init, bf16 autocast with fp32 weights and gradients, SGD; DDP
+    gradient buckets allreduced over SHM by ddp.flexshm_hook."""
+    import torch
+    import torch.distributed as dist
+    import torch.nn.functional as F
+    import torchvision
+
+    from paper_2511_09143_b200 import ddp as fddp
+    from paper_2511_09143_b200 import instance as inst_mod
+    from paper_2511_09143_b200.comm import init_process_group
+
+    gpu_id, inst_id = cfg["instances"][rank]
+    inst = inst_mod.bind(gpu_id, inst_id, cfg["profiles"][rank], mode=inst_mode, device=gpu_local)
+    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n,
+                              transport=cfg["transport"], timeout_s=300)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(cfg["port"])
+    pg = dist.new_group(backend="gloo") if dist.is_initialized() else None
+    if pg is None:
+        dist.init_process_group("gloo", rank=rank, world_size=n)
+        pg = dist.group.WORLD
+    stream = inst.stream
+    torch.manual_seed(0)
+    with torch.cuda.stream(stream):
+        model = torchvision.models.resnet50().cuda(gpu_local).to(memory_format=torch.channels_last)
+        net = fddp.wrap(model, comm, control_group=pg)
+        opt = torch.optim.SGD(net.parameters(), lr=0.01, momentum=0.9)
+        g = torch.Generator(device="cpu").manual_seed(100 + rank)
+        x = torch.randn(cfg["batch"], 3, 224, 224, generator=g).cuda(gpu_local)
+        x = x.to(memory_format=torch.channels_last)
+        y = torch.randint(0, 1000, (cfg["batch"],), generator=g).cuda(gpu_local)
+
+    def step():
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = F.cross_entropy(net(x), y)
+        opt.zero_grad(set_to_none=True)
+        loss.backward()
+        opt.step()
+        return loss
+
+    with torch.cuda.stream(stream):
+        for _ in range(cfg["train_warmup"]):
+            step()
+    torch.cuda.synchronize()
+    comm.barrier(300)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = comm.kernel_launches()
+    ev0.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(cfg["train_steps"]):
+            loss = step()
+    ev1.record(stream)
+    ev1.synchronize()
+    comm.barrier(300)
+    out = {"rank": rank, "ms_total": ev0.elapsed_time(ev1), "loss": float(loss.item()),
+           "launches": comm.kernel_launches() - l0,
+           "param_digest": float(sum(p.detach().double().sum().item() for p in model.parameters()))}
+    dist.destroy_process_group()
+    comm.destroy()
+    return out
+
+
+def _spawned_train(rank, job_key, n, cfg, inst_mode, gpu_local):
+    return train_body(rank, job_key, n, cfg, inst_mode, gpu_local)
+
+
 # ----------------------------------------------------------------------------- arms
 
 
-def run_ours(args) -> dict | None:
+def run_ranks(body, spawned, mine, job_key, n, cfg, inst_mode, gpu_local, sampler=None):
+    """Rank mine[0] runs in this process, the rest in spawned processes."""
     import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    mps = None
+    results, errors = {}, []
+    if inst_mode == "mps":
+        from paper_2511_09143_b200.launcher import MPS_PERCENT, MpsDaemon
+        mps = MpsDaemon(job_key)
+        if not mps.start():
+            raise RuntimeError("MPS daemon failed to start")
+        os.environ.update(mps.env)
+        os.environ["CUDA_MPS_ACTIVE_THREAD_PERCENTAGE"] = str(MPS_PERCENT)
+    try:
+        with ctx.Pool(max(1, len(mine) - 1)) as pool:
+            pending = [pool.apply_async(spawned, (r, job_key, n, cfg, inst_mode, gpu_local))
+                       for r in mine[1:]]
+            if sampler is not None:
+                sampler.start()
+            try:
+                results[mine[0]] = body(mine[0], job_key, n, cfg, inst_mode, gpu_local)
+            except BaseException as exc:  # noqa: BLE001
+                errors.append((mine[0], exc))
+            for r, a in zip(mine[1:], pending):
+                try:
+                    results[r] = a.get(timeout=900)
+                except BaseException as exc:  # noqa: BLE001
+                    errors.append((r, exc))
+    finally:
+        if mps is not None:
+            mps.stop()
+            for k in list(mps.env) + ["CUDA_MPS_ACTIVE_THREAD_PERCENTAGE"]:
+                os.environ.pop(k, None)
+    if errors:
+        raise RuntimeError(f"rank {errors[0][0]} failed: {errors[0][1]!r}") from errors[0][1]
+    return results
 
+
+def run_train(args, d, job_key) -> dict:
+    """ResNet-50 DP img/s on the same instances (single-GPU layout only)."""
+    n = len(d.instances)
+    cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
+           "batch": args.batch, "train_steps": args.train_steps, "train_warmup": args.train_warmup,
+           "port": 29000 + os.getpid() % 1000}
+    res = run_ranks(train_body, _spawned_train, list(range(n)), job_key + "-t", n, cfg,
+                    args.train_mode, 0)
+    t = max(r["ms_total"] for r in res.values()) / 1e3
+    digests = {round(r["param_digest"], 3) for r in res.values()}
+    return {"img_s": n * args.batch * args.train_steps / t, "instances": n, "batch_per_instance":
+            args.batch, "ms_per_step": t * 1e3 / args.train_steps, "steps": args.train_steps,
+            "warmup": args.train_warmup, "instance_mode": args.train_mode,
+            "precision": "bf16 autocast, fp32 weights/grads (fp32 SHM allreduce)",
+            "replicas_agree": len(digests) == 1, "loss": res[0]["loss"],
+            "gpu_launches": sum(r["launches"] for r in res.values()),
+            "model": "torchvision resnet50, random init, synthetic 224x224 inputs"}
+
+
+def run_ours(args) -> dict | None:
     import torch
 
     grank, world, local = dist_env()
@@ -260,8 +390,6 @@ def run_ours(args) -> dict | None:
     my_gpu = grank if world > 1 else 0
     mine = [r for r, (g, _) in enumerate(d.instances) if g == my_gpu] if world > 1 else list(range(n))
     gpu_local = local if world > 1 else 0
-    if world > 1:
-        os.environ["CUDA_VISIBLE_DEVICES"] = os.environ.get("CUDA_VISIBLE_DEVICES", str(local))
     inst_mode = args.mode
     sampler = ClockSampler()
     results = {}
@@ -281,32 +409,11 @@ def run_ours(args) -> dict | None:
         for t in ts:
             t.join()
     else:
-        ctx = mp.get_context("spawn")
-        mps = None
-        if inst_mode == "mps":
-            from paper_2511_09143_b200.launcher import MPS_PERCENT, MpsDaemon
-            mps = MpsDaemon(job_key)
-            if not mps.start():
-                raise RuntimeError("MPS daemon failed to start")
-            os.environ.update(mps.env)
-            os.environ["CUDA_MPS_ACTIVE_THREAD_PERCENTAGE"] = str(MPS_PERCENT)
         try:
-            with ctx.Pool(len(mine) - 1) as pool:
-                async_res = [pool.apply_async(_spawned_rank, (r, job_key, n, cfg, inst_mode, gpu_local))
-                             for r in mine[1:]]
-                sampler.start()
-                try:
-                    results[mine[0]] = rank_body(mine[0], job_key, n, cfg, inst_mode, gpu_local)
-                except BaseException as exc:  # noqa: BLE001
-                    errors.append((mine[0], exc))
-                for r, a in zip(mine[1:], async_res):
-                    try:
-                        results[r] = a.get(timeout=900)
-                    except BaseException as exc:  # noqa: BLE001
-                        errors.append((r, exc))
-        finally:
-            if mps is not None:
-                mps.stop()
+            results = run_ranks(rank_body, _spawned_rank, mine, job_key, n, cfg, inst_mode,
+                                gpu_local, sampler)
+        except BaseException as exc:  # noqa: BLE001
+            errors.append((mine[0], exc))
     clocks = sampler.stop()
     if errors:
         raise RuntimeError(f"rank {errors[0][0]} failed: {errors[0][1]!r}") from errors[0][1]
@@ -414,9 +521,16 @@ def main(argv=None):
                         "the same SHM RS/AG algorithm, oracle/flexshm_oracle.c"}
         print(json.dumps(line))
         return 0
+    if args.train_only:
+        d = decision_for(args.gpus, args.ranks_per_gpu)
+        print(json.dumps({"resnet50": run_train(args, d, f"train-{os.getpid()}")}))
+        return 0
     line = run_ours(args)
     if line is None:
         return 0
+    if args.train and (args.gpus == 1 and world == 1):
+        d = decision_for(1, args.ranks_per_gpu)
+        line["resnet50"] = run_train(args, d, f"train-{os.getpid()}")
     if not args.no_cpu_baseline:
         r = run_cpu_reference(args.count, n, args.dtype, 1, 1, seconds=args.cpu_seconds)
         line["cpu_baseline"] = {"value": r["value"], "unit": line["unit"], "cores": r["cores"],

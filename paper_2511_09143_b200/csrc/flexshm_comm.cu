@@ -98,6 +98,10 @@ struct fmx_comm {
   uint32_t ar_round = 0, bc_round = 0;
   int64_t barrier_gen = 0;
   char* scratch = nullptr;  // CE transport: n * slice_bytes of HBM
+  cudaStream_t lane[2] = {nullptr, nullptr};
+  cudaEvent_t fork = nullptr, joined[2] = {nullptr, nullptr};
+  bool result_via_ce = false;  // CE transport: result slot by copy engine, not SM stores
+  bool copy2d = true;          // coalesce regular copy runs into cudaMemcpy2DAsync
   cudaEvent_t done = nullptr;
   bool has_done = false;
   uint64_t launches = 0;
@@ -135,13 +139,21 @@ void unmap(fmx_comm* c) {
 // ---- the plan: what one rank enqueues for one collective -----------------------
 //
 // plan_allreduce / plan_broadcast describe the schedule once, against a Sink.
-// CudaSink turns it into stream operations; TraceSink records the SHM bytes
-// each step reads / writes and the flags it signals / waits on, so the
+// Work is issued on two lanes (CUDA streams) per rank so the two link
+// directions overlap inside a rank: lane 0 stages (HBM -> SHM, D2H), lane 1
+// fetches, reduces and gathers (SHM -> HBM, H2D).  Lanes fork from / join
+// back into the caller's stream at every collective.  CudaSink turns the
+// plan into stream operations; TraceSink records, per lane, every SHM and
+// user-buffer byte range touched and every flag signalled / waited on, so the
 // schedule of every rank of any world size can be model-checked on a CPU
 // (fmx_trace_plan, tests/test_protocol_model.py).
 
-// SHM side of a data movement, for the trace: byte range relative to the
-// segment base, the rank that (should have) written it and in which round.
+constexpr int kLaneStage = 0;  // D2H lane
+constexpr int kLaneMain = 1;   // H2D + reduce lane
+
+// One data-movement end for the trace: SHM byte range (relative to the
+// segment) or user-buffer byte range (relative to the buffer start), plus the
+// rank/round that (should have) written SHM bytes.
 struct Annot {
   int64_t off = -1;
   size_t bytes = 0;
@@ -153,27 +165,29 @@ struct PlanSeg {
   const char* src;
   char* dst;
   size_t bytes;
-  Annot shm;          // the SHM end of this segment
-  bool shm_is_dst;    // true: this step writes SHM; false: reads it
+  Annot shm;        // the SHM end of this segment
+  bool shm_is_dst;  // true: this step writes SHM; false: reads it
+  Annot user;       // the user-buffer end (off < 0: none, e.g. HBM scratch)
 };
 
 struct PlanReduce {
   ReduceArgs args;
   std::vector<Annot> reads;  // SHM inputs (ZC transport)
-  Annot write;               // SHM result slot
+  Annot write;               // SHM result slot (written by the kernel)
+  Annot user_rw;             // own piece of the user buffer (read + written)
   int dtype;
   bool aligned;
 };
 
 struct Sink {
   virtual ~Sink() {}
-  virtual int copy(const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel) = 0;
-  virtual int reduce(const PlanReduce& r) = 0;
-  virtual int signal(int flag, uint32_t v) = 0;
-  virtual int signal2(int f0, uint32_t v0, int f1, uint32_t v1) = 0;
-  virtual int wait_peers(int flag, uint32_t v, int skip) = 0;
-  virtual int wait_rank(int q, int flag, uint32_t v) = 0;
-  virtual int d2d(void* dst, const void* src, size_t bytes) = 0;
+  virtual int copy(int lane, const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel) = 0;
+  virtual int reduce(int lane, const PlanReduce& r) = 0;
+  virtual int signal(int lane, int flag, uint32_t v) = 0;
+  virtual int signal2(int lane, int f0, uint32_t v0, int f1, uint32_t v1) = 0;
+  virtual int wait_peers(int lane, int flag, uint32_t v, int skip) = 0;
+  virtual int wait_rank(int lane, int q, int flag, uint32_t v) = 0;
+  virtual int d2d(int lane, void* dst, const void* src, size_t bytes, Annot from, Annot to) = 0;
 };
 
 int grid_for(size_t work_items, int threads, int cap) {
@@ -183,13 +197,34 @@ int grid_for(size_t work_items, int threads, int cap) {
 
 class CudaSink final : public Sink {
  public:
-  CudaSink(fmx_comm* c, cudaStream_t s) : c_(c), s_(s) {}
+  CudaSink(fmx_comm* c) : c_(c) {}
 
-  int copy(const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel) override {
+  int copy(int lane, const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel) override {
     if (segs.empty()) return FMX_OK;
+    cudaStream_t s = c_->lane[lane];
     if (!use_kernel) {
-      for (const PlanSeg& g : segs)
-        FMX_CUDA(cudaMemcpyAsync(g.dst, g.src, g.bytes, cudaMemcpyDefault, s_));
+      // copy engine; coalesce equal-size, equal-stride runs into one 2D copy
+      size_t i = 0;
+      while (i < segs.size()) {
+        size_t k = 1;
+        if (c_->copy2d && i + 1 < segs.size()) {
+          const ptrdiff_t ds = segs[i + 1].dst - segs[i].dst, ss = segs[i + 1].src - segs[i].src;
+          if (ds >= (ptrdiff_t)segs[i].bytes && ss >= (ptrdiff_t)segs[i].bytes && ds < (1ll << 31) &&
+              ss < (1ll << 31))
+            while (i + k < segs.size() && segs[i + k].bytes == segs[i].bytes &&
+                   segs[i + k].dst - segs[i + k - 1].dst == ds &&
+                   segs[i + k].src - segs[i + k - 1].src == ss)
+              ++k;
+          if (k > 1) {
+            FMX_CUDA(cudaMemcpy2DAsync(segs[i].dst, (size_t)ds, segs[i].src, (size_t)ss,
+                                       segs[i].bytes, k, cudaMemcpyDefault, s));
+            i += k;
+            continue;
+          }
+        }
+        FMX_CUDA(cudaMemcpyAsync(segs[i].dst, segs[i].src, segs[i].bytes, cudaMemcpyDefault, s));
+        ++i;
+      }
       return FMX_OK;
     }
     for (size_t i0 = 0; i0 < segs.size(); i0 += kMaxSegs) {
@@ -205,47 +240,48 @@ class CudaSink final : public Sink {
       constexpr int kThreads = 512, kU = 4;
       int gx = grid_for((maxb / 16 + kU - 1) / kU, kThreads, std::max(1, 1184 / a.nseg));
       dim3 grid(gx, a.nseg);
-      fmx_copy_kernel<kU><<<grid, kThreads, 0, s_>>>(a);
+      fmx_copy_kernel<kU><<<grid, kThreads, 0, s>>>(a);
       FMX_CUDA(cudaGetLastError());
       c_->launches++;
     }
     return FMX_OK;
   }
 
-  int reduce(const PlanReduce& r) override {
+  int reduce(int lane, const PlanReduce& r) override {
     const ReduceArgs& a = r.args;
     if (a.len == 0) return FMX_OK;
+    cudaStream_t s = c_->lane[lane];
     constexpr int kThreads = 256, kU = 2;
     const int V = r.dtype == FMX_FLOAT32 ? 4 : 8;
     if (r.aligned) {
       int g = grid_for((a.len / V + kU - 1) / kU + 1, kThreads, 1184);
       if (r.dtype == FMX_FLOAT32)
-        fmx_reduce_kernel<float, kU><<<g, kThreads, 0, s_>>>(a);
+        fmx_reduce_kernel<float, kU><<<g, kThreads, 0, s>>>(a);
       else
-        fmx_reduce_kernel<__nv_bfloat16, kU><<<g, kThreads, 0, s_>>>(a);
+        fmx_reduce_kernel<__nv_bfloat16, kU><<<g, kThreads, 0, s>>>(a);
     } else {
       int g = grid_for(a.len, kThreads, 1184);
       if (r.dtype == FMX_FLOAT32)
-        fmx_reduce_scalar_kernel<float><<<g, kThreads, 0, s_>>>(a);
+        fmx_reduce_scalar_kernel<float><<<g, kThreads, 0, s>>>(a);
       else
-        fmx_reduce_scalar_kernel<__nv_bfloat16><<<g, kThreads, 0, s_>>>(a);
+        fmx_reduce_scalar_kernel<__nv_bfloat16><<<g, kThreads, 0, s>>>(a);
     }
     FMX_CUDA(cudaGetLastError());
     c_->launches++;
     return FMX_OK;
   }
 
-  int signal(int flag, uint32_t v) override {
+  int signal(int lane, int flag, uint32_t v) override {
     CUstreamBatchMemOpParams op;
     memset(&op, 0, sizeof op);
     op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
     op.writeValue.address = c_->flag_dev(c_->rank, flag);
     op.writeValue.value = v;
     op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;  // fence before the write
-    return batch(&op, 1);
+    return batch(lane, &op, 1);
   }
 
-  int signal2(int f0, uint32_t v0, int f1, uint32_t v1) override {
+  int signal2(int lane, int f0, uint32_t v0, int f1, uint32_t v1) override {
     CUstreamBatchMemOpParams op[2];
     memset(op, 0, sizeof op);
     op[0].writeValue.operation = op[1].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
@@ -253,27 +289,27 @@ class CudaSink final : public Sink {
     op[0].writeValue.value = v0;
     op[1].writeValue.address = c_->flag_dev(c_->rank, f1);
     op[1].writeValue.value = v1;
-    return batch(op, 2);
+    return batch(lane, op, 2);
   }
 
-  int wait_peers(int flag, uint32_t v, int skip) override {
+  int wait_peers(int lane, int flag, uint32_t v, int skip) override {
     ops_.clear();
     for (int q = 0; q < c_->nranks; ++q)
       if (q != skip) ops_.push_back(wait_op(q, flag, v));
     for (size_t i = 0; i < ops_.size(); i += kBatchMax) {
-      int rc = batch(ops_.data() + i, (unsigned)std::min<size_t>(kBatchMax, ops_.size() - i));
+      int rc = batch(lane, ops_.data() + i, (unsigned)std::min<size_t>(kBatchMax, ops_.size() - i));
       if (rc) return rc;
     }
     return FMX_OK;
   }
 
-  int wait_rank(int q, int flag, uint32_t v) override {
+  int wait_rank(int lane, int q, int flag, uint32_t v) override {
     CUstreamBatchMemOpParams op = wait_op(q, flag, v);
-    return batch(&op, 1);
+    return batch(lane, &op, 1);
   }
 
-  int d2d(void* dst, const void* src, size_t bytes) override {
-    FMX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s_));
+  int d2d(int lane, void* dst, const void* src, size_t bytes, Annot, Annot) override {
+    FMX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c_->lane[lane]));
     return FMX_OK;
   }
 
@@ -287,54 +323,76 @@ class CudaSink final : public Sink {
     op.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;  // cyclic >=
     return op;
   }
-  int batch(CUstreamBatchMemOpParams* ops, unsigned n) {
-    CUresult r = g_batch((CUstream)s_, n, ops, 0);
+  int batch(int lane, CUstreamBatchMemOpParams* ops, unsigned n) {
+    CUresult r = g_batch((CUstream)c_->lane[lane], n, ops, 0);
     if (r != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "cuStreamBatchMemOp failed (%d)", (int)r);
     return FMX_OK;
   }
   fmx_comm* c_;
-  cudaStream_t s_;
   std::vector<CUstreamBatchMemOpParams> ops_;
 };
 
-// Text trace, one line per SHM access / flag operation:
-//   W <off> <bytes> <round>            this rank writes SHM bytes of `round`
-//   R <off> <bytes> <writer> <round>   reads bytes `writer` wrote in `round`
-//   S <flag> <value>                   signal own flag
-//   A <rank> <flag> <value>            wait until rank's flag >= value
+// Text trace, one line per access / flag operation, prefixed by the lane:
+//   <lane> W <off> <bytes> <round>           write SHM bytes of `round`
+//   <lane> R <off> <bytes> <writer> <round>  read SHM bytes `writer` wrote in `round`
+//   <lane> UR <off> <bytes> / UW <off> <bytes>   read / write own user buffer
+//   <lane> S <flag> <value>                  signal own flag
+//   <lane> A <rank> <flag> <value>           wait until rank's flag >= value
+//   J                                        both lanes join (collective boundary)
 class TraceSink final : public Sink {
  public:
   explicit TraceSink(std::string* out) : out_(out) {}
-  int copy(const std::vector<PlanSeg>& segs, bool, bool) override {
-    for (const PlanSeg& g : segs) access(g.shm, g.shm_is_dst);
+  int copy(int lane, const std::vector<PlanSeg>& segs, bool, bool) override {
+    for (const PlanSeg& g : segs) {
+      if (g.shm_is_dst) {
+        user(lane, g.user, false);
+        shm(lane, g.shm, true);
+      } else {
+        shm(lane, g.shm, false);
+        user(lane, g.user, true);
+      }
+    }
     return FMX_OK;
   }
-  int reduce(const PlanReduce& r) override {
-    for (const Annot& a : r.reads) access(a, false);
-    access(r.write, true);
+  int reduce(int lane, const PlanReduce& r) override {
+    for (const Annot& a : r.reads) shm(lane, a, false);
+    user(lane, r.user_rw, false);
+    user(lane, r.user_rw, true);
+    shm(lane, r.write, true);
     return FMX_OK;
   }
-  int signal(int flag, uint32_t v) override { return line("S %d %u\n", flag, v); }
-  int signal2(int f0, uint32_t v0, int f1, uint32_t v1) override {
-    line("S %d %u\n", f0, v0);
-    return line("S %d %u\n", f1, v1);
+  int signal(int lane, int flag, uint32_t v) override { return line("%d S %d %u\n", lane, flag, v); }
+  int signal2(int lane, int f0, uint32_t v0, int f1, uint32_t v1) override {
+    line("%d S %d %u\n", lane, f0, v0);
+    return line("%d S %d %u\n", lane, f1, v1);
   }
-  int wait_peers(int flag, uint32_t v, int skip) override {
+  int wait_peers(int lane, int flag, uint32_t v, int skip) override {
     for (int q = 0; q < nranks; ++q)
-      if (q != skip) line("A %d %d %u\n", q, flag, v);
+      if (q != skip) line("%d A %d %d %u\n", lane, q, flag, v);
     return FMX_OK;
   }
-  int wait_rank(int q, int flag, uint32_t v) override { return line("A %d %d %u\n", q, flag, v); }
-  int d2d(void*, const void*, size_t) override { return FMX_OK; }
+  int wait_rank(int lane, int q, int flag, uint32_t v) override {
+    return line("%d A %d %d %u\n", lane, q, flag, v);
+  }
+  int d2d(int lane, void*, const void*, size_t, Annot from, Annot to) override {
+    user(lane, from, false);
+    user(lane, to, true);
+    return FMX_OK;
+  }
+  int join() { return line("J\n"); }
   int nranks = 0;
 
  private:
-  void access(const Annot& a, bool write) {
+  void shm(int lane, const Annot& a, bool write) {
     if (a.off < 0 || a.bytes == 0) return;
     if (write)
-      line("W %lld %zu %u\n", (long long)a.off, a.bytes, a.round);
+      line("%d W %lld %zu %u\n", lane, (long long)a.off, a.bytes, a.round);
     else
-      line("R %lld %zu %d %u\n", (long long)a.off, a.bytes, a.writer, a.round);
+      line("%d R %lld %zu %d %u\n", lane, (long long)a.off, a.bytes, a.writer, a.round);
+  }
+  void user(int lane, const Annot& a, bool write) {
+    if (a.off < 0 || a.bytes == 0) return;
+    line("%d %s %lld %zu\n", lane, write ? "UW" : "UR", (long long)a.off, a.bytes);
   }
   int line(const char* fmt, ...) __attribute__((format(printf, 2, 3))) {
     char buf[128];
@@ -372,8 +430,21 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype) {
   return g;
 }
 
-// Reduce-scatter + all-gather through the segment, pipelined in rounds
-// (schedule and its hazard argument: DESIGN.md §3.3).
+Annot ubuf(size_t off_bytes, size_t bytes) { return Annot{(int64_t)off_bytes, bytes, -1, 0}; }
+
+// Reduce-scatter + all-gather through the segment, pipelined in rounds on two
+// lanes.  Round R uses slot R % 2.  Hazards and why each wait exists:
+//  lane 0, stage(R) into in[R%2][o][me]: the slot was last read by owner o's
+//      reduce(R-2)                        -> wait REDUCED[o] >= R-1 (all o)
+//  lane 1, reduce(R) reads in[R%2][me][q]  -> wait STAGED[q]  >= R+1 (all q)
+//          and writes out[R%2][me], last read by every q's gather(R-2): implied,
+//          my gather(R-1) waited REDUCED[q] >= R, and q's lane 1 runs
+//          gather(R-2) before reduce(R-1) (the model checker confirms no
+//          extra flag is needed)
+//  lane 1, gather(R) reads out[R%2][q]     -> wait REDUCED[q] >= R+1 (all q)
+//  in place (send == recv): gather(R) overwrites pieces of round R of the
+//      other chunks; my stage(R) read them first because every owner's
+//      reduce(R) waited for my STAGED >= R+1.
 int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
                    int op, float factor, bool aligned) {
   const int n = c->nranks, me = c->rank;
@@ -381,27 +452,29 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
   const Geometry g = allreduce_geometry(c, count, dtype);
   std::vector<PlanSeg> segs;
   int rc;
+  const uint32_t R0 = c->ar_round;
 
-  auto stage = [&](uint32_t j) -> int {
-    const uint32_t R = c->ar_round + j;
+  // lane 0: stage every round as soon as its slot is free
+  for (uint32_t j = 0; j < g.rounds; ++j) {
+    const uint32_t R = R0 + j;
+    if (R >= 2 && (rc = k.wait_peers(kLaneStage, kReduced, R - 1, me))) return rc;
     segs.clear();
     for (int o = 0; o < n; ++o) {
       const size_t len = o == me ? 0 : g.len(o, j);
       if (!len) continue;
       const size_t off = c->in_off(R, o, me);
       segs.push_back({src + g.lo(o, j) * g.esz, c->at(zc, off), len * g.esz,
-                      Annot{(int64_t)off, len * g.esz, me, R}, true});
+                      Annot{(int64_t)off, len * g.esz, me, R}, true,
+                      ubuf(g.lo(o, j) * g.esz, len * g.esz)});
     }
-    int r = k.copy(segs, false, zc);
-    return r ? r : k.signal(kStaged, R + 1);
-  };
+    if ((rc = k.copy(kLaneStage, segs, false, zc))) return rc;
+    if ((rc = k.signal(kLaneStage, kStaged, R + 1))) return rc;
+  }
 
-  if ((rc = stage(0))) return rc;
+  // lane 1: reduce-scatter my chunk (ascending rank order), then all-gather
   for (uint32_t j = 0; j < g.rounds; ++j) {
-    const uint32_t R = c->ar_round + j;
-    if (j + 1 < g.rounds && (rc = stage(j + 1))) return rc;  // prefetch next round
-    // reduce-scatter of my chunk, ascending rank order
-    if ((rc = k.wait_peers(kStaged, R + 1, me))) return rc;
+    const uint32_t R = R0 + j;
+    if ((rc = k.wait_peers(kLaneMain, kStaged, R + 1, me))) return rc;
     const size_t mylen = g.len(me, j);
     if (mylen) {
       PlanReduce pr;
@@ -415,17 +488,22 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
       a.factor = factor;
       a.out_dev = dst + g.lo(me, j) * g.esz;
       const size_t out_off = c->out_off(R, me);
-      a.out_sys = c->at(true, out_off);
-      pr.write = Annot{(int64_t)out_off, mylen * g.esz, me, R};
+      pr.user_rw = ubuf(g.lo(me, j) * g.esz, mylen * g.esz);
+      const bool via_ce = !zc && c->result_via_ce;
+      if (!via_ce) {
+        a.out_sys = c->at(true, out_off);
+        pr.write = Annot{(int64_t)out_off, mylen * g.esz, me, R};
+      }
       if (!zc) {  // copy engine pulls the n-1 contributions into HBM scratch first
         segs.clear();
         for (int q = 0; q < n; ++q) {
           if (q == me) continue;
           const size_t off = c->in_off(R, me, q);
           segs.push_back({c->at(false, off), c->scratch + (size_t)q * c->slice_bytes,
-                          mylen * g.esz, Annot{(int64_t)off, mylen * g.esz, q, R}, false});
+                          mylen * g.esz, Annot{(int64_t)off, mylen * g.esz, q, R}, false,
+                          Annot{}});
         }
-        if ((rc = k.copy(segs, true, false))) return rc;
+        if ((rc = k.copy(kLaneMain, segs, true, false))) return rc;
       }
       for (int q = 0; q < n; ++q) {
         if (q == me) {
@@ -439,20 +517,27 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
           a.src[q] = c->scratch + (size_t)q * c->slice_bytes;
         }
       }
-      if ((rc = k.reduce(pr))) return rc;
+      if ((rc = k.reduce(kLaneMain, pr))) return rc;
+      if (via_ce) {  // result slot written by the copy engine from HBM
+        segs.clear();
+        segs.push_back({dst + g.lo(me, j) * g.esz, c->at(false, out_off), mylen * g.esz,
+                        Annot{(int64_t)out_off, mylen * g.esz, me, R}, true,
+                        ubuf(g.lo(me, j) * g.esz, mylen * g.esz)});
+        if ((rc = k.copy(kLaneMain, segs, false, false))) return rc;
+      }
     }
-    if ((rc = k.signal(kReduced, R + 1))) return rc;
-    // all-gather of the other owners' results
-    if ((rc = k.wait_peers(kReduced, R + 1, me))) return rc;
+    if ((rc = k.signal(kLaneMain, kReduced, R + 1))) return rc;
+    if ((rc = k.wait_peers(kLaneMain, kReduced, R + 1, me))) return rc;
     segs.clear();
     for (int q = 0; q < n; ++q) {
       const size_t len = q == me ? 0 : g.len(q, j);
       if (!len) continue;
       const size_t off = c->out_off(R, q);
       segs.push_back({c->at(zc, off), dst + g.lo(q, j) * g.esz, len * g.esz,
-                      Annot{(int64_t)off, len * g.esz, q, R}, false});
+                      Annot{(int64_t)off, len * g.esz, q, R}, false,
+                      ubuf(g.lo(q, j) * g.esz, len * g.esz)});
     }
-    if ((rc = k.copy(segs, true, zc))) return rc;
+    if ((rc = k.copy(kLaneMain, segs, true, zc))) return rc;
   }
   c->ar_round += g.rounds;
   return FMX_OK;
@@ -460,10 +545,11 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
 
 // Root stages rounds of n*slice bytes into the broadcast slot; every other
 // rank copies them out and signals BC_DONE, which the root waits on before
-// reusing a slot (two rounds later).
+// reusing a slot (two rounds later).  Single lane (lane 1).
 int plan_broadcast(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
                    int root) {
   const int me = c->rank;
+  const int L = kLaneMain;
   const bool zc = c->transport == FMX_TRANSPORT_ZC;
   const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;
   const size_t bslice = (size_t)c->nranks * c->slice_bytes / esz;
@@ -476,20 +562,38 @@ int plan_broadcast(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
     const size_t off = c->bc_slot_off(R);
     const Annot an{(int64_t)off, len * esz, root, R};
     if (me == root) {
-      if (R + 1 > (uint32_t)c->nslots && (rc = k.wait_peers(kBcDone, R + 1 - c->nslots, me)))
+      if (R + 1 > (uint32_t)c->nslots && (rc = k.wait_peers(L, kBcDone, R + 1 - c->nslots, me)))
         return rc;
-      segs[0] = {src + lo * esz, c->at(zc, off), len * esz, an, true};
-      if ((rc = k.copy(segs, false, zc))) return rc;
-      if ((rc = k.signal2(kBcStaged, R + 1, kBcDone, R + 1))) return rc;
-      if (src != dst && (rc = k.d2d(dst + lo * esz, src + lo * esz, len * esz))) return rc;
+      segs[0] = {src + lo * esz, c->at(zc, off), len * esz, an, true, ubuf(lo * esz, len * esz)};
+      if ((rc = k.copy(L, segs, false, zc))) return rc;
+      if ((rc = k.signal2(L, kBcStaged, R + 1, kBcDone, R + 1))) return rc;
+      if (src != dst &&
+          (rc = k.d2d(L, dst + lo * esz, src + lo * esz, len * esz, Annot{}, Annot{})))
+        return rc;
     } else {
-      if ((rc = k.wait_rank(root, kBcStaged, R + 1))) return rc;
-      segs[0] = {c->at(zc, off), dst + lo * esz, len * esz, an, false};
-      if ((rc = k.copy(segs, true, zc))) return rc;
-      if ((rc = k.signal(kBcDone, R + 1))) return rc;
+      if ((rc = k.wait_rank(L, root, kBcStaged, R + 1))) return rc;
+      segs[0] = {c->at(zc, off), dst + lo * esz, len * esz, an, false, ubuf(lo * esz, len * esz)};
+      if ((rc = k.copy(L, segs, true, zc))) return rc;
+      if ((rc = k.signal(L, kBcDone, R + 1))) return rc;
     }
   }
   c->bc_round += rounds;
+  return FMX_OK;
+}
+
+// Fork the lanes off the caller's stream, run the plan, join them back.
+template <typename F>
+int on_lanes(fmx_comm* c, cudaStream_t user, F&& body) {
+  FMX_CUDA(cudaEventRecord(c->fork, user));
+  for (int l = 0; l < 2; ++l) FMX_CUDA(cudaStreamWaitEvent(c->lane[l], c->fork, 0));
+  int rc = body();
+  for (int l = 0; l < 2; ++l) {
+    FMX_CUDA(cudaEventRecord(c->joined[l], c->lane[l]));
+    FMX_CUDA(cudaStreamWaitEvent(user, c->joined[l], 0));
+  }
+  if (rc) return rc;
+  FMX_CUDA(cudaEventRecord(c->done, user));
+  c->has_done = true;
   return FMX_OK;
 }
 
@@ -502,11 +606,6 @@ int check_comm(fmx_comm* c, bool needs_device = true) {
   return FMX_OK;
 }
 
-int record_done(fmx_comm* c, cudaStream_t s) {
-  FMX_CUDA(cudaEventRecord(c->done, s));
-  c->has_done = true;
-  return FMX_OK;
-}
 
 }  // namespace
 
@@ -684,6 +783,13 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (e == cudaSuccess && c->transport == FMX_TRANSPORT_CE)
     e = cudaMalloc((void**)&c->scratch, (size_t)nranks * c->slice_bytes);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+  for (int l = 0; l < 2 && e == cudaSuccess; ++l) {
+    e = cudaStreamCreateWithFlags(&c->lane[l], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->joined[l], cudaEventDisableTiming);
+  }
+  if (const char* v = getenv("FMX_RESULT_VIA_CE")) c->result_via_ce = atoi(v) != 0;
+  if (const char* v = getenv("FMX_COPY2D")) c->copy2d = atoi(v) != 0;
   if (e != cudaSuccess) {
     h->aborted.store(1);
     fail(FMX_ERR_CUDA, "device mapping of %zu-byte segment failed: %s", c->total_bytes,
@@ -721,11 +827,14 @@ int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int 
   cudaStream_t s = (cudaStream_t)stream;
   const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;
   const bool aligned = (((uintptr_t)send | (uintptr_t)recv) & 15) == 0;
-  CudaSink sink(c, s);
+  CudaSink sink(c);
   if (c->nranks == 1) {  // nothing to exchange: apply the scale convention locally
-    if (op == FMX_OP_SUM) {
-      if (send != recv) FMX_CUDA(cudaMemcpyAsync(recv, send, count * esz, cudaMemcpyDeviceToDevice, s));
-    } else {
+    return on_lanes(c, s, [&]() -> int {
+      if (op == FMX_OP_SUM) {
+        if (send != recv)
+          FMX_CUDA(cudaMemcpyAsync(recv, send, count * esz, cudaMemcpyDeviceToDevice, c->lane[kLaneMain]));
+        return FMX_OK;
+      }
       PlanReduce pr;
       memset(&pr.args, 0, sizeof pr.args);
       pr.args.src[0] = (const char*)send;
@@ -736,14 +845,13 @@ int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int 
       pr.args.factor = factor;
       pr.dtype = dtype;
       pr.aligned = aligned;
-      if ((rc = sink.reduce(pr))) return rc;
-    }
-    return record_done(c, s);
+      return sink.reduce(kLaneMain, pr);
+    });
   }
-  if ((rc = plan_allreduce(c, sink, (const char*)send, (char*)recv, count, dtype, op, factor,
-                           aligned)))
-    return rc;
-  return record_done(c, s);
+  return on_lanes(c, s, [&]() {
+    return plan_allreduce(c, sink, (const char*)send, (char*)recv, count, dtype, op, factor,
+                          aligned);
+  });
 }
 
 int fmx_broadcast(fmx_comm_t c, const void* send, void* recv, size_t count, int dtype, int root,
@@ -757,13 +865,17 @@ int fmx_broadcast(fmx_comm_t c, const void* send, void* recv, size_t count, int 
   const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;
   if (!recv || (c->rank == root && !send)) return fail(FMX_ERR_INVALID_ARG, "null buffer");
   cudaStream_t s = (cudaStream_t)stream;
+  CudaSink sink(c);
   if (c->nranks == 1) {
-    if (send != recv) FMX_CUDA(cudaMemcpyAsync(recv, send, count * esz, cudaMemcpyDeviceToDevice, s));
-    return record_done(c, s);
+    return on_lanes(c, s, [&]() -> int {
+      if (send != recv)
+        FMX_CUDA(cudaMemcpyAsync(recv, send, count * esz, cudaMemcpyDeviceToDevice, c->lane[kLaneMain]));
+      return FMX_OK;
+    });
   }
-  CudaSink sink(c, s);
-  if ((rc = plan_broadcast(c, sink, (const char*)send, (char*)recv, count, dtype, root))) return rc;
-  return record_done(c, s);
+  return on_lanes(c, s, [&]() {
+    return plan_broadcast(c, sink, (const char*)send, (char*)recv, count, dtype, root);
+  });
 }
 
 int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int nops,
@@ -780,6 +892,7 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   c.slice_bytes = slice_bytes;
   c.L = compute_layout(nranks, 2, slice_bytes);
   c.total_bytes = c.L.total;
+  if (const char* v = getenv("FMX_RESULT_VIA_CE")) c.result_via_ce = atoi(v) != 0;
   std::string out;
   TraceSink sink(&out);
   sink.nranks = nranks;
@@ -787,7 +900,7 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   static char dummy[16] __attribute__((aligned(16)));
   for (int i = 0; i < nops; ++i) {
     int rc;
-    out.append("#\n");
+    sink.join();
     if (kinds[i] != 0 && (!roots || roots[i] < 0 || roots[i] >= nranks))
       return fail(FMX_ERR_INVALID_ARG, "bad broadcast root");
     if (kinds[i] == 0)
@@ -796,6 +909,7 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
       rc = plan_broadcast(&c, sink, dummy, dummy, counts[i], dtypes[i], roots ? roots[i] : 0);
     if (rc) return rc;
   }
+  sink.join();
   if (used) *used = out.size() + 1;
   if (!buf || cap < out.size() + 1) return fail(FMX_ERR_INVALID_ARG, "trace buffer too small");
   memcpy(buf, out.c_str(), out.size() + 1);
@@ -824,6 +938,11 @@ int fmx_comm_destroy(fmx_comm_t c) {
   if (c->has_done && cudaEventSynchronize(c->done) != cudaSuccess)
     rc = fail(FMX_ERR_CUDA, "pending collective failed: %s", cudaGetErrorString(cudaGetLastError()));
   if (c->done) cudaEventDestroy(c->done);
+  if (c->fork) cudaEventDestroy(c->fork);
+  for (int l = 0; l < 2; ++l) {
+    if (c->lane[l]) cudaStreamDestroy(c->lane[l]);
+    if (c->joined[l]) cudaEventDestroy(c->joined[l]);
+  }
   if (c->scratch) cudaFree(c->scratch);
   if (c->registered) cudaHostUnregister(c->base);
   if (c->hdr) c->hdr->departed.fetch_add(1);

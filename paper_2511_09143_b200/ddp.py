@@ -1,0 +1,109 @@
+"""PyTorch DDP / ZeRO integration of the SHM communicator.
+
+In the paper the SHM allreduce is reached from DDP's gradient buckets and
+ZeRO's shard broadcasts (reference PAPER.md:353-354, 485).  Stock NCCL cannot
+even initialise with several ranks on one GPU ("Duplicate GPU detected",
+PAPER.md:264-271), so here:
+
+* the DDP control plane (parameter-shape verification) runs on a gloo
+  process group over the same ranks - small metadata only;
+* the init-time parameter broadcast (DDP `_sync_module_states`) goes through
+  `ShmCommunicator.broadcast` of the flattened parameters;
+* every gradient bucket is allreduced by `flexshm_hook`, which keeps DDP's
+  default-hook arithmetic - divide by world size, then SUM
+  (torch/distributed/algorithms/ddp_comm_hooks/default_hooks.py:18-33) -
+  fused into one pass (op="avg" = FMX_OP_PREDIV_SUM) with the fixed
+  ascending-rank fp32 summation;
+* `ZeroShardBroadcast` re-broadcasts each owner's updated parameter shard
+  after a sharded optimizer step (the ZeroRedundancyOptimizer pattern,
+  torch/distributed/optim/zero_redundancy_optimizer.py:785-801).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .comm import ShmCommunicator
+
+
+def flexshm_hook(comm: ShmCommunicator, bucket) -> torch.futures.Future:
+    """DDP communication hook: bucket.buffer() <- mean over ranks.
+
+    The allreduce is enqueued on the current stream (the stream autograd runs
+    the bucket's producers on), so the future can complete immediately: every
+    consumer of the returned tensor is stream-ordered after the collective.
+    """
+    buf = bucket.buffer()
+    comm.allreduce(buf, op="avg")
+    fut: torch.futures.Future = torch.futures.Future()
+    fut.set_result(buf)
+    return fut
+
+
+def broadcast_parameters(module: torch.nn.Module, comm: ShmCommunicator, root: int = 0) -> None:
+    """Make every rank's parameters (and floating buffers) equal to root's."""
+    tensors = [p.data for p in module.parameters()] + \
+              [b for b in module.buffers() if b.is_floating_point()]
+    by_dtype: dict[torch.dtype, list[torch.Tensor]] = {}
+    for t in tensors:
+        by_dtype.setdefault(t.dtype, []).append(t)
+    for dtype, group in by_dtype.items():
+        if dtype not in (torch.float32, torch.bfloat16):
+            raise TypeError(f"cannot broadcast {dtype} parameters over SHM")
+        flat = torch.cat([t.reshape(-1) for t in group])
+        comm.broadcast(flat, root=root)
+        off = 0
+        with torch.no_grad():
+            for t in group:
+                k = t.numel()
+                t.copy_(flat[off:off + k].view_as(t))
+                off += k
+
+
+def wrap(module: torch.nn.Module, comm: ShmCommunicator, control_group=None,
+         bucket_cap_mb: float = 25.0, **ddp_kwargs):
+    """DistributedDataParallel over `control_group` (gloo) with gradients on
+    the SHM path.  Parameters are synchronised from rank 0 first."""
+    from torch.nn.parallel import DistributedDataParallel as DDP
+
+    broadcast_parameters(module, comm, root=0)
+    ddp = DDP(module, process_group=control_group, bucket_cap_mb=bucket_cap_mb,
+              broadcast_buffers=False, init_sync=False, **ddp_kwargs)
+    ddp.register_comm_hook(comm, flexshm_hook)
+    return ddp
+
+
+class ZeroShardBroadcast:
+    """After a sharded optimizer step, rank r owns parameter shard r; every
+    shard is broadcast from its owner so all replicas agree again."""
+
+    def __init__(self, params: list[torch.nn.Parameter], comm: ShmCommunicator):
+        self.comm = comm
+        self.params = list(params)
+        sizes = [p.numel() for p in self.params]
+        total = sum(sizes)
+        per = (total + comm.size - 1) // comm.size
+        # greedy contiguous partition of the parameter list into size-balanced shards
+        self.owner, acc, r = [], 0, 0
+        for s in sizes:
+            if acc >= per * (r + 1) and r < comm.size - 1:
+                r += 1
+            self.owner.append(r)
+            acc += s
+
+    def owned(self, rank: int) -> list[torch.nn.Parameter]:
+        return [p for p, o in zip(self.params, self.owner) if o == rank]
+
+    @torch.no_grad()
+    def sync(self) -> None:
+        for r in range(self.comm.size):
+            group = [p for p, o in zip(self.params, self.owner) if o == r]
+            if not group:
+                continue
+            flat = torch.cat([p.data.reshape(-1) for p in group])
+            self.comm.broadcast(flat, root=r)
+            off = 0
+            for p in group:
+                k = p.numel()
+                p.data.copy_(flat[off:off + k].view_as(p))
+                off += k

@@ -96,11 +96,18 @@ class MpsDaemon:
         return self.started
 
     def stop(self) -> None:
+        """Ask the daemon to quit.  It exits once its last client does (the
+        calling process may itself be a client), so do not wait for it."""
         if self.started:
-            subprocess.run(["nvidia-cuda-mps-control"], input=b"quit\n",
-                           env={**os.environ, **self.env}, timeout=30, capture_output=True)
+            p = subprocess.Popen(["nvidia-cuda-mps-control"], stdin=subprocess.PIPE,
+                                 stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL,
+                                 env={**os.environ, **self.env})
+            try:
+                p.stdin.write(b"quit\n")
+                p.stdin.close()
+            except OSError:
+                pass
             self.started = False
-        shutil.rmtree(self.dir, ignore_errors=True)
 
 
 def launch(fn, decision: AllocationDecision, args: tuple = (), *, job_key: str | None = None,

@@ -28,22 +28,21 @@ from paper_2511_09143_b200 import _lib
 
 
 def parse(text: str):
-    ops = []
+    """-> [lane0 ops, lane1 ops]; a 'J' line is a join point in both lanes."""
+    lanes = [[], []]
+    joins = 0
     for line in text.splitlines():
-        if not line or line == "#":
+        if not line:
+            continue
+        if line == "J":
+            for ops in lanes:
+                ops.append(("J", joins))
+            joins += 1
             continue
         f = line.split()
-        if f[0] == "W":
-            ops.append(("W", int(f[1]), int(f[2]), int(f[3])))
-        elif f[0] == "R":
-            ops.append(("R", int(f[1]), int(f[2]), int(f[3]), int(f[4])))
-        elif f[0] == "S":
-            ops.append(("S", int(f[1]), int(f[2])))
-        elif f[0] == "A":
-            ops.append(("A", int(f[1]), int(f[2]), int(f[3])))
-        else:
-            raise AssertionError(line)
-    return ops
+        lane, kind, rest = int(f[0]), f[1], [int(x) for x in f[2:]]
+        lanes[lane].append((kind, *rest))
+    return lanes
 
 
 def geq(a: int, b: int) -> bool:
@@ -53,71 +52,99 @@ def geq(a: int, b: int) -> bool:
 
 
 def simulate(progs, seed: int, burst: int = 3):
+    """progs[rank] = [lane0, lane1].  Actors are (rank, lane) pairs, each a
+    sequential program (one CUDA stream); lanes of a rank meet at joins."""
     n = len(progs)
+    actors = [(r, l) for r in range(n) for l in range(2)]
+    idx = {a: i for i, a in enumerate(actors)}
+    m = len(actors)
     rng = random.Random(seed)
-    pc = [0] * n
-    clock = [[0] * n for _ in range(n)]
+    pc = {a: 0 for a in actors}
+    clock = {a: [0] * m for a in actors}
     flags = {}
-    last_write = {}   # off -> (rank, time, bytes, round)
-    reads = {}        # off -> [(rank, time)] since last write
-    starts = []
+    last_write = {}   # key -> (actor, time, bytes, round)
+    reads = {}        # key -> [(actor, time)] since last write
+
+    def op_of(a):
+        prog = progs[a[0]][a[1]]
+        return prog[pc[a]] if pc[a] < len(prog) else None
+
+    def ready(a):
+        op = op_of(a)
+        if op is None:
+            return False
+        if op[0] == "A":
+            return geq(flags.get((op[1], op[2]), (0, None))[0], op[3])
+        if op[0] == "J":
+            other = (a[0], 1 - a[1])
+            return op_of(other) == op
+        return True
+
+    def hb(prev_actor, prev_time, me):
+        return prev_time <= clock[me][idx[prev_actor]]
+
+    def access(a, key, nbytes, write, expect=None):
+        me = clock[a]
+        me[idx[a]] += 1
+        lw = last_write.get(key)
+        if write:
+            if lw is not None and lw[0] != a:
+                assert hb(lw[0], lw[1], a), f"write-write race on {key}: {lw[0]} vs {a}"
+            for ra, t in reads.get(key, []):
+                if ra != a:
+                    assert hb(ra, t, a), f"read-write race on {key}: {ra} read, {a} wrote"
+            last_write[key] = (a, me[idx[a]], nbytes, expect)
+            reads[key] = []
+        else:
+            if expect is not None:
+                assert lw is not None, f"{a} reads {key} before anyone wrote it"
+                assert (lw[0][0], lw[3]) == expect, (
+                    f"{a} expected {expect} at {key}, found round {lw[3]} of rank {lw[0][0]}")
+                assert nbytes <= lw[2], f"{a} reads {nbytes} B of {key}, only {lw[2]} written"
+            if lw is not None and lw[0] != a:
+                assert hb(lw[0], lw[1], a), f"read of {key} not ordered after its write"
+            reads.setdefault(key, []).append((a, me[idx[a]]))
+
     while True:
-        runnable = []
-        for r in range(n):
-            if pc[r] >= len(progs[r]):
-                continue
-            op = progs[r][pc[r]]
-            if op[0] == "A":
-                v, _ = flags.get((op[1], op[2]), (0, None))
-                if not geq(v, op[3]):
-                    continue
-            runnable.append(r)
+        runnable = [a for a in actors if ready(a)]
         if not runnable:
-            stuck = [(r, progs[r][pc[r]]) for r in range(n) if pc[r] < len(progs[r])]
+            stuck = [(a, op_of(a)) for a in actors if op_of(a) is not None]
             assert not stuck, f"deadlock: {stuck[:4]}"
             return
-        r = rng.choice(runnable)
+        a = rng.choice(runnable)
         for _ in range(rng.randint(1, burst)):
-            if pc[r] >= len(progs[r]):
+            if not ready(a):
                 break
-            op = progs[r][pc[r]]
-            me = clock[r]
+            op = op_of(a)
+            me = clock[a]
+            r = a[0]
             if op[0] == "A":
-                v, c = flags.get((op[1], op[2]), (0, None))
-                if not geq(v, op[3]):
-                    break
+                c = flags.get((op[1], op[2]), (0, None))[1]
                 if c is not None:
-                    for k in range(n):
+                    for k in range(m):
                         me[k] = max(me[k], c[k])
+            elif op[0] == "J":
+                other = (r, 1 - a[1])
+                joined = [max(x, y) for x, y in zip(me, clock[other])]
+                clock[a][:] = joined
+                clock[other][:] = joined
+                pc[other] += 1
             elif op[0] == "S":
-                me[r] += 1
+                me[idx[a]] += 1
                 prev = flags.get((r, op[1]), (0, None))[0]
                 assert geq(op[2], prev), f"rank {r} flag {op[1]} went backwards"
                 flags[(r, op[1])] = (op[2], list(me))
             elif op[0] == "W":
-                me[r] += 1
-                _, off, nbytes, rnd = op
-                lw = last_write.get(off)
-                if lw is not None and lw[0] != r:
-                    assert lw[1] <= me[lw[0]], f"write-write race at {off} ({lw[0]} vs {r})"
-                for rr, t in reads.get(off, []):
-                    if rr != r:
-                        assert t <= me[rr], f"read-write race at {off}: rank {rr} read, {r} wrote"
-                last_write[off] = (r, me[r], nbytes, rnd)
-                reads[off] = []
-                starts.append(off)
-            else:  # R
-                me[r] += 1
-                _, off, nbytes, writer, rnd = op
-                lw = last_write.get(off)
-                assert lw is not None, f"rank {r} reads {off} before anyone wrote it"
-                assert (lw[0], lw[3]) == (writer, rnd), (
-                    f"rank {r} expected round {rnd} of rank {writer} at {off}, "
-                    f"found round {lw[3]} of rank {lw[0]}")
-                assert nbytes <= lw[2], f"rank {r} reads {nbytes} B, only {lw[2]} written"
-                assert lw[1] <= me[lw[0]], f"read of {off} not ordered after its write"
-                reads.setdefault(off, []).append((r, me[r]))
-            pc[r] += 1
+                access(a, ("shm", op[1]), op[2], True, op[3])
+            elif op[0] == "R":
+                access(a, ("shm", op[1]), op[2], False, (op[3], op[4]))
+            elif op[0] == "UW":
+                access(a, ("user", r, op[1]), op[2], True)
+            elif op[0] == "UR":
+                access(a, ("user", r, op[1]), op[2], False)
+            else:
+                raise AssertionError(op)
+            pc[a] += 1
 
 
 def programs(n, ops, slice_bytes, transport):
@@ -153,16 +180,27 @@ def test_protocol_multi_gpu_world_sizes(n):
         simulate(progs, seed, burst=8)
 
 
-def test_model_catches_a_broken_schedule():
-    """Sanity: drop one rank's STAGED wait and the checker must object."""
-    progs = programs(3, [("allreduce", 30_000, 0)], 4096, "ce")
-    victim = progs[1]
-    i = next(k for k, op in enumerate(victim) if op[0] == "A" and op[2] == 0)
-    broken = [victim[:i] + victim[i + 1:] if r == 1 else p for r, p in enumerate(progs)]
+@pytest.mark.parametrize("flag", [0, 1])
+def test_model_catches_a_broken_schedule(flag):
+    """Sanity: drop every wait of one rank on one flag (STAGED or REDUCED)
+    and the checker must object.  (A third flag, GATHERED, was dropped from
+    the protocol after this checker showed its waits were implied.)"""
+    progs = programs(3, [("allreduce", 60_000, 0), ("allreduce", 60_000, 0)], 4096, "ce")
+    lanes = progs[1]
+    broken_lanes = [[op for op in lane if not (op[0] == "A" and op[2] == flag)] for lane in lanes]
+    assert broken_lanes != lanes
+    broken = [broken_lanes if r == 1 else p for r, p in enumerate(progs)]
     failures = 0
-    for seed in range(40):
+    for seed in range(60):
         try:
             simulate(broken, seed)
         except AssertionError:
             failures += 1
     assert failures > 0
+
+
+def test_result_via_copy_engine_variant(monkeypatch):
+    monkeypatch.setenv("FMX_RESULT_VIA_CE", "1")
+    progs = programs(4, SEQUENCES["mixed"], 4096, "ce")
+    for seed in range(8):
+        simulate(progs, seed)
