@@ -107,6 +107,56 @@ def step_roofline(n, per_gpu, s_bytes, t_s, peaks):
             "peak_source": "profiles/r01_probe/bw.jsonl (cudaMemcpyAsync pinned, best of 5)"}
 
 
+# SM zero-copy store peak to mapped host memory (profiles/r01_probe/bw.jsonl, "zc"
+# write_gbs, any grid >= 8 CTAs) - the bound of the reduce kernel's result store.
+ZC_WRITE_PEAK = 52.7
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def kernel_roofline(args, n, s_bytes, kernel_ms, kernel_count):
+    """Roofline of the dominant kernel, fmx_reduce_kernel, from its live
+    CUDA-event durations (lane stream) over the timed region.
+
+    Algorithmic bytes of all reduce launches of one allreduce (all ranks):
+    HBM reads n*S (CE: n-1 contributions from scratch + own piece), HBM
+    write S, and - unless the result slot is written by the copy engine
+    (FMX_RESULT_VIA_CE=1) - a zero-copy store of S over PCIe, which is then
+    the binding resource.  ZC transport: (n-1)*S cross PCIe as loads."""
+    if kernel_count == 0:
+        return None
+    steps = args.steps
+    t_launch = kernel_ms / kernel_count / 1e3          # mean launch duration, s
+    per_launch = lambda total: total * steps / kernel_count
+    via_ce = os.environ.get("FMX_RESULT_VIA_CE", "0") not in ("", "0")
+    zc = args.transport == "zc"
+    traffic = None
+    try:
+        traffic = json.load(open(TRAFFIC_PATH)).get("fmx_reduce_kernel_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    if zc:
+        link = per_launch((n - 1) * s_bytes + s_bytes)
+        return {"kernel": "fmx_reduce_kernel", "bound": "host_link", "achieved": link / t_launch / 1e9,
+                "peak": LINK_PEAK_FALLBACK["bidir"], "unit": "GB/s",
+                "frac": link / t_launch / 1e9 / LINK_PEAK_FALLBACK["bidir"], "traffic": traffic,
+                "launch_us": t_launch * 1e6, "launches": kernel_count,
+                "peak_source": "measured CE bidirectional (profiles/r01_probe/bw.jsonl)"}
+    if via_ce:
+        hbm = per_launch((n + 1) * s_bytes)
+        peak = json.load(open(PEAKS_PATH))["hbm_gbs"] if os.path.exists(PEAKS_PATH) else 6552.3
+        return {"kernel": "fmx_reduce_kernel", "bound": "hbm", "achieved": hbm / t_launch / 1e9,
+                "peak": peak, "unit": "GB/s", "frac": hbm / t_launch / 1e9 / peak,
+                "traffic": traffic, "launch_us": t_launch * 1e6, "launches": kernel_count,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    link = per_launch(s_bytes)
+    return {"kernel": "fmx_reduce_kernel", "bound": "host_link",
+            "achieved": link / t_launch / 1e9, "peak": ZC_WRITE_PEAK, "unit": "GB/s",
+            "frac": link / t_launch / 1e9 / ZC_WRITE_PEAK, "traffic": traffic,
+            "hbm_bytes_per_launch": per_launch((n + 1) * s_bytes),
+            "launch_us": t_launch * 1e6, "launches": kernel_count,
+            "peak_source": "measured SM zero-copy store peak (profiles/r01_probe/bw.jsonl)"}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -163,10 +213,13 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- rank body
 
 
-def rank_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_local: int,
-              barrier_comm=None):
-    """One instance rank: bind, join, warm up, time K device-resident
-    allreduces, then K end-to-end (host buffer) allreduces."""
+def rank_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_local: int):
+    """One instance rank: bind, join, warm up, then time K allreduces three
+    ways - (1) device-resident gradient (`value`), (2) host-resident
+    gradient in the rank's registered host buffer, read and written over the
+    host link by fmx_allreduce_host (`e2e`), (3) host gradient copied H2D,
+    allreduced on the device, copied D2H (`e2e_device_buffers`).  Every
+    allreduce uses DDP's convention (divide by world size, then sum)."""
     import torch
 
     from paper_2511_09143_b200 import instance as inst_mod
@@ -174,61 +227,72 @@ def rank_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_lo
 
     gpu_id, inst_id = cfg["instances"][rank]
     inst = inst_mod.bind(gpu_id, inst_id, cfg["profiles"][rank], mode=inst_mode, device=gpu_local)
+    count = cfg["count"]
+    tdt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
+    esz = 4 if cfg["dtype"] == "f32" else 2
     comm = init_process_group(None, rank, job_key, instance=inst, nranks=n,
                               transport=cfg["transport"], slice_bytes=cfg["slice_bytes"],
-                              timeout_s=300)
+                              host_bytes=count * esz if cfg["e2e"] else 0, timeout_s=300)
     stream = inst.stream
-    tdt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
-    count = cfg["count"]
     gen = torch.Generator(device="cpu").manual_seed(1234 + rank)
     host = (torch.randn(count, generator=gen) * (1e-3 if cfg["dtype"] == "f32" else 1e-2)).to(tdt)
     with torch.cuda.stream(stream):
         buf = host.to(f"cuda:{gpu_local}")
-        base = buf.clone()
     out = {"rank": rank}
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
-    def timed(k: int, e2e: bool, pinned_in=None, pinned_out=None):
+    def timed(k: int, step, kernel_timing: bool = False):
         comm.barrier(300)
         torch.cuda.synchronize()
         comm.barrier(300)
         l0 = comm.kernel_launches()
+        comm.set_kernel_timing(kernel_timing)
         ev0.record(stream)
         with torch.cuda.stream(stream):
             for _ in range(k):
-                if e2e:
-                    buf.copy_(pinned_in, non_blocking=True)
-                    comm.allreduce(buf, stream=stream)
-                    pinned_out.copy_(buf, non_blocking=True)
-                else:
-                    comm.allreduce(buf, stream=stream)
+                step()
         ev1.record(stream)
         ev1.synchronize()
         comm.barrier(300)
+        if kernel_timing:
+            out["kernel_ms"], out["kernel_count"] = comm.kernel_time()
+            comm.set_kernel_timing(False)
         return ev0.elapsed_time(ev1), comm.kernel_launches() - l0
 
-    # warm-up (untimed)
-    with torch.cuda.stream(stream):
-        for _ in range(cfg["warmup"]):
-            comm.allreduce(buf, stream=stream)
+    def device_step():
+        comm.allreduce(buf, op="avg", stream=stream)
+
+    for _ in range(cfg["warmup"]):
+        device_step()
     torch.cuda.synchronize()
-    ms, launches = timed(cfg["steps"], False)
-    out["ms_total"], out["launches"] = ms, launches
+    out["ms_total"], out["launches"] = timed(cfg["steps"], device_step, kernel_timing=True)
     if cfg["e2e"]:
+        # (2) registered host buffer: the gradient lives in pinned host memory
+        region = comm.host_buffer()[:count * esz].view(tdt)
+        region.copy_(host)
+
+        def host_step():
+            comm.allreduce_host(region, op="avg", stream=stream)
+
+        for _ in range(cfg["warmup"]):
+            host_step()
+        torch.cuda.synchronize()
+        out["ms_total_e2e"], out["launches_e2e"] = timed(cfg["steps"], host_step)
+        out["e2e_digest"] = int(region.view(torch.int32 if esz == 4 else torch.int16)
+                                .to(torch.int64).sum().item())
+        # (3) device buffers with explicit H2D / D2H copies of the gradient
         pin_in = host.pin_memory()
         pin_out = torch.empty_like(pin_in).pin_memory()
-        with torch.cuda.stream(stream):
+
+        def copy_step():
             buf.copy_(pin_in, non_blocking=True)
-            comm.allreduce(buf, stream=stream)
+            comm.allreduce(buf, op="avg", stream=stream)
             pin_out.copy_(buf, non_blocking=True)
+
+        with torch.cuda.stream(stream):
+            copy_step()
         torch.cuda.synchronize()
-        ms_e2e, l_e2e = timed(cfg["steps"], True, pin_in, pin_out)
-        out["ms_total_e2e"], out["launches_e2e"] = ms_e2e, l_e2e
-        # parity spot check of the e2e result against the device path: every
-        # rank must hold the same bytes
-        out["e2e_digest"] = int(pin_out.view(torch.int32 if tdt == torch.float32 else torch.int16)
-                                .to(torch.int64).sum().item())
-    del base
+        out["ms_total_e2e_dev"], _ = timed(cfg["steps"], copy_step)
     comm.destroy()
     return out
 
@@ -419,16 +483,21 @@ def run_ours(args) -> dict | None:
         raise RuntimeError(f"rank {errors[0][0]} failed: {errors[0][1]!r}") from errors[0][1]
     local_max = max(r["ms_total"] for r in results.values())
     local_max_e2e = max(r.get("ms_total_e2e", 0.0) for r in results.values())
+    local_max_e2e_dev = max(r.get("ms_total_e2e_dev", 0.0) for r in results.values())
     launches = sum(r["launches"] for r in results.values())
+    kernel_ms = sum(r.get("kernel_ms", 0.0) for r in results.values())
+    kernel_count = sum(r.get("kernel_count", 0) for r in results.values())
     digests = {r.get("e2e_digest") for r in results.values()}
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([local_max, local_max_e2e, float(launches)], dtype=torch.float64)
+        t = torch.tensor([local_max, local_max_e2e, float(launches), kernel_ms, float(kernel_count),
+                          local_max_e2e_dev], dtype=torch.float64)
         mx = t.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         sm = t.clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        local_max, local_max_e2e, launches = mx[0].item(), mx[1].item(), int(sm[2].item())
+        local_max, local_max_e2e, local_max_e2e_dev = mx[0].item(), mx[1].item(), mx[5].item()
+        launches, kernel_ms, kernel_count = int(sm[2].item()), sm[3].item(), int(sm[4].item())
         if grank != 0:
             dist.destroy_process_group()
             return None
@@ -445,7 +514,8 @@ def run_ours(args) -> dict | None:
         "n_gpus": gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "float32" if args.dtype == "f32" else "bfloat16",
-        "data": "synthetic (seeded N(0,1)*1e-3 gradient per rank)",
+        "data": "synthetic (seeded N(0,1)*1e-3 gradient per rank); op = DDP mean "
+                "(divide by world size, then rank-order fp32 sum)",
         "config": {"workload": f"ResNet-50-sized gradient allreduce ({args.count} "
                                f"{args.dtype}) across {args.ranks_per_gpu} 1g instances per "
                                f"B200 x {gpus} (BASELINE configs[1] comm step)",
@@ -454,16 +524,26 @@ def run_ours(args) -> dict | None:
                    "transport": args.transport, "l2": "inputs > L2 (7 x 102 MB per GPU)",
                    "rank_order": "fm_select round-robin"},
         "busbw_gbs": s_bytes / t_step / 1e9 * 2 * (n - 1) / n,
+        "roofline": kernel_roofline(args, n, s_bytes, kernel_ms, kernel_count),
         "step_roofline": step_roofline(n, per_gpu, s_bytes, t_step, peaks),
         "gpu_launches": launches,
         "clocks": clocks,
     }
     if not args.no_e2e:
         t_e2e = local_max_e2e / 1e3 / args.steps
+        t_dev = local_max_e2e_dev / 1e3 / args.steps
         line["e2e"] = {"value": s_bytes / t_e2e / 1e9, "unit": line["unit"],
                        "ms_per_step": t_e2e * 1e3,
+                       "api": "ShmCommunicator.allreduce_host -> fmx_allreduce_host (C ABI): "
+                              "every rank's gradient in its registered pinned host buffer; the "
+                              "GPUs read the inputs (H2D) and write the results (D2H) in the "
+                              "timed region",
                        "h2d_bytes_per_step": n * s_bytes, "d2h_bytes_per_step": n * s_bytes,
                        "ranks_agree": len(digests) == 1}
+        line["e2e_device_buffers"] = {
+            "value": s_bytes / t_dev / 1e9, "unit": line["unit"], "ms_per_step": t_dev * 1e3,
+            "api": "pinned host -> device copy, ShmCommunicator.allreduce, device -> pinned host",
+            "h2d_bytes_per_step": n * s_bytes, "d2h_bytes_per_step": n * s_bytes}
     return line
 
 
@@ -478,13 +558,13 @@ def run_cpu_reference(count: int, n: int, dtype: str, steps: int, warmup: int,
     bufs = [orc.synthetic_gradient(r, count, dt) for r in range(n)]
     shm = orc.ShmAllreduce(n, count, dt, nthreads)
     for _ in range(warmup):
-        shm(bufs)
+        shm(bufs, orc.OP_PREDIV_SUM, float(n))
     times = []
     t_end = time.perf_counter() + (seconds or 0)
     k = 0
     while k < steps or (seconds and time.perf_counter() < t_end):
         t0 = time.perf_counter()
-        shm(bufs)
+        shm(bufs, orc.OP_PREDIV_SUM, float(n))
         times.append(time.perf_counter() - t0)
         k += 1
     t = sum(times) / len(times)

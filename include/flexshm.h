@@ -127,10 +127,12 @@ int fmx_restore_bus_id(const char* label, char* out);
  * pinned and device-mapped (cudaHostRegister Mapped|Portable) in the calling
  * thread's current CUDA context.  slice_bytes = bytes per (owner,
  * contributor) pipeline slot, 0 = default; nslots must be 2 (double
- * buffering) or 0 = default.  timeout_s bounds every bootstrap wait. */
+ * buffering) or 0 = default.  host_bytes = size of every rank's registered
+ * host buffer (fmx_host_buffer), 0 = none.  Rank 0's slice_bytes / host_bytes
+ * win.  timeout_s bounds every bootstrap wait. */
 int fmx_comm_init(fmx_comm_t* comm, const char* job_key, int nranks, int rank,
                   const fmx_peer_info* self, int mig_aware, size_t slice_bytes, int nslots,
-                  int transport, double timeout_s);
+                  size_t host_bytes, int transport, double timeout_s);
 
 /* In-place allowed (send == recv).  count elements of dtype; op/factor per
  * enum fmx_op.  Enqueued on `stream` (a cudaStream_t); returns immediately. */
@@ -140,6 +142,21 @@ int fmx_allreduce(fmx_comm_t comm, const void* send, void* recv, size_t count, i
 /* Root's send buffer -> every rank's recv buffer (bit copy). */
 int fmx_broadcast(fmx_comm_t comm, const void* send, void* recv, size_t count, int dtype,
                   int root, void* stream);
+
+/* Registered host buffers (the NCCL user-buffer-registration idea for host
+ * memory): every rank owns a pinned, device-mapped region of host_bytes inside
+ * the segment; any rank's region can be mapped (for inspection).  */
+int fmx_host_buffer(fmx_comm_t comm, int rank, void** ptr, size_t* bytes);
+
+/* Allreduce of host-resident data, in place over every rank's region bytes
+ * [offset, offset + count*size(dtype)): the GPU reads each owner's chunk out of
+ * all regions and writes the rank-order result back into all regions - no
+ * staging copy and no all-gather (k*S H2D + k*S D2H per GPU).  Same
+ * arithmetic and op/factor semantics as fmx_allreduce.  The caller must have
+ * finished writing its region before the call and may read it after the
+ * stream has drained. */
+int fmx_allreduce_host(fmx_comm_t comm, size_t offset, size_t count, int dtype, int op,
+                       float factor, void* stream);
 
 /* Host-side barrier over the communicator (SHM counter; no GPU work). */
 int fmx_barrier(fmx_comm_t comm, double timeout_s);
@@ -157,6 +174,12 @@ int fmx_comm_config(fmx_comm_t comm, size_t* slice_bytes, int* transport, size_t
 /* Snapshot of every rank's flag counters (nranks x 4: STAGED, REDUCED,
  * BC_STAGED, BC_DONE), read from host memory - for hang diagnosis. */
 int fmx_comm_flags(fmx_comm_t comm, uint32_t* out, int cap);
+/* Live timing of the reduction kernel: with timing on, every reduce launch
+ * is bracketed by CUDA events on the lane stream it runs on; kernel_time
+ * returns the summed device time and the number of timed launches since
+ * timing was (re)enabled.  Used by bench.py for the per-kernel roofline. */
+int fmx_comm_set_timing(fmx_comm_t comm, int on);
+int fmx_comm_kernel_time(fmx_comm_t comm, double* total_ms, uint64_t* count);
 /* Number of device kernels this communicator has launched so far. */
 int fmx_comm_kernel_launches(fmx_comm_t comm, uint64_t* launches);
 
@@ -164,7 +187,7 @@ int fmx_comm_kernel_launches(fmx_comm_t comm, uint64_t* launches);
 
 /* Write the schedule `rank` of an `nranks` communicator would enqueue for a
  * sequence of `nops` collectives (kinds[i]: 0 allreduce, 1 broadcast with
- * roots[i]) as text: one line per SHM access ("W off bytes round", "R off
+ * roots[i], 2 host-buffer allreduce) as text: one line per SHM access ("W off bytes round", "R off
  * bytes writer round") or flag op ("S flag value", "A rank flag value"),
  * "#" between collectives.  Used to model-check the protocol for any world
  * size on a CPU (tests/test_protocol_model.py).  *used = bytes needed. */

@@ -45,9 +45,10 @@ MAX_RANKS = 64
 # Every symbol include/flexshm.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "fmx_check_peer", "fmx_validate_peers", "fmx_topology", "fmx_restore_bus_id",
-    "fmx_comm_init", "fmx_allreduce", "fmx_broadcast", "fmx_barrier", "fmx_comm_destroy",
+    "fmx_comm_init", "fmx_allreduce", "fmx_broadcast", "fmx_host_buffer", "fmx_allreduce_host", "fmx_barrier", "fmx_comm_destroy",
     "fmx_comm_abort", "fmx_comm_rank", "fmx_comm_count", "fmx_comm_peer", "fmx_comm_config",
-    "fmx_comm_kernel_launches", "fmx_comm_flags", "fmx_trace_plan", "fmx_last_error", "fmx_dup_ranks",
+    "fmx_comm_kernel_launches", "fmx_comm_flags", "fmx_comm_set_timing", "fmx_comm_kernel_time",
+    "fmx_trace_plan", "fmx_last_error", "fmx_dup_ranks",
     "fmx_abi_version",
 )
 
@@ -98,7 +99,9 @@ def lib() -> ctypes.CDLL:
         "fmx_topology": [P(PeerInfoC), c_int, ctypes.c_char_p, ctypes.c_char_p, P(c_int), P(c_int)],
         "fmx_restore_bus_id": [ctypes.c_char_p, ctypes.c_char_p],
         "fmx_comm_init": [P(c_void), ctypes.c_char_p, c_int, c_int, P(PeerInfoC), c_int, c_size,
-                          c_int, c_int, c_double],
+                          c_int, c_size, c_int, c_double],
+        "fmx_host_buffer": [c_void, c_int, P(c_void), P(c_size)],
+        "fmx_allreduce_host": [c_void, c_size, c_size, c_int, c_int, c_float, c_void],
         "fmx_allreduce": [c_void, c_void, c_void, c_size, c_int, c_int, c_float, c_void],
         "fmx_broadcast": [c_void, c_void, c_void, c_size, c_int, c_int, c_void],
         "fmx_barrier": [c_void, c_double],
@@ -110,6 +113,8 @@ def lib() -> ctypes.CDLL:
         "fmx_comm_config": [c_void, P(c_size), P(c_int), P(c_size)],
         "fmx_comm_kernel_launches": [c_void, P(ctypes.c_uint64)],
         "fmx_comm_flags": [c_void, P(ctypes.c_uint32), c_int],
+        "fmx_comm_set_timing": [c_void, c_int],
+        "fmx_comm_kernel_time": [c_void, P(c_double), P(ctypes.c_uint64)],
         "fmx_trace_plan": [c_int, c_int, c_int, c_size, c_int, P(c_int), P(c_size), P(c_int),
                            P(c_int), ctypes.c_char_p, c_size, P(c_size)],
         "fmx_dup_ranks": [P(c_int), P(c_int)],
@@ -132,7 +137,8 @@ def trace_plan(nranks: int, rank: int, ops: list[tuple], slice_bytes: int = 4096
     """Schedule text of `rank` for ops = [("allreduce", count, dtype) |
     ("broadcast", count, dtype, root)] (see fmx_trace_plan)."""
     n = len(ops)
-    kinds = (ctypes.c_int * max(1, n))(*[0 if o[0] == "allreduce" else 1 for o in ops])
+    code = {"allreduce": 0, "broadcast": 1, "allreduce_host": 2}
+    kinds = (ctypes.c_int * max(1, n))(*[code[o[0]] for o in ops])
     counts = (ctypes.c_size_t * max(1, n))(*[o[1] for o in ops])
     dtypes = (ctypes.c_int * max(1, n))(*[o[2] for o in ops])
     roots = (ctypes.c_int * max(1, n))(*[o[3] if len(o) > 3 else 0 for o in ops])

@@ -113,6 +113,39 @@ class ShmCommunicator:
         _lib.check(rc, "fmx_broadcast")
         return tensor
 
+    def host_buffer(self, rank: int | None = None):
+        """This rank's (or `rank`'s) registered host buffer as a uint8 CPU
+        tensor over the pinned, device-mapped SHM region (no copy)."""
+        import numpy as np
+        import torch
+        ptr, nbytes = ctypes.c_void_p(), ctypes.c_size_t()
+        _lib.check(_lib.lib().fmx_host_buffer(self._h, self.rank if rank is None else rank,
+                                              ctypes.byref(ptr), ctypes.byref(nbytes)))
+        if nbytes.value == 0:
+            raise ValueError("communicator was created with host_bytes=0")
+        arr = np.ctypeslib.as_array((ctypes.c_uint8 * nbytes.value).from_address(ptr.value))
+        return torch.from_numpy(arr)
+
+    def allreduce_host(self, tensor, op: str = "sum", factor: float | None = None, stream=None):
+        """In-place allreduce of `tensor`, a view into this rank's host_buffer()
+        (float32 / bfloat16): inputs are read and results written over the host
+        link directly, no device copy of the buffer is made."""
+        self._alive()
+        base = self.host_buffer()
+        offset = tensor.data_ptr() - base.data_ptr()
+        if tensor.is_cuda or not tensor.is_contiguous() or offset < 0 or \
+                offset + tensor.numel() * tensor.element_size() > base.numel():
+            raise ValueError("tensor must be a contiguous view into host_buffer()")
+        if op == "avg":
+            op, factor = "prediv", float(self.size)
+        if op not in OPS:
+            raise ValueError(f"unknown op {op!r}")
+        factor = 1.0 if factor is None else factor
+        rc = _lib.lib().fmx_allreduce_host(self._h, offset, tensor.numel(), _dtype_code(tensor),
+                                           OPS[op], ctypes.c_float(factor), self._stream(stream))
+        _lib.check(rc, "fmx_allreduce_host")
+        return tensor
+
     def barrier(self, timeout_s: float = 120.0) -> None:
         self._alive()
         _lib.check(_lib.lib().fmx_barrier(self._h, timeout_s), "fmx_barrier")
@@ -121,6 +154,16 @@ class ShmCommunicator:
         v = ctypes.c_uint64()
         _lib.check(_lib.lib().fmx_comm_kernel_launches(self._h, ctypes.byref(v)))
         return v.value
+
+    def set_kernel_timing(self, on: bool) -> None:
+        """Bracket every reduction kernel with CUDA events (on its own stream)."""
+        _lib.check(_lib.lib().fmx_comm_set_timing(self._h, 1 if on else 0))
+
+    def kernel_time(self) -> tuple[float, int]:
+        """(summed device ms, launches) of the reduction kernels timed so far."""
+        ms, n = ctypes.c_double(), ctypes.c_uint64()
+        _lib.check(_lib.lib().fmx_comm_kernel_time(self._h, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
 
     def flags(self) -> list[list[int]]:
         """Every rank's [STAGED, REDUCED, BC_STAGED, BC_DONE] counters."""
@@ -147,7 +190,7 @@ class ShmCommunicator:
 def init_process_group(decision: AllocationDecision | None, rank: int, job_key: str, *,
                        instance=None, peer: PeerInfo | None = None, nranks: int | None = None,
                        mig_aware: bool = True, slice_bytes: int = 0, transport: str = "auto",
-                       timeout_s: float = 120.0) -> ShmCommunicator:
+                       host_bytes: int = 0, timeout_s: float = 120.0) -> ShmCommunicator:
     """Join the communicator of `decision` as `rank` (collective, blocking).
 
     The published identity is `peer` if given, else `instance.peer_info`.
@@ -170,7 +213,7 @@ def init_process_group(decision: AllocationDecision | None, rank: int, job_key: 
     me = _lib.peer_to_c(peer.rank, peer.pcie_bus_id, peer.mig_id, peer.host_hash, peer.pid_hash)
     h = ctypes.c_void_p()
     rc = _lib.lib().fmx_comm_init(ctypes.byref(h), job_key.encode(), n, rank, ctypes.byref(me),
-                                  1 if mig_aware else 0, slice_bytes, 0,
+                                  1 if mig_aware else 0, slice_bytes, 0, host_bytes,
                                   _lib.TRANSPORTS[transport], timeout_s)
     _lib.check(rc, "fmx_comm_init")
     peers = []

@@ -99,9 +99,14 @@ struct fmx_comm {
   int64_t barrier_gen = 0;
   char* scratch = nullptr;  // CE transport: n * slice_bytes of HBM
   cudaStream_t lane[2] = {nullptr, nullptr};
+  cudaEvent_t ev[8] = {};  // intra-rank lane sync (see the kEv* ids)
   cudaEvent_t fork = nullptr, joined[2] = {nullptr, nullptr};
   bool result_via_ce = false;  // CE transport: result slot by copy engine, not SM stores
   bool copy2d = true;          // coalesce regular copy runs into cudaMemcpy2DAsync
+  // live kernel timing (fmx_comm_set_timing): event pairs around every reduce
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
+  size_t timed_used = 0;
   cudaEvent_t done = nullptr;
   bool has_done = false;
   uint64_t launches = 0;
@@ -118,6 +123,7 @@ struct fmx_comm {
   size_t bc_slot_off(uint32_t R) const {
     return L.bc_off + (size_t)(R % nslots) * nranks * slice_bytes;
   }
+  size_t user_region_off(int r) const { return L.user_off + (size_t)r * L.user_bytes; }
   // host (dev=false) or device (dev=true) address of a segment offset
   char* at(bool dev, size_t off) const { return (dev ? dbase : base) + off; }
   CUdeviceptr flag_dev(int r, int f) const {
@@ -188,6 +194,11 @@ struct Sink {
   virtual int wait_peers(int lane, int flag, uint32_t v, int skip) = 0;
   virtual int wait_rank(int lane, int q, int flag, uint32_t v) = 0;
   virtual int d2d(int lane, void* dst, const void* src, size_t bytes, Annot from, Annot to) = 0;
+  // intra-rank lane ordering through CUDA events (enqueue-order semantics)
+  virtual int record(int lane, int ev) = 0;
+  virtual int wait_event(int lane, int ev) = 0;
+  // host-program accesses to SHM around a collective (trace only)
+  virtual int host_access(int lane, const Annot& a, bool write) { return FMX_OK; }
 };
 
 int grid_for(size_t work_items, int threads, int cap) {
@@ -251,6 +262,19 @@ class CudaSink final : public Sink {
     const ReduceArgs& a = r.args;
     if (a.len == 0) return FMX_OK;
     cudaStream_t s = c_->lane[lane];
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (c_->timing) {
+      if (c_->timed_used == c_->timed.size()) {
+        cudaEvent_t x, y;
+        FMX_CUDA(cudaEventCreate(&x));
+        FMX_CUDA(cudaEventCreate(&y));
+        c_->timed.push_back({x, y});
+      }
+      t0 = c_->timed[c_->timed_used].first;
+      t1 = c_->timed[c_->timed_used].second;
+      c_->timed_used++;
+      FMX_CUDA(cudaEventRecord(t0, s));
+    }
     constexpr int kThreads = 256, kU = 2;
     const int V = r.dtype == FMX_FLOAT32 ? 4 : 8;
     if (r.aligned) {
@@ -267,6 +291,7 @@ class CudaSink final : public Sink {
         fmx_reduce_scalar_kernel<__nv_bfloat16><<<g, kThreads, 0, s>>>(a);
     }
     FMX_CUDA(cudaGetLastError());
+    if (t1) FMX_CUDA(cudaEventRecord(t1, s));
     c_->launches++;
     return FMX_OK;
   }
@@ -310,6 +335,16 @@ class CudaSink final : public Sink {
 
   int d2d(int lane, void* dst, const void* src, size_t bytes, Annot, Annot) override {
     FMX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c_->lane[lane]));
+    return FMX_OK;
+  }
+
+  int record(int lane, int ev) override {
+    FMX_CUDA(cudaEventRecord(c_->ev[ev], c_->lane[lane]));
+    return FMX_OK;
+  }
+
+  int wait_event(int lane, int ev) override {
+    FMX_CUDA(cudaStreamWaitEvent(c_->lane[lane], c_->ev[ev], 0));
     return FMX_OK;
   }
 
@@ -379,6 +414,14 @@ class TraceSink final : public Sink {
     user(lane, to, true);
     return FMX_OK;
   }
+  int record(int lane, int ev) override { return line("%d E %d %d\n", lane, ev, ++seq_[ev]); }
+  int wait_event(int lane, int ev) override {
+    return seq_[ev] ? line("%d X %d %d\n", lane, ev, seq_[ev]) : FMX_OK;
+  }
+  int host_access(int lane, const Annot& a, bool write) override {
+    shm(lane, a, write);
+    return FMX_OK;
+  }
   int join() { return line("J\n"); }
   int nranks = 0;
 
@@ -404,6 +447,7 @@ class TraceSink final : public Sink {
     return FMX_OK;
   }
   std::string* out_;
+  int seq_[8] = {};
 };
 
 struct Geometry {
@@ -433,18 +477,29 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype) {
 Annot ubuf(size_t off_bytes, size_t bytes) { return Annot{(int64_t)off_bytes, bytes, -1, 0}; }
 
 // Reduce-scatter + all-gather through the segment, pipelined in rounds on two
-// lanes.  Round R uses slot R % 2.  Hazards and why each wait exists:
-//  lane 0, stage(R) into in[R%2][o][me]: the slot was last read by owner o's
-//      reduce(R-2)                        -> wait REDUCED[o] >= R-1 (all o)
-//  lane 1, reduce(R) reads in[R%2][me][q]  -> wait STAGED[q]  >= R+1 (all q)
-//          and writes out[R%2][me], last read by every q's gather(R-2): implied,
-//          my gather(R-1) waited REDUCED[q] >= R, and q's lane 1 runs
-//          gather(R-2) before reduce(R-1) (the model checker confirms no
-//          extra flag is needed)
-//  lane 1, gather(R) reads out[R%2][q]     -> wait REDUCED[q] >= R+1 (all q)
-//  in place (send == recv): gather(R) overwrites pieces of round R of the
-//      other chunks; my stage(R) read them first because every owner's
-//      reduce(R) waited for my STAGED >= R+1.
+// lanes.  Round R uses slot R % 2.
+//
+// Enqueue order is itself a valid single-stream schedule: every wait (flag or
+// event) points at work enqueued earlier, by this rank or by peers that enqueue
+// in the same order.  So however the driver maps the two lane streams onto
+// hardware queues - even one shared FIFO - nothing can deadlock; separate queues
+// only add overlap.  Lane 0 never waits on a flag: only on events of lane 1.
+// The model checker checks both the two-lane and the merged single-FIFO reading.
+//
+// Hazards and the wait that covers each:
+//  stage(R) into in[R%2][o][me], last read by every owner's reduce(R-2):
+//      lane-1 event recorded after my wait REDUCED[*] >= R-1 (round R-2 reduced
+//      everywhere); rounds of an earlier collective are covered by the fork.
+//  reduce(R) reads in[R%2][me][q]          -> wait STAGED[q] >= R+1
+//  reduce(R) writes out[R%2][me], last read by every q's gather(R-2): my
+//      gather(R-1) waited REDUCED[q] >= R, and q's lane 1 runs gather(R-2)
+//      before reduce(R-1).
+//  gather(R) reads out[R%2][q]             -> wait REDUCED[q] >= R+1
+//  in place: gather(R) overwrites pieces of round R of other chunks; my
+//      stage(R) read them first, because every owner's reduce(R) waited for my
+//      STAGED >= R+1.
+enum { kEvSlotFree = 0 };  // + slot: lane 1 -> lane 0, "slot reusable"
+
 int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
                    int op, float factor, bool aligned) {
   const int n = c->nranks, me = c->rank;
@@ -454,10 +509,11 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
   int rc;
   const uint32_t R0 = c->ar_round;
 
-  // lane 0: stage every round as soon as its slot is free
-  for (uint32_t j = 0; j < g.rounds; ++j) {
+  auto stage = [&](uint32_t j) -> int {
     const uint32_t R = R0 + j;
-    if (R >= 2 && (rc = k.wait_peers(kLaneStage, kReduced, R - 1, me))) return rc;
+    // slot R%2 was read by round R-2's reductions; within this collective the
+    // lane-1 event of round R-2's REDUCED wait says they are done
+    if (j >= 2 && (rc = k.wait_event(kLaneStage, kEvSlotFree + R % 2))) return rc;
     segs.clear();
     for (int o = 0; o < n; ++o) {
       const size_t len = o == me ? 0 : g.len(o, j);
@@ -468,12 +524,14 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
                       ubuf(g.lo(o, j) * g.esz, len * g.esz)});
     }
     if ((rc = k.copy(kLaneStage, segs, false, zc))) return rc;
-    if ((rc = k.signal(kLaneStage, kStaged, R + 1))) return rc;
-  }
+    return k.signal(kLaneStage, kStaged, R + 1);
+  };
 
-  // lane 1: reduce-scatter my chunk (ascending rank order), then all-gather
+  if ((rc = stage(0))) return rc;
   for (uint32_t j = 0; j < g.rounds; ++j) {
     const uint32_t R = R0 + j;
+    if (j + 1 < g.rounds && (rc = stage(j + 1))) return rc;  // one round ahead, lane 0
+    // lane 1: reduce-scatter my chunk in ascending rank order
     if ((rc = k.wait_peers(kLaneMain, kStaged, R + 1, me))) return rc;
     const size_t mylen = g.len(me, j);
     if (mylen) {
@@ -527,7 +585,9 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
       }
     }
     if ((rc = k.signal(kLaneMain, kReduced, R + 1))) return rc;
+    // all-gather of the other owners' results
     if ((rc = k.wait_peers(kLaneMain, kReduced, R + 1, me))) return rc;
+    if ((rc = k.record(kLaneMain, kEvSlotFree + R % 2))) return rc;  // in[R%2] reusable
     segs.clear();
     for (int q = 0; q < n; ++q) {
       const size_t len = q == me ? 0 : g.len(q, j);
@@ -540,6 +600,89 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
     if ((rc = k.copy(kLaneMain, segs, true, zc))) return rc;
   }
   c->ar_round += g.rounds;
+  return FMX_OK;
+}
+
+// Allreduce over the ranks' registered host buffers (the regions at the end of
+// the segment): in place, no staging and no all-gather.  Every input already
+// sits in host memory, so owner r copy-engines piece j of chunk r out of all n
+// regions into HBM scratch (lane 0), reduces it in rank order (lane 1) and
+// copy-engines the result into piece j of chunk r of every region (lane 1).
+// Per GPU that is k*S H2D + k*S D2H, against 2k(n-1)/n*S + k*S (+ the
+// caller's own k*S in and k*S out) for device buffers.
+constexpr uint32_t kInputTag = 1u << 31;  // trace: "input written by the host for round R"
+enum { kEvFetched = 2, kEvReduced = 4, kEvInputs = 6 };  // (+ slot 0/1)
+
+int plan_allreduce_host(fmx_comm* c, Sink& k, size_t off_bytes, size_t count, int dtype, int op,
+                        float factor) {
+  const int n = c->nranks, me = c->rank;
+  const Geometry g = allreduce_geometry(c, count, dtype);
+  const uint32_t R0 = c->ar_round, P = g.rounds;
+  const size_t sb = c->slice_bytes;
+  auto region = [&](int q, int o, uint32_t j) {
+    return c->user_region_off(q) + off_bytes + g.lo(o, j) * g.esz;
+  };
+  std::vector<PlanSeg> segs;
+  int rc;
+  // the caller wrote its whole input before the call (host program order)
+  for (int o = 0; o < n; ++o)
+    for (uint32_t j = 0; j < P; ++j)
+      if (size_t len = g.len(o, j))
+        k.host_access(kLaneMain, Annot{(int64_t)region(me, o, j), len * g.esz, me,
+                                       (R0 + j) | kInputTag}, true);
+  // every rank's inputs are in place: exchange STAGED on lane 1, release lane 0
+  if ((rc = k.signal(kLaneMain, kStaged, R0 + P))) return rc;
+  if ((rc = k.wait_peers(kLaneMain, kStaged, R0 + P, me))) return rc;
+  if ((rc = k.record(kLaneMain, kEvInputs))) return rc;
+  if ((rc = k.wait_event(kLaneStage, kEvInputs))) return rc;
+  for (uint32_t j = 0; j < P; ++j) {
+    const uint32_t R = R0 + j, slot = j % 2;
+    const size_t len = g.len(me, j);
+    char* fetch = c->scratch + (size_t)slot * n * sb;
+    char* result = c->scratch + ((size_t)2 * n + slot) * sb;
+    // lane 0: pull piece j of my chunk out of every region (scratch slot free
+    // once lane 1 finished round j-2)
+    if (j >= 2 && (rc = k.wait_event(kLaneStage, kEvReduced + slot))) return rc;
+    segs.clear();
+    for (int q = 0; q < n && len; ++q) {
+      const size_t off = region(q, me, j);
+      segs.push_back({c->at(false, off), fetch + (size_t)q * sb, len * g.esz,
+                      Annot{(int64_t)off, len * g.esz, q, R | kInputTag}, false, Annot{}});
+    }
+    if ((rc = k.copy(kLaneStage, segs, true, false))) return rc;
+    if ((rc = k.record(kLaneStage, kEvFetched + slot))) return rc;
+    // lane 1: reduce in rank order, push the result into every region
+    if ((rc = k.wait_event(kLaneMain, kEvFetched + slot))) return rc;
+    if (len) {
+      PlanReduce pr;
+      memset(&pr.args, 0, sizeof pr.args);
+      pr.dtype = dtype;
+      pr.aligned = true;
+      pr.args.nsrc = n;
+      pr.args.len = len;
+      pr.args.op = op;
+      pr.args.factor = factor;
+      pr.args.out_dev = result;
+      for (int q = 0; q < n; ++q) pr.args.src[q] = fetch + (size_t)q * sb;
+      if ((rc = k.reduce(kLaneMain, pr))) return rc;
+      segs.clear();
+      for (int q = 0; q < n; ++q) {
+        const size_t off = region(q, me, j);
+        segs.push_back({result, c->at(false, off), len * g.esz,
+                        Annot{(int64_t)off, len * g.esz, me, R}, true, Annot{}});
+      }
+      if ((rc = k.copy(kLaneMain, segs, false, false))) return rc;
+    }
+    if ((rc = k.record(kLaneMain, kEvReduced + slot))) return rc;
+  }
+  if ((rc = k.signal(kLaneMain, kReduced, R0 + P))) return rc;
+  if ((rc = k.wait_peers(kLaneMain, kReduced, R0 + P, me))) return rc;
+  // the caller then reads its whole region (host program order)
+  for (int o = 0; o < n; ++o)
+    for (uint32_t j = 0; j < P; ++j)
+      if (size_t len = g.len(o, j))
+        k.host_access(kLaneMain, Annot{(int64_t)region(me, o, j), len * g.esz, o, R0 + j}, false);
+  c->ar_round += P;
   return FMX_OK;
 }
 
@@ -613,7 +756,7 @@ extern "C" {
 
 int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
                   const fmx_peer_info* self, int mig_aware, size_t slice_bytes, int nslots,
-                  int transport, double timeout_s) {
+                  size_t host_bytes, int transport, double timeout_s) {
   if (!out || !job_key || !self) return fail(FMX_ERR_INVALID_ARG, "null argument");
   *out = nullptr;
   if (nranks < 1 || nranks > FMX_MAX_RANKS)
@@ -647,7 +790,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
       sb = std::min(kDefaultSliceCap, kSegmentBudget / per);
     }
     sb = std::max<size_t>(4096, sb / 4096 * 4096);
-    Layout L = compute_layout(nranks, c->nslots, sb);
+    Layout L = compute_layout(nranks, c->nslots, sb, host_bytes);
     shm_unlink(name.c_str());  // stale segment of a crashed job with the same key
     int fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
     if (fd < 0) {
@@ -680,6 +823,8 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
     h->ar_in_off = L.ar_in_off;
     h->ar_out_off = L.ar_out_off;
     h->bc_off = L.bc_off;
+    h->user_off = L.user_off;
+    h->user_bytes = L.user_bytes;
     h->creator_pid = (int32_t)getpid();
     h->mig_aware = mig_aware ? 1 : 0;
     snprintf(h->job_key, sizeof h->job_key, "%s", job_key);
@@ -727,7 +872,8 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   }
   Header* h = c->hdr = (Header*)c->base;
   c->slice_bytes = h->slice_bytes;
-  c->L = Layout{h->peers_off, h->flags_off, h->ar_in_off, h->ar_out_off, h->bc_off, h->total_bytes};
+  c->L = Layout{h->peers_off, h->flags_off, h->ar_in_off, h->ar_out_off, h->bc_off,
+                h->user_off, h->user_bytes, h->total_bytes};
   c->mig_aware = h->mig_aware;
 
   // publish this rank's PeerInfo
@@ -780,8 +926,10 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
     c->registered = true;
     e = cudaHostGetDevicePointer((void**)&c->dbase, c->base, 0);
   }
-  if (e == cudaSuccess && c->transport == FMX_TRANSPORT_CE)
-    e = cudaMalloc((void**)&c->scratch, (size_t)nranks * c->slice_bytes);
+  // HBM scratch: CE contributions [n] (device path) / [2][n] fetch + [2] result (host path)
+  if (e == cudaSuccess) e = cudaMalloc((void**)&c->scratch, (2 * (size_t)nranks + 2) * c->slice_bytes);
+  for (int i = 0; i < 8 && e == cudaSuccess; ++i)
+    e = cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
   for (int l = 0; l < 2 && e == cudaSuccess; ++l) {
@@ -854,6 +1002,34 @@ int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int 
   });
 }
 
+int fmx_host_buffer(fmx_comm_t c, int rank, void** ptr, size_t* bytes) {
+  if (!c || !c->base || !ptr || rank < 0 || rank >= c->nranks)
+    return fail(FMX_ERR_INVALID_ARG, "bad arguments");
+  *ptr = c->base + c->user_region_off(rank);
+  if (bytes) *bytes = c->L.user_bytes;
+  return FMX_OK;
+}
+
+int fmx_allreduce_host(fmx_comm_t c, size_t offset, size_t count, int dtype, int op, float factor,
+                       void* stream) {
+  int rc = check_comm(c);
+  if (rc) return rc;
+  if (dtype != FMX_FLOAT32 && dtype != FMX_BFLOAT16)
+    return fail(FMX_ERR_INVALID_ARG, "bad dtype %d", dtype);
+  if (op < FMX_OP_SUM || op > FMX_OP_PREDIV_SUM) return fail(FMX_ERR_INVALID_ARG, "bad op %d", op);
+  if (op != FMX_OP_SUM && !std::isfinite(factor))
+    return fail(FMX_ERR_INVALID_ARG, "factor must be finite");
+  const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;
+  if (offset % 16 || offset + count * esz > c->L.user_bytes)
+    return fail(FMX_ERR_INVALID_ARG, "host range [%zu, +%zu) outside the %zu-byte region (16-B aligned offset required)",
+                offset, count * esz, (size_t)c->L.user_bytes);
+  if (count == 0) return FMX_OK;
+  CudaSink sink(c);
+  return on_lanes(c, (cudaStream_t)stream, [&]() {
+    return plan_allreduce_host(c, sink, offset, count, dtype, op, factor);
+  });
+}
+
 int fmx_broadcast(fmx_comm_t c, const void* send, void* recv, size_t count, int dtype, int root,
                   void* stream) {
   int rc = check_comm(c);
@@ -890,7 +1066,9 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   c.nslots = 2;
   c.transport = transport == FMX_TRANSPORT_ZC ? FMX_TRANSPORT_ZC : FMX_TRANSPORT_CE;
   c.slice_bytes = slice_bytes;
-  c.L = compute_layout(nranks, 2, slice_bytes);
+  size_t max_bytes = 0;
+  for (int i = 0; i < nops; ++i) max_bytes = std::max(max_bytes, counts[i] * (dtypes[i] ? 2 : 4));
+  c.L = compute_layout(nranks, 2, slice_bytes, max_bytes);
   c.total_bytes = c.L.total;
   if (const char* v = getenv("FMX_RESULT_VIA_CE")) c.result_via_ce = atoi(v) != 0;
   std::string out;
@@ -901,10 +1079,12 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   for (int i = 0; i < nops; ++i) {
     int rc;
     sink.join();
-    if (kinds[i] != 0 && (!roots || roots[i] < 0 || roots[i] >= nranks))
+    if (kinds[i] == 1 && (!roots || roots[i] < 0 || roots[i] >= nranks))
       return fail(FMX_ERR_INVALID_ARG, "bad broadcast root");
     if (kinds[i] == 0)
       rc = plan_allreduce(&c, sink, dummy, dummy, counts[i], dtypes[i], FMX_OP_SUM, 1.0f, true);
+    else if (kinds[i] == 2)
+      rc = plan_allreduce_host(&c, sink, 0, counts[i], dtypes[i], FMX_OP_SUM, 1.0f);
     else
       rc = plan_broadcast(&c, sink, dummy, dummy, counts[i], dtypes[i], roots ? roots[i] : 0);
     if (rc) return rc;
@@ -939,6 +1119,12 @@ int fmx_comm_destroy(fmx_comm_t c) {
     rc = fail(FMX_ERR_CUDA, "pending collective failed: %s", cudaGetErrorString(cudaGetLastError()));
   if (c->done) cudaEventDestroy(c->done);
   if (c->fork) cudaEventDestroy(c->fork);
+  for (int i = 0; i < 8; ++i)
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  for (auto& pr : c->timed) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
   for (int l = 0; l < 2; ++l) {
     if (c->lane[l]) cudaStreamDestroy(c->lane[l]);
     if (c->joined[l]) cudaEventDestroy(c->joined[l]);
@@ -996,6 +1182,27 @@ int fmx_comm_flags(fmx_comm_t c, uint32_t* out, int cap) {
     return fail(FMX_ERR_INVALID_ARG, "bad arguments");
   for (int r = 0; r < c->nranks; ++r)
     for (int f = 0; f < kFlagsPerRank; ++f) out[r * kFlagsPerRank + f] = *c->flag_host(r, f);
+  return FMX_OK;
+}
+
+int fmx_comm_set_timing(fmx_comm_t c, int on) {
+  if (!c) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
+  c->timing = on != 0;
+  c->timed_used = 0;
+  return FMX_OK;
+}
+
+int fmx_comm_kernel_time(fmx_comm_t c, double* total_ms, uint64_t* count) {
+  if (!c || !total_ms || !count) return fail(FMX_ERR_INVALID_ARG, "null argument");
+  double sum = 0;
+  for (size_t i = 0; i < c->timed_used; ++i) {
+    FMX_CUDA(cudaEventSynchronize(c->timed[i].second));
+    float ms = 0;
+    FMX_CUDA(cudaEventElapsedTime(&ms, c->timed[i].first, c->timed[i].second));
+    sum += ms;
+  }
+  *total_ms = sum;
+  *count = c->timed_used;
   return FMX_OK;
 }
 

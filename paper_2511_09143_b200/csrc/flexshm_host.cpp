@@ -43,7 +43,7 @@ double now_s() {
   return duration<double>(steady_clock::now().time_since_epoch()).count();
 }
 
-Layout compute_layout(int nranks, int nslots, size_t slice_bytes) {
+Layout compute_layout(int nranks, int nslots, size_t slice_bytes, size_t user_bytes) {
   Layout L;
   const size_t page = 4096;
   size_t off = page;  // header
@@ -57,6 +57,9 @@ Layout compute_layout(int nranks, int nslots, size_t slice_bytes) {
   off += (size_t)nslots * nranks * slice_bytes;
   L.bc_off = off;
   off += (size_t)nslots * nranks * slice_bytes;
+  L.user_off = off = align_up(off, page);
+  L.user_bytes = align_up(user_bytes, page);
+  off += (size_t)nranks * L.user_bytes;
   L.total = align_up(off, page);
   return L;
 }

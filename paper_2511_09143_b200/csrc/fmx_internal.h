@@ -16,6 +16,7 @@ void set_dup(int a, int b);
 
 // ---- SHM segment layout ----------------------------------------------------
 // [header 4 KiB][peer table][flag lines][AR in-slots][AR out-slots][BC slots]
+// [user region of rank 0] ... [user region of rank n-1]
 // Every region starts on a 4 KiB boundary; every flag owns a 64-byte line.
 constexpr uint32_t kMagicReady = 0x464D5831u;  // "FMX1"
 constexpr uint32_t kVersion = 1;
@@ -36,6 +37,7 @@ struct Header {
   uint64_t slice_bytes;
   uint64_t total_bytes;
   uint64_t peers_off, flags_off, ar_in_off, ar_out_off, bc_off;
+  uint64_t user_off, user_bytes;  // per-rank registered host buffers
   int32_t creator_pid;
   int32_t mig_aware;
   alignas(64) std::atomic<int32_t> arrived;
@@ -47,9 +49,9 @@ struct Header {
 };
 
 struct Layout {
-  size_t peers_off, flags_off, ar_in_off, ar_out_off, bc_off, total;
+  size_t peers_off, flags_off, ar_in_off, ar_out_off, bc_off, user_off, user_bytes, total;
 };
-Layout compute_layout(int nranks, int nslots, size_t slice_bytes);
+Layout compute_layout(int nranks, int nslots, size_t slice_bytes, size_t user_bytes);
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 

@@ -24,7 +24,8 @@ def digest(a: np.ndarray) -> str:
 
 
 def suite_worker(rank: int, job_key: str, n: int, transport: str, mode: str, scenarios: list,
-                 slice_bytes: int = 0, peer_override: dict | None = None):
+                 slice_bytes: int = 0, peer_override: dict | None = None,
+                 host_bytes: int = 0):
     import torch
 
     from paper_2511_09143_b200 import instance as inst_mod
@@ -37,7 +38,8 @@ def suite_worker(rank: int, job_key: str, n: int, transport: str, mode: str, sce
         peer = PeerInfo(rank, peer.pcie_bus_id, peer_override[rank], peer.host_hash, peer.pid_hash)
     try:
         comm = init_process_group(None, rank, job_key, instance=inst, peer=peer, nranks=n,
-                                  slice_bytes=slice_bytes, transport=transport, timeout_s=120)
+                                  slice_bytes=slice_bytes, transport=transport, timeout_s=120,
+                                  host_bytes=host_bytes)
     except Exception as exc:  # bootstrap failures are part of what we test
         return {"init_error": type(exc).__name__, "args": getattr(exc, "rank_a", None),
                 "args_b": getattr(exc, "rank_b", None)}
@@ -46,6 +48,24 @@ def suite_worker(rank: int, job_key: str, n: int, transport: str, mode: str, sce
     for sc in scenarios:
         x = make_input(rank, sc)
         tdtype = torch.float32 if sc["dtype"] == "f32" else torch.bfloat16
+        if sc["kind"] == "allreduce_host":
+            region = comm.host_buffer()
+            off = sc.get("host_offset", 0)
+            view = region[off:off + x.nbytes].view(tdtype)
+            view.view(torch.uint8).copy_(torch.from_numpy(x.view(np.uint8)))
+            comm.allreduce_host(view, op=sc.get("op", "sum"), factor=sc.get("factor"),
+                                stream=stream)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            t0 = time.time()
+            while not ev.query():
+                if time.time() - t0 > 60:
+                    return {"stuck": sc, "index": len(out), "flags": comm.flags(), "rank": rank}
+                time.sleep(0.002)
+            comm.barrier(60)  # every rank done reading before anyone rewrites its region
+            got = view.view(torch.uint8).numpy().view(x.dtype).copy()
+            out.append(digest(got) if sc.get("ret") == "sha" else got)
+            continue
         host = torch.from_numpy(x.view(np.float32) if sc["dtype"] == "f32" else x.view(np.int16))
         off = sc.get("offset", 0)
         buf = torch.empty(sc["count"] + off, dtype=tdtype, device="cuda")
@@ -76,3 +96,42 @@ def suite_worker(rank: int, job_key: str, n: int, transport: str, mode: str, sce
     comm.barrier()
     comm.destroy()
     return {"results": out, "launches": launches, "pid": os.getpid()}
+
+
+def ddp_worker(rank: int, job_key: str, n: int, port: int, mode: str = "green"):
+    """Tiny model: local gradients without DDP, then the same step under DDP
+    with the flexshm comm hook; returns both (flattened fp32)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_09143_b200 import ddp as fddp
+    from paper_2511_09143_b200 import instance as inst_mod
+    from paper_2511_09143_b200.comm import init_process_group
+
+    inst = inst_mod.bind(0, rank + 1, mode=mode)
+    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n, timeout_s=120)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=n)
+    stream = inst.stream
+    with torch.cuda.stream(stream):
+        torch.manual_seed(1000 + rank)     # different init per rank: broadcast must fix it
+        model = torch.nn.Sequential(torch.nn.Linear(64, 300), torch.nn.GELU(),
+                                    torch.nn.Linear(300, 10)).cuda()
+        g = torch.Generator(device="cpu").manual_seed(7 + rank)
+        x = torch.randn(32, 64, generator=g).cuda()
+        y = torch.randint(0, 10, (32,), generator=g).cuda()
+        net = fddp.wrap(model, comm, control_group=dist.group.WORLD, bucket_cap_mb=0.05)
+        params0 = torch.cat([p.detach().reshape(-1) for p in model.parameters()]).cpu()
+        # local gradient (no communication): no_sync skips the reducer
+        with net.no_sync():
+            torch.nn.functional.cross_entropy(net(x), y).backward()
+        local = torch.cat([p.grad.reshape(-1) for p in model.parameters()]).clone()
+        for p in model.parameters():
+            p.grad = None
+        torch.nn.functional.cross_entropy(net(x), y).backward()
+        synced = torch.cat([p.grad.reshape(-1) for p in model.parameters()]).clone()
+    stream.synchronize()
+    dist.destroy_process_group()
+    comm.destroy()
+    return {"params0": params0.numpy(), "local": local.cpu().numpy(), "synced": synced.cpu().numpy()}

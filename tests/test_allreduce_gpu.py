@@ -26,6 +26,7 @@ def expected(sc: dict, n: int) -> np.ndarray:
     dt = orc.F32 if sc["dtype"] == "f32" else orc.BF16
     if sc["kind"] == "broadcast":
         return xs[sc["root"]].copy()
+    # "allreduce" and "allreduce_host" share the contract
     op = sc.get("op", "sum")
     factor = sc.get("factor")
     if op == "avg":
@@ -50,7 +51,7 @@ def assert_same(got: np.ndarray, want: np.ndarray, what: str):
 
 
 def run(n: int, scenarios: list, transport: str = "auto", mode: str = "green",
-        slice_bytes: int = 0, peer_override=None):
+        slice_bytes: int = 0, peer_override=None, host_bytes: int = 0):
     from paper_2511_09143_b200.launcher import launch, new_job_key
     from paper_2511_09143_b200.scheduler import fm_select, make_cluster
     from paper_2511_09143_b200.workload import Job
@@ -58,7 +59,7 @@ def run(n: int, scenarios: list, transport: str = "auto", mode: str = "green",
     decision = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1 if n <= 7 else 2))
     key = new_job_key("t")
     return launch(_workers.suite_worker, decision,
-                  args=(key, n, transport, mode, scenarios, slice_bytes, peer_override),
+                  args=(key, n, transport, mode, scenarios, slice_bytes, peer_override, host_bytes),
                   job_key=key, mode=mode, timeout_s=300, gpu_map={0: "0", 1: "0"})
 
 
@@ -113,6 +114,29 @@ def test_resnet50_gradient_seven_ranks_bit_exact():
     scen = [dict(kind="allreduce", count=25_557_032, dtype="f32", ret="sha"),
             dict(kind="allreduce", count=25_557_032, dtype="f32", op="avg", ret="sha")]
     check_all(7, scen, run(7, scen))
+
+
+HOST = [
+    dict(kind="allreduce_host", count=1_000_003, dtype="f32"),
+    dict(kind="allreduce_host", count=1_000_003, dtype="f32", op="avg"),
+    dict(kind="allreduce_host", count=500_001, dtype="bf16", op="avg", host_offset=4096),
+    dict(kind="allreduce_host", count=3, dtype="f32", op="postscale", factor=0.5),
+    dict(kind="allreduce", count=200_000, dtype="f32"),            # mixed with device path
+    dict(kind="allreduce_host", count=40_000, dtype="f32", inputs="adversarial"),
+    dict(kind="allreduce_host", count=40_003, dtype="bf16", inputs="adversarial"),
+]
+
+
+@pytest.mark.parametrize("n", [2, 7])
+def test_host_buffer_allreduce(n):
+    """Registered host buffers (fmx_allreduce_host): inputs read and results
+    written straight over the host link, same bit-exact contract."""
+    check_all(n, HOST, run(n, HOST, slice_bytes=128 << 10, host_bytes=8 << 20))
+
+
+def test_host_buffer_resnet50_gradient_bit_exact():
+    scen = [dict(kind="allreduce_host", count=25_557_032, dtype="f32", op="avg", ret="sha")]
+    check_all(7, scen, run(7, scen, host_bytes=25_557_032 * 4))
 
 
 def test_mig_aware_rejects_double_binding():

@@ -1,0 +1,34 @@
+"""DDP integration: parameters broadcast over SHM, and
+every gradient bucket allreduced by ddp.flexshm_hook with DDP's default
+arithmetic (divide by world size, then sum) fused into the fixed rank-order
+fp32 sum - bit-exact against the oracle applied to the ranks' local
+gradients."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from tests import _workers
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_ddp_hook_matches_oracle(n):
+    from paper_2511_09143_b200.launcher import launch, new_job_key
+    from paper_2511_09143_b200.scheduler import fm_select, make_cluster
+    from paper_2511_09143_b200.workload import Job
+
+    d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
+    key = new_job_key("ddp")
+    port = 20000 + os.getpid() % 20000
+    res = launch(_workers.ddp_worker, d, args=(key, n, port), job_key=key, timeout_s=300)
+    for r in res[1:]:
+        assert np.array_equal(r["params0"], res[0]["params0"]), "parameter broadcast"
+    want = orc.allreduce_c([r["local"] for r in res], orc.F32, orc.OP_PREDIV_SUM, float(n))
+    for rank, r in enumerate(res):
+        assert np.array_equal(r["synced"].view(np.uint32), want.view(np.uint32)), rank

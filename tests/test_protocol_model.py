@@ -27,12 +27,19 @@ import pytest
 from paper_2511_09143_b200 import _lib
 
 
-def parse(text: str):
-    """-> [lane0 ops, lane1 ops]; a 'J' line is a join point in both lanes."""
+def parse(text: str, merged: bool = False):
+    """-> [lane0 ops, lane1 ops]; a 'J' line is a join point in both lanes.
+    merged=True reads the trace as ONE sequential program in enqueue order -
+    what the hardware runs if the driver puts both lane streams on one FIFO."""
     lanes = [[], []]
     joins = 0
     for line in text.splitlines():
         if not line:
+            continue
+        if merged:
+            if line != "J":
+                f = line.split()
+                lanes[0].append((f[1], *[int(x) for x in f[2:]]))
             continue
         if line == "J":
             for ops in lanes:
@@ -62,6 +69,7 @@ def simulate(progs, seed: int, burst: int = 3):
     pc = {a: 0 for a in actors}
     clock = {a: [0] * m for a in actors}
     flags = {}
+    events = {}       # (rank, event id, seq) -> clock at record
     last_write = {}   # key -> (actor, time, bytes, round)
     reads = {}        # key -> [(actor, time)] since last write
 
@@ -78,6 +86,8 @@ def simulate(progs, seed: int, burst: int = 3):
         if op[0] == "J":
             other = (a[0], 1 - a[1])
             return op_of(other) == op
+        if op[0] == "X":
+            return (a[0], op[1], op[2]) in events
         return True
 
     def hb(prev_actor, prev_time, me):
@@ -129,6 +139,13 @@ def simulate(progs, seed: int, burst: int = 3):
                 clock[a][:] = joined
                 clock[other][:] = joined
                 pc[other] += 1
+            elif op[0] == "E":
+                me[idx[a]] += 1
+                events[(r, op[1], op[2])] = list(me)
+            elif op[0] == "X":
+                c = events[(r, op[1], op[2])]
+                for k in range(m):
+                    me[k] = max(me[k], c[k])
             elif op[0] == "S":
                 me[idx[a]] += 1
                 prev = flags.get((r, op[1]), (0, None))[0]
@@ -147,12 +164,15 @@ def simulate(progs, seed: int, burst: int = 3):
             pc[a] += 1
 
 
-def programs(n, ops, slice_bytes, transport):
-    ops = [o if o[0] == "allreduce" else (o[0], o[1], o[2], o[3] % n) for o in ops]
-    return [parse(_lib.trace_plan(n, r, ops, slice_bytes, transport)) for r in range(n)]
+def programs(n, ops, slice_bytes, transport, merged=False):
+    ops = [o if o[0] != "broadcast" else (o[0], o[1], o[2], o[3] % n) for o in ops]
+    return [parse(_lib.trace_plan(n, r, ops, slice_bytes, transport), merged) for r in range(n)]
 
 
 SEQUENCES = {
+    "host-buffer": [("allreduce_host", 90_001, 0), ("allreduce_host", 5, 1),
+                    ("allreduce", 30_000, 0), ("allreduce_host", 40_000, 1),
+                    ("broadcast", 9_000, 0, 1), ("allreduce_host", 123_456, 0)],
     "allreduce-multi-round": [("allreduce", 200_003, 0), ("allreduce", 200_003, 1)],
     "mixed": [("allreduce", 50_000, 0), ("broadcast", 70_001, 0, 1), ("allreduce", 7, 1),
               ("broadcast", 5, 1, 0), ("allreduce", 123_457, 0), ("broadcast", 90_000, 0, 2),
@@ -170,6 +190,17 @@ def test_protocol_is_race_and_deadlock_free(n, seq, transport):
         simulate(progs, seed)
 
 
+@pytest.mark.parametrize("n", [2, 3, 7])
+@pytest.mark.parametrize("seq", sorted(SEQUENCES))
+def test_enqueue_order_is_a_valid_single_stream_schedule(n, seq):
+    """If the driver serialises a rank's two lane streams onto one hardware
+    FIFO, the rank executes its trace in enqueue order: that must not deadlock
+    either (the bug a first two-lane version hit on the B200)."""
+    progs = programs(n, SEQUENCES[seq], 4096, "ce", merged=True)
+    for seed in range(8):
+        simulate(progs, seed)
+
+
 @pytest.mark.parametrize("n", [14, 28])
 def test_protocol_multi_gpu_world_sizes(n):
     """World sizes of the 2/4-GPU configs (C4: 14 ranks; 28 = 7 x 4)."""
@@ -178,6 +209,22 @@ def test_protocol_multi_gpu_world_sizes(n):
     progs = programs(n, ops, 4096, "ce")
     for seed in range(3):
         simulate(progs, seed, burst=8)
+
+
+def test_model_catches_a_broken_host_schedule():
+    """Drop the REDUCED wait at the end of a host-buffer allreduce: the next
+    call's host write of the input races with a slow owner's result write."""
+    progs = programs(3, [("allreduce_host", 60_000, 0), ("allreduce_host", 60_000, 0)], 4096, "ce")
+    lanes = progs[1]
+    broken_lanes = [[op for op in lane if not (op[0] == "A" and op[2] == 1)] for lane in lanes]
+    broken = [broken_lanes if r == 1 else p for r, p in enumerate(progs)]
+    failures = 0
+    for seed in range(60):
+        try:
+            simulate(broken, seed)
+        except AssertionError:
+            failures += 1
+    assert failures > 0
 
 
 @pytest.mark.parametrize("flag", [0, 1])
