@@ -19,14 +19,12 @@ PAPER.md:264-271), so here:
   torch/distributed/optim/zero_redundancy_optimizer.py:785-801).
 """
 
-from __future__ import annotations
-
 import torch
 
 from .comm import ShmCommunicator
 
 
-def flexshm_hook(comm: ShmCommunicator, bucket) -> torch.futures.Future:
+def flexshm_hook(comm: ShmCommunicator, bucket) -> torch.futures.Future[torch.Tensor]:
     """DDP communication hook: bucket.buffer() <- mean over ranks.
 
     The allreduce is enqueued on the current stream (the stream autograd runs
@@ -35,7 +33,7 @@ def flexshm_hook(comm: ShmCommunicator, bucket) -> torch.futures.Future:
     """
     buf = bucket.buffer()
     comm.allreduce(buf, op="avg")
-    fut: torch.futures.Future = torch.futures.Future()
+    fut = torch.futures.Future()
     fut.set_result(buf)
     return fut
 
@@ -44,7 +42,7 @@ def broadcast_parameters(module: torch.nn.Module, comm: ShmCommunicator, root: i
     """Make every rank's parameters (and floating buffers) equal to root's."""
     tensors = [p.data for p in module.parameters()] + \
               [b for b in module.buffers() if b.is_floating_point()]
-    by_dtype: dict[torch.dtype, list[torch.Tensor]] = {}
+    by_dtype = {}
     for t in tensors:
         by_dtype.setdefault(t.dtype, []).append(t)
     for dtype, group in by_dtype.items():

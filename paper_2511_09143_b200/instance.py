@@ -35,6 +35,9 @@ from dataclasses import dataclass, field
 from .commsim import PeerInfo, canonical_bus_id
 
 MODES = ("mig", "green", "mps", "full")
+# Green contexts live as long as the process: tensors allocated under one are
+# freed at interpreter exit, after any local Instance is gone.
+_KEEP_ALIVE: list = []
 ONE_G_FRACTION = 1.0 / 7.0   # compute share of a 1g slice (7 compute slices)
 GREEN_SM_GRANULE = 8         # SM count granularity we request green contexts in
 
@@ -111,6 +114,7 @@ def bind(gpu_id: int, instance_id: int, profile: str = "1g.5gb", mode: str = "gr
         gc = torch.cuda.GreenContext.create(inst.sm_count, device)
         gc.set_context()
         inst.green_ctx = gc
+        _KEEP_ALIVE.append(gc)
         s = gc.Stream()
         inst.stream = s if isinstance(s, torch.cuda.Stream) else torch.cuda.ExternalStream(
             s.cuda_stream, device=device)
