@@ -487,17 +487,18 @@ Annot ubuf(size_t off_bytes, size_t bytes) { return Annot{(int64_t)off_bytes, by
 // The model checker checks both the two-lane and the merged single-FIFO reading.
 //
 // Hazards and the wait that covers each:
-//  stage(R) into in[R%2][o][me], last read by every owner's reduce(R-2):
-//      lane-1 event recorded after my wait REDUCED[*] >= R-1 (round R-2 reduced
-//      everywhere); rounds of an earlier collective are covered by the fork.
-//  reduce(R) reads in[R%2][me][q]          -> wait STAGED[q] >= R+1
+//  stage(R) into in[R%2][o][me], last read by owner o's fetch of round R-2:
+//      lane-1 event recorded after my waits REDUCED[q] >= R-1 for every q
+//      (each owner signals REDUCED after its fetches); rounds of an earlier
+//      collective are covered by the fork.
+//  fetch(R) of in[R%2][me][q]              -> wait STAGED_TO[q][me] >= R+1
+//      (per contributor: a piece moves as soon as it was staged)
 //  reduce(R) writes out[R%2][me], last read by every q's gather(R-2): my
 //      gather(R-1) waited REDUCED[q] >= R, and q's lane 1 runs gather(R-2)
 //      before reduce(R-1).
-//  gather(R) reads out[R%2][q]             -> wait REDUCED[q] >= R+1
-//  in place: gather(R) overwrites pieces of round R of other chunks; my
-//      stage(R) read them first, because every owner's reduce(R) waited for my
-//      STAGED >= R+1.
+//  gather(R) reads out[R%2][q]             -> wait REDUCED[q] >= R+1 (per owner)
+//  in place: gather(R) overwrites piece (q, R); my stage(R) read it first,
+//      because owner q's reduce(R) waited for my STAGED_TO[me][q] >= R+1.
 enum { kEvSlotFree = 0 };  // + slot: lane 1 -> lane 0, "slot reusable"
 
 int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
@@ -508,23 +509,29 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
   std::vector<PlanSeg> segs;
   int rc;
   const uint32_t R0 = c->ar_round;
+  // peers in rotated order starting after me, so that at any moment the
+  // ranks work on different owners / contributors instead of all on one
+  auto rot = [&](int i) { return (me + 1 + i) % n; };
 
   auto stage = [&](uint32_t j) -> int {
     const uint32_t R = R0 + j;
-    // slot R%2 was read by round R-2's reductions; within this collective the
-    // lane-1 event of round R-2's REDUCED wait says they are done
+    // slot R%2 was read by round R-2's fetches; within this collective the
+    // lane-1 event after round R-2's REDUCED waits says they are done
     if (j >= 2 && (rc = k.wait_event(kLaneStage, kEvSlotFree + R % 2))) return rc;
-    segs.clear();
-    for (int o = 0; o < n; ++o) {
-      const size_t len = o == me ? 0 : g.len(o, j);
-      if (!len) continue;
-      const size_t off = c->in_off(R, o, me);
-      segs.push_back({src + g.lo(o, j) * g.esz, c->at(zc, off), len * g.esz,
-                      Annot{(int64_t)off, len * g.esz, me, R}, true,
-                      ubuf(g.lo(o, j) * g.esz, len * g.esz)});
+    for (int i = 0; i < n - 1; ++i) {
+      const int o = rot(i);
+      const size_t len = g.len(o, j);
+      segs.clear();
+      if (len) {
+        const size_t off = c->in_off(R, o, me);
+        segs.push_back({src + g.lo(o, j) * g.esz, c->at(zc, off), len * g.esz,
+                        Annot{(int64_t)off, len * g.esz, me, R}, true,
+                        ubuf(g.lo(o, j) * g.esz, len * g.esz)});
+        if ((rc = k.copy(kLaneStage, segs, false, zc))) return rc;
+      }
+      if ((rc = k.signal(kLaneStage, kStagedTo + o, R + 1))) return rc;
     }
-    if ((rc = k.copy(kLaneStage, segs, false, zc))) return rc;
-    return k.signal(kLaneStage, kStaged, R + 1);
+    return FMX_OK;
   };
 
   if ((rc = stage(0))) return rc;
@@ -532,7 +539,6 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
     const uint32_t R = R0 + j;
     if (j + 1 < g.rounds && (rc = stage(j + 1))) return rc;  // one round ahead, lane 0
     // lane 1: reduce-scatter my chunk in ascending rank order
-    if ((rc = k.wait_peers(kLaneMain, kStaged, R + 1, me))) return rc;
     const size_t mylen = g.len(me, j);
     if (mylen) {
       PlanReduce pr;
@@ -552,16 +558,18 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
         a.out_sys = c->at(true, out_off);
         pr.write = Annot{(int64_t)out_off, mylen * g.esz, me, R};
       }
-      if (!zc) {  // copy engine pulls the n-1 contributions into HBM scratch first
-        segs.clear();
-        for (int q = 0; q < n; ++q) {
-          if (q == me) continue;
+      // each contribution is fetched as soon as its contributor staged it
+      for (int i = 0; i < n - 1; ++i) {
+        const int q = rot(i);
+        if ((rc = k.wait_rank(kLaneMain, q, kStagedTo + me, R + 1))) return rc;
+        if (!zc) {
           const size_t off = c->in_off(R, me, q);
+          segs.clear();
           segs.push_back({c->at(false, off), c->scratch + (size_t)q * c->slice_bytes,
                           mylen * g.esz, Annot{(int64_t)off, mylen * g.esz, q, R}, false,
                           Annot{}});
+          if ((rc = k.copy(kLaneMain, segs, true, false))) return rc;
         }
-        if ((rc = k.copy(kLaneMain, segs, true, false))) return rc;
       }
       for (int q = 0; q < n; ++q) {
         if (q == me) {
@@ -585,19 +593,21 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
       }
     }
     if ((rc = k.signal(kLaneMain, kReduced, R + 1))) return rc;
-    // all-gather of the other owners' results
-    if ((rc = k.wait_peers(kLaneMain, kReduced, R + 1, me))) return rc;
-    if ((rc = k.record(kLaneMain, kEvSlotFree + R % 2))) return rc;  // in[R%2] reusable
-    segs.clear();
-    for (int q = 0; q < n; ++q) {
-      const size_t len = q == me ? 0 : g.len(q, j);
+    // all-gather: each owner's result as soon as that owner has it
+    for (int i = 0; i < n - 1; ++i) {
+      const int q = rot(i);
+      if ((rc = k.wait_rank(kLaneMain, q, kReduced, R + 1))) return rc;
+      const size_t len = g.len(q, j);
       if (!len) continue;
       const size_t off = c->out_off(R, q);
+      segs.clear();
       segs.push_back({c->at(zc, off), dst + g.lo(q, j) * g.esz, len * g.esz,
                       Annot{(int64_t)off, len * g.esz, q, R}, false,
                       ubuf(g.lo(q, j) * g.esz, len * g.esz)});
+      if ((rc = k.copy(kLaneMain, segs, true, zc))) return rc;
     }
-    if ((rc = k.copy(kLaneMain, segs, true, zc))) return rc;
+    // every owner has fetched round R: in[R%2] may be restaged (round R+2)
+    if ((rc = k.record(kLaneMain, kEvSlotFree + R % 2))) return rc;
   }
   c->ar_round += g.rounds;
   return FMX_OK;
@@ -1178,10 +1188,10 @@ int fmx_comm_config(fmx_comm_t c, size_t* slice_bytes, int* transport, size_t* s
 }
 
 int fmx_comm_flags(fmx_comm_t c, uint32_t* out, int cap) {
-  if (!c || !c->base || !out || cap < c->nranks * kFlagsPerRank)
+  if (!c || !c->base || !out || cap < c->nranks * 4)
     return fail(FMX_ERR_INVALID_ARG, "bad arguments");
   for (int r = 0; r < c->nranks; ++r)
-    for (int f = 0; f < kFlagsPerRank; ++f) out[r * kFlagsPerRank + f] = *c->flag_host(r, f);
+    for (int f = 0; f < 4; ++f) out[r * 4 + f] = *c->flag_host(r, f);
   return FMX_OK;
 }
 

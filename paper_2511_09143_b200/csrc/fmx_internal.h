@@ -20,8 +20,9 @@ void set_dup(int a, int b);
 // Every region starts on a 4 KiB boundary; every flag owns a 64-byte line.
 constexpr uint32_t kMagicReady = 0x464D5831u;  // "FMX1"
 constexpr uint32_t kVersion = 1;
-constexpr int kFlagsPerRank = 8;  // 4 used, room for more
-enum Flag { kStaged = 0, kReduced = 1, kBcStaged = 2, kBcDone = 3 };
+// Per rank: 8 scalar flags, then one STAGED_TO flag per destination owner.
+enum Flag { kStaged = 0, kReduced = 1, kBcStaged = 2, kBcDone = 3, kStagedTo = 8 };
+constexpr int kFlagsPerRank = kStagedTo + FMX_MAX_RANKS;
 
 struct alignas(64) PeerSlot {
   std::atomic<int32_t> state;  // 0 empty, 1 published

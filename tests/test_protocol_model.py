@@ -227,14 +227,19 @@ def test_model_catches_a_broken_host_schedule():
     assert failures > 0
 
 
-@pytest.mark.parametrize("flag", [0, 1])
+STAGED_TO = 8   # kStagedTo: per-(contributor, owner) flags start here
+REDUCED = 1
+
+
+@pytest.mark.parametrize("flag", ["staged_to", "reduced"])
 def test_model_catches_a_broken_schedule(flag):
-    """Sanity: drop every wait of one rank on one flag (STAGED or REDUCED)
-    and the checker must object.  (A third flag, GATHERED, was dropped from
+    """Sanity: drop every wait of one rank on one kind of flag (STAGED_TO or
+    REDUCED) and the checker must object.  (A GATHERED flag was dropped from
     the protocol after this checker showed its waits were implied.)"""
     progs = programs(3, [("allreduce", 60_000, 0), ("allreduce", 60_000, 0)], 4096, "ce")
     lanes = progs[1]
-    broken_lanes = [[op for op in lane if not (op[0] == "A" and op[2] == flag)] for lane in lanes]
+    hit = (lambda f: f >= STAGED_TO) if flag == "staged_to" else (lambda f: f == REDUCED)
+    broken_lanes = [[op for op in lane if not (op[0] == "A" and hit(op[2]))] for lane in lanes]
     assert broken_lanes != lanes
     broken = [broken_lanes if r == 1 else p for r, p in enumerate(progs)]
     failures = 0
