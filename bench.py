@@ -63,6 +63,7 @@ def parse_args(argv=None):
                    help="ranks as threads of one process (for ncu); not the headline layout")
     p.add_argument("--out", default=None, help="also write the JSON line here")
     p.add_argument("--no-train", action="store_true", help="skip the ResNet-50 DP img/s leg")
+    p.add_argument("--timeline", default=None, help="write a host-polled flag timeline here")
     p.add_argument("--train-only", action="store_true")
     p.add_argument("--train-mode", choices=["green", "mps", "full"], default="green")
     p.add_argument("--batch", type=int, default=32)
@@ -113,7 +114,7 @@ ZC_WRITE_PEAK = 52.7
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
 
-def kernel_roofline(args, n, s_bytes, kernel_ms, kernel_count):
+def kernel_roofline(args, n, s_bytes, kernel_ms, kernel_count, iso_us=None, iso_piece=None):
     """Roofline of the dominant kernel, fmx_reduce_kernel, from its live
     CUDA-event durations (lane stream) over the timed region.
 
@@ -149,12 +150,22 @@ def kernel_roofline(args, n, s_bytes, kernel_ms, kernel_count):
                 "traffic": traffic, "launch_us": t_launch * 1e6, "launches": kernel_count,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     link = per_launch(s_bytes)
-    return {"kernel": "fmx_reduce_kernel", "bound": "host_link",
+    line = {"kernel": "fmx_reduce_kernel", "bound": "host_link",
             "achieved": link / t_launch / 1e9, "peak": ZC_WRITE_PEAK, "unit": "GB/s",
             "frac": link / t_launch / 1e9 / ZC_WRITE_PEAK, "traffic": traffic,
-            "hbm_bytes_per_launch": per_launch((n + 1) * s_bytes),
+            "bytes_per_launch": {"pcie_store": link, "hbm_read": per_launch(n * s_bytes),
+                                 "hbm_write": link},
             "launch_us": t_launch * 1e6, "launches": kernel_count,
+            "timing": "CUDA events around every reduce launch on its lane stream, inside the "
+                      "timed region; includes time-slice waits behind the other 6 processes",
             "peak_source": "measured SM zero-copy store peak (profiles/r01_probe/bw.jsonl)"}
+    if iso_us:
+        line["isolated"] = {"launch_us": iso_us, "piece_bytes": iso_piece,
+                            "achieved": iso_piece / (iso_us * 1e-6) / 1e9,
+                            "frac": iso_piece / (iso_us * 1e-6) / 1e9 / ZC_WRITE_PEAK,
+                            "hbm_gbs": (n + 1) * iso_piece / (iso_us * 1e-6) / 1e9,
+                            "timing": "same kernel, same piece, rank 0 alone (peers parked)"}
+    return line
 
 
 class ClockSampler:
@@ -266,6 +277,50 @@ def rank_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_lo
         device_step()
     torch.cuda.synchronize()
     out["ms_total"], out["launches"] = timed(cfg["steps"], device_step, kernel_timing=True)
+    if cfg.get("timeline"):
+        # host-side flag timeline of 2 allreduces (rank 0 polls the segment)
+        import threading as _th
+        rec = {}
+        comm.barrier(300)
+        torch.cuda.synchronize()
+        if rank == 0:
+            mon = _th.Thread(target=lambda: rec.setdefault("ev", comm.monitor(0.4)))
+            mon.start()
+            time.sleep(0.01)
+        comm.barrier(300)
+        t_host = time.perf_counter()
+        for _ in range(2):
+            device_step()
+        torch.cuda.synchronize()
+        out["timeline_host_s"] = time.perf_counter() - t_host
+        if rank == 0:
+            mon.join()
+            with open(cfg["timeline"], "w") as f:
+                json.dump({"n": n, "slice_bytes": comm.slice_bytes, "count": count,
+                           "events": rec.get("ev", [])}, f)
+        comm.barrier(300)
+    # isolated kernel timing (rank 0 only, every other rank parked at the
+    # barrier, so no time-slicing with peers): fmx_reduce_kernel on one
+    # pipeline piece, n HBM sources, zero-copy result store to pinned host
+    # memory - exactly what each round of the CE transport launches
+    if rank == 0:
+        from paper_2511_09143_b200.comm import reduce_local
+        piece = min(comm.slice_bytes // esz, (count + n - 1) // n)
+        srcs = [torch.randn(piece, device=f"cuda:{gpu_local}").to(tdt) for _ in range(n)]
+        kout = torch.empty(piece, dtype=tdt, device=f"cuda:{gpu_local}")
+        kout_host = torch.empty(piece, dtype=tdt).pin_memory()
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                reduce_local(srcs, kout, op="avg", out_host=kout_host, stream=stream)
+            ev0.record(stream)
+            for _ in range(20):
+                reduce_local(srcs, kout, op="avg", out_host=kout_host, stream=stream)
+            ev1.record(stream)
+        ev1.synchronize()
+        out["iso_kernel_us"] = ev0.elapsed_time(ev1) * 1e3 / 20
+        out["iso_piece_bytes"] = piece * esz
+        del srcs, kout, kout_host
+    comm.barrier(300)
     if cfg["e2e"]:
         # (2) registered host buffer: the gradient lives in pinned host memory
         region = comm.host_buffer()[:count * esz].view(tdt)
@@ -442,7 +497,8 @@ def run_ours(args) -> dict | None:
     n = len(d.instances)
     cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
            "slice_bytes": args.slice_bytes, "dtype": args.dtype, "count": args.count,
-           "warmup": args.warmup, "steps": args.steps, "e2e": not args.no_e2e}
+           "warmup": args.warmup, "steps": args.steps, "e2e": not args.no_e2e,
+           "timeline": args.timeline}
     # one job key for all processes of all GPUs
     job_key = os.environ.get("FMX_BENCH_KEY") or f"bench-{os.environ.get('MASTER_PORT', '0')}-" \
         f"{os.environ.get('TORCHELASTIC_RUN_ID', str(os.getppid()))}"
@@ -524,7 +580,9 @@ def run_ours(args) -> dict | None:
                    "transport": args.transport, "l2": "inputs > L2 (7 x 102 MB per GPU)",
                    "rank_order": "fm_select round-robin"},
         "busbw_gbs": s_bytes / t_step / 1e9 * 2 * (n - 1) / n,
-        "roofline": kernel_roofline(args, n, s_bytes, kernel_ms, kernel_count),
+        "roofline": kernel_roofline(args, n, s_bytes, kernel_ms, kernel_count,
+                                    results.get(0, {}).get("iso_kernel_us"),
+                                    results.get(0, {}).get("iso_piece_bytes")),
         "step_roofline": step_roofline(n, per_gpu, s_bytes, t_step, peaks),
         "gpu_launches": launches,
         "clocks": clocks,

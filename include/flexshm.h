@@ -158,6 +158,14 @@ int fmx_host_buffer(fmx_comm_t comm, int rank, void** ptr, size_t* bytes);
 int fmx_allreduce_host(fmx_comm_t comm, size_t offset, size_t count, int dtype, int op,
                        float factor, void* stream);
 
+/* The owner-side reduction kernel on its own (no communicator): dst[i] =
+ * rank-order fp32 sum of srcs[0..nsrc)[i] with the op/factor convention,
+ * optionally also stored to dst_sys (mapped host memory, zero-copy).  Bit
+ * `q` of sys_mask marks srcs[q] as mapped host memory (cache-volatile loads).
+ * Used to test the kernel against the oracle and to time it in isolation. */
+int fmx_reduce_local(const void* const* srcs, int nsrc, uint64_t sys_mask, void* dst,
+                     void* dst_sys, size_t count, int dtype, int op, float factor, void* stream);
+
 /* Host-side barrier over the communicator (SHM counter; no GPU work). */
 int fmx_barrier(fmx_comm_t comm, double timeout_s);
 
@@ -174,6 +182,13 @@ int fmx_comm_config(fmx_comm_t comm, size_t* slice_bytes, int* transport, size_t
 /* Snapshot of every rank's flag counters (nranks x 4: STAGED, REDUCED,
  * BC_STAGED, BC_DONE), read from host memory - for hang diagnosis. */
 int fmx_comm_flags(fmx_comm_t comm, uint32_t* out, int cap);
+/* Timeline probe: poll every flag of every rank (host reads of the segment,
+ * no GPU involvement) for `seconds` and record each change as two uint64s:
+ * ns since the call, and (rank << 48 | flag << 32 | value).  *n_out = number
+ * of changes.  Flag ids: 0 STAGED, 1 REDUCED, 2 BC_STAGED, 3 BC_DONE,
+ * 8 + o STAGED_TO[o]. */
+int fmx_comm_monitor(fmx_comm_t comm, double seconds, uint64_t* out, size_t cap, size_t* n_out);
+
 /* Live timing of the reduction kernel: with timing on, every reduce launch
  * is bracketed by CUDA events on the lane stream it runs on; kernel_time
  * returns the summed device time and the number of timed launches since

@@ -45,9 +45,11 @@ MAX_RANKS = 64
 # Every symbol include/flexshm.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "fmx_check_peer", "fmx_validate_peers", "fmx_topology", "fmx_restore_bus_id",
-    "fmx_comm_init", "fmx_allreduce", "fmx_broadcast", "fmx_host_buffer", "fmx_allreduce_host", "fmx_barrier", "fmx_comm_destroy",
+    "fmx_comm_init", "fmx_allreduce", "fmx_broadcast", "fmx_host_buffer", "fmx_allreduce_host",
+    "fmx_reduce_local", "fmx_barrier", "fmx_comm_destroy",
     "fmx_comm_abort", "fmx_comm_rank", "fmx_comm_count", "fmx_comm_peer", "fmx_comm_config",
     "fmx_comm_kernel_launches", "fmx_comm_flags", "fmx_comm_set_timing", "fmx_comm_kernel_time",
+    "fmx_comm_monitor",
     "fmx_trace_plan", "fmx_last_error", "fmx_dup_ranks",
     "fmx_abi_version",
 )
@@ -102,6 +104,8 @@ def lib() -> ctypes.CDLL:
                           c_int, c_size, c_int, c_double],
         "fmx_host_buffer": [c_void, c_int, P(c_void), P(c_size)],
         "fmx_allreduce_host": [c_void, c_size, c_size, c_int, c_int, c_float, c_void],
+        "fmx_reduce_local": [P(c_void), c_int, ctypes.c_uint64, c_void, c_void, c_size, c_int,
+                             c_int, c_float, c_void],
         "fmx_allreduce": [c_void, c_void, c_void, c_size, c_int, c_int, c_float, c_void],
         "fmx_broadcast": [c_void, c_void, c_void, c_size, c_int, c_int, c_void],
         "fmx_barrier": [c_void, c_double],
@@ -114,6 +118,7 @@ def lib() -> ctypes.CDLL:
         "fmx_comm_kernel_launches": [c_void, P(ctypes.c_uint64)],
         "fmx_comm_flags": [c_void, P(ctypes.c_uint32), c_int],
         "fmx_comm_set_timing": [c_void, c_int],
+        "fmx_comm_monitor": [c_void, c_double, P(ctypes.c_uint64), c_size, P(c_size)],
         "fmx_comm_kernel_time": [c_void, P(c_double), P(ctypes.c_uint64)],
         "fmx_trace_plan": [c_int, c_int, c_int, c_size, c_int, P(c_int), P(c_size), P(c_int),
                            P(c_int), ctypes.c_char_p, c_size, P(c_size)],

@@ -49,6 +49,29 @@ def _check_tensor(t, what: str):
         raise ValueError(f"{what} must be contiguous (flat gradient buffer)")
 
 
+def reduce_local(sources, out, op: str = "sum", factor: float | None = None, out_host=None,
+                 host_sources=(), stream=None):
+    """The owner-side reduction kernel alone: out = rank-order fp32 sum of
+    `sources` (same-size CUDA tensors, or host tensors listed by index in
+    `host_sources` that live in mapped pinned memory), op/factor as in
+    allreduce; `out_host` (pinned host tensor) also receives the result."""
+    import torch
+    if op == "avg":
+        op, factor = "prediv", float(len(sources))
+    ptrs = (ctypes.c_void_p * len(sources))(*[t.data_ptr() for t in sources])
+    mask = 0
+    for q in host_sources:
+        mask |= 1 << q
+    s = stream if stream is not None else torch.cuda.current_stream()
+    rc = _lib.lib().fmx_reduce_local(ptrs, len(sources), mask, out.data_ptr(),
+                                     out_host.data_ptr() if out_host is not None else None,
+                                     out.numel(), _dtype_code(out), OPS[op],
+                                     ctypes.c_float(1.0 if factor is None else factor),
+                                     int(s.cuda_stream))
+    _lib.check(rc, "fmx_reduce_local")
+    return out
+
+
 class ShmCommunicator:
     """Handle of one rank's membership in a host-SHM communicator."""
 
@@ -164,6 +187,15 @@ class ShmCommunicator:
         ms, n = ctypes.c_double(), ctypes.c_uint64()
         _lib.check(_lib.lib().fmx_comm_kernel_time(self._h, ctypes.byref(ms), ctypes.byref(n)))
         return ms.value, n.value
+
+    def monitor(self, seconds: float, cap: int = 1 << 20) -> list[tuple[int, int, int, int]]:
+        """Poll every rank's flags from the host for `seconds` (call it from a
+        helper thread while collectives run): [(ns, rank, flag, value)]."""
+        buf = (ctypes.c_uint64 * (2 * cap))()
+        n = ctypes.c_size_t()
+        _lib.check(_lib.lib().fmx_comm_monitor(self._h, seconds, buf, 2 * cap, ctypes.byref(n)))
+        return [(buf[2 * i], buf[2 * i + 1] >> 48, (buf[2 * i + 1] >> 32) & 0xFFFF,
+                 buf[2 * i + 1] & 0xFFFFFFFF) for i in range(n.value)]
 
     def flags(self) -> list[list[int]]:
         """Every rank's [STAGED, REDUCED, BC_STAGED, BC_DONE] counters."""

@@ -87,6 +87,9 @@ bool pid_alive(int pid) { return pid > 0 && (kill(pid, 0) == 0 || errno == EPERM
 
 }  // namespace
 
+struct fmx_comm;
+static inline cudaStream_t lane_stream(const fmx_comm* c, int lane);
+
 struct fmx_comm {
   int rank = -1, nranks = 0, nslots = 2, transport = FMX_TRANSPORT_CE, mig_aware = 1;
   size_t slice_bytes = 0, total_bytes = 0;
@@ -103,6 +106,8 @@ struct fmx_comm {
   cudaEvent_t fork = nullptr, joined[2] = {nullptr, nullptr};
   bool result_via_ce = false;  // CE transport: result slot by copy engine, not SM stores
   bool copy2d = true;          // coalesce regular copy runs into cudaMemcpy2DAsync
+  bool coarse = false;         // FMX_GRAIN=coarse: all-peer waits instead of per-piece
+  bool single_lane = false;    // FMX_LANES=1: both lanes on one stream
   // live kernel timing (fmx_comm_set_timing): event pairs around every reduce
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
@@ -133,6 +138,10 @@ struct fmx_comm {
     return (volatile uint32_t*)(base + L.flags_off + ((size_t)r * kFlagsPerRank + f) * 64);
   }
 };
+
+static inline cudaStream_t lane_stream(const fmx_comm* c, int lane) {
+  return c->single_lane ? c->lane[1] : c->lane[lane];
+}
 
 namespace {
 
@@ -212,7 +221,7 @@ class CudaSink final : public Sink {
 
   int copy(int lane, const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel) override {
     if (segs.empty()) return FMX_OK;
-    cudaStream_t s = c_->lane[lane];
+    cudaStream_t s = lane_stream(c_, lane);
     if (!use_kernel) {
       // copy engine; coalesce equal-size, equal-stride runs into one 2D copy
       size_t i = 0;
@@ -261,7 +270,7 @@ class CudaSink final : public Sink {
   int reduce(int lane, const PlanReduce& r) override {
     const ReduceArgs& a = r.args;
     if (a.len == 0) return FMX_OK;
-    cudaStream_t s = c_->lane[lane];
+    cudaStream_t s = lane_stream(c_, lane);
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (c_->timing) {
       if (c_->timed_used == c_->timed.size()) {
@@ -334,17 +343,17 @@ class CudaSink final : public Sink {
   }
 
   int d2d(int lane, void* dst, const void* src, size_t bytes, Annot, Annot) override {
-    FMX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c_->lane[lane]));
+    FMX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, lane_stream(c_, lane)));
     return FMX_OK;
   }
 
   int record(int lane, int ev) override {
-    FMX_CUDA(cudaEventRecord(c_->ev[ev], c_->lane[lane]));
+    FMX_CUDA(cudaEventRecord(c_->ev[ev], lane_stream(c_, lane)));
     return FMX_OK;
   }
 
   int wait_event(int lane, int ev) override {
-    FMX_CUDA(cudaStreamWaitEvent(c_->lane[lane], c_->ev[ev], 0));
+    FMX_CUDA(cudaStreamWaitEvent(lane_stream(c_, lane), c_->ev[ev], 0));
     return FMX_OK;
   }
 
@@ -359,7 +368,7 @@ class CudaSink final : public Sink {
     return op;
   }
   int batch(int lane, CUstreamBatchMemOpParams* ops, unsigned n) {
-    CUresult r = g_batch((CUstream)c_->lane[lane], n, ops, 0);
+    CUresult r = g_batch((CUstream)lane_stream(c_, lane), n, ops, 0);
     if (r != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "cuStreamBatchMemOp failed (%d)", (int)r);
     return FMX_OK;
   }
@@ -518,6 +527,19 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
     // slot R%2 was read by round R-2's fetches; within this collective the
     // lane-1 event after round R-2's REDUCED waits says they are done
     if (j >= 2 && (rc = k.wait_event(kLaneStage, kEvSlotFree + R % 2))) return rc;
+    if (c->coarse) {  // one batch of copies, one STAGED signal
+      segs.clear();
+      for (int o = 0; o < n; ++o) {
+        const size_t len = o == me ? 0 : g.len(o, j);
+        if (!len) continue;
+        const size_t off = c->in_off(R, o, me);
+        segs.push_back({src + g.lo(o, j) * g.esz, c->at(zc, off), len * g.esz,
+                        Annot{(int64_t)off, len * g.esz, me, R}, true,
+                        ubuf(g.lo(o, j) * g.esz, len * g.esz)});
+      }
+      if ((rc = k.copy(kLaneStage, segs, false, zc))) return rc;
+      return k.signal(kLaneStage, kStaged, R + 1);
+    }
     for (int i = 0; i < n - 1; ++i) {
       const int o = rot(i);
       const size_t len = g.len(o, j);
@@ -559,7 +581,21 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
         pr.write = Annot{(int64_t)out_off, mylen * g.esz, me, R};
       }
       // each contribution is fetched as soon as its contributor staged it
-      for (int i = 0; i < n - 1; ++i) {
+      if (c->coarse) {
+        if ((rc = k.wait_peers(kLaneMain, kStaged, R + 1, me))) return rc;
+        if (!zc) {
+          segs.clear();
+          for (int q = 0; q < n; ++q) {
+            if (q == me) continue;
+            const size_t off = c->in_off(R, me, q);
+            segs.push_back({c->at(false, off), c->scratch + (size_t)q * c->slice_bytes,
+                            mylen * g.esz, Annot{(int64_t)off, mylen * g.esz, q, R}, false,
+                            Annot{}});
+          }
+          if ((rc = k.copy(kLaneMain, segs, true, false))) return rc;
+        }
+      }
+      for (int i = 0; i < n - 1 && !c->coarse; ++i) {
         const int q = rot(i);
         if ((rc = k.wait_rank(kLaneMain, q, kStagedTo + me, R + 1))) return rc;
         if (!zc) {
@@ -594,7 +630,20 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
     }
     if ((rc = k.signal(kLaneMain, kReduced, R + 1))) return rc;
     // all-gather: each owner's result as soon as that owner has it
-    for (int i = 0; i < n - 1; ++i) {
+    if (c->coarse) {
+      if ((rc = k.wait_peers(kLaneMain, kReduced, R + 1, me))) return rc;
+      segs.clear();
+      for (int q = 0; q < n; ++q) {
+        const size_t len = q == me ? 0 : g.len(q, j);
+        if (!len) continue;
+        const size_t off = c->out_off(R, q);
+        segs.push_back({c->at(zc, off), dst + g.lo(q, j) * g.esz, len * g.esz,
+                        Annot{(int64_t)off, len * g.esz, q, R}, false,
+                        ubuf(g.lo(q, j) * g.esz, len * g.esz)});
+      }
+      if ((rc = k.copy(kLaneMain, segs, true, zc))) return rc;
+    }
+    for (int i = 0; i < n - 1 && !c->coarse; ++i) {
       const int q = rot(i);
       if ((rc = k.wait_rank(kLaneMain, q, kReduced, R + 1))) return rc;
       const size_t len = g.len(q, j);
@@ -948,6 +997,8 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   }
   if (const char* v = getenv("FMX_RESULT_VIA_CE")) c->result_via_ce = atoi(v) != 0;
   if (const char* v = getenv("FMX_COPY2D")) c->copy2d = atoi(v) != 0;
+  if (const char* v = getenv("FMX_GRAIN")) c->coarse = strcmp(v, "coarse") == 0;
+  if (const char* v = getenv("FMX_LANES")) c->single_lane = atoi(v) == 1;
   if (e != cudaSuccess) {
     h->aborted.store(1);
     fail(FMX_ERR_CUDA, "device mapping of %zu-byte segment failed: %s", c->total_bytes,
@@ -1010,6 +1061,49 @@ int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int 
     return plan_allreduce(c, sink, (const char*)send, (char*)recv, count, dtype, op, factor,
                           aligned);
   });
+}
+
+int fmx_reduce_local(const void* const* srcs, int nsrc, uint64_t sys_mask, void* dst,
+                     void* dst_sys, size_t count, int dtype, int op, float factor, void* stream) {
+  if (!srcs || nsrc < 1 || nsrc > FMX_MAX_RANKS || !dst)
+    return fail(FMX_ERR_INVALID_ARG, "bad arguments");
+  if (dtype != FMX_FLOAT32 && dtype != FMX_BFLOAT16)
+    return fail(FMX_ERR_INVALID_ARG, "bad dtype %d", dtype);
+  if (op < FMX_OP_SUM || op > FMX_OP_PREDIV_SUM) return fail(FMX_ERR_INVALID_ARG, "bad op %d", op);
+  if (count == 0) return FMX_OK;
+  ReduceArgs a;
+  memset(&a, 0, sizeof a);
+  uintptr_t bits = (uintptr_t)dst | (uintptr_t)dst_sys;
+  for (int q = 0; q < nsrc; ++q) {
+    if (!srcs[q]) return fail(FMX_ERR_INVALID_ARG, "null source %d", q);
+    a.src[q] = (const char*)srcs[q];
+    bits |= (uintptr_t)srcs[q];
+  }
+  a.nsrc = nsrc;
+  a.sys_mask = sys_mask;
+  a.out_dev = (char*)dst;
+  a.out_sys = (char*)dst_sys;
+  a.len = count;
+  a.op = op;
+  a.factor = factor;
+  cudaStream_t s = (cudaStream_t)stream;
+  constexpr int kThreads = 256, kU = 2;
+  const int V = dtype == FMX_FLOAT32 ? 4 : 8;
+  if ((bits & 15) == 0) {
+    int g = grid_for((count / V + kU - 1) / kU + 1, kThreads, 1184);
+    if (dtype == FMX_FLOAT32)
+      fmx_reduce_kernel<float, kU><<<g, kThreads, 0, s>>>(a);
+    else
+      fmx_reduce_kernel<__nv_bfloat16, kU><<<g, kThreads, 0, s>>>(a);
+  } else {
+    int g = grid_for(count, kThreads, 1184);
+    if (dtype == FMX_FLOAT32)
+      fmx_reduce_scalar_kernel<float><<<g, kThreads, 0, s>>>(a);
+    else
+      fmx_reduce_scalar_kernel<__nv_bfloat16><<<g, kThreads, 0, s>>>(a);
+  }
+  FMX_CUDA(cudaGetLastError());
+  return FMX_OK;
 }
 
 int fmx_host_buffer(fmx_comm_t c, int rank, void** ptr, size_t* bytes) {
@@ -1081,6 +1175,7 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   c.L = compute_layout(nranks, 2, slice_bytes, max_bytes);
   c.total_bytes = c.L.total;
   if (const char* v = getenv("FMX_RESULT_VIA_CE")) c.result_via_ce = atoi(v) != 0;
+  if (const char* v = getenv("FMX_GRAIN")) c.coarse = strcmp(v, "coarse") == 0;
   std::string out;
   TraceSink sink(&out);
   sink.nranks = nranks;
@@ -1192,6 +1287,32 @@ int fmx_comm_flags(fmx_comm_t c, uint32_t* out, int cap) {
     return fail(FMX_ERR_INVALID_ARG, "bad arguments");
   for (int r = 0; r < c->nranks; ++r)
     for (int f = 0; f < 4; ++f) out[r * 4 + f] = *c->flag_host(r, f);
+  return FMX_OK;
+}
+
+int fmx_comm_monitor(fmx_comm_t c, double seconds, uint64_t* out, size_t cap, size_t* n_out) {
+  if (!c || !c->base || !out || !n_out) return fail(FMX_ERR_INVALID_ARG, "bad arguments");
+  const int n = c->nranks, nf = kStagedTo + n;
+  std::vector<uint32_t> last((size_t)n * nf);
+  for (int r = 0; r < n; ++r)
+    for (int f = 0; f < nf; ++f) last[(size_t)r * nf + f] = *c->flag_host(r, f);
+  size_t k = 0;
+  const double t0 = now_s(), t_end = t0 + seconds;
+  double t = t0;
+  while (t < t_end && k + 2 <= cap) {
+    for (int r = 0; r < n; ++r)
+      for (int f = 0; f < nf; ++f) {
+        const uint32_t v = *c->flag_host(r, f);
+        uint32_t& l = last[(size_t)r * nf + f];
+        if (v != l && k + 2 <= cap) {
+          l = v;
+          out[k++] = (uint64_t)((t - t0) * 1e9);
+          out[k++] = ((uint64_t)r << 48) | ((uint64_t)f << 32) | v;
+        }
+      }
+    t = now_s();
+  }
+  *n_out = k / 2;
   return FMX_OK;
 }
 

@@ -251,6 +251,17 @@ def test_model_catches_a_broken_schedule(flag):
     assert failures > 0
 
 
+@pytest.mark.parametrize("n", [2, 7])
+def test_coarse_grain_variant(monkeypatch, n):
+    monkeypatch.setenv("FMX_GRAIN", "coarse")
+    progs = programs(n, SEQUENCES["mixed"], 4096, "ce")
+    for seed in range(6):
+        simulate(progs, seed)
+    merged = programs(n, SEQUENCES["mixed"], 4096, "ce", merged=True)
+    for seed in range(6):
+        simulate(merged, seed)
+
+
 def test_result_via_copy_engine_variant(monkeypatch):
     monkeypatch.setenv("FMX_RESULT_VIA_CE", "1")
     progs = programs(4, SEQUENCES["mixed"], 4096, "ce")
