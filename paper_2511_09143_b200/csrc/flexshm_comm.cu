@@ -54,20 +54,31 @@ namespace {
 
 typedef CUresult (*PFN_batchMemOp)(CUstream, unsigned int, CUstreamBatchMemOpParams*,
                                    unsigned int);
+typedef CUresult (*PFN_streamGetCtx)(CUstream, CUcontext*);
+typedef CUresult (*PFN_ctxPush)(CUcontext);
+typedef CUresult (*PFN_ctxPop)(CUcontext*);
 PFN_batchMemOp g_batch = nullptr;
+PFN_streamGetCtx g_stream_ctx = nullptr;
+PFN_ctxPush g_ctx_push = nullptr;
+PFN_ctxPop g_ctx_pop = nullptr;
 std::once_flag g_driver_once;
 int g_driver_status = FMX_OK;
 
 int load_driver() {
   std::call_once(g_driver_once, [] {
-    cudaDriverEntryPointQueryResult q;
-    cudaError_t e = cudaGetDriverEntryPointByVersion("cuStreamBatchMemOp", (void**)&g_batch,
-                                                     12000, cudaEnableDefault, &q);
-    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !g_batch)
-      g_driver_status = FMX_ERR_UNSUPPORTED;
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      cudaError_t e = cudaGetDriverEntryPointByVersion(name, fn, 12000, cudaEnableDefault, &q);
+      if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !*fn)
+        g_driver_status = FMX_ERR_UNSUPPORTED;
+    };
+    get("cuStreamBatchMemOp", (void**)&g_batch);
+    get("cuStreamGetCtx", (void**)&g_stream_ctx);
+    get("cuCtxPushCurrent", (void**)&g_ctx_push);
+    get("cuCtxPopCurrent", (void**)&g_ctx_pop);
   });
   if (g_driver_status != FMX_OK)
-    return fail(FMX_ERR_UNSUPPORTED, "cuStreamBatchMemOp entry point unavailable");
+    return fail(FMX_ERR_UNSUPPORTED, "driver entry points (stream mem ops / contexts) unavailable");
   return FMX_OK;
 }
 
@@ -101,12 +112,15 @@ struct fmx_comm {
   uint32_t ar_round = 0, bc_round = 0;
   int64_t barrier_gen = 0;
   char* scratch = nullptr;  // CE transport: n * slice_bytes of HBM
-  cudaStream_t lane[2] = {nullptr, nullptr};
+  cudaStream_t lane[2] = {nullptr, nullptr};  // lane[1] unused: lane 1 is the caller's stream
+  cudaStream_t user = nullptr;                 // caller's stream of the current collective
+  CUcontext lane_ctx = nullptr;                // context the lane objects were created in
   cudaEvent_t ev[8] = {};  // intra-rank lane sync (see the kEv* ids)
   cudaEvent_t fork = nullptr, joined[2] = {nullptr, nullptr};
   bool result_via_ce = false;  // CE transport: result slot by copy engine, not SM stores
   bool copy2d = true;          // coalesce regular copy runs into cudaMemcpy2DAsync
-  bool coarse = false;         // FMX_GRAIN=coarse: all-peer waits instead of per-piece
+  bool coarse = true;          // FMX_GRAIN=fine: per-piece waits instead of all-peer
+  bool ramp = true;            // FMX_RAMP=0: equal rounds (no pipeline-fill ramp)
   bool single_lane = false;    // FMX_LANES=1: both lanes on one stream
   // live kernel timing (fmx_comm_set_timing): event pairs around every reduce
   bool timing = false;
@@ -140,7 +154,7 @@ struct fmx_comm {
 };
 
 static inline cudaStream_t lane_stream(const fmx_comm* c, int lane) {
-  return c->single_lane ? c->lane[1] : c->lane[lane];
+  return (c->single_lane || lane == 1) ? c->user : c->lane[0];
 }
 
 namespace {
@@ -459,15 +473,30 @@ class TraceSink final : public Sink {
   int seq_[8] = {};
 };
 
+// Round j of every chunk covers [prefix(j), prefix(j) + size(j)).  With ramp
+// the first rounds are slice/8, /4, /2: the pipeline fills (stage of round 0 is
+// pure D2H with the H2D direction idle) in 1/8 of the time a full slice takes.
 struct Geometry {
   size_t count, esz, chunk, slice;
   uint32_t rounds;
-  size_t lo(int owner, uint32_t j) const { return (size_t)owner * chunk + (size_t)j * slice; }
+  bool ramp = false;
+  size_t size(uint32_t j) const {
+    if (!ramp || j >= 3) return slice;
+    return std::max<size_t>(16 / esz, slice >> (3 - j));
+  }
+  size_t prefix(uint32_t j) const {
+    if (!ramp) return (size_t)j * slice;
+    size_t p = 0;
+    for (uint32_t i = 0; i < j && i < 3; ++i) p += size(i);
+    if (j > 3) p += (size_t)(j - 3) * slice;
+    return p;
+  }
+  size_t lo(int owner, uint32_t j) const { return (size_t)owner * chunk + prefix(j); }
   size_t len(int owner, uint32_t j) const {
     size_t a = lo(owner, j);
     size_t end = std::min((size_t)(owner + 1) * chunk, count);
     if (a >= end) return 0;
-    return std::min(slice, end - a);
+    return std::min(size(j), end - a);
   }
 };
 
@@ -479,7 +508,9 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype) {
   const size_t vec = 16 / g.esz;
   g.chunk = ((count + n - 1) / n + vec - 1) / vec * vec;  // 16-byte aligned chunk starts
   g.slice = c->slice_bytes / g.esz;
-  g.rounds = (uint32_t)((g.chunk + g.slice - 1) / g.slice);
+  g.ramp = c->ramp && g.chunk > g.slice;
+  g.rounds = 0;
+  while (g.prefix(g.rounds) < g.chunk) ++g.rounds;
   return g;
 }
 
@@ -784,14 +815,50 @@ int plan_broadcast(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
 }
 
 // Fork the lanes off the caller's stream, run the plan, join them back.
+// (Re)create the lane-0 stream and the lane events in `ctx`, the context of
+// the caller's stream (a green context, an MPS client's, or the primary one),
+// so every lane object lives where the caller's work lives.
+int make_lane_objects(fmx_comm* c, CUcontext ctx) {
+  c->lane[0] = nullptr;  // objects of an earlier context are abandoned, not destroyed
+  FMX_CUDA(cudaStreamCreateWithFlags(&c->lane[0], cudaStreamNonBlocking));
+  FMX_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+  FMX_CUDA(cudaEventCreateWithFlags(&c->joined[0], cudaEventDisableTiming));
+  FMX_CUDA(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
+  for (int i = 0; i < 8; ++i) FMX_CUDA(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
+  for (auto& pr : c->timed) pr = {nullptr, nullptr};
+  c->timed.clear();
+  c->timed_used = 0;
+  c->lane_ctx = ctx;
+  return FMX_OK;
+}
+
+// Run one collective: lane 1 is the caller's stream, lane 0 forks off it and
+// joins back.  Every runtime call happens with the caller's stream context
+// current (DDP calls hooks from autograd threads whose current context may be
+// another one).
 template <typename F>
 int on_lanes(fmx_comm* c, cudaStream_t user, F&& body) {
-  FMX_CUDA(cudaEventRecord(c->fork, user));
-  for (int l = 0; l < 2; ++l) FMX_CUDA(cudaStreamWaitEvent(c->lane[l], c->fork, 0));
-  int rc = body();
-  for (int l = 0; l < 2; ++l) {
-    FMX_CUDA(cudaEventRecord(c->joined[l], c->lane[l]));
-    FMX_CUDA(cudaStreamWaitEvent(user, c->joined[l], 0));
+  CUcontext ctx = nullptr;
+  if (g_stream_ctx((CUstream)user, &ctx) != CUDA_SUCCESS || !ctx)
+    return fail(FMX_ERR_CUDA, "cannot resolve the context of the caller's stream");
+  if (g_ctx_push(ctx) != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "cuCtxPushCurrent failed");
+  struct Pop {
+    ~Pop() {
+      CUcontext dummy;
+      g_ctx_pop(&dummy);
+    }
+  } pop;
+  int rc;
+  if (ctx != c->lane_ctx && (rc = make_lane_objects(c, ctx))) return rc;
+  c->user = user;
+  if (!c->single_lane) {
+    FMX_CUDA(cudaEventRecord(c->fork, user));
+    FMX_CUDA(cudaStreamWaitEvent(c->lane[0], c->fork, 0));
+  }
+  rc = body();
+  if (!c->single_lane) {
+    FMX_CUDA(cudaEventRecord(c->joined[0], c->lane[0]));
+    FMX_CUDA(cudaStreamWaitEvent(user, c->joined[0], 0));
   }
   if (rc) return rc;
   FMX_CUDA(cudaEventRecord(c->done, user));
@@ -987,18 +1054,13 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   }
   // HBM scratch: CE contributions [n] (device path) / [2][n] fetch + [2] result (host path)
   if (e == cudaSuccess) e = cudaMalloc((void**)&c->scratch, (2 * (size_t)nranks + 2) * c->slice_bytes);
-  for (int i = 0; i < 8 && e == cudaSuccess; ++i)
-    e = cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
-  for (int l = 0; l < 2 && e == cudaSuccess; ++l) {
-    e = cudaStreamCreateWithFlags(&c->lane[l], cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->joined[l], cudaEventDisableTiming);
-  }
+
+
   if (const char* v = getenv("FMX_RESULT_VIA_CE")) c->result_via_ce = atoi(v) != 0;
   if (const char* v = getenv("FMX_COPY2D")) c->copy2d = atoi(v) != 0;
-  if (const char* v = getenv("FMX_GRAIN")) c->coarse = strcmp(v, "coarse") == 0;
+  if (const char* v = getenv("FMX_GRAIN")) c->coarse = strcmp(v, "fine") != 0;
   if (const char* v = getenv("FMX_LANES")) c->single_lane = atoi(v) == 1;
+  if (const char* v = getenv("FMX_RAMP")) c->ramp = atoi(v) != 0;
   if (e != cudaSuccess) {
     h->aborted.store(1);
     fail(FMX_ERR_CUDA, "device mapping of %zu-byte segment failed: %s", c->total_bytes,
@@ -1041,7 +1103,7 @@ int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int 
     return on_lanes(c, s, [&]() -> int {
       if (op == FMX_OP_SUM) {
         if (send != recv)
-          FMX_CUDA(cudaMemcpyAsync(recv, send, count * esz, cudaMemcpyDeviceToDevice, c->lane[kLaneMain]));
+          FMX_CUDA(cudaMemcpyAsync(recv, send, count * esz, cudaMemcpyDeviceToDevice, lane_stream(c, kLaneMain)));
         return FMX_OK;
       }
       PlanReduce pr;
@@ -1149,7 +1211,7 @@ int fmx_broadcast(fmx_comm_t c, const void* send, void* recv, size_t count, int 
   if (c->nranks == 1) {
     return on_lanes(c, s, [&]() -> int {
       if (send != recv)
-        FMX_CUDA(cudaMemcpyAsync(recv, send, count * esz, cudaMemcpyDeviceToDevice, c->lane[kLaneMain]));
+        FMX_CUDA(cudaMemcpyAsync(recv, send, count * esz, cudaMemcpyDeviceToDevice, lane_stream(c, kLaneMain)));
       return FMX_OK;
     });
   }
@@ -1175,7 +1237,8 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   c.L = compute_layout(nranks, 2, slice_bytes, max_bytes);
   c.total_bytes = c.L.total;
   if (const char* v = getenv("FMX_RESULT_VIA_CE")) c.result_via_ce = atoi(v) != 0;
-  if (const char* v = getenv("FMX_GRAIN")) c.coarse = strcmp(v, "coarse") == 0;
+  if (const char* v = getenv("FMX_GRAIN")) c.coarse = strcmp(v, "fine") != 0;
+  if (const char* v = getenv("FMX_RAMP")) c.ramp = atoi(v) != 0;
   std::string out;
   TraceSink sink(&out);
   sink.nranks = nranks;
@@ -1220,6 +1283,7 @@ int fmx_barrier(fmx_comm_t c, double timeout_s) {
 int fmx_comm_destroy(fmx_comm_t c) {
   if (!c) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
   int rc = FMX_OK;
+  const bool pushed = c->lane_ctx && g_ctx_push && g_ctx_push(c->lane_ctx) == CUDA_SUCCESS;
   if (c->has_done && cudaEventSynchronize(c->done) != cudaSuccess)
     rc = fail(FMX_ERR_CUDA, "pending collective failed: %s", cudaGetErrorString(cudaGetLastError()));
   if (c->done) cudaEventDestroy(c->done);
@@ -1233,6 +1297,10 @@ int fmx_comm_destroy(fmx_comm_t c) {
   for (int l = 0; l < 2; ++l) {
     if (c->lane[l]) cudaStreamDestroy(c->lane[l]);
     if (c->joined[l]) cudaEventDestroy(c->joined[l]);
+  }
+  if (pushed) {
+    CUcontext dummy;
+    g_ctx_pop(&dummy);
   }
   if (c->scratch) cudaFree(c->scratch);
   if (c->registered) cudaHostUnregister(c->base);
@@ -1326,6 +1394,14 @@ int fmx_comm_set_timing(fmx_comm_t c, int on) {
 int fmx_comm_kernel_time(fmx_comm_t c, double* total_ms, uint64_t* count) {
   if (!c || !total_ms || !count) return fail(FMX_ERR_INVALID_ARG, "null argument");
   double sum = 0;
+  const bool pushed = c->lane_ctx && g_ctx_push(c->lane_ctx) == CUDA_SUCCESS;
+  struct Pop {
+    bool on;
+    ~Pop() {
+      CUcontext d;
+      if (on) g_ctx_pop(&d);
+    }
+  } pop{pushed};
   for (size_t i = 0; i < c->timed_used; ++i) {
     FMX_CUDA(cudaEventSynchronize(c->timed[i].second));
     float ms = 0;

@@ -238,7 +238,7 @@ def test_model_catches_a_broken_schedule(flag):
     the protocol after this checker showed its waits were implied.)"""
     progs = programs(3, [("allreduce", 60_000, 0), ("allreduce", 60_000, 0)], 4096, "ce")
     lanes = progs[1]
-    hit = (lambda f: f >= STAGED_TO) if flag == "staged_to" else (lambda f: f == REDUCED)
+    hit = (lambda f: f == 0 or f >= STAGED_TO) if flag == "staged_to" else (lambda f: f == REDUCED)
     broken_lanes = [[op for op in lane if not (op[0] == "A" and hit(op[2]))] for lane in lanes]
     assert broken_lanes != lanes
     broken = [broken_lanes if r == 1 else p for r, p in enumerate(progs)]
@@ -252,8 +252,10 @@ def test_model_catches_a_broken_schedule(flag):
 
 
 @pytest.mark.parametrize("n", [2, 7])
-def test_coarse_grain_variant(monkeypatch, n):
-    monkeypatch.setenv("FMX_GRAIN", "coarse")
+@pytest.mark.parametrize("grain,ramp", [("fine", "1"), ("coarse", "0"), ("fine", "0")])
+def test_schedule_variants(monkeypatch, n, grain, ramp):
+    monkeypatch.setenv("FMX_GRAIN", grain)
+    monkeypatch.setenv("FMX_RAMP", ramp)
     progs = programs(n, SEQUENCES["mixed"], 4096, "ce")
     for seed in range(6):
         simulate(progs, seed)
