@@ -54,7 +54,7 @@ def parse_args(argv=None):
     p.add_argument("--count", type=int, default=RESNET50_PARAMS)
     p.add_argument("--dtype", choices=["f32", "bf16"], default="f32")
     p.add_argument("--transport", choices=["auto", "ce", "zc"], default="auto")
-    p.add_argument("--mode", choices=["green", "mps", "full"], default="green")
+    p.add_argument("--mode", choices=["green", "mps", "mps+green", "full"], default="green")
     p.add_argument("--slice-bytes", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -65,7 +65,7 @@ def parse_args(argv=None):
     p.add_argument("--no-train", action="store_true", help="skip the ResNet-50 DP img/s leg")
     p.add_argument("--timeline", default=None, help="write a host-polled flag timeline here")
     p.add_argument("--train-only", action="store_true")
-    p.add_argument("--train-mode", choices=["green", "mps", "full"], default="green")
+    p.add_argument("--train-mode", choices=["green", "mps", "mps+green", "full"], default="green")
     p.add_argument("--batch", type=int, default=32)
     p.add_argument("--train-steps", type=int, default=10)
     p.add_argument("--train-warmup", type=int, default=5)
@@ -432,15 +432,9 @@ def run_ranks(body, spawned, mine, job_key, n, cfg, inst_mode, gpu_local, sample
     """Rank mine[0] runs in this process, the rest in spawned processes."""
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
-    mps = None
     results, errors = {}, []
-    if inst_mode == "mps":
-        from paper_2511_09143_b200.launcher import MPS_PERCENT, MpsDaemon
-        mps = MpsDaemon(job_key)
-        if not mps.start():
-            raise RuntimeError("MPS daemon failed to start")
-        os.environ.update(mps.env)
-        os.environ["CUDA_MPS_ACTIVE_THREAD_PERCENTAGE"] = str(MPS_PERCENT)
+    if inst_mode in ("mps", "mps+green") and "CUDA_MPS_PIPE_DIRECTORY" not in os.environ:
+        raise RuntimeError("MPS instance mode needs the daemon started by main()")
     try:
         with ctx.Pool(max(1, len(mine) - 1)) as pool:
             pending = [pool.apply_async(spawned, (r, job_key, n, cfg, inst_mode, gpu_local))
@@ -457,10 +451,7 @@ def run_ranks(body, spawned, mine, job_key, n, cfg, inst_mode, gpu_local, sample
                 except BaseException as exc:  # noqa: BLE001
                     errors.append((r, exc))
     finally:
-        if mps is not None:
-            mps.stop()
-            for k in list(mps.env) + ["CUDA_MPS_ACTIVE_THREAD_PERCENTAGE"]:
-                os.environ.pop(k, None)
+        pass
     if errors:
         raise RuntimeError(f"rank {errors[0][0]} failed: {errors[0][1]!r}") from errors[0][1]
     return results
@@ -659,6 +650,24 @@ def main(argv=None):
                         "the same SHM RS/AG algorithm, oracle/flexshm_oracle.c"}
         print(json.dumps(line))
         return 0
+    mps = None
+    if "mps" in args.mode or (not args.no_train and "mps" in args.train_mode):
+        # one private MPS daemon for the whole run (every rank process, this one
+        # included, is a client); 1g share of the SMs per client
+        from paper_2511_09143_b200.launcher import MPS_PERCENT, MpsDaemon
+        mps = MpsDaemon(f"bench-{os.getpid()}")
+        if not mps.start():
+            raise RuntimeError("MPS daemon failed to start")
+        os.environ.update(mps.env)
+        os.environ["CUDA_MPS_ACTIVE_THREAD_PERCENTAGE"] = str(MPS_PERCENT)
+    try:
+        return _main(args, world, n, unit)
+    finally:
+        if mps is not None:
+            mps.stop()
+
+
+def _main(args, world, n, unit):
     if args.train_only:
         d = decision_for(args.gpus, args.ranks_per_gpu)
         print(json.dumps({"resnet50": run_train(args, d, f"train-{os.getpid()}")}))

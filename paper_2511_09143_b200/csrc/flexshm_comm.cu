@@ -120,6 +120,7 @@ struct fmx_comm {
   bool result_via_ce = false;  // CE transport: result slot by copy engine, not SM stores
   bool copy2d = true;          // coalesce regular copy runs into cudaMemcpy2DAsync
   bool coarse = true;          // FMX_GRAIN=fine: per-piece waits instead of all-peer
+  bool coarse_gather = true;   // FMX_GATHER_GRAIN=fine: per-owner gather waits only
   bool ramp = true;            // FMX_RAMP=0: equal rounds (no pipeline-fill ramp)
   bool single_lane = false;    // FMX_LANES=1: both lanes on one stream
   // live kernel timing (fmx_comm_set_timing): event pairs around every reduce
@@ -473,25 +474,16 @@ class TraceSink final : public Sink {
   int seq_[8] = {};
 };
 
-// Round j of every chunk covers [prefix(j), prefix(j) + size(j)).  With ramp
-// the first rounds are slice/8, /4, /2: the pipeline fills (stage of round 0 is
-// pure D2H with the H2D direction idle) in 1/8 of the time a full slice takes.
+// Round j of every chunk covers [prefix(j), prefix(j) + size(j)).  With the
+// ramp, the first rounds are slice/8, /4, /2 and the last ones /2, /4, /8: the
+// pipeline fills (round 0's stage is pure D2H, the H2D direction idle) and
+// drains (the last gather is pure H2D) in 1/8 of the time a full slice takes.
 struct Geometry {
   size_t count, esz, chunk, slice;
   uint32_t rounds;
-  bool ramp = false;
-  size_t size(uint32_t j) const {
-    if (!ramp || j >= 3) return slice;
-    return std::max<size_t>(16 / esz, slice >> (3 - j));
-  }
-  size_t prefix(uint32_t j) const {
-    if (!ramp) return (size_t)j * slice;
-    size_t p = 0;
-    for (uint32_t i = 0; i < j && i < 3; ++i) p += size(i);
-    if (j > 3) p += (size_t)(j - 3) * slice;
-    return p;
-  }
-  size_t lo(int owner, uint32_t j) const { return (size_t)owner * chunk + prefix(j); }
+  std::vector<size_t> start;  // start[j] = prefix of round j; start[rounds] >= chunk
+  size_t size(uint32_t j) const { return start[j + 1] - start[j]; }
+  size_t lo(int owner, uint32_t j) const { return (size_t)owner * chunk + start[j]; }
   size_t len(int owner, uint32_t j) const {
     size_t a = lo(owner, j);
     size_t end = std::min((size_t)(owner + 1) * chunk, count);
@@ -508,9 +500,42 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype) {
   const size_t vec = 16 / g.esz;
   g.chunk = ((count + n - 1) / n + vec - 1) / vec * vec;  // 16-byte aligned chunk starts
   g.slice = c->slice_bytes / g.esz;
-  g.ramp = c->ramp && g.chunk > g.slice;
-  g.rounds = 0;
-  while (g.prefix(g.rounds) < g.chunk) ++g.rounds;
+  std::vector<size_t> sizes;
+  const size_t s = g.slice;
+  if (c->ramp && g.chunk > 2 * s) {
+    const size_t up[3] = {s / 8, s / 4, s / 2}, down[3] = {s / 2, s / 4, s / 8};
+    const size_t tail = s / 2 + s / 4 + s / 8;
+    size_t left = g.chunk;
+    for (size_t x : up) {
+      sizes.push_back(x);
+      left -= x;
+    }
+    while (left > tail + s) {
+      sizes.push_back(s);
+      left -= s;
+    }
+    // split what is left (<= s + tail) into at most one slice plus the ramp-down
+    if (left > tail) {
+      sizes.push_back(left - tail);
+      left = tail;
+    }
+    for (size_t x : down) {
+      if (!left) break;
+      const size_t y = std::min(x, left);
+      sizes.push_back(y);
+      left -= y;
+    }
+  } else {
+    for (size_t left = g.chunk; left;) {
+      const size_t y = std::min(s, left);
+      sizes.push_back(y);
+      left -= y;
+    }
+  }
+  if (sizes.empty()) sizes.push_back(0);  // count == 0 never reaches here; keep rounds >= 1
+  g.rounds = (uint32_t)sizes.size();
+  g.start.assign(g.rounds + 1, 0);
+  for (uint32_t j = 0; j < g.rounds; ++j) g.start[j + 1] = g.start[j] + sizes[j];
   return g;
 }
 
@@ -661,7 +686,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
     }
     if ((rc = k.signal(kLaneMain, kReduced, R + 1))) return rc;
     // all-gather: each owner's result as soon as that owner has it
-    if (c->coarse) {
+    if (c->coarse_gather) {
       if ((rc = k.wait_peers(kLaneMain, kReduced, R + 1, me))) return rc;
       segs.clear();
       for (int q = 0; q < n; ++q) {
@@ -674,7 +699,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
       }
       if ((rc = k.copy(kLaneMain, segs, true, zc))) return rc;
     }
-    for (int i = 0; i < n - 1 && !c->coarse; ++i) {
+    for (int i = 0; i < n - 1 && !c->coarse_gather; ++i) {
       const int q = rot(i);
       if ((rc = k.wait_rank(kLaneMain, q, kReduced, R + 1))) return rc;
       const size_t len = g.len(q, j);
@@ -1059,6 +1084,8 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (const char* v = getenv("FMX_RESULT_VIA_CE")) c->result_via_ce = atoi(v) != 0;
   if (const char* v = getenv("FMX_COPY2D")) c->copy2d = atoi(v) != 0;
   if (const char* v = getenv("FMX_GRAIN")) c->coarse = strcmp(v, "fine") != 0;
+  c->coarse_gather = c->coarse;
+  if (const char* v = getenv("FMX_GATHER_GRAIN")) c->coarse_gather = strcmp(v, "fine") != 0;
   if (const char* v = getenv("FMX_LANES")) c->single_lane = atoi(v) == 1;
   if (const char* v = getenv("FMX_RAMP")) c->ramp = atoi(v) != 0;
   if (e != cudaSuccess) {
@@ -1238,6 +1265,8 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   c.total_bytes = c.L.total;
   if (const char* v = getenv("FMX_RESULT_VIA_CE")) c.result_via_ce = atoi(v) != 0;
   if (const char* v = getenv("FMX_GRAIN")) c.coarse = strcmp(v, "fine") != 0;
+  c.coarse_gather = c.coarse;
+  if (const char* v = getenv("FMX_GATHER_GRAIN")) c.coarse_gather = strcmp(v, "fine") != 0;
   if (const char* v = getenv("FMX_RAMP")) c.ramp = atoi(v) != 0;
   std::string out;
   TraceSink sink(&out);

@@ -252,9 +252,11 @@ def test_model_catches_a_broken_schedule(flag):
 
 
 @pytest.mark.parametrize("n", [2, 7])
-@pytest.mark.parametrize("grain,ramp", [("fine", "1"), ("coarse", "0"), ("fine", "0")])
-def test_schedule_variants(monkeypatch, n, grain, ramp):
+@pytest.mark.parametrize("grain,gather,ramp", [("fine", "fine", "1"), ("coarse", "coarse", "0"),
+                                               ("fine", "fine", "0"), ("coarse", "fine", "1")])
+def test_schedule_variants(monkeypatch, n, grain, gather, ramp):
     monkeypatch.setenv("FMX_GRAIN", grain)
+    monkeypatch.setenv("FMX_GATHER_GRAIN", gather)
     monkeypatch.setenv("FMX_RAMP", ramp)
     progs = programs(n, SEQUENCES["mixed"], 4096, "ce")
     for seed in range(6):
