@@ -66,6 +66,8 @@ def parse_args(argv=None):
     p.add_argument("--timeline", default=None, help="write a host-polled flag timeline here")
     p.add_argument("--train-only", action="store_true")
     p.add_argument("--train-mode", choices=["green", "mps", "mps+green", "full"], default="green")
+    p.add_argument("--sweep", action="store_true", help="message-size sweep (configs[4]) instead")
+    p.add_argument("--sweep-max", type=int, default=1 << 30)
     p.add_argument("--batch", type=int, default=32)
     p.add_argument("--train-steps", type=int, default=10)
     p.add_argument("--train-warmup", type=int, default=5)
@@ -354,6 +356,78 @@ def rank_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_lo
 
 def _spawned_rank(rank, job_key, n, cfg, inst_mode, gpu_local):
     return rank_body(rank, job_key, n, cfg, inst_mode, gpu_local)
+
+
+SWEEP_SIZES = [1 << k for k in range(10, 31, 2)]  # 1 KiB ... 1 GiB (BASELINE configs[4])
+
+
+def sweep_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_local: int):
+    """Size sweep (BASELINE configs[4]): device-buffer allreduce latency /
+    algbw from 1 KiB to 1 GiB.  Per size: warm-up, then enough back-to-back
+    calls for ~0.2 s of work, CUDA events on the rank's stream."""
+    import torch
+
+    from paper_2511_09143_b200 import instance as inst_mod
+    from paper_2511_09143_b200.comm import init_process_group
+
+    gpu_id, inst_id = cfg["instances"][rank]
+    inst = inst_mod.bind(gpu_id, inst_id, cfg["profiles"][rank], mode=inst_mode, device=gpu_local)
+    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n,
+                              transport=cfg["transport"], slice_bytes=cfg["slice_bytes"],
+                              timeout_s=300)
+    stream = inst.stream
+    esz = 4 if cfg["dtype"] == "f32" else 2
+    tdt = torch.float32 if esz == 4 else torch.bfloat16
+    sizes = [b for b in cfg["sizes"]]
+    with torch.cuda.stream(stream):
+        buf = torch.randn(max(sizes) // esz, device=f"cuda:{gpu_local}").to(tdt)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    out = {"rank": rank, "ms": {}}
+    for b in sizes:
+        x = buf[: b // esz]
+        k = max(3, min(200, int(0.2 / max(b * 2 / 50e9 * n, 40e-6))))
+        for _ in range(3):
+            comm.allreduce(x, op="avg", stream=stream)
+        comm.barrier(300)
+        torch.cuda.synchronize()
+        comm.barrier(300)
+        ev0.record(stream)
+        for _ in range(k):
+            comm.allreduce(x, op="avg", stream=stream)
+        ev1.record(stream)
+        ev1.synchronize()
+        out["ms"][b] = (ev0.elapsed_time(ev1) / k, k)
+    comm.barrier(300)
+    comm.destroy()
+    return out
+
+
+def _spawned_sweep(rank, job_key, n, cfg, inst_mode, gpu_local):
+    return sweep_body(rank, job_key, n, cfg, inst_mode, gpu_local)
+
+
+def run_sweep(args) -> list[dict]:
+    """One JSON line per message size, ranks of one GPU (1-GPU layout)."""
+    d = decision_for(args.gpus, args.ranks_per_gpu)
+    n = len(d.instances)
+    cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
+           "slice_bytes": args.slice_bytes, "dtype": args.dtype,
+           "sizes": [b for b in SWEEP_SIZES if b <= args.sweep_max]}
+    res = run_ranks(sweep_body, _spawned_sweep, list(range(n)), f"sweep-{os.getpid()}", n, cfg,
+                    args.mode, 0)
+    lines = []
+    for b in cfg["sizes"]:
+        ms = max(r["ms"][b][0] for r in res.values())
+        per_gpu = [n]
+        lines.append({"sweep": "allreduce size sweep (BASELINE configs[4])", "bytes": b,
+                      "ranks": n, "instance_mode": args.mode, "dtype": args.dtype,
+                      "ms": ms, "algbw_gbs": b / ms / 1e6,
+                      "busbw_gbs": b / ms / 1e6 * 2 * (n - 1) / n,
+                      "iters": res[0]["ms"][b][1],
+                      "step_roofline_frac": step_roofline(n, per_gpu, b, ms / 1e3,
+                                                          LINK_PEAK_FALLBACK)["frac"]})
+    return lines
 
 
 def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_local: int):
@@ -668,6 +742,14 @@ def main(argv=None):
 
 
 def _main(args, world, n, unit):
+    if args.sweep:
+        lines = run_sweep(args)
+        for ln in lines:
+            print(json.dumps(ln))
+        if args.out:
+            with open(args.out, "w") as f:
+                f.writelines(json.dumps(ln) + "\n" for ln in lines)
+        return 0
     if args.train_only:
         d = decision_for(args.gpus, args.ranks_per_gpu)
         print(json.dumps({"resnet50": run_train(args, d, f"train-{os.getpid()}")}))

@@ -50,6 +50,7 @@ extern "C" {
 #define FMX_MIG_ID_LEN 128
 #define FMX_MAX_RANKS 64
 #define FMX_MAX_RANKS_PER_BUS 10
+#define FMX_MAX_SLOTS 4 /* pipeline depth limit (slots per SHM region) */
 
 enum fmx_status {
   FMX_OK = 0,
@@ -126,10 +127,10 @@ int fmx_restore_bus_id(const char* label, char* out);
  * the table is validated with the rules above (mig_aware), the segment is
  * pinned and device-mapped (cudaHostRegister Mapped|Portable) in the calling
  * thread's current CUDA context.  slice_bytes = bytes per (owner,
- * contributor) pipeline slot, 0 = default; nslots must be 2 (double
- * buffering) or 0 = default.  host_bytes = size of every rank's registered
- * host buffer (fmx_host_buffer), 0 = none.  Rank 0's slice_bytes / host_bytes
- * win.  timeout_s bounds every bootstrap wait. */
+ * contributor) pipeline slot, 0 = default; nslots = pipeline depth, 2 (double
+ * buffering) .. FMX_MAX_SLOTS, 0 = default (2, or env FMX_SLOTS).  host_bytes =
+ * size of every rank's registered host buffer (fmx_host_buffer), 0 = none.
+ * Rank 0's slice_bytes / nslots / host_bytes win.  timeout_s bounds every bootstrap wait. */
 int fmx_comm_init(fmx_comm_t* comm, const char* job_key, int nranks, int rank,
                   const fmx_peer_info* self, int mig_aware, size_t slice_bytes, int nslots,
                   size_t host_bytes, int transport, double timeout_s);

@@ -93,6 +93,7 @@ int load_driver() {
 constexpr size_t kDefaultSliceCap = 4u << 20;   // bytes per (owner, contributor) slot
 constexpr size_t kSegmentBudget = 1ull << 30;   // default cap on data-slot bytes
 constexpr int kBatchMax = 128;                  // memops per cuStreamBatchMemOp call
+constexpr int kNumEvents = 2 * FMX_MAX_SLOTS + 5;  // W[K], G[K], fetched[2], reduced[2], inputs
 
 bool pid_alive(int pid) { return pid > 0 && (kill(pid, 0) == 0 || errno == EPERM); }
 
@@ -112,17 +113,17 @@ struct fmx_comm {
   uint32_t ar_round = 0, bc_round = 0;
   int64_t barrier_gen = 0;
   char* scratch = nullptr;  // CE transport: n * slice_bytes of HBM
-  cudaStream_t lane[2] = {nullptr, nullptr};  // lane[1] unused: lane 1 is the caller's stream
+  cudaStream_t lane[2] = {nullptr, nullptr};  // lane 0 (stage) and lane 2 (gather); lane 1 is the caller's stream
   cudaStream_t user = nullptr;                 // caller's stream of the current collective
   CUcontext lane_ctx = nullptr;                // context the lane objects were created in
-  cudaEvent_t ev[8] = {};  // intra-rank lane sync (see the kEv* ids)
+  cudaEvent_t ev[kNumEvents] = {};  // intra-rank lane sync (see the kEv* ids)
   cudaEvent_t fork = nullptr, joined[2] = {nullptr, nullptr};
   bool result_via_ce = false;  // CE transport: result slot by copy engine, not SM stores
   bool copy2d = true;          // coalesce regular copy runs into cudaMemcpy2DAsync
   bool coarse = true;          // FMX_GRAIN=fine: per-piece waits instead of all-peer
   bool coarse_gather = true;   // FMX_GATHER_GRAIN=fine: per-owner gather waits only
   bool ramp = true;            // FMX_RAMP=0: equal rounds (no pipeline-fill ramp)
-  bool single_lane = false;    // FMX_LANES=1: both lanes on one stream
+  int nlanes = 3;              // FMX_LANES=1: one stream; 2: gather on the reduce lane
   // live kernel timing (fmx_comm_set_timing): event pairs around every reduce
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
@@ -155,7 +156,9 @@ struct fmx_comm {
 };
 
 static inline cudaStream_t lane_stream(const fmx_comm* c, int lane) {
-  return (c->single_lane || lane == 1) ? c->user : c->lane[0];
+  if (c->nlanes == 1 || lane == 1) return c->user;
+  if (lane == 0) return c->lane[0];
+  return c->nlanes == 3 ? c->lane[1] : c->user;
 }
 
 namespace {
@@ -178,8 +181,9 @@ void unmap(fmx_comm* c) {
 // schedule of every rank of any world size can be model-checked on a CPU
 // (fmx_trace_plan, tests/test_protocol_model.py).
 
-constexpr int kLaneStage = 0;  // D2H lane
-constexpr int kLaneMain = 1;   // H2D + reduce lane
+constexpr int kLaneStage = 0;   // D2H lane
+constexpr int kLaneMain = 1;    // fetch (H2D) + reduce lane: the caller's stream
+constexpr int kLaneGather = 2;  // all-gather (H2D) lane
 
 // One data-movement end for the trace: SHM byte range (relative to the
 // segment) or user-buffer byte range (relative to the buffer start), plus the
@@ -471,7 +475,7 @@ class TraceSink final : public Sink {
     return FMX_OK;
   }
   std::string* out_;
-  int seq_[8] = {};
+  int seq_[kNumEvents] = {};
 };
 
 // Round j of every chunk covers [prefix(j), prefix(j) + size(j)).  With the
@@ -541,35 +545,45 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype) {
 
 Annot ubuf(size_t off_bytes, size_t bytes) { return Annot{(int64_t)off_bytes, bytes, -1, 0}; }
 
-// Reduce-scatter + all-gather through the segment, pipelined in rounds on two
-// lanes.  Round R uses slot R % 2.
+// Reduce-scatter + all-gather through the segment, pipelined in rounds on three
+// lanes: lane 0 stages (D2H), lane 1 fetches and reduces (H2D + kernel), lane 2
+// gathers (H2D).  Round R uses slot R % 2.  With the gather on its own lane, a
+// rank fetches round R+1 while it still waits for the slowest owner of round R,
+// so the H2D direction never idles at a round boundary.
 //
 // Enqueue order is itself a valid single-stream schedule: every wait (flag or
 // event) points at work enqueued earlier, by this rank or by peers that enqueue
-// in the same order.  So however the driver maps the two lane streams onto
+// in the same order.  So however the driver maps the lane streams onto
 // hardware queues - even one shared FIFO - nothing can deadlock; separate queues
-// only add overlap.  Lane 0 never waits on a flag: only on events of lane 1.
-// The model checker checks both the two-lane and the merged single-FIFO reading.
+// only add overlap.  Lane 0 never waits on a flag: only on events of lane 2.
+// The model checker checks both the multi-lane and the merged single-FIFO reading.
+//
+// Events (slot = round parity): W(R) is recorded on the gather lane once every
+// peer's REDUCED >= R+1 was seen, G(R) once gather(R) completed.  REDUCED(R)
+// (value R+1) is signalled after reduce(R) AND G(R-1), so "REDUCED[q] >= R+1"
+// also says "q finished gathering round R-1".
 //
 // Hazards and the wait that covers each:
 //  stage(R) into in[R%2][o][me], last read by owner o's fetch of round R-2:
-//      lane-1 event recorded after my waits REDUCED[q] >= R-1 for every q
-//      (each owner signals REDUCED after its fetches); rounds of an earlier
-//      collective are covered by the fork.
-//  fetch(R) of in[R%2][me][q]              -> wait STAGED_TO[q][me] >= R+1
-//      (per contributor: a piece moves as soon as it was staged)
-//  reduce(R) writes out[R%2][me], last read by every q's gather(R-2): my
-//      gather(R-1) waited REDUCED[q] >= R, and q's lane 1 runs gather(R-2)
-//      before reduce(R-1).
-//  gather(R) reads out[R%2][q]             -> wait REDUCED[q] >= R+1 (per owner)
+//      W(R-2) (every owner signalled REDUCED after its fetches of R-2); rounds
+//      of an earlier collective are covered by the fork.
+//  fetch(R) of in[R%2][me][q]              -> wait STAGED(_TO)[q] >= R+1
+//  reduce(R) writes out[R%2][me], last read by every q's gather(R-2):
+//      W(R-1): every q signalled REDUCED >= R, which q issued after G_q(R-2).
+//  gather(R) reads out[R%2][q]             -> wait REDUCED[q] >= R+1
 //  in place: gather(R) overwrites piece (q, R); my stage(R) read it first,
-//      because owner q's reduce(R) waited for my STAGED_TO[me][q] >= R+1.
-enum { kEvSlotFree = 0 };  // + slot: lane 1 -> lane 0, "slot reusable"
+//      because owner q's reduce(R) waited for my STAGED >= R+1.
+// With FMX_LANES=2 the gather runs on lane 1 and the W/G waits are implied by
+// stream order (the schedule of the first B200 runs).
+enum { kEvSlotFree = 0, kEvGathered = FMX_MAX_SLOTS };  // + R % K: W(R) and G(R) above
 
 int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
                    int op, float factor, bool aligned) {
   const int n = c->nranks, me = c->rank;
   const bool zc = c->transport == FMX_TRANSPORT_ZC;
+  const int LG = c->nlanes == 3 ? kLaneGather : kLaneMain;
+  const int K = c->nslots;  // pipeline depth: slots per region
+  const bool split = LG != kLaneMain;  // gather on its own lane: explicit W / G waits
   const Geometry g = allreduce_geometry(c, count, dtype);
   std::vector<PlanSeg> segs;
   int rc;
@@ -580,9 +594,8 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
 
   auto stage = [&](uint32_t j) -> int {
     const uint32_t R = R0 + j;
-    // slot R%2 was read by round R-2's fetches; within this collective the
-    // lane-1 event after round R-2's REDUCED waits says they are done
-    if (j >= 2 && (rc = k.wait_event(kLaneStage, kEvSlotFree + R % 2))) return rc;
+    // slot R%K was read by round R-K's fetches: W(R-K)
+    if (j >= K && (rc = k.wait_event(kLaneStage, kEvSlotFree + R % K))) return rc;
     if (c->coarse) {  // one batch of copies, one STAGED signal
       segs.clear();
       for (int o = 0; o < n; ++o) {
@@ -612,11 +625,14 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
     return FMX_OK;
   };
 
-  if ((rc = stage(0))) return rc;
+  // lane 0 stages K-1 rounds ahead of the reduction
+  const uint32_t ahead = (uint32_t)K - 1;
+  for (uint32_t j = 0; j < ahead && j < g.rounds; ++j)
+    if ((rc = stage(j))) return rc;
   for (uint32_t j = 0; j < g.rounds; ++j) {
     const uint32_t R = R0 + j;
-    if (j + 1 < g.rounds && (rc = stage(j + 1))) return rc;  // one round ahead, lane 0
-    // lane 1: reduce-scatter my chunk in ascending rank order
+    if (j + ahead < g.rounds && (rc = stage(j + ahead))) return rc;
+    // lane 1: fetch, then reduce-scatter my chunk in ascending rank order
     const size_t mylen = g.len(me, j);
     if (mylen) {
       PlanReduce pr;
@@ -675,6 +691,9 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
           a.src[q] = c->scratch + (size_t)q * c->slice_bytes;
         }
       }
+      // out[R%K][me] is free once every peer gathered round R-K: W(R-K+1)
+      if (split && j + 1 >= K && (rc = k.wait_event(kLaneMain, kEvSlotFree + (R + 1 - K) % K)))
+        return rc;
       if ((rc = k.reduce(kLaneMain, pr))) return rc;
       if (via_ce) {  // result slot written by the copy engine from HBM
         segs.clear();
@@ -684,10 +703,13 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
         if ((rc = k.copy(kLaneMain, segs, false, false))) return rc;
       }
     }
+    // REDUCED(R) also says "my gather(R-1) is done": G(R-1)
+    if (split && j >= 1 && (rc = k.wait_event(kLaneMain, kEvGathered + (R - 1) % K))) return rc;
     if ((rc = k.signal(kLaneMain, kReduced, R + 1))) return rc;
-    // all-gather: each owner's result as soon as that owner has it
+    // all-gather (lane LG): each owner's result as soon as that owner has it
     if (c->coarse_gather) {
-      if ((rc = k.wait_peers(kLaneMain, kReduced, R + 1, me))) return rc;
+      if ((rc = k.wait_peers(LG, kReduced, R + 1, me))) return rc;
+      if ((rc = k.record(LG, kEvSlotFree + R % K))) return rc;  // W(R)
       segs.clear();
       for (int q = 0; q < n; ++q) {
         const size_t len = q == me ? 0 : g.len(q, j);
@@ -697,22 +719,23 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
                         Annot{(int64_t)off, len * g.esz, q, R}, false,
                         ubuf(g.lo(q, j) * g.esz, len * g.esz)});
       }
-      if ((rc = k.copy(kLaneMain, segs, true, zc))) return rc;
+      if ((rc = k.copy(LG, segs, true, zc))) return rc;
+    } else {
+      for (int i = 0; i < n - 1; ++i) {
+        const int q = rot(i);
+        if ((rc = k.wait_rank(LG, q, kReduced, R + 1))) return rc;
+        const size_t len = g.len(q, j);
+        if (!len) continue;
+        const size_t off = c->out_off(R, q);
+        segs.clear();
+        segs.push_back({c->at(zc, off), dst + g.lo(q, j) * g.esz, len * g.esz,
+                        Annot{(int64_t)off, len * g.esz, q, R}, false,
+                        ubuf(g.lo(q, j) * g.esz, len * g.esz)});
+        if ((rc = k.copy(LG, segs, true, zc))) return rc;
+      }
+      if ((rc = k.record(LG, kEvSlotFree + R % K))) return rc;  // W(R)
     }
-    for (int i = 0; i < n - 1 && !c->coarse_gather; ++i) {
-      const int q = rot(i);
-      if ((rc = k.wait_rank(kLaneMain, q, kReduced, R + 1))) return rc;
-      const size_t len = g.len(q, j);
-      if (!len) continue;
-      const size_t off = c->out_off(R, q);
-      segs.clear();
-      segs.push_back({c->at(zc, off), dst + g.lo(q, j) * g.esz, len * g.esz,
-                      Annot{(int64_t)off, len * g.esz, q, R}, false,
-                      ubuf(g.lo(q, j) * g.esz, len * g.esz)});
-      if ((rc = k.copy(kLaneMain, segs, true, zc))) return rc;
-    }
-    // every owner has fetched round R: in[R%2] may be restaged (round R+2)
-    if ((rc = k.record(kLaneMain, kEvSlotFree + R % 2))) return rc;
+    if (split && (rc = k.record(LG, kEvGathered + R % K))) return rc;  // G(R)
   }
   c->ar_round += g.rounds;
   return FMX_OK;
@@ -726,7 +749,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
 // Per GPU that is k*S H2D + k*S D2H, against 2k(n-1)/n*S + k*S (+ the
 // caller's own k*S in and k*S out) for device buffers.
 constexpr uint32_t kInputTag = 1u << 31;  // trace: "input written by the host for round R"
-enum { kEvFetched = 2, kEvReduced = 4, kEvInputs = 6 };  // (+ slot 0/1)
+enum { kEvFetched = 2 * FMX_MAX_SLOTS, kEvReduced = kEvFetched + 2, kEvInputs = kEvFetched + 4 };
 
 int plan_allreduce_host(fmx_comm* c, Sink& k, size_t off_bytes, size_t count, int dtype, int op,
                         float factor) {
@@ -844,12 +867,14 @@ int plan_broadcast(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
 // the caller's stream (a green context, an MPS client's, or the primary one),
 // so every lane object lives where the caller's work lives.
 int make_lane_objects(fmx_comm* c, CUcontext ctx) {
-  c->lane[0] = nullptr;  // objects of an earlier context are abandoned, not destroyed
-  FMX_CUDA(cudaStreamCreateWithFlags(&c->lane[0], cudaStreamNonBlocking));
+  c->lane[0] = c->lane[1] = nullptr;  // objects of an earlier context are abandoned, not destroyed
+  for (int l = 0; l < 2; ++l) {
+    FMX_CUDA(cudaStreamCreateWithFlags(&c->lane[l], cudaStreamNonBlocking));
+    FMX_CUDA(cudaEventCreateWithFlags(&c->joined[l], cudaEventDisableTiming));
+  }
   FMX_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
-  FMX_CUDA(cudaEventCreateWithFlags(&c->joined[0], cudaEventDisableTiming));
   FMX_CUDA(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
-  for (int i = 0; i < 8; ++i) FMX_CUDA(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
+  for (int i = 0; i < kNumEvents; ++i) FMX_CUDA(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
   for (auto& pr : c->timed) pr = {nullptr, nullptr};
   c->timed.clear();
   c->timed_used = 0;
@@ -876,14 +901,13 @@ int on_lanes(fmx_comm* c, cudaStream_t user, F&& body) {
   int rc;
   if (ctx != c->lane_ctx && (rc = make_lane_objects(c, ctx))) return rc;
   c->user = user;
-  if (!c->single_lane) {
-    FMX_CUDA(cudaEventRecord(c->fork, user));
-    FMX_CUDA(cudaStreamWaitEvent(c->lane[0], c->fork, 0));
-  }
+  const int forked = c->nlanes - 1;  // lane 0, then lane 2 (lane 1 is `user`)
+  if (forked > 0) FMX_CUDA(cudaEventRecord(c->fork, user));
+  for (int l = 0; l < forked; ++l) FMX_CUDA(cudaStreamWaitEvent(c->lane[l], c->fork, 0));
   rc = body();
-  if (!c->single_lane) {
-    FMX_CUDA(cudaEventRecord(c->joined[0], c->lane[0]));
-    FMX_CUDA(cudaStreamWaitEvent(user, c->joined[0], 0));
+  for (int l = 0; l < forked; ++l) {
+    FMX_CUDA(cudaEventRecord(c->joined[l], c->lane[l]));
+    FMX_CUDA(cudaStreamWaitEvent(user, c->joined[l], 0));
   }
   if (rc) return rc;
   FMX_CUDA(cudaEventRecord(c->done, user));
@@ -917,7 +941,12 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   size_t klen = strlen(job_key);
   if (klen == 0 || klen > 100 || strchr(job_key, '/'))
     return fail(FMX_ERR_INVALID_ARG, "job_key must be 1..100 chars without '/'");
-  if (nslots != 0 && nslots != 2) return fail(FMX_ERR_INVALID_ARG, "nslots must be 2");
+  if (nslots == 0) {
+    nslots = 2;
+    if (const char* v = getenv("FMX_SLOTS")) nslots = atoi(v);
+  }
+  if (nslots < 2 || nslots > FMX_MAX_SLOTS)
+    return fail(FMX_ERR_INVALID_ARG, "nslots must be 2..%d", FMX_MAX_SLOTS);
   if (transport < FMX_TRANSPORT_AUTO || transport > FMX_TRANSPORT_HOST)
     return fail(FMX_ERR_INVALID_ARG, "bad transport %d", transport);
   if (timeout_s <= 0) timeout_s = 120.0;
@@ -930,7 +959,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   auto* c = new fmx_comm();
   c->rank = rank;
   c->nranks = nranks;
-  c->nslots = 2;
+  c->nslots = nslots;
   const std::string name = std::string("/fmx-") + job_key;
   const double t_end = now_s() + timeout_s;
 
@@ -1023,6 +1052,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   }
   Header* h = c->hdr = (Header*)c->base;
   c->slice_bytes = h->slice_bytes;
+  c->nslots = h->nslots;  // rank 0's choice wins
   c->L = Layout{h->peers_off, h->flags_off, h->ar_in_off, h->ar_out_off, h->bc_off,
                 h->user_off, h->user_bytes, h->total_bytes};
   c->mig_aware = h->mig_aware;
@@ -1086,7 +1116,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (const char* v = getenv("FMX_GRAIN")) c->coarse = strcmp(v, "fine") != 0;
   c->coarse_gather = c->coarse;
   if (const char* v = getenv("FMX_GATHER_GRAIN")) c->coarse_gather = strcmp(v, "fine") != 0;
-  if (const char* v = getenv("FMX_LANES")) c->single_lane = atoi(v) == 1;
+  if (const char* v = getenv("FMX_LANES")) c->nlanes = std::min(3, std::max(1, atoi(v)));
   if (const char* v = getenv("FMX_RAMP")) c->ramp = atoi(v) != 0;
   if (e != cudaSuccess) {
     h->aborted.store(1);
@@ -1257,17 +1287,19 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   c.rank = rank;
   c.nranks = nranks;
   c.nslots = 2;
+  if (const char* v = getenv("FMX_SLOTS")) c.nslots = std::min(FMX_MAX_SLOTS, std::max(2, atoi(v)));
   c.transport = transport == FMX_TRANSPORT_ZC ? FMX_TRANSPORT_ZC : FMX_TRANSPORT_CE;
   c.slice_bytes = slice_bytes;
   size_t max_bytes = 0;
   for (int i = 0; i < nops; ++i) max_bytes = std::max(max_bytes, counts[i] * (dtypes[i] ? 2 : 4));
-  c.L = compute_layout(nranks, 2, slice_bytes, max_bytes);
+  c.L = compute_layout(nranks, c.nslots, slice_bytes, max_bytes);
   c.total_bytes = c.L.total;
   if (const char* v = getenv("FMX_RESULT_VIA_CE")) c.result_via_ce = atoi(v) != 0;
   if (const char* v = getenv("FMX_GRAIN")) c.coarse = strcmp(v, "fine") != 0;
   c.coarse_gather = c.coarse;
   if (const char* v = getenv("FMX_GATHER_GRAIN")) c.coarse_gather = strcmp(v, "fine") != 0;
   if (const char* v = getenv("FMX_RAMP")) c.ramp = atoi(v) != 0;
+  if (const char* v = getenv("FMX_LANES")) c.nlanes = std::min(3, std::max(1, atoi(v)));
   std::string out;
   TraceSink sink(&out);
   sink.nranks = nranks;
@@ -1317,7 +1349,7 @@ int fmx_comm_destroy(fmx_comm_t c) {
     rc = fail(FMX_ERR_CUDA, "pending collective failed: %s", cudaGetErrorString(cudaGetLastError()));
   if (c->done) cudaEventDestroy(c->done);
   if (c->fork) cudaEventDestroy(c->fork);
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < kNumEvents; ++i)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   for (auto& pr : c->timed) {
     cudaEventDestroy(pr.first);

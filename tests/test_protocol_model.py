@@ -27,11 +27,15 @@ import pytest
 from paper_2511_09143_b200 import _lib
 
 
+LANES = 3  # 0 stage (D2H), 1 fetch + reduce (the caller's stream), 2 gather (H2D)
+
+
 def parse(text: str, merged: bool = False):
-    """-> [lane0 ops, lane1 ops]; a 'J' line is a join point in both lanes.
-    merged=True reads the trace as ONE sequential program in enqueue order -
-    what the hardware runs if the driver puts both lane streams on one FIFO."""
-    lanes = [[], []]
+    """-> [lane0 ops, lane1 ops, lane2 ops]; a 'J' line is a join point in
+    every lane.  merged=True reads the trace as ONE sequential program in
+    enqueue order - what the hardware runs if the driver puts all lane streams
+    on one FIFO."""
+    lanes = [[] for _ in range(LANES)]
     joins = 0
     for line in text.splitlines():
         if not line:
@@ -59,10 +63,10 @@ def geq(a: int, b: int) -> bool:
 
 
 def simulate(progs, seed: int, burst: int = 3):
-    """progs[rank] = [lane0, lane1].  Actors are (rank, lane) pairs, each a
-    sequential program (one CUDA stream); lanes of a rank meet at joins."""
+    """progs[rank] = [lane0, lane1, lane2].  Actors are (rank, lane) pairs,
+    each a sequential program (one CUDA stream); lanes of a rank meet at joins."""
     n = len(progs)
-    actors = [(r, l) for r in range(n) for l in range(2)]
+    actors = [(r, l) for r in range(n) for l in range(LANES)]
     idx = {a: i for i, a in enumerate(actors)}
     m = len(actors)
     rng = random.Random(seed)
@@ -84,8 +88,7 @@ def simulate(progs, seed: int, burst: int = 3):
         if op[0] == "A":
             return geq(flags.get((op[1], op[2]), (0, None))[0], op[3])
         if op[0] == "J":
-            other = (a[0], 1 - a[1])
-            return op_of(other) == op
+            return all(op_of((a[0], l)) == op for l in range(LANES))
         if op[0] == "X":
             return (a[0], op[1], op[2]) in events
         return True
@@ -134,11 +137,12 @@ def simulate(progs, seed: int, burst: int = 3):
                     for k in range(m):
                         me[k] = max(me[k], c[k])
             elif op[0] == "J":
-                other = (r, 1 - a[1])
-                joined = [max(x, y) for x, y in zip(me, clock[other])]
+                others = [(r, l) for l in range(LANES) if l != a[1]]
+                joined = [max(xs) for xs in zip(me, *(clock[o] for o in others))]
                 clock[a][:] = joined
-                clock[other][:] = joined
-                pc[other] += 1
+                for o in others:
+                    clock[o][:] = joined
+                    pc[o] += 1
             elif op[0] == "E":
                 me[idx[a]] += 1
                 events[(r, op[1], op[2])] = list(me)
@@ -252,12 +256,18 @@ def test_model_catches_a_broken_schedule(flag):
 
 
 @pytest.mark.parametrize("n", [2, 7])
-@pytest.mark.parametrize("grain,gather,ramp", [("fine", "fine", "1"), ("coarse", "coarse", "0"),
-                                               ("fine", "fine", "0"), ("coarse", "fine", "1")])
-def test_schedule_variants(monkeypatch, n, grain, gather, ramp):
+@pytest.mark.parametrize("grain,gather,ramp,lanes,slots", [
+    ("fine", "fine", "1", "3", "2"), ("coarse", "coarse", "0", "3", "2"),
+    ("fine", "fine", "0", "2", "2"), ("coarse", "fine", "1", "3", "2"),
+    ("coarse", "coarse", "1", "2", "2"), ("coarse", "fine", "1", "1", "2"),
+    ("coarse", "coarse", "1", "3", "3"), ("fine", "fine", "1", "3", "4"),
+    ("coarse", "coarse", "0", "2", "3"), ("coarse", "fine", "1", "3", "4")])
+def test_schedule_variants(monkeypatch, n, grain, gather, ramp, lanes, slots):
     monkeypatch.setenv("FMX_GRAIN", grain)
     monkeypatch.setenv("FMX_GATHER_GRAIN", gather)
     monkeypatch.setenv("FMX_RAMP", ramp)
+    monkeypatch.setenv("FMX_LANES", lanes)
+    monkeypatch.setenv("FMX_SLOTS", slots)
     progs = programs(n, SEQUENCES["mixed"], 4096, "ce")
     for seed in range(6):
         simulate(progs, seed)
@@ -271,3 +281,24 @@ def test_result_via_copy_engine_variant(monkeypatch):
     progs = programs(4, SEQUENCES["mixed"], 4096, "ce")
     for seed in range(8):
         simulate(progs, seed)
+
+
+@pytest.mark.parametrize("event", [0, 4])
+def test_model_catches_a_missing_gather_lane_event(event):
+    """Three-lane schedule: drop lane 1's waits on W (event ids 0..3: "every peer
+    reduced the previous round") or on G (4..7: "my previous gather is done").
+    Either lets an owner overwrite its result slot while a peer's gather still
+    reads it, and the checker must object."""
+    progs = programs(3, [("allreduce", 60_000, 0), ("allreduce", 60_000, 0)], 4096, "ce")
+    lanes = progs[1]
+    broken_lanes = [lanes[0], [op for op in lanes[1] if not (op[0] == "X" and event <= op[1] < event + 4)],
+                    lanes[2]]
+    assert broken_lanes[1] != lanes[1]
+    broken = [broken_lanes if r == 1 else p for r, p in enumerate(progs)]
+    failures = 0
+    for seed in range(80):
+        try:
+            simulate(broken, seed)
+        except AssertionError:
+            failures += 1
+    assert failures > 0
