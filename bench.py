@@ -54,7 +54,8 @@ def parse_args(argv=None):
     p.add_argument("--count", type=int, default=RESNET50_PARAMS)
     p.add_argument("--dtype", choices=["f32", "bf16"], default="f32")
     p.add_argument("--transport", choices=["auto", "ce", "zc"], default="auto")
-    p.add_argument("--mode", choices=["green", "mps", "mps+green", "full"], default="green")
+    p.add_argument("--mode", choices=["green", "mps", "full"], default="mps",
+                   help="instance stand-in on a GPU without MIG (instance.py)")
     p.add_argument("--slice-bytes", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -65,7 +66,10 @@ def parse_args(argv=None):
     p.add_argument("--no-train", action="store_true", help="skip the ResNet-50 DP img/s leg")
     p.add_argument("--timeline", default=None, help="write a host-polled flag timeline here")
     p.add_argument("--train-only", action="store_true")
-    p.add_argument("--train-mode", choices=["green", "mps", "mps+green", "full"], default="green")
+    p.add_argument("--train-mode", choices=["green", "mps", "full"], default="mps")
+    p.add_argument("--dry-run", action="store_true",
+                   help="orchestration only (no CUDA): stub rank bodies; for the CPU tests of "
+                        "the torchrun N>1 path")
     p.add_argument("--sweep", action="store_true", help="message-size sweep (configs[4]) instead")
     p.add_argument("--sweep-max", type=int, default=1 << 30)
     p.add_argument("--batch", type=int, default=32)
@@ -134,14 +138,18 @@ def kernel_roofline(args, n, s_bytes, kernel_ms, kernel_count, iso_us=None, iso_
     zc = args.transport == "zc"
     traffic = None
     try:
-        traffic = json.load(open(TRAFFIC_PATH)).get("fmx_reduce_kernel_bytes_per_launch")
-    except (OSError, ValueError):
+        # ncu --set full capture of one full piece (profiles/ncu_traffic.json), DRAM bytes
+        # per piece byte, scaled to the mean piece of the live launches like `achieved`
+        t = json.load(open(TRAFFIC_PATH))
+        traffic = (t["dram_read_bytes"] + t["dram_write_bytes"]) / t["piece_bytes"] * \
+            per_launch(s_bytes)
+    except (OSError, ValueError, KeyError):
         pass
     if zc:
         link = per_launch((n - 1) * s_bytes + s_bytes)
         return {"kernel": "fmx_reduce_kernel", "bound": "host_link", "achieved": link / t_launch / 1e9,
                 "peak": LINK_PEAK_FALLBACK["bidir"], "unit": "GB/s",
-                "frac": link / t_launch / 1e9 / LINK_PEAK_FALLBACK["bidir"], "traffic": traffic,
+                "frac": link / t_launch / 1e9 / LINK_PEAK_FALLBACK["bidir"], "traffic": None,
                 "launch_us": t_launch * 1e6, "launches": kernel_count,
                 "peak_source": "measured CE bidirectional (profiles/r01_probe/bw.jsonl)"}
     if via_ce:
@@ -507,7 +515,7 @@ def run_ranks(body, spawned, mine, job_key, n, cfg, inst_mode, gpu_local, sample
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     results, errors = {}, []
-    if inst_mode in ("mps", "mps+green") and "CUDA_MPS_PIPE_DIRECTORY" not in os.environ:
+    if inst_mode == "mps" and "CUDA_MPS_PIPE_DIRECTORY" not in os.environ:
         raise RuntimeError("MPS instance mode needs the daemon started by main()")
     try:
         with ctx.Pool(max(1, len(mine) - 1)) as pool:
@@ -557,7 +565,8 @@ def run_ours(args) -> dict | None:
     gpus = args.gpus if world == 1 else world
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("gloo")
+        if not dist.is_initialized():
+            dist.init_process_group("gloo")
     d = decision_for(gpus, args.ranks_per_gpu)
     n = len(d.instances)
     cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
@@ -576,11 +585,17 @@ def run_ours(args) -> dict | None:
     mine = [r for r, (g, _) in enumerate(d.instances) if g == my_gpu] if world > 1 else list(range(n))
     gpu_local = local if world > 1 else 0
     inst_mode = args.mode
-    sampler = ClockSampler()
+    sampler = ClockSampler() if not args.dry_run else None
     results = {}
     errors = []
 
-    if args.inproc:
+    if args.dry_run:
+        # stub ranks: distinct, known timings so the MAX-over-ranks reduction is checkable
+        results = {r: {"rank": r, "ms_total": 10.0 * (r + 1), "launches": 1, "kernel_ms": 0.0,
+                       "kernel_count": 0, "ms_total_e2e": 5.0 * (r + 1),
+                       "ms_total_e2e_dev": 6.0 * (r + 1), "e2e_digest": 0, "job_key": job_key}
+                   for r in mine}
+    elif args.inproc:
         # all ranks of this GPU as threads (ncu-friendly); primary context
         def th(r):
             try:
@@ -599,7 +614,8 @@ def run_ours(args) -> dict | None:
                                 gpu_local, sampler)
         except BaseException as exc:  # noqa: BLE001
             errors.append((mine[0], exc))
-    clocks = sampler.stop()
+    clocks = sampler.stop() if sampler is not None else {"sm_mhz": None, "sm_max_mhz": None,
+                                                          "reasons": ["dry run"]}
     if errors:
         raise RuntimeError(f"rank {errors[0][0]} failed: {errors[0][1]!r}") from errors[0][1]
     local_max = max(r["ms_total"] for r in results.values())
@@ -620,9 +636,7 @@ def run_ours(args) -> dict | None:
         local_max, local_max_e2e, local_max_e2e_dev = mx[0].item(), mx[1].item(), mx[5].item()
         launches, kernel_ms, kernel_count = int(sm[2].item()), sm[3].item(), int(sm[4].item())
         if grank != 0:
-            dist.destroy_process_group()
             return None
-        dist.destroy_process_group()
     esz = 4 if args.dtype == "f32" else 2
     s_bytes = args.count * esz
     t_step = local_max / 1e3 / args.steps
@@ -643,6 +657,8 @@ def run_ours(args) -> dict | None:
                    "ranks": n, "ranks_per_gpu": per_gpu, "bytes": s_bytes,
                    "instance_mode": "threads" if args.inproc else inst_mode,
                    "transport": args.transport, "l2": "inputs > L2 (7 x 102 MB per GPU)",
+                   "slots": int(os.environ.get("FMX_SLOTS", "2")),
+                   "lanes": int(os.environ.get("FMX_LANES", "3")),
                    "rank_order": "fm_select round-robin"},
         "busbw_gbs": s_bytes / t_step / 1e9 * 2 * (n - 1) / n,
         "roofline": kernel_roofline(args, n, s_bytes, kernel_ms, kernel_count,
@@ -652,6 +668,8 @@ def run_ours(args) -> dict | None:
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    if getattr(args, "mps_fallback", None):
+        line["config"]["mps_fallback"] = args.mps_fallback
     if not args.no_e2e:
         t_e2e = local_max_e2e / 1e3 / args.steps
         t_dev = local_max_e2e_dev / 1e3 / args.steps
@@ -724,21 +742,62 @@ def main(argv=None):
                         "the same SHM RS/AG algorithm, oracle/flexshm_oracle.c"}
         print(json.dumps(line))
         return 0
-    mps = None
-    if "mps" in args.mode or (not args.no_train and "mps" in args.train_mode):
-        # one private MPS daemon for the whole run (every rank process, this one
-        # included, is a client); 1g share of the SMs per client
-        from paper_2511_09143_b200.launcher import MPS_PERCENT, MpsDaemon
-        mps = MpsDaemon(f"bench-{os.getpid()}")
-        if not mps.start():
-            raise RuntimeError("MPS daemon failed to start")
-        os.environ.update(mps.env)
-        os.environ["CUDA_MPS_ACTIVE_THREAD_PERCENTAGE"] = str(MPS_PERCENT)
+    mps = start_mps(args, world)
     try:
         return _main(args, world, n, unit)
     finally:
-        if mps is not None:
-            mps.stop()
+        stop_mps(mps, world)
+        if world > 1:
+            import torch.distributed as dist
+            if dist.is_initialized():
+                dist.destroy_process_group()
+
+
+def _local_rank0() -> bool:
+    return int(os.environ.get("LOCAL_RANK", "0")) == 0
+
+
+def start_mps(args, world):
+    """Instances are MPS clients by default (concurrent, 1g SM share each:
+    the closest stand-in for MIG slices on a box without MIG).  One private
+    MPS control daemon per node, started by local rank 0 (all torchrun ranks
+    of the node share it).  If it cannot start, every rank falls back to
+    green-context instances and says so in the JSON line."""
+    wants = args.mode == "mps" or (not args.no_train and args.train_mode == "mps")
+    if not wants:
+        return None
+    from paper_2511_09143_b200.launcher import MPS_PERCENT, MpsDaemon
+    tag = f"bench-{os.environ.get('MASTER_PORT', os.getpid())}"
+    mps = MpsDaemon(tag)
+    ok = mps.start() if _local_rank0() else True
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            dist.init_process_group("gloo")
+        flag = torch.tensor([1 if ok else 0])
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        ok = bool(flag.item())
+    if not ok:
+        args.mps_fallback = "MPS daemon failed to start: green-context instances instead"
+        if args.mode == "mps":
+            args.mode = "green"
+        if args.train_mode == "mps":
+            args.train_mode = "green"
+        return mps if _local_rank0() else None
+    os.environ.update(mps.env)
+    os.environ["CUDA_MPS_ACTIVE_THREAD_PERCENTAGE"] = str(MPS_PERCENT)
+    return mps
+
+
+def stop_mps(mps, world):
+    """Every rank meets here (N>1) before local rank 0 asks the daemon to quit."""
+    if world > 1:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.barrier()
+    if mps is not None and _local_rank0():
+        mps.stop()
 
 
 def _main(args, world, n, unit):

@@ -23,6 +23,9 @@
  *                          DDP (nccl.h:379)
  *   fmx_broadcast       <- ncclBroadcast (ZeRO shard / DDP init broadcast,
  *                          PAPER.md:485; nccl.h:392)
+ *   fmx_reduce_scatter  <- ncclReduceScatter (nccl.h:408)
+ *   fmx_allgather       <- ncclAllGather (inference jobs, PAPER.md:485;
+ *                          nccl.h:425)
  *   fmx_comm_destroy / fmx_comm_abort <- ncclCommDestroy / ncclCommAbort
  *
  * Status codes map 1:1 to Python exceptions (paper_2511_09143_b200/_lib.py):
@@ -144,6 +147,18 @@ int fmx_allreduce(fmx_comm_t comm, const void* send, void* recv, size_t count, i
 int fmx_broadcast(fmx_comm_t comm, const void* send, void* recv, size_t count, int dtype,
                   int root, void* stream);
 
+/* NCCL layout: send holds nranks*recvcount elements, rank r receives the
+ * rank-order reduction (op/factor as fmx_allreduce) of elements
+ * [r*recvcount, (r+1)*recvcount) in recv.  In place when
+ * recv == send + rank*recvcount. */
+int fmx_reduce_scatter(fmx_comm_t comm, const void* send, void* recv, size_t recvcount, int dtype,
+                       int op, float factor, void* stream);
+
+/* NCCL layout: every rank's sendcount elements land at recv[r*sendcount] of
+ * every rank (bit copy).  In place when send == recv + rank*sendcount. */
+int fmx_allgather(fmx_comm_t comm, const void* send, void* recv, size_t sendcount, int dtype,
+                  void* stream);
+
 /* Registered host buffers (the NCCL user-buffer-registration idea for host
  * memory): every rank owns a pinned, device-mapped region of host_bytes inside
  * the segment; any rank's region can be mapped (for inspection).  */
@@ -203,7 +218,8 @@ int fmx_comm_kernel_launches(fmx_comm_t comm, uint64_t* launches);
 
 /* Write the schedule `rank` of an `nranks` communicator would enqueue for a
  * sequence of `nops` collectives (kinds[i]: 0 allreduce, 1 broadcast with
- * roots[i], 2 host-buffer allreduce) as text: one line per SHM access ("W off bytes round", "R off
+ * roots[i], 2 host-buffer allreduce, 3 reduce-scatter and 4 all-gather with
+ * counts[i] per rank) as text: one line per SHM access ("W off bytes round", "R off
  * bytes writer round") or flag op ("S flag value", "A rank flag value"),
  * "#" between collectives.  Used to model-check the protocol for any world
  * size on a CPU (tests/test_protocol_model.py).  *used = bytes needed. */

@@ -45,7 +45,8 @@ MAX_RANKS = 64
 # Every symbol include/flexshm.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "fmx_check_peer", "fmx_validate_peers", "fmx_topology", "fmx_restore_bus_id",
-    "fmx_comm_init", "fmx_allreduce", "fmx_broadcast", "fmx_host_buffer", "fmx_allreduce_host",
+    "fmx_comm_init", "fmx_allreduce", "fmx_broadcast", "fmx_reduce_scatter", "fmx_allgather",
+    "fmx_host_buffer", "fmx_allreduce_host",
     "fmx_reduce_local", "fmx_barrier", "fmx_comm_destroy",
     "fmx_comm_abort", "fmx_comm_rank", "fmx_comm_count", "fmx_comm_peer", "fmx_comm_config",
     "fmx_comm_kernel_launches", "fmx_comm_flags", "fmx_comm_set_timing", "fmx_comm_kernel_time",
@@ -108,6 +109,8 @@ def lib() -> ctypes.CDLL:
                              c_int, c_float, c_void],
         "fmx_allreduce": [c_void, c_void, c_void, c_size, c_int, c_int, c_float, c_void],
         "fmx_broadcast": [c_void, c_void, c_void, c_size, c_int, c_int, c_void],
+        "fmx_reduce_scatter": [c_void, c_void, c_void, c_size, c_int, c_int, c_float, c_void],
+        "fmx_allgather": [c_void, c_void, c_void, c_size, c_int, c_void],
         "fmx_barrier": [c_void, c_double],
         "fmx_comm_destroy": [c_void],
         "fmx_comm_abort": [c_void],
@@ -139,10 +142,13 @@ def lib() -> ctypes.CDLL:
 
 def trace_plan(nranks: int, rank: int, ops: list[tuple], slice_bytes: int = 4096,
                transport: str = "ce") -> str:
-    """Schedule text of `rank` for ops = [("allreduce", count, dtype) |
-    ("broadcast", count, dtype, root)] (see fmx_trace_plan)."""
+    """Schedule text of `rank` for ops = [("allreduce" | "allreduce_host" |
+    "reduce_scatter" | "allgather", count, dtype) | ("broadcast", count,
+    dtype, root)] (see fmx_trace_plan; reduce_scatter / allgather counts are
+    per rank)."""
     n = len(ops)
-    code = {"allreduce": 0, "broadcast": 1, "allreduce_host": 2}
+    code = {"allreduce": 0, "broadcast": 1, "allreduce_host": 2, "reduce_scatter": 3,
+            "allgather": 4}
     kinds = (ctypes.c_int * max(1, n))(*[code[o[0]] for o in ops])
     counts = (ctypes.c_size_t * max(1, n))(*[o[1] for o in ops])
     dtypes = (ctypes.c_int * max(1, n))(*[o[2] for o in ops])

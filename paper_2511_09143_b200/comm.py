@@ -136,6 +136,41 @@ class ShmCommunicator:
         _lib.check(rc, "fmx_broadcast")
         return tensor
 
+    def reduce_scatter(self, tensor, out, op: str = "sum", factor: float | None = None,
+                       stream=None):
+        """NCCL layout: `tensor` holds size * out.numel() elements; this rank
+        receives the rank-order reduction of its block (op/factor as in
+        allreduce) in `out`."""
+        self._alive()
+        _check_tensor(tensor, "tensor")
+        _check_tensor(out, "out")
+        if out.dtype != tensor.dtype or tensor.numel() != out.numel() * self.size:
+            raise ValueError("tensor must hold size * out.numel() elements of out's dtype")
+        if op == "avg":
+            op, factor = "prediv", float(self.size)
+        if op not in OPS:
+            raise ValueError(f"unknown op {op!r}")
+        factor = 1.0 if factor is None else factor
+        if op != "sum" and not math.isfinite(factor):
+            raise ValueError("factor must be finite")
+        rc = _lib.lib().fmx_reduce_scatter(self._h, tensor.data_ptr(), out.data_ptr(), out.numel(),
+                                           _dtype_code(tensor), OPS[op], ctypes.c_float(factor),
+                                           self._stream(stream))
+        _lib.check(rc, "fmx_reduce_scatter")
+        return out
+
+    def allgather(self, tensor, out, stream=None):
+        """NCCL layout: every rank's `tensor` lands at out[r * tensor.numel()]."""
+        self._alive()
+        _check_tensor(tensor, "tensor")
+        _check_tensor(out, "out")
+        if out.dtype != tensor.dtype or out.numel() != tensor.numel() * self.size:
+            raise ValueError("out must hold size * tensor.numel() elements of tensor's dtype")
+        rc = _lib.lib().fmx_allgather(self._h, tensor.data_ptr(), out.data_ptr(), tensor.numel(),
+                                      _dtype_code(tensor), self._stream(stream))
+        _lib.check(rc, "fmx_allgather")
+        return out
+
     def host_buffer(self, rank: int | None = None):
         """This rank's (or `rank`'s) registered host buffer as a uint8 CPU
         tensor over the pinned, device-mapped SHM region (no copy)."""

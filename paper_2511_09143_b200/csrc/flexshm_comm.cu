@@ -496,13 +496,16 @@ struct Geometry {
   }
 };
 
-Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype) {
+// chunk_elems = 0: allreduce chunking (16-byte aligned chunk starts over
+// `count`); otherwise every rank's chunk has exactly chunk_elems elements and
+// count = n * chunk_elems (reduce-scatter / all-gather, NCCL's layout).
+Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t chunk_elems = 0) {
   Geometry g;
   const int n = c->nranks;
-  g.count = count;
   g.esz = dtype == FMX_FLOAT32 ? 4 : 2;
   const size_t vec = 16 / g.esz;
-  g.chunk = ((count + n - 1) / n + vec - 1) / vec * vec;  // 16-byte aligned chunk starts
+  g.count = chunk_elems ? chunk_elems * n : count;
+  g.chunk = chunk_elems ? chunk_elems : ((count + n - 1) / n + vec - 1) / vec * vec;
   g.slice = c->slice_bytes / g.esz;
   std::vector<size_t> sizes;
   const size_t s = g.slice;
@@ -577,14 +580,29 @@ Annot ubuf(size_t off_bytes, size_t bytes) { return Annot{(int64_t)off_bytes, by
 // stream order (the schedule of the first B200 runs).
 enum { kEvSlotFree = 0, kEvGathered = FMX_MAX_SLOTS };  // + R % K: W(R) and G(R) above
 
+// The three owner-chunk collectives share one schedule:
+//   kAllreduce     stage -> fetch -> reduce (HBM + result slot) -> gather
+//   kReduceScatter stage -> fetch -> reduce into recv (no result slot, no gather copies)
+//   kAllgather     publish my chunk (result slot + my part of recv) -> gather
+// Flags, events and slot reuse are identical, so one model-checked protocol
+// covers all three.  For the last two, `count` is the per-rank count and the
+// buffers follow NCCL: send/recv of reduce-scatter hold n*count / count
+// elements, those of all-gather count / n*count.
+enum Kind { kAllreduce = 0, kReduceScatter = 1, kAllgather = 2 };
+
 int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
-                   int op, float factor, bool aligned) {
+                   int op, float factor, bool aligned, int kind = kAllreduce) {
   const int n = c->nranks, me = c->rank;
   const bool zc = c->transport == FMX_TRANSPORT_ZC;
   const int LG = c->nlanes == 3 ? kLaneGather : kLaneMain;
   const int K = c->nslots;  // pipeline depth: slots per region
   const bool split = LG != kLaneMain;  // gather on its own lane: explicit W / G waits
-  const Geometry g = allreduce_geometry(c, count, dtype);
+  const bool ar = kind == kAllreduce, rs = kind == kReduceScatter, ag = kind == kAllgather;
+  const Geometry g = allreduce_geometry(c, count, dtype, ar ? 0 : count);
+  // where piece (me, j) of the result goes, and where my contribution / my
+  // published chunk comes from (all-gather's send holds only my chunk)
+  auto my_out = [&](uint32_t j) { return dst + (rs ? g.start[j] : g.lo(me, j)) * g.esz; };
+  auto my_in = [&](uint32_t j) { return src + (ag ? g.start[j] : g.lo(me, j)) * g.esz; };
   std::vector<PlanSeg> segs;
   int rc;
   const uint32_t R0 = c->ar_round;
@@ -594,6 +612,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
 
   auto stage = [&](uint32_t j) -> int {
     const uint32_t R = R0 + j;
+    if (ag) return FMX_OK;  // nothing to reduce: no contributions to stage
     // slot R%K was read by round R-K's fetches: W(R-K)
     if (j >= K && (rc = k.wait_event(kLaneStage, kEvSlotFree + R % K))) return rc;
     if (c->coarse) {  // one batch of copies, one STAGED signal
@@ -634,7 +653,22 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
     if (j + ahead < g.rounds && (rc = stage(j + ahead))) return rc;
     // lane 1: fetch, then reduce-scatter my chunk in ascending rank order
     const size_t mylen = g.len(me, j);
-    if (mylen) {
+    if (mylen && ag) {
+      // publish: my piece into my result slot (and into my part of recv)
+      const size_t out_off = c->out_off(R, me);
+      if (split && j + 1 >= K && (rc = k.wait_event(kLaneMain, kEvSlotFree + (R + 1 - K) % K)))
+        return rc;
+      segs.clear();
+      segs.push_back({my_in(j), c->at(zc, out_off), mylen * g.esz,
+                      Annot{(int64_t)out_off, mylen * g.esz, me, R}, true,
+                      ubuf(g.lo(me, j) * g.esz, mylen * g.esz)});
+      if ((rc = k.copy(kLaneMain, segs, false, zc))) return rc;
+      if (my_out(j) != my_in(j) &&
+          (rc = k.d2d(kLaneMain, my_out(j), my_in(j), mylen * g.esz,
+                      ubuf(g.lo(me, j) * g.esz, mylen * g.esz),
+                      ubuf(g.lo(me, j) * g.esz, mylen * g.esz))))
+        return rc;
+    } else if (mylen) {
       PlanReduce pr;
       memset(&pr.args, 0, sizeof pr.args);
       pr.dtype = dtype;
@@ -644,11 +678,11 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
       a.len = mylen;
       a.op = op;
       a.factor = factor;
-      a.out_dev = dst + g.lo(me, j) * g.esz;
+      a.out_dev = my_out(j);
       const size_t out_off = c->out_off(R, me);
       pr.user_rw = ubuf(g.lo(me, j) * g.esz, mylen * g.esz);
-      const bool via_ce = !zc && c->result_via_ce;
-      if (!via_ce) {
+      const bool via_ce = ar && !zc && c->result_via_ce;
+      if (ar && !via_ce) {
         a.out_sys = c->at(true, out_off);
         pr.write = Annot{(int64_t)out_off, mylen * g.esz, me, R};
       }
@@ -681,7 +715,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
       }
       for (int q = 0; q < n; ++q) {
         if (q == me) {
-          a.src[q] = src + g.lo(me, j) * g.esz;
+          a.src[q] = my_in(j);
         } else if (zc) {
           const size_t off = c->in_off(R, me, q);
           a.src[q] = c->at(true, off);
@@ -697,7 +731,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
       if ((rc = k.reduce(kLaneMain, pr))) return rc;
       if (via_ce) {  // result slot written by the copy engine from HBM
         segs.clear();
-        segs.push_back({dst + g.lo(me, j) * g.esz, c->at(false, out_off), mylen * g.esz,
+        segs.push_back({my_out(j), c->at(false, out_off), mylen * g.esz,
                         Annot{(int64_t)out_off, mylen * g.esz, me, R}, true,
                         ubuf(g.lo(me, j) * g.esz, mylen * g.esz)});
         if ((rc = k.copy(kLaneMain, segs, false, false))) return rc;
@@ -711,7 +745,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
       if ((rc = k.wait_peers(LG, kReduced, R + 1, me))) return rc;
       if ((rc = k.record(LG, kEvSlotFree + R % K))) return rc;  // W(R)
       segs.clear();
-      for (int q = 0; q < n; ++q) {
+      for (int q = 0; q < n && !rs; ++q) {
         const size_t len = q == me ? 0 : g.len(q, j);
         if (!len) continue;
         const size_t off = c->out_off(R, q);
@@ -724,7 +758,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
       for (int i = 0; i < n - 1; ++i) {
         const int q = rot(i);
         if ((rc = k.wait_rank(LG, q, kReduced, R + 1))) return rc;
-        const size_t len = g.len(q, j);
+        const size_t len = rs ? 0 : g.len(q, j);
         if (!len) continue;
         const size_t off = c->out_off(R, q);
         segs.clear();
@@ -1182,6 +1216,66 @@ int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int 
   });
 }
 
+// Shared argument checks of the dtype / op / factor triple.
+static int check_reduction_args(int dtype, int op, float factor) {
+  if (dtype != FMX_FLOAT32 && dtype != FMX_BFLOAT16)
+    return fail(FMX_ERR_INVALID_ARG, "bad dtype %d", dtype);
+  if (op < FMX_OP_SUM || op > FMX_OP_PREDIV_SUM) return fail(FMX_ERR_INVALID_ARG, "bad op %d", op);
+  if (op != FMX_OP_SUM && !std::isfinite(factor))
+    return fail(FMX_ERR_INVALID_ARG, "factor must be finite");
+  return FMX_OK;
+}
+
+int fmx_reduce_scatter(fmx_comm_t c, const void* send, void* recv, size_t recvcount, int dtype,
+                       int op, float factor, void* stream) {
+  int rc = check_comm(c);
+  if (rc || (rc = check_reduction_args(dtype, op, factor))) return rc;
+  if (recvcount == 0) return FMX_OK;
+  if (!send || !recv) return fail(FMX_ERR_INVALID_ARG, "null buffer");
+  const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;
+  const bool aligned = (((uintptr_t)send | (uintptr_t)recv) & 15) == 0 && (recvcount * esz) % 16 == 0;
+  CudaSink sink(c);
+  return on_lanes(c, (cudaStream_t)stream, [&]() -> int {
+    if (c->nranks == 1) {  // my chunk is the whole buffer: apply the scale convention
+      PlanReduce pr;
+      memset(&pr.args, 0, sizeof pr.args);
+      pr.args.src[0] = (const char*)send;
+      pr.args.nsrc = 1;
+      pr.args.out_dev = (char*)recv;
+      pr.args.len = recvcount;
+      pr.args.op = op;
+      pr.args.factor = factor;
+      pr.dtype = dtype;
+      pr.aligned = (((uintptr_t)send | (uintptr_t)recv) & 15) == 0;
+      return sink.reduce(kLaneMain, pr);
+    }
+    return plan_allreduce(c, sink, (const char*)send, (char*)recv, recvcount, dtype, op, factor,
+                          aligned, kReduceScatter);
+  });
+}
+
+int fmx_allgather(fmx_comm_t c, const void* send, void* recv, size_t sendcount, int dtype,
+                  void* stream) {
+  int rc = check_comm(c);
+  if (rc) return rc;
+  if (dtype != FMX_FLOAT32 && dtype != FMX_BFLOAT16)
+    return fail(FMX_ERR_INVALID_ARG, "bad dtype %d", dtype);
+  if (sendcount == 0) return FMX_OK;
+  if (!send || !recv) return fail(FMX_ERR_INVALID_ARG, "null buffer");
+  const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;
+  CudaSink sink(c);
+  return on_lanes(c, (cudaStream_t)stream, [&]() -> int {
+    if (c->nranks == 1) {
+      if (send != recv)
+        FMX_CUDA(cudaMemcpyAsync(recv, send, sendcount * esz, cudaMemcpyDeviceToDevice,
+                                 lane_stream(c, kLaneMain)));
+      return FMX_OK;
+    }
+    return plan_allreduce(c, sink, (const char*)send, (char*)recv, sendcount, dtype, FMX_OP_SUM,
+                          1.0f, true, kAllgather);
+  });
+}
+
 int fmx_reduce_local(const void* const* srcs, int nsrc, uint64_t sys_mask, void* dst,
                      void* dst_sys, size_t count, int dtype, int op, float factor, void* stream) {
   if (!srcs || nsrc < 1 || nsrc > FMX_MAX_RANKS || !dst)
@@ -1312,6 +1406,9 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
       return fail(FMX_ERR_INVALID_ARG, "bad broadcast root");
     if (kinds[i] == 0)
       rc = plan_allreduce(&c, sink, dummy, dummy, counts[i], dtypes[i], FMX_OP_SUM, 1.0f, true);
+    else if (kinds[i] == 3 || kinds[i] == 4)  // reduce-scatter / all-gather, in place
+      rc = plan_allreduce(&c, sink, dummy, dummy, counts[i], dtypes[i], FMX_OP_SUM, 1.0f, true,
+                          kinds[i] == 3 ? kReduceScatter : kAllgather);
     else if (kinds[i] == 2)
       rc = plan_allreduce_host(&c, sink, 0, counts[i], dtypes[i], FMX_OP_SUM, 1.0f);
     else

@@ -13,10 +13,11 @@ stood in for by:
   `torch.cuda.set_per_process_memory_fraction`, no peer access;
 * `mps`   - an MPS client capped by `CUDA_MPS_ACTIVE_THREAD_PERCENTAGE`
   (set by the launcher before CUDA initialises); unlike green contexts in
-  separate processes, MPS clients run concurrently;
-* `mps+green` - both: an MPS client (concurrent with its peers) whose work
-  runs in a green context of exactly the 1g SM share - the closest stand-in
-  for a MIG slice (concurrent, SM-partitioned, separate address space);
+  separate processes, which the driver time-slices, MPS clients run
+  concurrently - the closest stand-in for a MIG slice (concurrent,
+  SM-partitioned, separate address space).  A green context inside an MPS
+  client is refused by this driver (CUDA "resources insufficient"), so the
+  two are not combined;
 * `full`  - the whole GPU (one rank per GPU, the NCCL-comparison layout).
 
 In every mode the data path is the same host-SHM transport: P2P/NVLink are
@@ -37,7 +38,7 @@ from dataclasses import dataclass, field
 
 from .commsim import PeerInfo, canonical_bus_id
 
-MODES = ("mig", "green", "mps", "mps+green", "full")
+MODES = ("mig", "green", "mps", "full")
 # Green contexts live as long as the process: tensors allocated under one are
 # freed at interpreter exit, after any local Instance is gone.
 _KEEP_ALIVE: list = []
@@ -112,7 +113,7 @@ def bind(gpu_id: int, instance_id: int, profile: str = "1g.5gb", mode: str = "gr
     inst.gpu_uuid = str(props.uuid)
     inst.bus_id = canonical_bus_id(
         f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0")
-    if mode in ("green", "mps+green"):
+    if mode == "green":
         inst.sm_count = sm_count or default_sm_count(props.multi_processor_count)
         gc = torch.cuda.GreenContext.create(inst.sm_count, device)
         gc.set_context()
@@ -125,7 +126,7 @@ def bind(gpu_id: int, instance_id: int, profile: str = "1g.5gb", mode: str = "gr
     else:
         inst.stream = torch.cuda.Stream(device)
         torch.cuda.set_stream(inst.stream)
-    if memory_fraction is None and mode in ("green", "mps", "mps+green"):
+    if memory_fraction is None and mode in ("green", "mps"):
         memory_fraction = ONE_G_FRACTION
     if memory_fraction:
         torch.cuda.set_per_process_memory_fraction(memory_fraction, device)

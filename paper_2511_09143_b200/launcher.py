@@ -123,7 +123,7 @@ def launch(fn, decision: AllocationDecision, args: tuple = (), *, job_key: str |
     q = ctx.Queue()
     mps = None
     extra = dict(env_extra or {})
-    if mode in ("mps", "mps+green"):
+    if mode == "mps":
         mps = MpsDaemon(job_key)
         if not mps.start():
             raise RuntimeError("mode='mps' requested but the MPS daemon could not start")

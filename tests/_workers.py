@@ -79,6 +79,20 @@ def suite_worker(rank: int, job_key: str, n: int, transport: str, mode: str, sce
                 res = torch.empty_like(t)
                 comm.allreduce(t, op=sc.get("op", "sum"), factor=sc.get("factor"), out=res,
                                stream=stream)
+        elif sc["kind"] == "reduce_scatter":   # t holds n blocks; mine comes back reduced
+            c = sc["count"] // n
+            res = t[rank * c:(rank + 1) * c] if sc.get("inplace") else torch.empty(
+                c, dtype=tdtype, device="cuda")
+            comm.reduce_scatter(t, res, op=sc.get("op", "sum"), factor=sc.get("factor"),
+                                stream=stream)
+        elif sc["kind"] == "allgather":        # t is my block of the n-block result
+            c = sc["count"]
+            res = torch.empty(n * c + off, dtype=tdtype, device="cuda")[off:]
+            if sc.get("inplace"):
+                res[rank * c:(rank + 1) * c].copy_(t)
+                comm.allgather(res[rank * c:(rank + 1) * c], res, stream=stream)
+            else:
+                comm.allgather(t, res, stream=stream)
         else:
             comm.broadcast(t, root=sc["root"], stream=stream)
             res = t

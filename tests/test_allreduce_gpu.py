@@ -26,6 +26,8 @@ def expected(sc: dict, n: int) -> np.ndarray:
     dt = orc.F32 if sc["dtype"] == "f32" else orc.BF16
     if sc["kind"] == "broadcast":
         return xs[sc["root"]].copy()
+    if sc["kind"] == "allgather":
+        return np.concatenate(xs)
     # "allreduce" and "allreduce_host" share the contract
     op = sc.get("op", "sum")
     factor = sc.get("factor")
@@ -69,8 +71,12 @@ def check_all(n, scenarios, results):
         assert "results" in res, f"rank {r}: {res}"
         assert res["launches"] > 0, "no CUDA kernel launched"
     for i, sc in enumerate(scenarios):
-        want = expected(sc, n)
+        want_all = expected(sc, n)
         for r, res in enumerate(results):
+            want = want_all
+            if sc["kind"] == "reduce_scatter":  # rank r's block of the allreduce result
+                c = sc["count"] // n
+                want = want_all[r * c:(r + 1) * c]
             got = res["results"][i]
             if isinstance(got, str):
                 assert got == _workers.digest(want), f"scenario {i} {sc} rank {r}: sha mismatch"
@@ -144,3 +150,27 @@ def test_mig_aware_rejects_double_binding():
     for r in res:
         assert r["init_error"] == "DuplicateDeviceError"
         assert (r["args"], r["args_b"]) == (0, 1)
+
+
+def rs_ag_scenarios(n: int) -> list:
+    """Reduce-scatter / all-gather: NCCL layouts, fp32 and
+    bf16, aligned and ragged block sizes, in place and out of place."""
+    return [
+        dict(kind="reduce_scatter", count=n * 250_000, dtype="f32"),
+        dict(kind="reduce_scatter", count=n * 250_001, dtype="f32", op="avg", inplace=True),
+        dict(kind="reduce_scatter", count=n * 77_777, dtype="bf16", op="postscale", factor=0.5),
+        dict(kind="reduce_scatter", count=n * 3, dtype="bf16", op="avg"),
+        dict(kind="reduce_scatter", count=n * 40_000, dtype="f32", inputs="adversarial"),
+        dict(kind="allgather", count=300_001, dtype="f32"),
+        dict(kind="allgather", count=300_000, dtype="bf16", inplace=True),
+        dict(kind="allgather", count=5, dtype="f32", offset=1),
+        dict(kind="allreduce", count=500_001, dtype="f32", op="avg"),   # shares the round counters
+        dict(kind="allgather", count=1_000_000, dtype="f32", ret="sha"),
+    ]
+
+
+@pytest.mark.parametrize("transport", ["ce", "zc"])
+@pytest.mark.parametrize("n", [2, 7])
+def test_reduce_scatter_and_allgather(n, transport):
+    sc = rs_ag_scenarios(n)
+    check_all(n, sc, run(n, sc, transport=transport, slice_bytes=1 << 18))

@@ -182,6 +182,9 @@ SEQUENCES = {
               ("broadcast", 5, 1, 0), ("allreduce", 123_457, 0), ("broadcast", 90_000, 0, 2),
               ("allreduce", 1, 0)],
     "broadcast-roots": [("broadcast", 40_000, 0, r % 3) for r in range(6)],
+    "rs-ag": [("reduce_scatter", 30_001, 0), ("allgather", 20_000, 1), ("allreduce", 50_000, 0),
+              ("allgather", 3, 0), ("reduce_scatter", 70_000, 1), ("broadcast", 9_000, 0, 1),
+              ("reduce_scatter", 1, 0), ("allgather", 45_000, 0)],
 }
 
 
