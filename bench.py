@@ -65,6 +65,8 @@ def parse_args(argv=None):
     p.add_argument("--out", default=None, help="also write the JSON line here")
     p.add_argument("--no-train", action="store_true", help="skip the ResNet-50 DP img/s leg")
     p.add_argument("--timeline", default=None, help="write a host-polled flag timeline here")
+    p.add_argument("--stamps", default=None,
+                   help="write a GPU-clock timeline of one allreduce (every op of every rank)")
     p.add_argument("--train-only", action="store_true")
     p.add_argument("--train-mode", choices=["green", "mps", "full"], default="mps")
     p.add_argument("--dry-run", action="store_true",
@@ -309,6 +311,18 @@ def rank_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_lo
                 json.dump({"n": n, "slice_bytes": comm.slice_bytes, "count": count,
                            "events": rec.get("ev", [])}, f)
         comm.barrier(300)
+    if cfg.get("stamps"):
+        # pipeline timeline probe: one device-buffer allreduce with a GPU-clock
+        # stamp after every operation of every lane (bench --stamps)
+        comm.barrier(300)
+        torch.cuda.synchronize()
+        comm.set_stamps(1 << 14)
+        comm.barrier(300)
+        device_step()
+        torch.cuda.synchronize()
+        out["stamps_device"] = comm.stamps(1 << 14)
+        comm.set_stamps(0)
+        comm.barrier(300)
     # isolated kernel timing (rank 0 only, every other rank parked at the
     # barrier, so no time-slicing with peers): fmx_reduce_kernel on one
     # pipeline piece, n HBM sources, zero-copy result store to pinned host
@@ -345,6 +359,16 @@ def rank_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_lo
         out["ms_total_e2e"], out["launches_e2e"] = timed(cfg["steps"], host_step)
         out["e2e_digest"] = int(region.view(torch.int32 if esz == 4 else torch.int16)
                                 .to(torch.int64).sum().item())
+        if cfg.get("stamps"):
+            comm.barrier(300)
+            torch.cuda.synchronize()
+            comm.set_stamps(1 << 14)
+            comm.barrier(300)
+            host_step()
+            torch.cuda.synchronize()
+            out["stamps_host"] = comm.stamps(1 << 14)
+            comm.set_stamps(0)
+            comm.barrier(300)
         # (3) device buffers with explicit H2D / D2H copies of the gradient
         pin_in = host.pin_memory()
         pin_out = torch.empty_like(pin_in).pin_memory()
@@ -572,7 +596,7 @@ def run_ours(args) -> dict | None:
     cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
            "slice_bytes": args.slice_bytes, "dtype": args.dtype, "count": args.count,
            "warmup": args.warmup, "steps": args.steps, "e2e": not args.no_e2e,
-           "timeline": args.timeline}
+           "timeline": args.timeline, "stamps": bool(args.stamps)}
     # one job key for all processes of all GPUs
     job_key = os.environ.get("FMX_BENCH_KEY") or f"bench-{os.environ.get('MASTER_PORT', '0')}-" \
         f"{os.environ.get('TORCHELASTIC_RUN_ID', str(os.getppid()))}"
@@ -618,6 +642,12 @@ def run_ours(args) -> dict | None:
                                                           "reasons": ["dry run"]}
     if errors:
         raise RuntimeError(f"rank {errors[0][0]} failed: {errors[0][1]!r}") from errors[0][1]
+    if args.stamps and results:
+        with open(args.stamps, "w") as f:
+            json.dump({"n": n, "slots": int(os.environ.get("FMX_SLOTS", "2")),
+                       "lanes": int(os.environ.get("FMX_LANES", "3")),
+                       "device": {r: v.get("stamps_device", []) for r, v in results.items()},
+                       "host": {r: v.get("stamps_host", []) for r, v in results.items()}}, f)
     local_max = max(r["ms_total"] for r in results.values())
     local_max_e2e = max(r.get("ms_total_e2e", 0.0) for r in results.values())
     local_max_e2e_dev = max(r.get("ms_total_e2e_dev", 0.0) for r in results.values())

@@ -211,6 +211,17 @@ int fmx_comm_monitor(fmx_comm_t comm, double seconds, uint64_t* out, size_t cap,
  * timing was (re)enabled.  Used by bench.py for the per-kernel roofline. */
 int fmx_comm_set_timing(fmx_comm_t comm, int on);
 int fmx_comm_kernel_time(fmx_comm_t comm, double* total_ms, uint64_t* count);
+/* Pipeline timeline probe.  set_stamps(capacity > 0) allocates a device ring
+ * of `capacity` entries and, from then on, enqueues after every operation
+ * (copy batch, reduction, flag signal, flag / event wait) a one-thread kernel
+ * that records the GPU global timer (one clock for all processes on a GPU)
+ * with a (lane << 8 | op) tag and an info word; capacity 0 turns it off.
+ * fmx_comm_stamps synchronises the device and returns up to cap/2 entries as
+ * pairs (t_ns, tag << 32 | info).  Op kinds: 1 wait-peers, 2 wait-rank,
+ * 3 wait-event, 4 copy (info = bytes), 5 reduce (info = elements), 6 signal
+ * (info = value).  Stamp kernels are not counted by fmx_comm_kernel_launches. */
+int fmx_comm_set_stamps(fmx_comm_t comm, size_t capacity);
+int fmx_comm_stamps(fmx_comm_t comm, uint64_t* out, size_t cap, size_t* n_out);
 /* Number of device kernels this communicator has launched so far. */
 int fmx_comm_kernel_launches(fmx_comm_t comm, uint64_t* launches);
 

@@ -50,7 +50,7 @@ EXPORTS = (
     "fmx_reduce_local", "fmx_barrier", "fmx_comm_destroy",
     "fmx_comm_abort", "fmx_comm_rank", "fmx_comm_count", "fmx_comm_peer", "fmx_comm_config",
     "fmx_comm_kernel_launches", "fmx_comm_flags", "fmx_comm_set_timing", "fmx_comm_kernel_time",
-    "fmx_comm_monitor",
+    "fmx_comm_monitor", "fmx_comm_set_stamps", "fmx_comm_stamps",
     "fmx_trace_plan", "fmx_last_error", "fmx_dup_ranks",
     "fmx_abi_version",
 )
@@ -123,6 +123,8 @@ def lib() -> ctypes.CDLL:
         "fmx_comm_set_timing": [c_void, c_int],
         "fmx_comm_monitor": [c_void, c_double, P(ctypes.c_uint64), c_size, P(c_size)],
         "fmx_comm_kernel_time": [c_void, P(c_double), P(ctypes.c_uint64)],
+        "fmx_comm_set_stamps": [c_void, c_size],
+        "fmx_comm_stamps": [c_void, P(ctypes.c_uint64), c_size, P(c_size)],
         "fmx_trace_plan": [c_int, c_int, c_int, c_size, c_int, P(c_int), P(c_size), P(c_int),
                            P(c_int), ctypes.c_char_p, c_size, P(c_size)],
         "fmx_dup_ranks": [P(c_int), P(c_int)],

@@ -232,6 +232,23 @@ class ShmCommunicator:
         return [(buf[2 * i], buf[2 * i + 1] >> 48, (buf[2 * i + 1] >> 32) & 0xFFFF,
                  buf[2 * i + 1] & 0xFFFFFFFF) for i in range(n.value)]
 
+    def set_stamps(self, capacity: int) -> None:
+        """Timeline probe on (capacity entries) or off (0); see fmx_comm_set_stamps."""
+        _lib.check(_lib.lib().fmx_comm_set_stamps(self._h, int(capacity)), "fmx_comm_set_stamps")
+
+    def stamps(self, cap: int = 1 << 16) -> list[tuple[int, int, int, int]]:
+        """[(t_ns, lane, op kind, info)] of the stamps recorded so far."""
+        buf = (ctypes.c_uint64 * (2 * cap))()
+        n = ctypes.c_size_t()
+        _lib.check(_lib.lib().fmx_comm_stamps(self._h, buf, 2 * cap, ctypes.byref(n)),
+                   "fmx_comm_stamps")
+        out = []
+        for i in range(n.value):
+            t, w = buf[2 * i], buf[2 * i + 1]
+            tag, info = w >> 32, w & 0xFFFFFFFF
+            out.append((t, tag >> 8, tag & 0xFF, info))
+        return out
+
     def flags(self) -> list[list[int]]:
         """Every rank's [STAGED, REDUCED, BC_STAGED, BC_DONE] counters."""
         buf = (ctypes.c_uint32 * (4 * self.size))()

@@ -93,7 +93,7 @@ int load_driver() {
 constexpr size_t kDefaultSliceCap = 4u << 20;   // bytes per (owner, contributor) slot
 constexpr size_t kSegmentBudget = 1ull << 30;   // default cap on data-slot bytes
 constexpr int kBatchMax = 128;                  // memops per cuStreamBatchMemOp call
-constexpr int kNumEvents = 2 * FMX_MAX_SLOTS + 5;  // W[K], G[K], fetched[2], reduced[2], inputs
+constexpr int kNumEvents = 2 * FMX_MAX_SLOTS + 7;  // W[K], G[K]; host path F[2], C[2], inputs, P[2]
 
 bool pid_alive(int pid) { return pid > 0 && (kill(pid, 0) == 0 || errno == EPERM); }
 
@@ -131,6 +131,9 @@ struct fmx_comm {
   cudaEvent_t done = nullptr;
   bool has_done = false;
   uint64_t launches = 0;
+  // pipeline timeline probe (fmx_comm_set_stamps): device ring of Stamp entries
+  Stamp* stamps = nullptr;
+  size_t stamp_cap = 0, stamp_used = 0;
   std::vector<fmx_peer_info> peers;
   std::vector<CUstreamBatchMemOpParams> ops;
 
@@ -193,6 +196,7 @@ struct Annot {
   size_t bytes = 0;
   int writer = -1;
   uint32_t round = 0;
+  bool scratch = false;  // a range of the rank's HBM scratch, not of the user buffer
 };
 
 struct PlanSeg {
@@ -209,6 +213,8 @@ struct PlanReduce {
   std::vector<Annot> reads;  // SHM inputs (ZC transport)
   Annot write;               // SHM result slot (written by the kernel)
   Annot user_rw;             // own piece of the user buffer (read + written)
+  std::vector<Annot> scratch_reads;  // HBM scratch inputs (CE transport, host path)
+  Annot scratch_write;               // HBM scratch result (host path)
   int dtype;
   bool aligned;
 };
@@ -234,11 +240,22 @@ int grid_for(size_t work_items, int threads, int cap) {
   return (int)std::max<size_t>(1, std::min<size_t>(g, (size_t)cap));
 }
 
+enum StampKind { kStWaitPeers = 1, kStWaitRank, kStWaitEvent, kStCopy, kStReduce, kStSignal };
+
 class CudaSink final : public Sink {
  public:
   CudaSink(fmx_comm* c) : c_(c) {}
 
-  int copy(int lane, const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel) override {
+  // timeline probe: stamp the completion of the op just enqueued on `lane`
+  int stamp(int lane, int kind, uint32_t info) {
+    if (!c_->stamps || c_->stamp_used >= c_->stamp_cap) return FMX_OK;
+    fmx_stamp_kernel<<<1, 1, 0, lane_stream(c_, lane)>>>(c_->stamps + c_->stamp_used++,
+                                                          (uint32_t)(lane << 8 | kind), info);
+    FMX_CUDA(cudaGetLastError());
+    return FMX_OK;
+  }
+
+  int copy_impl(int lane, const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel) {
     if (segs.empty()) return FMX_OK;
     cudaStream_t s = lane_stream(c_, lane);
     if (!use_kernel) {
@@ -286,7 +303,7 @@ class CudaSink final : public Sink {
     return FMX_OK;
   }
 
-  int reduce(int lane, const PlanReduce& r) override {
+  int reduce_impl(int lane, const PlanReduce& r) {
     const ReduceArgs& a = r.args;
     if (a.len == 0) return FMX_OK;
     cudaStream_t s = lane_stream(c_, lane);
@@ -324,7 +341,7 @@ class CudaSink final : public Sink {
     return FMX_OK;
   }
 
-  int signal(int lane, int flag, uint32_t v) override {
+  int signal_impl(int lane, int flag, uint32_t v) {
     CUstreamBatchMemOpParams op;
     memset(&op, 0, sizeof op);
     op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
@@ -334,7 +351,7 @@ class CudaSink final : public Sink {
     return batch(lane, &op, 1);
   }
 
-  int signal2(int lane, int f0, uint32_t v0, int f1, uint32_t v1) override {
+  int signal2_impl(int lane, int f0, uint32_t v0, int f1, uint32_t v1) {
     CUstreamBatchMemOpParams op[2];
     memset(op, 0, sizeof op);
     op[0].writeValue.operation = op[1].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
@@ -345,7 +362,7 @@ class CudaSink final : public Sink {
     return batch(lane, op, 2);
   }
 
-  int wait_peers(int lane, int flag, uint32_t v, int skip) override {
+  int wait_peers_impl(int lane, int flag, uint32_t v, int skip) {
     ops_.clear();
     for (int q = 0; q < c_->nranks; ++q)
       if (q != skip) ops_.push_back(wait_op(q, flag, v));
@@ -356,7 +373,7 @@ class CudaSink final : public Sink {
     return FMX_OK;
   }
 
-  int wait_rank(int lane, int q, int flag, uint32_t v) override {
+  int wait_rank_impl(int lane, int q, int flag, uint32_t v) {
     CUstreamBatchMemOpParams op = wait_op(q, flag, v);
     return batch(lane, &op, 1);
   }
@@ -371,9 +388,41 @@ class CudaSink final : public Sink {
     return FMX_OK;
   }
 
-  int wait_event(int lane, int ev) override {
+  int wait_event_impl(int lane, int ev) {
     FMX_CUDA(cudaStreamWaitEvent(lane_stream(c_, lane), c_->ev[ev], 0));
     return FMX_OK;
+  }
+
+  // every op, then (timeline probe on) a stamp of its completion on its lane
+  int copy(int lane, const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel) override {
+    size_t bytes = 0;
+    for (const PlanSeg& g : segs) bytes += g.bytes;
+    int rc = copy_impl(lane, segs, src_sys, use_kernel);
+    return rc || segs.empty() ? rc : stamp(lane, kStCopy, (uint32_t)std::min<size_t>(bytes, ~0u));
+  }
+  int reduce(int lane, const PlanReduce& r) override {
+    int rc = reduce_impl(lane, r);
+    return rc || r.args.len == 0 ? rc : stamp(lane, kStReduce, (uint32_t)r.args.len);
+  }
+  int signal(int lane, int flag, uint32_t v) override {
+    int rc = signal_impl(lane, flag, v);
+    return rc ? rc : stamp(lane, kStSignal, v);
+  }
+  int signal2(int lane, int f0, uint32_t v0, int f1, uint32_t v1) override {
+    int rc = signal2_impl(lane, f0, v0, f1, v1);
+    return rc ? rc : stamp(lane, kStSignal, v0);
+  }
+  int wait_peers(int lane, int flag, uint32_t v, int skip) override {
+    int rc = wait_peers_impl(lane, flag, v, skip);
+    return rc ? rc : stamp(lane, kStWaitPeers, v);
+  }
+  int wait_rank(int lane, int q, int flag, uint32_t v) override {
+    int rc = wait_rank_impl(lane, q, flag, v);
+    return rc ? rc : stamp(lane, kStWaitRank, v);
+  }
+  int wait_event(int lane, int ev) override {
+    int rc = wait_event_impl(lane, ev);
+    return rc ? rc : stamp(lane, kStWaitEvent, (uint32_t)ev);
   }
 
  private:
@@ -419,8 +468,10 @@ class TraceSink final : public Sink {
   }
   int reduce(int lane, const PlanReduce& r) override {
     for (const Annot& a : r.reads) shm(lane, a, false);
+    for (const Annot& a : r.scratch_reads) user(lane, a, false);
     user(lane, r.user_rw, false);
     user(lane, r.user_rw, true);
+    user(lane, r.scratch_write, true);
     shm(lane, r.write, true);
     return FMX_OK;
   }
@@ -463,7 +514,8 @@ class TraceSink final : public Sink {
   }
   void user(int lane, const Annot& a, bool write) {
     if (a.off < 0 || a.bytes == 0) return;
-    line("%d %s %lld %zu\n", lane, write ? "UW" : "UR", (long long)a.off, a.bytes);
+    const char* kind = a.scratch ? (write ? "SW" : "SR") : (write ? "UW" : "UR");
+    line("%d %s %lld %zu\n", lane, kind, (long long)a.off, a.bytes);
   }
   int line(const char* fmt, ...) __attribute__((format(printf, 2, 3))) {
     char buf[128];
@@ -509,29 +561,24 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t c
   g.slice = c->slice_bytes / g.esz;
   std::vector<size_t> sizes;
   const size_t s = g.slice;
-  if (c->ramp && g.chunk > 2 * s) {
-    const size_t up[3] = {s / 8, s / 4, s / 2}, down[3] = {s / 2, s / 4, s / 8};
-    const size_t tail = s / 2 + s / 4 + s / 8;
-    size_t left = g.chunk;
-    for (size_t x : up) {
-      sizes.push_back(x);
-      left -= x;
+  if (c->ramp && g.chunk > s) {
+    // geometric ramp s/8, s/4, s/2 up and down (as much of it as fits in half
+    // the chunk each way), the middle in equal rounds of at most s
+    std::vector<size_t> up;
+    size_t ramp_sum = 0;
+    for (size_t x = s / 8; x < s && x > 0; x *= 2) {
+      if (2 * (ramp_sum + x) > g.chunk) break;
+      up.push_back(x);
+      ramp_sum += x;
     }
-    while (left > tail + s) {
-      sizes.push_back(s);
-      left -= s;
+    const size_t mid = g.chunk - 2 * ramp_sum;
+    const size_t k = (mid + s - 1) / s;
+    sizes = up;
+    for (size_t i = 0; i < k; ++i) {  // equal split, multiples of the vector width
+      const size_t lo = (mid * i / k) / vec * vec, hi = i + 1 == k ? mid : (mid * (i + 1) / k) / vec * vec;
+      if (hi > lo) sizes.push_back(hi - lo);
     }
-    // split what is left (<= s + tail) into at most one slice plus the ramp-down
-    if (left > tail) {
-      sizes.push_back(left - tail);
-      left = tail;
-    }
-    for (size_t x : down) {
-      if (!left) break;
-      const size_t y = std::min(x, left);
-      sizes.push_back(y);
-      left -= y;
-    }
+    sizes.insert(sizes.end(), up.rbegin(), up.rend());
   } else {
     for (size_t left = g.chunk; left;) {
       const size_t y = std::min(s, left);
@@ -547,6 +594,7 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t c
 }
 
 Annot ubuf(size_t off_bytes, size_t bytes) { return Annot{(int64_t)off_bytes, bytes, -1, 0}; }
+Annot sbuf(size_t off_bytes, size_t bytes) { return Annot{(int64_t)off_bytes, bytes, -1, 0, true}; }
 
 // Reduce-scatter + all-gather through the segment, pipelined in rounds on three
 // lanes: lane 0 stages (D2H), lane 1 fetches and reduces (H2D + kernel), lane 2
@@ -696,7 +744,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
             const size_t off = c->in_off(R, me, q);
             segs.push_back({c->at(false, off), c->scratch + (size_t)q * c->slice_bytes,
                             mylen * g.esz, Annot{(int64_t)off, mylen * g.esz, q, R}, false,
-                            Annot{}});
+                            sbuf((size_t)q * c->slice_bytes, mylen * g.esz)});
           }
           if ((rc = k.copy(kLaneMain, segs, true, false))) return rc;
         }
@@ -709,7 +757,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
           segs.clear();
           segs.push_back({c->at(false, off), c->scratch + (size_t)q * c->slice_bytes,
                           mylen * g.esz, Annot{(int64_t)off, mylen * g.esz, q, R}, false,
-                          Annot{}});
+                          sbuf((size_t)q * c->slice_bytes, mylen * g.esz)});
           if ((rc = k.copy(kLaneMain, segs, true, false))) return rc;
         }
       }
@@ -723,6 +771,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
           pr.reads.push_back(Annot{(int64_t)off, mylen * g.esz, q, R});
         } else {
           a.src[q] = c->scratch + (size_t)q * c->slice_bytes;
+          pr.scratch_reads.push_back(sbuf((size_t)q * c->slice_bytes, mylen * g.esz));
         }
       }
       // out[R%K][me] is free once every peer gathered round R-K: W(R-K+1)
@@ -783,7 +832,8 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
 // Per GPU that is k*S H2D + k*S D2H, against 2k(n-1)/n*S + k*S (+ the
 // caller's own k*S in and k*S out) for device buffers.
 constexpr uint32_t kInputTag = 1u << 31;  // trace: "input written by the host for round R"
-enum { kEvFetched = 2 * FMX_MAX_SLOTS, kEvReduced = kEvFetched + 2, kEvInputs = kEvFetched + 4 };
+enum { kEvFetched = 2 * FMX_MAX_SLOTS, kEvConsumed = kEvFetched + 2, kEvInputs = kEvFetched + 4,
+       kEvPushed = kEvFetched + 5 };
 
 int plan_allreduce_host(fmx_comm* c, Sink& k, size_t off_bytes, size_t count, int dtype, int op,
                         float factor) {
@@ -791,6 +841,7 @@ int plan_allreduce_host(fmx_comm* c, Sink& k, size_t off_bytes, size_t count, in
   const Geometry g = allreduce_geometry(c, count, dtype);
   const uint32_t R0 = c->ar_round, P = g.rounds;
   const size_t sb = c->slice_bytes;
+  const int LP = c->nlanes == 3 ? kLaneGather : kLaneMain;  // push lane
   auto region = [&](int q, int o, uint32_t j) {
     return c->user_region_off(q) + off_bytes + g.lo(o, j) * g.esz;
   };
@@ -810,21 +861,28 @@ int plan_allreduce_host(fmx_comm* c, Sink& k, size_t off_bytes, size_t count, in
   for (uint32_t j = 0; j < P; ++j) {
     const uint32_t R = R0 + j, slot = j % 2;
     const size_t len = g.len(me, j);
-    char* fetch = c->scratch + (size_t)slot * n * sb;
-    char* result = c->scratch + ((size_t)2 * n + slot) * sb;
-    // lane 0: pull piece j of my chunk out of every region (scratch slot free
-    // once lane 1 finished round j-2)
-    if (j >= 2 && (rc = k.wait_event(kLaneStage, kEvReduced + slot))) return rc;
+    // scratch: fetch slots [2][n], result replicas [2][n] (one per region, so
+    // the push is one 2D copy)
+    const size_t fetch_off = (size_t)slot * n * sb, result_off = ((size_t)2 * n + slot * n) * sb;
+    char* fetch = c->scratch + fetch_off;
+    char* result = c->scratch + result_off;
+    // lane 0: pull piece j of my chunk out of every region; the fetch slot is
+    // free once lane 1's reduce of round j-2 consumed it (C(j-2)), so fetches
+    // run up to two rounds ahead of the pushes
+    if (j >= 2 && (rc = k.wait_event(kLaneStage, kEvConsumed + slot))) return rc;
     segs.clear();
     for (int q = 0; q < n && len; ++q) {
       const size_t off = region(q, me, j);
       segs.push_back({c->at(false, off), fetch + (size_t)q * sb, len * g.esz,
-                      Annot{(int64_t)off, len * g.esz, q, R | kInputTag}, false, Annot{}});
+                      Annot{(int64_t)off, len * g.esz, q, R | kInputTag}, false,
+                      sbuf(fetch_off + (size_t)q * sb, len * g.esz)});
     }
     if ((rc = k.copy(kLaneStage, segs, true, false))) return rc;
     if ((rc = k.record(kLaneStage, kEvFetched + slot))) return rc;
-    // lane 1: reduce in rank order, push the result into every region
+    // lane 1: reduce in rank order; the result slot j%2 is free once lane LP
+    // pushed round j-2 (P(j-2))
     if ((rc = k.wait_event(kLaneMain, kEvFetched + slot))) return rc;
+    if (j >= 2 && LP != kLaneMain && (rc = k.wait_event(kLaneMain, kEvPushed + slot))) return rc;
     if (len) {
       PlanReduce pr;
       memset(&pr.args, 0, sizeof pr.args);
@@ -835,25 +893,38 @@ int plan_allreduce_host(fmx_comm* c, Sink& k, size_t off_bytes, size_t count, in
       pr.args.op = op;
       pr.args.factor = factor;
       pr.args.out_dev = result;
-      for (int q = 0; q < n; ++q) pr.args.src[q] = fetch + (size_t)q * sb;
+      pr.args.n_rep = n;
+      pr.args.rep_stride = sb;
+      for (int q = 0; q < n; ++q) {
+        pr.args.src[q] = fetch + (size_t)q * sb;
+        pr.scratch_reads.push_back(sbuf(fetch_off + (size_t)q * sb, len * g.esz));
+      }
+      pr.scratch_write = sbuf(result_off, n * sb);
       if ((rc = k.reduce(kLaneMain, pr))) return rc;
+    }
+    if ((rc = k.record(kLaneMain, kEvConsumed + slot))) return rc;  // C(j)
+    // lane LP: push the result into every region, off the reduce lane so the
+    // D2H direction never waits behind the next round's fetch
+    if (LP != kLaneMain && (rc = k.wait_event(LP, kEvConsumed + slot))) return rc;
+    if (len) {
       segs.clear();
       for (int q = 0; q < n; ++q) {
         const size_t off = region(q, me, j);
-        segs.push_back({result, c->at(false, off), len * g.esz,
-                        Annot{(int64_t)off, len * g.esz, me, R}, true, Annot{}});
+        segs.push_back({result + (size_t)q * sb, c->at(false, off), len * g.esz,
+                        Annot{(int64_t)off, len * g.esz, me, R}, true,
+                        sbuf(result_off, n * sb)});
       }
-      if ((rc = k.copy(kLaneMain, segs, false, false))) return rc;
+      if ((rc = k.copy(LP, segs, false, false))) return rc;
     }
-    if ((rc = k.record(kLaneMain, kEvReduced + slot))) return rc;
+    if (LP != kLaneMain && (rc = k.record(LP, kEvPushed + slot))) return rc;  // P(j)
   }
-  if ((rc = k.signal(kLaneMain, kReduced, R0 + P))) return rc;
-  if ((rc = k.wait_peers(kLaneMain, kReduced, R0 + P, me))) return rc;
+  if ((rc = k.signal(LP, kReduced, R0 + P))) return rc;
+  if ((rc = k.wait_peers(LP, kReduced, R0 + P, me))) return rc;
   // the caller then reads its whole region (host program order)
   for (int o = 0; o < n; ++o)
     for (uint32_t j = 0; j < P; ++j)
       if (size_t len = g.len(o, j))
-        k.host_access(kLaneMain, Annot{(int64_t)region(me, o, j), len * g.esz, o, R0 + j}, false);
+        k.host_access(LP, Annot{(int64_t)region(me, o, j), len * g.esz, o, R0 + j}, false);
   c->ar_round += P;
   return FMX_OK;
 }
@@ -1141,8 +1212,8 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
     c->registered = true;
     e = cudaHostGetDevicePointer((void**)&c->dbase, c->base, 0);
   }
-  // HBM scratch: CE contributions [n] (device path) / [2][n] fetch + [2] result (host path)
-  if (e == cudaSuccess) e = cudaMalloc((void**)&c->scratch, (2 * (size_t)nranks + 2) * c->slice_bytes);
+  // HBM scratch: CE contributions [n] (device path) / [2][n] fetch + [2][n] result replicas (host path)
+  if (e == cudaSuccess) e = cudaMalloc((void**)&c->scratch, 4 * (size_t)nranks * c->slice_bytes);
 
 
   if (const char* v = getenv("FMX_RESULT_VIA_CE")) c->result_via_ce = atoi(v) != 0;
@@ -1461,6 +1532,7 @@ int fmx_comm_destroy(fmx_comm_t c) {
     g_ctx_pop(&dummy);
   }
   if (c->scratch) cudaFree(c->scratch);
+  if (c->stamps) cudaFree(c->stamps);
   if (c->registered) cudaHostUnregister(c->base);
   if (c->hdr) c->hdr->departed.fetch_add(1);
   unmap(c);
@@ -1568,6 +1640,52 @@ int fmx_comm_kernel_time(fmx_comm_t c, double* total_ms, uint64_t* count) {
   }
   *total_ms = sum;
   *count = c->timed_used;
+  return FMX_OK;
+}
+
+int fmx_comm_set_stamps(fmx_comm_t c, size_t capacity) {
+  if (!c) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
+  const bool pushed = c->lane_ctx && g_ctx_push(c->lane_ctx) == CUDA_SUCCESS;
+  struct Pop {
+    bool on;
+    ~Pop() {
+      CUcontext d;
+      if (on) g_ctx_pop(&d);
+    }
+  } pop{pushed};
+  if (c->stamps) {
+    FMX_CUDA(cudaDeviceSynchronize());
+    FMX_CUDA(cudaFree(c->stamps));
+  }
+  c->stamps = nullptr;
+  c->stamp_cap = c->stamp_used = 0;
+  if (capacity) {
+    FMX_CUDA(cudaMalloc((void**)&c->stamps, capacity * sizeof(Stamp)));
+    c->stamp_cap = capacity;
+  }
+  return FMX_OK;
+}
+
+int fmx_comm_stamps(fmx_comm_t c, uint64_t* out, size_t cap, size_t* n_out) {
+  if (!c || !out || !n_out) return fail(FMX_ERR_INVALID_ARG, "null argument");
+  const size_t n = std::min(c->stamp_used, cap / 2);
+  *n_out = n;
+  if (!n) return FMX_OK;
+  const bool pushed = c->lane_ctx && g_ctx_push(c->lane_ctx) == CUDA_SUCCESS;
+  struct Pop {
+    bool on;
+    ~Pop() {
+      CUcontext d;
+      if (on) g_ctx_pop(&d);
+    }
+  } pop{pushed};
+  std::vector<Stamp> h(n);
+  FMX_CUDA(cudaDeviceSynchronize());
+  FMX_CUDA(cudaMemcpy(h.data(), c->stamps, n * sizeof(Stamp), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < n; ++i) {
+    out[2 * i] = h[i].t_ns;
+    out[2 * i + 1] = ((uint64_t)h[i].tag << 32) | h[i].info;
+  }
   return FMX_OK;
 }
 

@@ -41,6 +41,8 @@ struct ReduceArgs {
   uint64_t sys_mask;               // bit q set: src[q] is mapped host memory
   char* out_dev;                   // HBM result (may alias src[own])
   char* out_sys;                   // SHM result slot (may be null)
+  size_t rep_stride;               // n_rep > 1: also write the result at out_dev + k*rep_stride
+  int n_rep;                       // (host path: one replica per destination region)
   size_t len;                      // elements
   int nsrc;
   int op;
@@ -208,6 +210,7 @@ __global__ void __launch_bounds__(256) fmx_reduce_kernel(const __grid_constant__
       if (i + u * stride < nvec) {
         uint4 o = E::narrow(acc[u]);
         st_v4(a.out_dev + (i + u * stride) * 16, o);
+        for (int k = 1; k < a.n_rep; ++k) st_v4(a.out_dev + k * a.rep_stride + (i + u * stride) * 16, o);
         if (a.out_sys) st_v4(a.out_sys + (i + u * stride) * 16, o);
       }
     }
@@ -223,6 +226,7 @@ __global__ void __launch_bounds__(256) fmx_reduce_kernel(const __grid_constant__
     }
     if (a.op == FMX_OP_SUM_POSTSCALE) acc = __fmul_rn(acc, a.factor);
     E::store1(a.out_dev + e * esz, acc);
+    for (int k = 1; k < a.n_rep; ++k) E::store1(a.out_dev + k * a.rep_stride + e * esz, acc);
     if (a.out_sys) E::store1(a.out_sys + e * esz, acc);
   }
 }
@@ -242,8 +246,29 @@ __global__ void __launch_bounds__(256) fmx_reduce_scalar_kernel(const __grid_con
     }
     if (a.op == FMX_OP_SUM_POSTSCALE) acc = __fmul_rn(acc, a.factor);
     E::store1(a.out_dev + e * esz, acc);
+    for (int k = 1; k < a.n_rep; ++k) E::store1(a.out_dev + k * a.rep_stride + e * esz, acc);
     if (a.out_sys) E::store1(a.out_sys + e * esz, acc);
   }
+}
+
+// ---------------------------------------------------------------- stamps
+
+// Pipeline timeline probe (fmx_comm_set_stamps): one thread writes the GPU's
+// global nanosecond timer - the same clock for every process on the GPU - and
+// a (lane, op, info) tag into the next entry of a device buffer, so stamps
+// enqueued after each operation of every rank line up on one time axis.
+struct Stamp {
+  uint64_t t_ns;
+  uint32_t tag;   // lane << 8 | op kind
+  uint32_t info;  // flag value / bytes / event id
+};
+
+__global__ void fmx_stamp_kernel(Stamp* slot, uint32_t tag, uint32_t info) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  slot->t_ns = t;
+  slot->tag = tag;
+  slot->info = info;
 }
 
 }  // namespace fmx

@@ -163,6 +163,10 @@ def simulate(progs, seed: int, burst: int = 3):
                 access(a, ("user", r, op[1]), op[2], True)
             elif op[0] == "UR":
                 access(a, ("user", r, op[1]), op[2], False)
+            elif op[0] == "SW":   # the rank's HBM scratch (host path slots, CE fetch slots)
+                access(a, ("scratch", r, op[1]), op[2], True)
+            elif op[0] == "SR":
+                access(a, ("scratch", r, op[1]), op[2], False)
             else:
                 raise AssertionError(op)
             pc[a] += 1
@@ -298,6 +302,43 @@ def test_model_catches_a_missing_gather_lane_event(event):
                     lanes[2]]
     assert broken_lanes[1] != lanes[1]
     broken = [broken_lanes if r == 1 else p for r, p in enumerate(progs)]
+    failures = 0
+    for seed in range(80):
+        try:
+            simulate(broken, seed)
+        except AssertionError:
+            failures += 1
+    assert failures > 0
+
+
+def test_model_catches_a_broken_host_scratch_reuse():
+    """Host-buffer path: drop lane 0's waits on "fetch slot consumed" (event
+    ids 10/11) and a fetch overwrites a scratch slot the reduce still reads."""
+    progs = programs(2, [("allreduce_host", 200_000, 0)], 4096, "ce")
+    lanes = progs[0]
+    broken_lanes = [[op for op in lanes[0] if not (op[0] == "X" and op[1] in (10, 11))],
+                    lanes[1], lanes[2]]
+    assert broken_lanes[0] != lanes[0]
+    broken = [broken_lanes if r == 0 else p for r, p in enumerate(progs)]
+    failures = 0
+    for seed in range(80):
+        try:
+            simulate(broken, seed)
+        except AssertionError:
+            failures += 1
+    assert failures > 0
+
+
+def test_model_catches_a_broken_host_push_lane():
+    """Host-buffer path, three lanes: drop lane 1's waits on "result slot
+    pushed" (event ids 13/14) and a reduce overwrites a result slot the push
+    lane still reads."""
+    progs = programs(2, [("allreduce_host", 200_000, 0)], 4096, "ce")
+    lanes = progs[0]
+    broken_lanes = [lanes[0], [op for op in lanes[1] if not (op[0] == "X" and op[1] in (13, 14))],
+                    lanes[2]]
+    assert broken_lanes[1] != lanes[1]
+    broken = [broken_lanes if r == 0 else p for r, p in enumerate(progs)]
     failures = 0
     for seed in range(80):
         try:
