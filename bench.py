@@ -74,6 +74,10 @@ def parse_args(argv=None):
                         "the torchrun N>1 path")
     p.add_argument("--sweep", action="store_true", help="message-size sweep (configs[4]) instead")
     p.add_argument("--sweep-max", type=int, default=1 << 30)
+    p.add_argument("--train-model", choices=["resnet50", "mobilenet_v2", "bert"],
+                   default="resnet50", help="model of the --train-only leg")
+    p.add_argument("--train-no-sync", action="store_true",
+                   help="--train-only: also time the step without gradient sync (compute bound)")
     p.add_argument("--batch", type=int, default=32)
     p.add_argument("--train-steps", type=int, default=10)
     p.add_argument("--train-warmup", type=int, default=5)
@@ -488,18 +492,42 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
         pg = dist.group.WORLD
     stream = inst.stream
     torch.manual_seed(0)
+    name = cfg.get("model", "resnet50")
+    g = torch.Generator(device="cpu").manual_seed(100 + rank)
     with torch.cuda.stream(stream):
-        model = torchvision.models.resnet50().cuda(gpu_local).to(memory_format=torch.channels_last)
+        if name == "bert":
+            # BASELINE configs[3]: BERT-base fine-tune shape, bf16 weights and gradients
+            # (bf16 SHM allreduce), seq 128, 2 labels
+            from transformers import BertConfig, BertForSequenceClassification
+            model = BertForSequenceClassification(BertConfig(num_labels=2)).cuda(gpu_local)
+            model = model.to(torch.bfloat16)
+            x = torch.randint(0, 30522, (cfg["batch"], 128), generator=g).cuda(gpu_local)
+            y = torch.randint(0, 2, (cfg["batch"],), generator=g).cuda(gpu_local)
+        else:
+            ctor = {"resnet50": torchvision.models.resnet50,
+                    "mobilenet_v2": torchvision.models.mobilenet_v2}[name]
+            model = ctor().cuda(gpu_local).to(memory_format=torch.channels_last)
+            x = torch.randn(cfg["batch"], 3, 224, 224, generator=g).cuda(gpu_local)
+            x = x.to(memory_format=torch.channels_last)
+            y = torch.randint(0, 1000, (cfg["batch"],), generator=g).cuda(gpu_local)
         net = fddp.wrap(model, comm, control_group=pg)
-        opt = torch.optim.SGD(net.parameters(), lr=0.01, momentum=0.9)
-        g = torch.Generator(device="cpu").manual_seed(100 + rank)
-        x = torch.randn(cfg["batch"], 3, 224, 224, generator=g).cuda(gpu_local)
-        x = x.to(memory_format=torch.channels_last)
-        y = torch.randint(0, 1000, (cfg["batch"],), generator=g).cuda(gpu_local)
+        if name == "bert":
+            opt = torch.optim.AdamW(net.parameters(), lr=2e-5)
+        else:
+            opt = torch.optim.SGD(net.parameters(), lr=0.01, momentum=0.9)
+
+    from contextlib import nullcontext
 
     def step():
-        with torch.autocast("cuda", dtype=torch.bfloat16):
-            loss = F.cross_entropy(net(x), y)
+        with (net.no_sync() if cfg.get("no_sync") else nullcontext()):
+            return _step()
+
+    def _step():
+        if name == "bert":
+            loss = F.cross_entropy(net(input_ids=x).logits.float(), y)
+        else:
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                loss = F.cross_entropy(net(x), y)
         opt.zero_grad(set_to_none=True)
         loss.backward()
         opt.step()
@@ -563,23 +591,35 @@ def run_ranks(body, spawned, mine, job_key, n, cfg, inst_mode, gpu_local, sample
     return results
 
 
-def run_train(args, d, job_key) -> dict:
-    """ResNet-50 DP img/s on the same instances (single-GPU layout only)."""
+TRAIN_MODELS = {
+    "resnet50": ("torchvision resnet50, random init, synthetic 224x224 inputs",
+                 "bf16 autocast, fp32 weights/grads (fp32 SHM allreduce)", "img_s"),
+    "mobilenet_v2": ("torchvision mobilenet_v2, random init, synthetic 224x224 inputs "
+                     "(BASELINE configs[2] model)",
+                     "bf16 autocast, fp32 weights/grads (fp32 SHM allreduce)", "img_s"),
+    "bert": ("HF BertForSequenceClassification (bert-base config), random init, synthetic "
+             "seq-128 token ids (BASELINE configs[3] model)",
+             "bf16 weights and gradients (bf16 SHM allreduce, fp32 accumulate)", "seq_s"),
+}
+
+
+def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) -> dict:
+    """Data-parallel training throughput on the same instances (single-GPU
+    layout only); DDP buckets allreduced by ddp.flexshm_hook."""
     n = len(d.instances)
     cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
            "batch": args.batch, "train_steps": args.train_steps, "train_warmup": args.train_warmup,
-           "port": 29000 + os.getpid() % 1000}
+           "port": 29000 + os.getpid() % 1000, "model": model, "no_sync": no_sync}
     res = run_ranks(train_body, _spawned_train, list(range(n)), job_key + "-t", n, cfg,
                     args.train_mode, 0)
     t = max(r["ms_total"] for r in res.values()) / 1e3
     digests = {round(r["param_digest"], 3) for r in res.values()}
-    return {"img_s": n * args.batch * args.train_steps / t, "instances": n, "batch_per_instance":
+    desc, precision, unit = TRAIN_MODELS[model]
+    return {unit: n * args.batch * args.train_steps / t, "instances": n, "batch_per_instance":
             args.batch, "ms_per_step": t * 1e3 / args.train_steps, "steps": args.train_steps,
             "warmup": args.train_warmup, "instance_mode": args.train_mode,
-            "precision": "bf16 autocast, fp32 weights/grads (fp32 SHM allreduce)",
-            "replicas_agree": len(digests) == 1, "loss": res[0]["loss"],
-            "gpu_launches": sum(r["launches"] for r in res.values()),
-            "model": "torchvision resnet50, random init, synthetic 224x224 inputs"}
+            "precision": precision, "replicas_agree": len(digests) == 1, "loss": res[0]["loss"],
+            "gpu_launches": sum(r["launches"] for r in res.values()), "model": desc}
 
 
 def run_ours(args) -> dict | None:
@@ -841,7 +881,15 @@ def _main(args, world, n, unit):
         return 0
     if args.train_only:
         d = decision_for(args.gpus, args.ranks_per_gpu)
-        print(json.dumps({"resnet50": run_train(args, d, f"train-{os.getpid()}")}))
+        line = {args.train_model: run_train(args, d, f"train-{os.getpid()}", args.train_model)}
+        if args.train_no_sync:
+            # same instances, same step, gradients NOT synchronised: the compute-only bound
+            line[args.train_model]["no_sync"] = run_train(args, d, f"train-ns-{os.getpid()}",
+                                                          args.train_model, no_sync=True)
+        print(json.dumps(line))
+        if args.out:
+            with open(args.out, "w") as f:
+                f.write(json.dumps(line) + "\n")
         return 0
     line = run_ours(args)
     if line is None:

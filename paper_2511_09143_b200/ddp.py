@@ -9,7 +9,8 @@ PAPER.md:264-271), so here:
   process group over the same ranks - small metadata only;
 * the init-time parameter broadcast (DDP `_sync_module_states`) goes through
   `ShmCommunicator.broadcast` of the flattened parameters;
-* every gradient bucket is allreduced by `flexshm_hook`, which keeps DDP's
+* every gradient bucket is allreduced by `flexshm_hook` on a side stream
+  (overlapping the rest of the backward pass), keeping DDP's
   default-hook arithmetic - divide by world size, then SUM
   (torch/distributed/algorithms/ddp_comm_hooks/default_hooks.py:18-33) -
   fused into one pass (op="avg" = FMX_OP_PREDIV_SUM) with the fixed
@@ -24,17 +25,49 @@ import torch
 from .comm import ShmCommunicator
 
 
-def flexshm_hook(comm: ShmCommunicator, bucket) -> torch.futures.Future[torch.Tensor]:
+class HookState:
+    """What flexshm_hook needs: the communicator and a side stream for the
+    collectives, created in the same context as the rank's work (a green
+    context's stream in green mode), so bucket allreduces overlap the rest of
+    the backward pass instead of queueing on the autograd stream."""
+
+    def __init__(self, comm: ShmCommunicator, stream=None):
+        self.comm = comm
+        if stream is None:
+            inst = getattr(comm, "instance", None)
+            gc = getattr(inst, "green_ctx", None) if inst is not None else None
+            if gc is not None:
+                s = gc.Stream()
+                stream = s if isinstance(s, torch.cuda.Stream) else torch.cuda.ExternalStream(
+                    s.cuda_stream, device=inst.device)
+            else:
+                stream = torch.cuda.Stream()
+        self.stream = stream
+
+
+def flexshm_hook(state, bucket) -> torch.futures.Future[torch.Tensor]:
     """DDP communication hook: bucket.buffer() <- mean over ranks.
 
-    The allreduce is enqueued on the current stream (the stream autograd runs
-    the bucket's producers on), so the future can complete immediately: every
-    consumer of the returned tensor is stream-ordered after the collective.
+    The bucket's producers ran on the current (autograd) stream; the side
+    stream waits for them, runs the allreduce, and the CUDA-aware future
+    records its completion there.  DDP's wait on the future makes the
+    consumer stream wait for that event, so later backward kernels are not
+    queued behind the collective's flag waits.  `state` may also be a bare
+    ShmCommunicator (collective on the current stream, no overlap).
     """
     buf = bucket.buffer()
-    comm.allreduce(buf, op="avg")
-    fut = torch.futures.Future()
-    fut.set_result(buf)
+    if isinstance(state, ShmCommunicator):
+        state.allreduce(buf, op="avg")
+        fut = torch.futures.Future()
+        fut.set_result(buf)
+        return fut
+    cur = torch.cuda.current_stream(buf.device)
+    state.stream.wait_stream(cur)
+    with torch.cuda.stream(state.stream):
+        state.comm.allreduce(buf, op="avg", stream=state.stream)
+        buf.record_stream(state.stream)
+        fut = torch.futures.Future(devices=[buf.device])
+        fut.set_result(buf)
     return fut
 
 
@@ -59,15 +92,16 @@ def broadcast_parameters(module: torch.nn.Module, comm: ShmCommunicator, root: i
 
 
 def wrap(module: torch.nn.Module, comm: ShmCommunicator, control_group=None,
-         bucket_cap_mb: float = 25.0, **ddp_kwargs):
+         bucket_cap_mb: float = 25.0, overlap: bool = True, **ddp_kwargs):
     """DistributedDataParallel over `control_group` (gloo) with gradients on
-    the SHM path.  Parameters are synchronised from rank 0 first."""
+    the SHM path.  Parameters are synchronised from rank 0 first.  With
+    `overlap` the bucket allreduces run on a side stream (HookState)."""
     from torch.nn.parallel import DistributedDataParallel as DDP
 
     broadcast_parameters(module, comm, root=0)
     ddp = DDP(module, process_group=control_group, bucket_cap_mb=bucket_cap_mb,
               broadcast_buffers=False, init_sync=False, **ddp_kwargs)
-    ddp.register_comm_hook(comm, flexshm_hook)
+    ddp.register_comm_hook(HookState(comm) if overlap else comm, flexshm_hook)
     return ddp
 
 

@@ -112,7 +112,8 @@ def suite_worker(rank: int, job_key: str, n: int, transport: str, mode: str, sce
     return {"results": out, "launches": launches, "pid": os.getpid()}
 
 
-def ddp_worker(rank: int, job_key: str, n: int, port: int, mode: str = "green"):
+def ddp_worker(rank: int, job_key: str, n: int, port: int, mode: str = "green",
+               overlap: bool = True):
     """Tiny model: local gradients without DDP, then the same step under DDP
     with the flexshm comm hook; returns both (flattened fp32)."""
     import torch
@@ -135,7 +136,8 @@ def ddp_worker(rank: int, job_key: str, n: int, port: int, mode: str = "green"):
         g = torch.Generator(device="cpu").manual_seed(7 + rank)
         x = torch.randn(32, 64, generator=g).cuda()
         y = torch.randint(0, 10, (32,), generator=g).cuda()
-        net = fddp.wrap(model, comm, control_group=dist.group.WORLD, bucket_cap_mb=0.05)
+        net = fddp.wrap(model, comm, control_group=dist.group.WORLD, bucket_cap_mb=0.05,
+                        overlap=overlap)
         params0 = torch.cat([p.detach().reshape(-1) for p in model.parameters()]).cpu()
         # local gradient (no communication): no_sync skips the reducer
         with net.no_sync():

@@ -17,8 +17,9 @@ from tests import _workers
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n", [2, 3])
-def test_ddp_hook_matches_oracle(n):
+@pytest.mark.parametrize("n,overlap,mode", [(2, True, "green"), (3, True, "green"),
+                                            (2, False, "green"), (3, True, "mps")])
+def test_ddp_hook_matches_oracle(n, overlap, mode):
     from paper_2511_09143_b200.launcher import launch, new_job_key
     from paper_2511_09143_b200.scheduler import fm_select, make_cluster
     from paper_2511_09143_b200.workload import Job
@@ -26,7 +27,8 @@ def test_ddp_hook_matches_oracle(n):
     d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
     key = new_job_key("ddp")
     port = 20000 + os.getpid() % 20000
-    res = launch(_workers.ddp_worker, d, args=(key, n, port), job_key=key, timeout_s=300)
+    res = launch(_workers.ddp_worker, d, args=(key, n, port, mode, overlap), job_key=key,
+                 timeout_s=300, mode=mode)
     for r in res[1:]:
         assert np.array_equal(r["params0"], res[0]["params0"]), "parameter broadcast"
     want = orc.allreduce_c([r["local"] for r in res], orc.F32, orc.OP_PREDIV_SUM, float(n))
