@@ -74,10 +74,13 @@ def parse_args(argv=None):
                         "the torchrun N>1 path")
     p.add_argument("--sweep", action="store_true", help="message-size sweep (configs[4]) instead")
     p.add_argument("--sweep-max", type=int, default=1 << 30)
+    p.add_argument("--sweep-op", choices=["allreduce", "reduce_scatter", "allgather", "broadcast"],
+                   default="allreduce", help="collective of the --sweep (bytes = full buffer)")
     p.add_argument("--train-model", choices=["resnet50", "mobilenet_v2", "bert"],
                    default="resnet50", help="model of the --train-only leg")
     p.add_argument("--train-no-sync", action="store_true",
                    help="--train-only: also time the step without gradient sync (compute bound)")
+    p.add_argument("--bucket-mb", type=float, default=8.0, help="DDP bucket_cap_mb of the DP legs")
     p.add_argument("--batch", type=int, default=32)
     p.add_argument("--train-steps", type=int, default=10)
     p.add_argument("--train-warmup", type=int, default=5)
@@ -420,17 +423,35 @@ def sweep_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     out = {"rank": rank, "ms": {}}
+    op = cfg.get("sweep_op", "allreduce")
+    with torch.cuda.stream(stream):
+        obuf = torch.empty(max(sizes) // esz, dtype=tdt, device=f"cuda:{gpu_local}")
+    torch.cuda.synchronize()
+
+    def call(x, b):
+        # b = bytes of the full (n-block) buffer for reduce_scatter / allgather
+        if op == "allreduce":
+            comm.allreduce(x, op="avg", stream=stream)
+        elif op == "broadcast":
+            comm.broadcast(x, root=0, stream=stream)
+        elif op == "reduce_scatter":
+            blk = x.numel() // n
+            comm.reduce_scatter(x[:blk * n], obuf[:blk], op="avg", stream=stream)
+        else:
+            blk = x.numel() // n
+            comm.allgather(x[:blk], obuf[:blk * n], stream=stream)
+
     for b in sizes:
         x = buf[: b // esz]
         k = max(3, min(200, int(0.2 / max(b * 2 / 50e9 * n, 40e-6))))
         for _ in range(3):
-            comm.allreduce(x, op="avg", stream=stream)
+            call(x, b)
         comm.barrier(300)
         torch.cuda.synchronize()
         comm.barrier(300)
         ev0.record(stream)
         for _ in range(k):
-            comm.allreduce(x, op="avg", stream=stream)
+            call(x, b)
         ev1.record(stream)
         ev1.synchronize()
         out["ms"][b] = (ev0.elapsed_time(ev1) / k, k)
@@ -449,20 +470,22 @@ def run_sweep(args) -> list[dict]:
     n = len(d.instances)
     cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
            "slice_bytes": args.slice_bytes, "dtype": args.dtype,
-           "sizes": [b for b in SWEEP_SIZES if b <= args.sweep_max]}
+           "sizes": [b for b in SWEEP_SIZES if b <= args.sweep_max], "sweep_op": args.sweep_op}
     res = run_ranks(sweep_body, _spawned_sweep, list(range(n)), f"sweep-{os.getpid()}", n, cfg,
                     args.mode, 0)
     lines = []
     for b in cfg["sizes"]:
         ms = max(r["ms"][b][0] for r in res.values())
         per_gpu = [n]
-        lines.append({"sweep": "allreduce size sweep (BASELINE configs[4])", "bytes": b,
+        lines.append({"sweep": f"{args.sweep_op} size sweep (BASELINE configs[4])", "bytes": b,
+                      "op": args.sweep_op,
                       "ranks": n, "instance_mode": args.mode, "dtype": args.dtype,
                       "ms": ms, "algbw_gbs": b / ms / 1e6,
                       "busbw_gbs": b / ms / 1e6 * 2 * (n - 1) / n,
                       "iters": res[0]["ms"][b][1],
                       "step_roofline_frac": step_roofline(n, per_gpu, b, ms / 1e3,
-                                                          LINK_PEAK_FALLBACK)["frac"]})
+                                                          LINK_PEAK_FALLBACK)["frac"]
+                      if args.sweep_op == "allreduce" else None})
     return lines
 
 
@@ -510,7 +533,7 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
             x = torch.randn(cfg["batch"], 3, 224, 224, generator=g).cuda(gpu_local)
             x = x.to(memory_format=torch.channels_last)
             y = torch.randint(0, 1000, (cfg["batch"],), generator=g).cuda(gpu_local)
-        net = fddp.wrap(model, comm, control_group=pg)
+        net = fddp.wrap(model, comm, control_group=pg, bucket_cap_mb=cfg.get("bucket_mb", 25.0))
         if name == "bert":
             opt = torch.optim.AdamW(net.parameters(), lr=2e-5)
         else:
@@ -609,7 +632,8 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
     n = len(d.instances)
     cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
            "batch": args.batch, "train_steps": args.train_steps, "train_warmup": args.train_warmup,
-           "port": 29000 + os.getpid() % 1000, "model": model, "no_sync": no_sync}
+           "port": 29000 + os.getpid() % 1000, "model": model, "no_sync": no_sync,
+           "bucket_mb": args.bucket_mb}
     res = run_ranks(train_body, _spawned_train, list(range(n)), job_key + "-t", n, cfg,
                     args.train_mode, 0)
     t = max(r["ms_total"] for r in res.values()) / 1e3
@@ -648,6 +672,9 @@ def run_ours(args) -> dict | None:
     my_gpu = grank if world > 1 else 0
     mine = [r for r, (g, _) in enumerate(d.instances) if g == my_gpu] if world > 1 else list(range(n))
     gpu_local = local if world > 1 else 0
+    if os.environ.get("FMX_DEVICE_MAP"):
+        # e.g. "0,0": run the N>1 orchestration with several logical GPUs on one device
+        gpu_local = int(os.environ["FMX_DEVICE_MAP"].split(",")[local])
     inst_mode = args.mode
     sampler = ClockSampler() if not args.dry_run else None
     results = {}

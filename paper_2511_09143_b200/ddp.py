@@ -92,10 +92,13 @@ def broadcast_parameters(module: torch.nn.Module, comm: ShmCommunicator, root: i
 
 
 def wrap(module: torch.nn.Module, comm: ShmCommunicator, control_group=None,
-         bucket_cap_mb: float = 25.0, overlap: bool = True, **ddp_kwargs):
+         bucket_cap_mb: float = 8.0, overlap: bool = True, **ddp_kwargs):
     """DistributedDataParallel over `control_group` (gloo) with gradients on
     the SHM path.  Parameters are synchronised from rank 0 first.  With
-    `overlap` the bucket allreduces run on a side stream (HookState)."""
+    `overlap` the bucket allreduces run on a side stream (HookState).
+    bucket_cap_mb defaults to 8 (not DDP's 25): the last bucket's allreduce is
+    exposed after the backward pass, and 5-10 MB measured best for ResNet-50 on
+    7 instances (profiles/r01/r1y: 3357 img/s at 8 MB, 3218 at 25, 2905 at 50)."""
     from torch.nn.parallel import DistributedDataParallel as DDP
 
     broadcast_parameters(module, comm, root=0)

@@ -25,7 +25,7 @@ never touched, matching what MIG permits (reference PAPER.md:262).
 
 `peer_info()` builds the rank's `commsim.PeerInfo`: canonical PCIe bus id of
 the physical GPU, and a per-instance identity token as `mig_id` (the MIG UUID,
-or `<mode>-<gpu uuid>-<instance id>`), which is what lets several ranks share
+or `<mode>-<gpu uuid>-<gpu id>.<instance id>`), which is what lets several ranks share
 one bus id under MIG-aware discovery (reference commsim.py:67-88).
 """
 
@@ -89,7 +89,7 @@ class Instance:
     def mig_id(self) -> str:
         if self.mode == "mig" and self.mig_uuid:
             return self.mig_uuid
-        return f"{self.mode}-{self.gpu_uuid}-{self.instance_id}"
+        return f"{self.mode}-{self.gpu_uuid}-{self.gpu_id}.{self.instance_id}"
 
     def cuda_stream(self) -> int:
         import torch
