@@ -1205,6 +1205,28 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
     *out = c;
     return FMX_OK;
   }
+  // NUMA placement by first touch, before anyone pins the segment (pinning
+  // faults every page in on the pinning rank's node): each owner writes the
+  // regions only it reads or writes - its in-slots [k][me][*], its out-slots
+  // [k][me], its registered host buffer - so on a multi-socket host they land
+  // on the node of the CPUs the launcher pinned the rank to (the GPU's node).
+  {
+    const size_t sb = c->slice_bytes, n = (size_t)nranks;
+    for (int k = 0; k < c->nslots; ++k) {
+      memset(c->base + c->in_off(k, rank, 0), 0, n * sb);
+      memset(c->base + c->out_off(k, rank), 0, sb);
+    }
+    if (c->L.user_bytes) memset(c->base + c->user_region_off(rank), 0, c->L.user_bytes);
+    h->touched.fetch_add(1, std::memory_order_acq_rel);
+    while (h->touched.load(std::memory_order_acquire) < nranks) {
+      if (h->aborted.load() || now_s() > t_end) {
+        unmap(c);
+        delete c;
+        return fail(FMX_ERR_TIMEOUT, "bootstrap: a rank failed to initialise its regions");
+      }
+      usleep(200);
+    }
+  }
   // device mapping
   cudaError_t e = cudaHostRegister(c->base, c->total_bytes,
                                    cudaHostRegisterMapped | cudaHostRegisterPortable);

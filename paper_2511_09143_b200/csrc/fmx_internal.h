@@ -46,6 +46,7 @@ struct Header {
   alignas(64) std::atomic<int32_t> aborted;
   alignas(64) std::atomic<int64_t> barrier_count;
   alignas(64) std::atomic<int32_t> departed;
+  alignas(64) std::atomic<int32_t> touched;  // ranks done first-touching their regions
   char job_key[128];
 };
 

@@ -97,12 +97,32 @@ class Instance:
         return int(s.cuda_stream)
 
 
+def gpu_cpus(nvml_bus_id: str) -> set[int] | None:
+    """CPUs of the GPU's NUMA node (NVML ideal affinity) for a PCI id in NVML's
+    form (`00000000:9C:00.0`), or None if unknown."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            h = pynvml.nvmlDeviceGetHandleByPciBusId(nvml_bus_id)
+            words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+        finally:
+            pynvml.nvmlShutdown()
+    except Exception:  # noqa: BLE001 - no NVML / no such device: leave affinity alone
+        return None
+    cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+    allowed = os.sched_getaffinity(0)
+    return (cpus & allowed) or None
+
+
 def bind(gpu_id: int, instance_id: int, profile: str = "1g.5gb", mode: str = "green",
          device: int = 0, sm_count: int | None = None, memory_fraction: float | None = None,
-         mig_uuid: str | None = None) -> Instance:
+         mig_uuid: str | None = None, pin_cpus: bool = True) -> Instance:
     """Bind this process to one instance.  `device` is the torch device index
     the instance's GPU has in this process (0 when the launcher narrowed
-    CUDA_VISIBLE_DEVICES to it)."""
+    CUDA_VISIBLE_DEVICES to it).  `pin_cpus` restricts the process to the
+    CPUs of the GPU's NUMA node, so the SHM regions it first-touches in
+    fmx_comm_init are allocated next to its GPU on multi-socket hosts."""
     import torch
 
     if mode not in MODES:
@@ -113,6 +133,11 @@ def bind(gpu_id: int, instance_id: int, profile: str = "1g.5gb", mode: str = "gr
     inst.gpu_uuid = str(props.uuid)
     inst.bus_id = canonical_bus_id(
         f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0")
+    if pin_cpus:
+        cpus = gpu_cpus(f"{props.pci_domain_id:08X}:{props.pci_bus_id:02X}:"
+                        f"{props.pci_device_id:02X}.0")
+        if cpus:
+            os.sched_setaffinity(0, cpus)
     if mode == "green":
         inst.sm_count = sm_count or default_sm_count(props.multi_processor_count)
         gc = torch.cuda.GreenContext.create(inst.sm_count, device)
