@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include "../../include/flexshm.h"
+#include "fmx_args.h"
 
 namespace fmx {
 
@@ -36,18 +37,6 @@ struct CopyArgs {
   int src_sys;  // 1: sources live in mapped host memory -> ld.cv
 };
 
-struct ReduceArgs {
-  const char* src[FMX_MAX_RANKS];  // rank-ordered sources
-  uint64_t sys_mask;               // bit q set: src[q] is mapped host memory
-  char* out_dev;                   // HBM result (may alias src[own])
-  char* out_sys;                   // SHM result slot (may be null)
-  size_t rep_stride;               // n_rep > 1: also write the result at out_dev + k*rep_stride
-  int n_rep;                       // (host path: one replica per destination region)
-  size_t len;                      // elements
-  int nsrc;
-  int op;
-  float factor;
-};
 
 __device__ __forceinline__ uint4 ld_cv_v4(const void* p) {
   uint4 v;
@@ -205,14 +194,20 @@ __global__ void __launch_bounds__(256) fmx_reduce_kernel(const __grid_constant__
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (i + u * stride < nvec) reduce_vec<T>(a, (i + u * stride) * 16, acc[u]);
+    uint4 o[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (i + u * stride < nvec) {
-        uint4 o = E::narrow(acc[u]);
-        st_v4(a.out_dev + (i + u * stride) * 16, o);
-        for (int k = 1; k < a.n_rep; ++k) st_v4(a.out_dev + k * a.rep_stride + (i + u * stride) * 16, o);
-        if (a.out_sys) st_v4(a.out_sys + (i + u * stride) * 16, o);
+        o[u] = E::narrow(acc[u]);
+        st_v4(a.out_dev + (i + u * stride) * 16, o[u]);
+        if (a.out_sys) st_v4(a.out_sys + (i + u * stride) * 16, o[u]);
       }
+    }
+    // host path: the same result into every replica (one per destination region)
+    for (int k = 1; k < a.n_rep; ++k) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i + u * stride < nvec) st_v4(a.out_dev + k * a.rep_stride + (i + u * stride) * 16, o[u]);
     }
   }
   // element tail (len not a multiple of the vector width)
@@ -257,11 +252,6 @@ __global__ void __launch_bounds__(256) fmx_reduce_scalar_kernel(const __grid_con
 // global nanosecond timer - the same clock for every process on the GPU - and
 // a (lane, op, info) tag into the next entry of a device buffer, so stamps
 // enqueued after each operation of every rank line up on one time axis.
-struct Stamp {
-  uint64_t t_ns;
-  uint32_t tag;   // lane << 8 | op kind
-  uint32_t info;  // flag value / bytes / event id
-};
 
 __global__ void fmx_stamp_kernel(Stamp* slot, uint32_t tag, uint32_t info) {
   uint64_t t;

@@ -1,0 +1,579 @@
+// The schedule of libflexshm: what one rank enqueues for one collective,
+// written once against a Sink.  CudaSink (flexshm_comm.cu) turns it into
+// stream operations; TraceSink (here) records it as text so every rank of any
+// world size can be model-checked on a CPU (fmx_trace_plan,
+// tests/test_protocol_model.py).  No CUDA calls in this file.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "fmx_comm.h"
+
+namespace fmx {
+
+// Text trace, one line per access / flag operation, prefixed by the lane:
+//   <lane> W <off> <bytes> <round>           write SHM bytes of `round`
+//   <lane> R <off> <bytes> <writer> <round>  read SHM bytes `writer` wrote in `round`
+//   <lane> UR <off> <bytes> / UW <off> <bytes>   read / write own user buffer
+//   <lane> S <flag> <value>                  signal own flag
+//   <lane> A <rank> <flag> <value>           wait until rank's flag >= value
+//   J                                        both lanes join (collective boundary)
+class TraceSink final : public Sink {
+ public:
+  explicit TraceSink(std::string* out) : out_(out) {}
+  int copy(int lane, const std::vector<PlanSeg>& segs, bool, bool) override {
+    for (const PlanSeg& g : segs) {
+      if (g.shm_is_dst) {
+        user(lane, g.user, false);
+        shm(lane, g.shm, true);
+      } else {
+        shm(lane, g.shm, false);
+        user(lane, g.user, true);
+      }
+    }
+    return FMX_OK;
+  }
+  int reduce(int lane, const PlanReduce& r) override {
+    for (const Annot& a : r.reads) shm(lane, a, false);
+    for (const Annot& a : r.scratch_reads) user(lane, a, false);
+    user(lane, r.user_rw, false);
+    user(lane, r.user_rw, true);
+    user(lane, r.scratch_write, true);
+    shm(lane, r.write, true);
+    return FMX_OK;
+  }
+  int signal(int lane, int flag, uint32_t v) override { return line("%d S %d %u\n", lane, flag, v); }
+  int signal2(int lane, int f0, uint32_t v0, int f1, uint32_t v1) override {
+    line("%d S %d %u\n", lane, f0, v0);
+    return line("%d S %d %u\n", lane, f1, v1);
+  }
+  int wait_peers(int lane, int flag, uint32_t v, int skip) override {
+    for (int q = 0; q < nranks; ++q)
+      if (q != skip) line("%d A %d %d %u\n", lane, q, flag, v);
+    return FMX_OK;
+  }
+  int wait_rank(int lane, int q, int flag, uint32_t v) override {
+    return line("%d A %d %d %u\n", lane, q, flag, v);
+  }
+  int d2d(int lane, void*, const void*, size_t, Annot from, Annot to) override {
+    user(lane, from, false);
+    user(lane, to, true);
+    return FMX_OK;
+  }
+  int record(int lane, int ev) override { return line("%d E %d %d\n", lane, ev, ++seq_[ev]); }
+  int wait_event(int lane, int ev) override {
+    return seq_[ev] ? line("%d X %d %d\n", lane, ev, seq_[ev]) : FMX_OK;
+  }
+  int host_access(int lane, const Annot& a, bool write) override {
+    shm(lane, a, write);
+    return FMX_OK;
+  }
+  int join() { return line("J\n"); }
+  int nranks = 0;
+
+ private:
+  void shm(int lane, const Annot& a, bool write) {
+    if (a.off < 0 || a.bytes == 0) return;
+    if (write)
+      line("%d W %lld %zu %u\n", lane, (long long)a.off, a.bytes, a.round);
+    else
+      line("%d R %lld %zu %d %u\n", lane, (long long)a.off, a.bytes, a.writer, a.round);
+  }
+  void user(int lane, const Annot& a, bool write) {
+    if (a.off < 0 || a.bytes == 0) return;
+    const char* kind = a.scratch ? (write ? "SW" : "SR") : (write ? "UW" : "UR");
+    line("%d %s %lld %zu\n", lane, kind, (long long)a.off, a.bytes);
+  }
+  int line(const char* fmt, ...) __attribute__((format(printf, 2, 3))) {
+    char buf[128];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    out_->append(buf);
+    return FMX_OK;
+  }
+  std::string* out_;
+  int seq_[kNumEvents] = {};
+};
+
+// Round j of every chunk covers [prefix(j), prefix(j) + size(j)).  With the
+// ramp, the first rounds are slice/8, /4, /2 and the last ones /2, /4, /8: the
+// pipeline fills (round 0's stage is pure D2H, the H2D direction idle) and
+// drains (the last gather is pure H2D) in 1/8 of the time a full slice takes.
+// chunk_elems = 0: allreduce chunking (16-byte aligned chunk starts over
+// `count`); otherwise every rank's chunk has exactly chunk_elems elements and
+// count = n * chunk_elems (reduce-scatter / all-gather, NCCL's layout).
+Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t chunk_elems) {
+  Geometry g;
+  const int n = c->nranks;
+  g.esz = dtype == FMX_FLOAT32 ? 4 : 2;
+  const size_t vec = 16 / g.esz;
+  g.count = chunk_elems ? chunk_elems * n : count;
+  g.chunk = chunk_elems ? chunk_elems : ((count + n - 1) / n + vec - 1) / vec * vec;
+  g.slice = c->slice_bytes / g.esz;
+  std::vector<size_t> sizes;
+  const size_t s = g.slice;
+  if (c->ramp && g.chunk > s) {
+    // geometric ramp s/8, s/4, s/2 up and down (as much of it as fits in half
+    // the chunk each way), the middle in equal rounds of at most s
+    std::vector<size_t> up;
+    size_t ramp_sum = 0;
+    for (size_t x = s / 8; x < s && x > 0; x *= 2) {
+      if (2 * (ramp_sum + x) > g.chunk) break;
+      up.push_back(x);
+      ramp_sum += x;
+    }
+    const size_t mid = g.chunk - 2 * ramp_sum;
+    const size_t k = (mid + s - 1) / s;
+    sizes = up;
+    for (size_t i = 0; i < k; ++i) {  // equal split, multiples of the vector width
+      const size_t lo = (mid * i / k) / vec * vec, hi = i + 1 == k ? mid : (mid * (i + 1) / k) / vec * vec;
+      if (hi > lo) sizes.push_back(hi - lo);
+    }
+    sizes.insert(sizes.end(), up.rbegin(), up.rend());
+  } else {
+    for (size_t left = g.chunk; left;) {
+      const size_t y = std::min(s, left);
+      sizes.push_back(y);
+      left -= y;
+    }
+  }
+  if (sizes.empty()) sizes.push_back(0);  // count == 0 never reaches here; keep rounds >= 1
+  g.rounds = (uint32_t)sizes.size();
+  g.start.assign(g.rounds + 1, 0);
+  for (uint32_t j = 0; j < g.rounds; ++j) g.start[j + 1] = g.start[j] + sizes[j];
+  return g;
+}
+
+
+// Reduce-scatter + all-gather through the segment, pipelined in rounds on three
+// lanes: lane 0 stages (D2H), lane 1 fetches and reduces (H2D + kernel), lane 2
+// gathers (H2D).  Round R uses slot R % 2.  With the gather on its own lane, a
+// rank fetches round R+1 while it still waits for the slowest owner of round R,
+// so the H2D direction never idles at a round boundary.
+//
+// Enqueue order is itself a valid single-stream schedule: every wait (flag or
+// event) points at work enqueued earlier, by this rank or by peers that enqueue
+// in the same order.  So however the driver maps the lane streams onto
+// hardware queues - even one shared FIFO - nothing can deadlock; separate queues
+// only add overlap.  Lane 0 never waits on a flag: only on events of lane 2.
+// The model checker checks both the multi-lane and the merged single-FIFO reading.
+//
+// Events (slot = round parity): W(R) is recorded on the gather lane once every
+// peer's REDUCED >= R+1 was seen, G(R) once gather(R) completed.  REDUCED(R)
+// (value R+1) is signalled after reduce(R) AND G(R-1), so "REDUCED[q] >= R+1"
+// also says "q finished gathering round R-1".
+//
+// Hazards and the wait that covers each:
+//  stage(R) into in[R%2][o][me], last read by owner o's fetch of round R-2:
+//      W(R-2) (every owner signalled REDUCED after its fetches of R-2); rounds
+//      of an earlier collective are covered by the fork.
+//  fetch(R) of in[R%2][me][q]              -> wait STAGED(_TO)[q] >= R+1
+//  reduce(R) writes out[R%2][me], last read by every q's gather(R-2):
+//      W(R-1): every q signalled REDUCED >= R, which q issued after G_q(R-2).
+//  gather(R) reads out[R%2][q]             -> wait REDUCED[q] >= R+1
+//  in place: gather(R) overwrites piece (q, R); my stage(R) read it first,
+//      because owner q's reduce(R) waited for my STAGED >= R+1.
+// With FMX_LANES=2 the gather runs on lane 1 and the W/G waits are implied by
+// stream order (the schedule of the first B200 runs).
+enum { kEvSlotFree = 0, kEvGathered = FMX_MAX_SLOTS };  // + R % K: W(R) and G(R) above
+
+// The three owner-chunk collectives share one schedule:
+//   kAllreduce     stage -> fetch -> reduce (HBM + result slot) -> gather
+//   kReduceScatter stage -> fetch -> reduce into recv (no result slot, no gather copies)
+//   kAllgather     publish my chunk (result slot + my part of recv) -> gather
+// Flags, events and slot reuse are identical, so one model-checked protocol
+// covers all three.  For the last two, `count` is the per-rank count and the
+// buffers follow NCCL: send/recv of reduce-scatter hold n*count / count
+// elements, those of all-gather count / n*count.
+
+int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
+                   int op, float factor, bool aligned, int kind) {
+  const int n = c->nranks, me = c->rank;
+  const bool zc = c->transport == FMX_TRANSPORT_ZC;
+  const int LG = c->nlanes == 3 ? kLaneGather : kLaneMain;
+  const int K = c->nslots;  // pipeline depth: slots per region
+  const bool split = LG != kLaneMain;  // gather on its own lane: explicit W / G waits
+  const bool ar = kind == kAllreduce, rs = kind == kReduceScatter, ag = kind == kAllgather;
+  const Geometry g = allreduce_geometry(c, count, dtype, ar ? 0 : count);
+  // where piece (me, j) of the result goes, and where my contribution / my
+  // published chunk comes from (all-gather's send holds only my chunk)
+  auto my_out = [&](uint32_t j) { return dst + (rs ? g.start[j] : g.lo(me, j)) * g.esz; };
+  auto my_in = [&](uint32_t j) { return src + (ag ? g.start[j] : g.lo(me, j)) * g.esz; };
+  std::vector<PlanSeg> segs;
+  int rc;
+  const uint32_t R0 = c->ar_round;
+  // peers in rotated order starting after me, so that at any moment the
+  // ranks work on different owners / contributors instead of all on one
+  auto rot = [&](int i) { return (me + 1 + i) % n; };
+
+  auto stage = [&](uint32_t j) -> int {
+    const uint32_t R = R0 + j;
+    if (ag) return FMX_OK;  // nothing to reduce: no contributions to stage
+    // slot R%K was read by round R-K's fetches: W(R-K)
+    if (j >= K && (rc = k.wait_event(kLaneStage, kEvSlotFree + R % K))) return rc;
+    if (c->coarse) {  // one batch of copies, one STAGED signal
+      segs.clear();
+      for (int o = 0; o < n; ++o) {
+        const size_t len = o == me ? 0 : g.len(o, j);
+        if (!len) continue;
+        const size_t off = c->in_off(R, o, me);
+        segs.push_back({src + g.lo(o, j) * g.esz, c->at(zc, off), len * g.esz,
+                        Annot{(int64_t)off, len * g.esz, me, R}, true,
+                        ubuf(g.lo(o, j) * g.esz, len * g.esz)});
+      }
+      if ((rc = k.copy(kLaneStage, segs, false, zc))) return rc;
+      return k.signal(kLaneStage, kStaged, R + 1);
+    }
+    for (int i = 0; i < n - 1; ++i) {
+      const int o = rot(i);
+      const size_t len = g.len(o, j);
+      segs.clear();
+      if (len) {
+        const size_t off = c->in_off(R, o, me);
+        segs.push_back({src + g.lo(o, j) * g.esz, c->at(zc, off), len * g.esz,
+                        Annot{(int64_t)off, len * g.esz, me, R}, true,
+                        ubuf(g.lo(o, j) * g.esz, len * g.esz)});
+        if ((rc = k.copy(kLaneStage, segs, false, zc))) return rc;
+      }
+      if ((rc = k.signal(kLaneStage, kStagedTo + o, R + 1))) return rc;
+    }
+    return FMX_OK;
+  };
+
+  // lane 0 stages K-1 rounds ahead of the reduction
+  const uint32_t ahead = (uint32_t)K - 1;
+  for (uint32_t j = 0; j < ahead && j < g.rounds; ++j)
+    if ((rc = stage(j))) return rc;
+  for (uint32_t j = 0; j < g.rounds; ++j) {
+    const uint32_t R = R0 + j;
+    if (j + ahead < g.rounds && (rc = stage(j + ahead))) return rc;
+    // lane 1: fetch, then reduce-scatter my chunk in ascending rank order
+    const size_t mylen = g.len(me, j);
+    if (mylen && ag) {
+      // publish: my piece into my result slot (and into my part of recv)
+      const size_t out_off = c->out_off(R, me);
+      if (split && j + 1 >= K && (rc = k.wait_event(kLaneMain, kEvSlotFree + (R + 1 - K) % K)))
+        return rc;
+      segs.clear();
+      segs.push_back({my_in(j), c->at(zc, out_off), mylen * g.esz,
+                      Annot{(int64_t)out_off, mylen * g.esz, me, R}, true,
+                      ubuf(g.lo(me, j) * g.esz, mylen * g.esz)});
+      if ((rc = k.copy(kLaneMain, segs, false, zc))) return rc;
+      if (my_out(j) != my_in(j) &&
+          (rc = k.d2d(kLaneMain, my_out(j), my_in(j), mylen * g.esz,
+                      ubuf(g.lo(me, j) * g.esz, mylen * g.esz),
+                      ubuf(g.lo(me, j) * g.esz, mylen * g.esz))))
+        return rc;
+    } else if (mylen) {
+      PlanReduce pr;
+      memset(&pr.args, 0, sizeof pr.args);
+      pr.dtype = dtype;
+      pr.aligned = aligned;
+      ReduceArgs& a = pr.args;
+      a.nsrc = n;
+      a.len = mylen;
+      a.op = op;
+      a.factor = factor;
+      a.out_dev = my_out(j);
+      const size_t out_off = c->out_off(R, me);
+      pr.user_rw = ubuf(g.lo(me, j) * g.esz, mylen * g.esz);
+      const bool via_ce = ar && !zc && c->result_via_ce;
+      if (ar && !via_ce) {
+        a.out_sys = c->at(true, out_off);
+        pr.write = Annot{(int64_t)out_off, mylen * g.esz, me, R};
+      }
+      // each contribution is fetched as soon as its contributor staged it
+      if (c->coarse) {
+        if ((rc = k.wait_peers(kLaneMain, kStaged, R + 1, me))) return rc;
+        if (!zc) {
+          segs.clear();
+          for (int q = 0; q < n; ++q) {
+            if (q == me) continue;
+            const size_t off = c->in_off(R, me, q);
+            segs.push_back({c->at(false, off), c->scratch + (size_t)q * c->slice_bytes,
+                            mylen * g.esz, Annot{(int64_t)off, mylen * g.esz, q, R}, false,
+                            sbuf((size_t)q * c->slice_bytes, mylen * g.esz)});
+          }
+          if ((rc = k.copy(kLaneMain, segs, true, false))) return rc;
+        }
+      }
+      for (int i = 0; i < n - 1 && !c->coarse; ++i) {
+        const int q = rot(i);
+        if ((rc = k.wait_rank(kLaneMain, q, kStagedTo + me, R + 1))) return rc;
+        if (!zc) {
+          const size_t off = c->in_off(R, me, q);
+          segs.clear();
+          segs.push_back({c->at(false, off), c->scratch + (size_t)q * c->slice_bytes,
+                          mylen * g.esz, Annot{(int64_t)off, mylen * g.esz, q, R}, false,
+                          sbuf((size_t)q * c->slice_bytes, mylen * g.esz)});
+          if ((rc = k.copy(kLaneMain, segs, true, false))) return rc;
+        }
+      }
+      for (int q = 0; q < n; ++q) {
+        if (q == me) {
+          a.src[q] = my_in(j);
+        } else if (zc) {
+          const size_t off = c->in_off(R, me, q);
+          a.src[q] = c->at(true, off);
+          a.sys_mask |= 1ull << q;
+          pr.reads.push_back(Annot{(int64_t)off, mylen * g.esz, q, R});
+        } else {
+          a.src[q] = c->scratch + (size_t)q * c->slice_bytes;
+          pr.scratch_reads.push_back(sbuf((size_t)q * c->slice_bytes, mylen * g.esz));
+        }
+      }
+      // out[R%K][me] is free once every peer gathered round R-K: W(R-K+1)
+      if (split && j + 1 >= K && (rc = k.wait_event(kLaneMain, kEvSlotFree + (R + 1 - K) % K)))
+        return rc;
+      if ((rc = k.reduce(kLaneMain, pr))) return rc;
+      if (via_ce) {  // result slot written by the copy engine from HBM
+        segs.clear();
+        segs.push_back({my_out(j), c->at(false, out_off), mylen * g.esz,
+                        Annot{(int64_t)out_off, mylen * g.esz, me, R}, true,
+                        ubuf(g.lo(me, j) * g.esz, mylen * g.esz)});
+        if ((rc = k.copy(kLaneMain, segs, false, false))) return rc;
+      }
+    }
+    // REDUCED(R) also says "my gather(R-1) is done": G(R-1)
+    if (split && j >= 1 && (rc = k.wait_event(kLaneMain, kEvGathered + (R - 1) % K))) return rc;
+    if ((rc = k.signal(kLaneMain, kReduced, R + 1))) return rc;
+    // all-gather (lane LG): each owner's result as soon as that owner has it
+    if (c->coarse_gather) {
+      if ((rc = k.wait_peers(LG, kReduced, R + 1, me))) return rc;
+      if ((rc = k.record(LG, kEvSlotFree + R % K))) return rc;  // W(R)
+      segs.clear();
+      for (int q = 0; q < n && !rs; ++q) {
+        const size_t len = q == me ? 0 : g.len(q, j);
+        if (!len) continue;
+        const size_t off = c->out_off(R, q);
+        segs.push_back({c->at(zc, off), dst + g.lo(q, j) * g.esz, len * g.esz,
+                        Annot{(int64_t)off, len * g.esz, q, R}, false,
+                        ubuf(g.lo(q, j) * g.esz, len * g.esz)});
+      }
+      if ((rc = k.copy(LG, segs, true, zc))) return rc;
+    } else {
+      for (int i = 0; i < n - 1; ++i) {
+        const int q = rot(i);
+        if ((rc = k.wait_rank(LG, q, kReduced, R + 1))) return rc;
+        const size_t len = rs ? 0 : g.len(q, j);
+        if (!len) continue;
+        const size_t off = c->out_off(R, q);
+        segs.clear();
+        segs.push_back({c->at(zc, off), dst + g.lo(q, j) * g.esz, len * g.esz,
+                        Annot{(int64_t)off, len * g.esz, q, R}, false,
+                        ubuf(g.lo(q, j) * g.esz, len * g.esz)});
+        if ((rc = k.copy(LG, segs, true, zc))) return rc;
+      }
+      if ((rc = k.record(LG, kEvSlotFree + R % K))) return rc;  // W(R)
+    }
+    if (split && (rc = k.record(LG, kEvGathered + R % K))) return rc;  // G(R)
+  }
+  c->ar_round += g.rounds;
+  return FMX_OK;
+}
+
+// Allreduce over the ranks' registered host buffers (the regions at the end of
+// the segment): in place, no staging and no all-gather.  Every input already
+// sits in host memory, so owner r copy-engines piece j of chunk r out of all n
+// regions into HBM scratch (lane 0), reduces it in rank order (lane 1) and
+// copy-engines the result into piece j of chunk r of every region (lane 1).
+// Per GPU that is k*S H2D + k*S D2H, against 2k(n-1)/n*S + k*S (+ the
+// caller's own k*S in and k*S out) for device buffers.
+constexpr uint32_t kInputTag = 1u << 31;  // trace: "input written by the host for round R"
+enum { kEvFetched = 2 * FMX_MAX_SLOTS, kEvConsumed = kEvFetched + 2, kEvInputs = kEvFetched + 4,
+       kEvPushed = kEvFetched + 5 };
+
+int plan_allreduce_host(fmx_comm* c, Sink& k, size_t off_bytes, size_t count, int dtype, int op,
+                        float factor) {
+  const int n = c->nranks, me = c->rank;
+  const Geometry g = allreduce_geometry(c, count, dtype);
+  const uint32_t R0 = c->ar_round, P = g.rounds;
+  const size_t sb = c->slice_bytes;
+  const int LP = c->nlanes == 3 ? kLaneGather : kLaneMain;  // push lane
+  auto region = [&](int q, int o, uint32_t j) {
+    return c->user_region_off(q) + off_bytes + g.lo(o, j) * g.esz;
+  };
+  std::vector<PlanSeg> segs;
+  int rc;
+  // the caller wrote its whole input before the call (host program order)
+  for (int o = 0; o < n; ++o)
+    for (uint32_t j = 0; j < P; ++j)
+      if (size_t len = g.len(o, j))
+        k.host_access(kLaneMain, Annot{(int64_t)region(me, o, j), len * g.esz, me,
+                                       (R0 + j) | kInputTag}, true);
+  // every rank's inputs are in place: exchange STAGED on lane 1, release lane 0
+  if ((rc = k.signal(kLaneMain, kStaged, R0 + P))) return rc;
+  if ((rc = k.wait_peers(kLaneMain, kStaged, R0 + P, me))) return rc;
+  if ((rc = k.record(kLaneMain, kEvInputs))) return rc;
+  if ((rc = k.wait_event(kLaneStage, kEvInputs))) return rc;
+  for (uint32_t j = 0; j < P; ++j) {
+    const uint32_t R = R0 + j, slot = j % 2;
+    const size_t len = g.len(me, j);
+    // scratch: fetch slots [2][n], result replicas [2][n] (one per region, so
+    // the push is one 2D copy)
+    const size_t fetch_off = (size_t)slot * n * sb, result_off = ((size_t)2 * n + slot * n) * sb;
+    char* fetch = c->scratch + fetch_off;
+    char* result = c->scratch + result_off;
+    // lane 0: pull piece j of my chunk out of every region; the fetch slot is
+    // free once lane 1's reduce of round j-2 consumed it (C(j-2)), so fetches
+    // run up to two rounds ahead of the pushes
+    if (j >= 2 && (rc = k.wait_event(kLaneStage, kEvConsumed + slot))) return rc;
+    segs.clear();
+    for (int q = 0; q < n && len; ++q) {
+      const size_t off = region(q, me, j);
+      segs.push_back({c->at(false, off), fetch + (size_t)q * sb, len * g.esz,
+                      Annot{(int64_t)off, len * g.esz, q, R | kInputTag}, false,
+                      sbuf(fetch_off + (size_t)q * sb, len * g.esz)});
+    }
+    if ((rc = k.copy(kLaneStage, segs, true, false))) return rc;
+    if ((rc = k.record(kLaneStage, kEvFetched + slot))) return rc;
+    // lane 1: reduce in rank order; the result slot j%2 is free once lane LP
+    // pushed round j-2 (P(j-2))
+    if ((rc = k.wait_event(kLaneMain, kEvFetched + slot))) return rc;
+    if (j >= 2 && LP != kLaneMain && (rc = k.wait_event(kLaneMain, kEvPushed + slot))) return rc;
+    if (len) {
+      PlanReduce pr;
+      memset(&pr.args, 0, sizeof pr.args);
+      pr.dtype = dtype;
+      pr.aligned = true;
+      pr.args.nsrc = n;
+      pr.args.len = len;
+      pr.args.op = op;
+      pr.args.factor = factor;
+      pr.args.out_dev = result;
+      pr.args.n_rep = n;
+      pr.args.rep_stride = sb;
+      for (int q = 0; q < n; ++q) {
+        pr.args.src[q] = fetch + (size_t)q * sb;
+        pr.scratch_reads.push_back(sbuf(fetch_off + (size_t)q * sb, len * g.esz));
+      }
+      pr.scratch_write = sbuf(result_off, n * sb);
+      if ((rc = k.reduce(kLaneMain, pr))) return rc;
+    }
+    if ((rc = k.record(kLaneMain, kEvConsumed + slot))) return rc;  // C(j)
+    // lane LP: push the result into every region, off the reduce lane so the
+    // D2H direction never waits behind the next round's fetch
+    if (LP != kLaneMain && (rc = k.wait_event(LP, kEvConsumed + slot))) return rc;
+    if (len) {
+      segs.clear();
+      for (int q = 0; q < n; ++q) {
+        const size_t off = region(q, me, j);
+        segs.push_back({result + (size_t)q * sb, c->at(false, off), len * g.esz,
+                        Annot{(int64_t)off, len * g.esz, me, R}, true,
+                        sbuf(result_off, n * sb)});
+      }
+      if ((rc = k.copy(LP, segs, false, false))) return rc;
+    }
+    if (LP != kLaneMain && (rc = k.record(LP, kEvPushed + slot))) return rc;  // P(j)
+  }
+  if ((rc = k.signal(LP, kReduced, R0 + P))) return rc;
+  if ((rc = k.wait_peers(LP, kReduced, R0 + P, me))) return rc;
+  // the caller then reads its whole region (host program order)
+  for (int o = 0; o < n; ++o)
+    for (uint32_t j = 0; j < P; ++j)
+      if (size_t len = g.len(o, j))
+        k.host_access(LP, Annot{(int64_t)region(me, o, j), len * g.esz, o, R0 + j}, false);
+  c->ar_round += P;
+  return FMX_OK;
+}
+
+// Root stages rounds of n*slice bytes into the broadcast slot; every other
+// rank copies them out and signals BC_DONE, which the root waits on before
+// reusing a slot (two rounds later).  Single lane (lane 1).
+int plan_broadcast(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
+                   int root) {
+  const int me = c->rank;
+  const int L = kLaneMain;
+  const bool zc = c->transport == FMX_TRANSPORT_ZC;
+  const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;
+  const size_t bslice = (size_t)c->nranks * c->slice_bytes / esz;
+  const uint32_t rounds = (uint32_t)((count + bslice - 1) / bslice);
+  std::vector<PlanSeg> segs(1);
+  int rc;
+  for (uint32_t j = 0; j < rounds; ++j) {
+    const uint32_t R = c->bc_round + j;
+    const size_t lo = (size_t)j * bslice, len = std::min(bslice, count - lo);
+    const size_t off = c->bc_slot_off(R);
+    const Annot an{(int64_t)off, len * esz, root, R};
+    if (me == root) {
+      if (R + 1 > (uint32_t)c->nslots && (rc = k.wait_peers(L, kBcDone, R + 1 - c->nslots, me)))
+        return rc;
+      segs[0] = {src + lo * esz, c->at(zc, off), len * esz, an, true, ubuf(lo * esz, len * esz)};
+      if ((rc = k.copy(L, segs, false, zc))) return rc;
+      if ((rc = k.signal2(L, kBcStaged, R + 1, kBcDone, R + 1))) return rc;
+      if (src != dst &&
+          (rc = k.d2d(L, dst + lo * esz, src + lo * esz, len * esz, Annot{}, Annot{})))
+        return rc;
+    } else {
+      if ((rc = k.wait_rank(L, root, kBcStaged, R + 1))) return rc;
+      segs[0] = {c->at(zc, off), dst + lo * esz, len * esz, an, false, ubuf(lo * esz, len * esz)};
+      if ((rc = k.copy(L, segs, true, zc))) return rc;
+      if ((rc = k.signal(L, kBcDone, R + 1))) return rc;
+    }
+  }
+  c->bc_round += rounds;
+  return FMX_OK;
+}
+
+}  // namespace fmx
+
+using namespace fmx;
+
+extern "C" {
+
+int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int nops,
+                   const int* kinds, const size_t* counts, const int* dtypes, const int* roots,
+                   char* buf, size_t cap, size_t* used) {
+  if (nranks < 2 || nranks > FMX_MAX_RANKS || rank < 0 || rank >= nranks || nops < 0 ||
+      slice_bytes < 4096 || slice_bytes % 4096 || !kinds || !counts || !dtypes)
+    return fail(FMX_ERR_INVALID_ARG, "bad trace arguments");
+  fmx_comm c;  // geometry only: no segment, no CUDA
+  c.rank = rank;
+  c.nranks = nranks;
+  c.nslots = 2;
+  if (const char* v = getenv("FMX_SLOTS")) c.nslots = std::min(FMX_MAX_SLOTS, std::max(2, atoi(v)));
+  c.transport = transport == FMX_TRANSPORT_ZC ? FMX_TRANSPORT_ZC : FMX_TRANSPORT_CE;
+  c.slice_bytes = slice_bytes;
+  size_t max_bytes = 0;
+  for (int i = 0; i < nops; ++i) max_bytes = std::max(max_bytes, counts[i] * (dtypes[i] ? 2 : 4));
+  c.L = compute_layout(nranks, c.nslots, slice_bytes, max_bytes);
+  c.total_bytes = c.L.total;
+  if (const char* v = getenv("FMX_RESULT_VIA_CE")) c.result_via_ce = atoi(v) != 0;
+  if (const char* v = getenv("FMX_GRAIN")) c.coarse = strcmp(v, "fine") != 0;
+  c.coarse_gather = c.coarse;
+  if (const char* v = getenv("FMX_GATHER_GRAIN")) c.coarse_gather = strcmp(v, "fine") != 0;
+  if (const char* v = getenv("FMX_RAMP")) c.ramp = atoi(v) != 0;
+  if (const char* v = getenv("FMX_LANES")) c.nlanes = std::min(3, std::max(1, atoi(v)));
+  std::string out;
+  TraceSink sink(&out);
+  sink.nranks = nranks;
+  // fake user buffers: only their offsets matter and they never reach SHM
+  static char dummy[16] __attribute__((aligned(16)));
+  for (int i = 0; i < nops; ++i) {
+    int rc;
+    sink.join();
+    if (kinds[i] == 1 && (!roots || roots[i] < 0 || roots[i] >= nranks))
+      return fail(FMX_ERR_INVALID_ARG, "bad broadcast root");
+    if (kinds[i] == 0)
+      rc = plan_allreduce(&c, sink, dummy, dummy, counts[i], dtypes[i], FMX_OP_SUM, 1.0f, true);
+    else if (kinds[i] == 3 || kinds[i] == 4)  // reduce-scatter / all-gather, in place
+      rc = plan_allreduce(&c, sink, dummy, dummy, counts[i], dtypes[i], FMX_OP_SUM, 1.0f, true,
+                          kinds[i] == 3 ? kReduceScatter : kAllgather);
+    else if (kinds[i] == 2)
+      rc = plan_allreduce_host(&c, sink, 0, counts[i], dtypes[i], FMX_OP_SUM, 1.0f);
+    else
+      rc = plan_broadcast(&c, sink, dummy, dummy, counts[i], dtypes[i], roots ? roots[i] : 0);
+    if (rc) return rc;
+  }
+  sink.join();
+  if (used) *used = out.size() + 1;
+  if (!buf || cap < out.size() + 1) return fail(FMX_ERR_INVALID_ARG, "trace buffer too small");
+  memcpy(buf, out.c_str(), out.size() + 1);
+  return FMX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,32 @@
+// Argument blocks shared by the host schedule and the sm_100a kernels
+// (plain C++: no CUDA headers, so the schedule compiles with g++).
+#pragma once
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/flexshm.h"
+
+namespace fmx {
+
+struct ReduceArgs {
+  const char* src[FMX_MAX_RANKS];  // rank-ordered sources
+  uint64_t sys_mask;               // bit q set: src[q] is mapped host memory
+  char* out_dev;                   // HBM result (may alias src[own])
+  char* out_sys;                   // SHM result slot (may be null)
+  size_t rep_stride;               // n_rep > 1: also write the result at out_dev + k*rep_stride
+  int n_rep;                       // (host path: one replica per destination region)
+  size_t len;                      // elements
+  int nsrc;
+  int op;
+  float factor;
+};
+
+// Pipeline timeline probe entry (fmx_comm_set_stamps).
+struct Stamp {
+  uint64_t t_ns;
+  uint32_t tag;   // lane << 8 | op kind
+  uint32_t info;  // flag value / bytes / event id
+};
+
+}  // namespace fmx

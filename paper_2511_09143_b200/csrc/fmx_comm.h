@@ -1,0 +1,188 @@
+// The communicator object and the schedule interface of libflexshm, shared by
+// the CUDA half (flexshm_comm.cu: CudaSink, the C API) and the CUDA-free
+// schedule (flexshm_plan.cpp: the plans, TraceSink, fmx_trace_plan).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <utility>
+#include <vector>
+
+#include "fmx_args.h"
+#include "fmx_internal.h"
+
+namespace fmx {
+constexpr int kNumEvents = 2 * FMX_MAX_SLOTS + 7;  // W[K], G[K]; host path F[2], C[2], inputs, P[2]
+}  // namespace fmx
+
+using fmx::Header;
+using fmx::Layout;
+using fmx::Stamp;
+
+struct fmx_comm {
+  int rank = -1, nranks = 0, nslots = 2, transport = FMX_TRANSPORT_CE, mig_aware = 1;
+  size_t slice_bytes = 0, total_bytes = 0;
+  Layout L{};
+  char* base = nullptr;   // host VA of the mapping
+  char* dbase = nullptr;  // device VA of the same bytes
+  Header* hdr = nullptr;
+  bool registered = false;
+  uint32_t ar_round = 0, bc_round = 0;
+  int64_t barrier_gen = 0;
+  char* scratch = nullptr;  // CE transport: n * slice_bytes of HBM
+  cudaStream_t lane[2] = {nullptr, nullptr};  // lane 0 (stage) and lane 2 (gather); lane 1 is the caller's stream
+  cudaStream_t user = nullptr;                 // caller's stream of the current collective
+  CUcontext lane_ctx = nullptr;                // context the lane objects were created in
+  cudaEvent_t ev[fmx::kNumEvents] = {};  // intra-rank lane sync (see the kEv* ids)
+  cudaEvent_t fork = nullptr, joined[2] = {nullptr, nullptr};
+  bool result_via_ce = false;  // CE transport: result slot by copy engine, not SM stores
+  bool copy2d = true;          // coalesce regular copy runs into cudaMemcpy2DAsync
+  bool coarse = true;          // FMX_GRAIN=fine: per-piece waits instead of all-peer
+  bool coarse_gather = true;   // FMX_GATHER_GRAIN=fine: per-owner gather waits only
+  bool ramp = true;            // FMX_RAMP=0: equal rounds (no pipeline-fill ramp)
+  int nlanes = 3;              // FMX_LANES=1: one stream; 2: gather on the reduce lane
+  // live kernel timing (fmx_comm_set_timing): event pairs around every reduce
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
+  size_t timed_used = 0;
+  cudaEvent_t done = nullptr;
+  bool has_done = false;
+  uint64_t launches = 0;
+  // pipeline timeline probe (fmx_comm_set_stamps): device ring of Stamp entries
+  fmx::Stamp* stamps = nullptr;
+  size_t stamp_cap = 0, stamp_used = 0;
+  std::vector<fmx_peer_info> peers;
+  std::vector<CUstreamBatchMemOpParams> ops;
+
+  // byte offsets of the pipeline slots inside the segment
+  size_t in_off(uint32_t R, int owner, int contrib) const {
+    return L.ar_in_off + (((size_t)(R % nslots) * nranks + owner) * nranks + contrib) * slice_bytes;
+  }
+  size_t out_off(uint32_t R, int owner) const {
+    return L.ar_out_off + ((size_t)(R % nslots) * nranks + owner) * slice_bytes;
+  }
+  size_t bc_slot_off(uint32_t R) const {
+    return L.bc_off + (size_t)(R % nslots) * nranks * slice_bytes;
+  }
+  size_t user_region_off(int r) const { return L.user_off + (size_t)r * L.user_bytes; }
+  // host (dev=false) or device (dev=true) address of a segment offset
+  char* at(bool dev, size_t off) const { return (dev ? dbase : base) + off; }
+  CUdeviceptr flag_dev(int r, int f) const {
+    return (CUdeviceptr)(dbase + L.flags_off + ((size_t)r * fmx::kFlagsPerRank + f) * 64);
+  }
+  volatile uint32_t* flag_host(int r, int f) const {
+    return (volatile uint32_t*)(base + L.flags_off + ((size_t)r * fmx::kFlagsPerRank + f) * 64);
+  }
+};
+
+
+namespace fmx {
+
+inline cudaStream_t lane_stream(const fmx_comm* c, int lane) {
+  if (c->nlanes == 1 || lane == 1) return c->user;
+  if (lane == 0) return c->lane[0];
+  return c->nlanes == 3 ? c->lane[1] : c->user;
+}
+
+
+// ---- the plan: what one rank enqueues for one collective -----------------------
+//
+// plan_allreduce / plan_broadcast describe the schedule once, against a Sink.
+// Work is issued on two lanes (CUDA streams) per rank so the two link
+// directions overlap inside a rank: lane 0 stages (HBM -> SHM, D2H), lane 1
+// fetches, reduces and gathers (SHM -> HBM, H2D).  Lanes fork from / join
+// back into the caller's stream at every collective.  CudaSink turns the
+// plan into stream operations; TraceSink records, per lane, every SHM and
+// user-buffer byte range touched and every flag signalled / waited on, so the
+// schedule of every rank of any world size can be model-checked on a CPU
+// (fmx_trace_plan, tests/test_protocol_model.py).
+
+constexpr int kLaneStage = 0;   // D2H lane
+constexpr int kLaneMain = 1;    // fetch (H2D) + reduce lane: the caller's stream
+constexpr int kLaneGather = 2;  // all-gather (H2D) lane
+
+// One data-movement end for the trace: SHM byte range (relative to the
+// segment) or user-buffer byte range (relative to the buffer start), plus the
+// rank/round that (should have) written SHM bytes.
+struct Annot {
+  int64_t off = -1;
+  size_t bytes = 0;
+  int writer = -1;
+  uint32_t round = 0;
+  bool scratch = false;  // a range of the rank's HBM scratch, not of the user buffer
+};
+
+struct PlanSeg {
+  const char* src;
+  char* dst;
+  size_t bytes;
+  Annot shm;        // the SHM end of this segment
+  bool shm_is_dst;  // true: this step writes SHM; false: reads it
+  Annot user;       // the user-buffer end (off < 0: none, e.g. HBM scratch)
+};
+
+struct PlanReduce {
+  ReduceArgs args;
+  std::vector<Annot> reads;  // SHM inputs (ZC transport)
+  Annot write;               // SHM result slot (written by the kernel)
+  Annot user_rw;             // own piece of the user buffer (read + written)
+  std::vector<Annot> scratch_reads;  // HBM scratch inputs (CE transport, host path)
+  Annot scratch_write;               // HBM scratch result (host path)
+  int dtype;
+  bool aligned;
+};
+
+struct Sink {
+  virtual ~Sink() {}
+  virtual int copy(int lane, const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel) = 0;
+  virtual int reduce(int lane, const PlanReduce& r) = 0;
+  virtual int signal(int lane, int flag, uint32_t v) = 0;
+  virtual int signal2(int lane, int f0, uint32_t v0, int f1, uint32_t v1) = 0;
+  virtual int wait_peers(int lane, int flag, uint32_t v, int skip) = 0;
+  virtual int wait_rank(int lane, int q, int flag, uint32_t v) = 0;
+  virtual int d2d(int lane, void* dst, const void* src, size_t bytes, Annot from, Annot to) = 0;
+  // intra-rank lane ordering through CUDA events (enqueue-order semantics)
+  virtual int record(int lane, int ev) = 0;
+  virtual int wait_event(int lane, int ev) = 0;
+  // host-program accesses to SHM around a collective (trace only)
+  virtual int host_access(int lane, const Annot& a, bool write) { return FMX_OK; }
+};
+
+
+// Round geometry of one collective (allreduce_geometry, flexshm_plan.cpp).
+struct Geometry {
+  size_t count, esz, chunk, slice;
+  uint32_t rounds;
+  std::vector<size_t> start;  // start[j] = prefix of round j; start[rounds] >= chunk
+  size_t size(uint32_t j) const { return start[j + 1] - start[j]; }
+  size_t lo(int owner, uint32_t j) const { return (size_t)owner * chunk + start[j]; }
+  size_t len(int owner, uint32_t j) const {
+    size_t a = lo(owner, j);
+    size_t end = std::min((size_t)(owner + 1) * chunk, count);
+    if (a >= end) return 0;
+    return std::min(size(j), end - a);
+  }
+};
+
+// chunk_elems = 0: allreduce chunking (16-byte aligned chunk starts over
+// `count`); otherwise every rank's chunk has exactly chunk_elems elements and
+// count = n * chunk_elems (reduce-scatter / all-gather, NCCL's layout).
+Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t chunk_elems = 0);
+
+inline Annot ubuf(size_t off_bytes, size_t bytes) { return Annot{(int64_t)off_bytes, bytes, -1, 0}; }
+inline Annot sbuf(size_t off_bytes, size_t bytes) { return Annot{(int64_t)off_bytes, bytes, -1, 0, true}; }
+
+
+// The three owner-chunk collectives of plan_allreduce.
+enum Kind { kAllreduce = 0, kReduceScatter = 1, kAllgather = 2 };
+
+int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
+                   int op, float factor, bool aligned, int kind = kAllreduce);
+int plan_allreduce_host(fmx_comm* c, Sink& k, size_t off_bytes, size_t count, int dtype, int op,
+                        float factor);
+int plan_broadcast(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
+                   int root);
+
+}  // namespace fmx
