@@ -114,6 +114,14 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t c
   g.count = chunk_elems ? chunk_elems * n : count;
   g.chunk = chunk_elems ? chunk_elems : ((count + n - 1) / n + vec - 1) / vec * vec;
   g.slice = c->slice_bytes / g.esz;
+  if (c->min_rounds > 1) {
+    // small collectives (a DDP bucket is one chunk of ~1 MB per rank) are split
+    // too, so their stage / fetch / gather overlap inside the call; pieces stay
+    // >= 64 KiB so per-round latency does not dominate
+    const size_t floor_elems = (64u << 10) / g.esz;
+    const size_t want = (g.chunk + c->min_rounds - 1) / c->min_rounds;
+    g.slice = std::min(g.slice, std::max(floor_elems, (want + 8 * vec - 1) / (8 * vec) * (8 * vec)));
+  }
   std::vector<size_t> sizes;
   const size_t s = g.slice;
   if (c->ramp && g.chunk > s) {
@@ -121,7 +129,8 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t c
     // the chunk each way), the middle in equal rounds of at most s
     std::vector<size_t> up;
     size_t ramp_sum = 0;
-    for (size_t x = s / 8; x < s && x > 0; x *= 2) {
+    // ramp pieces are whole vectors so every piece start stays 16-byte aligned
+    for (size_t x = s / 8 / vec * vec; x < s && x > 0; x = x * 2 / vec * vec) {
       if (2 * (ramp_sum + x) > g.chunk) break;
       up.push_back(x);
       ramp_sum += x;
@@ -547,6 +556,7 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   c.coarse_gather = c.coarse;
   if (const char* v = getenv("FMX_GATHER_GRAIN")) c.coarse_gather = strcmp(v, "fine") != 0;
   if (const char* v = getenv("FMX_RAMP")) c.ramp = atoi(v) != 0;
+  if (const char* v = getenv("FMX_MIN_ROUNDS")) c.min_rounds = atoi(v);
   if (const char* v = getenv("FMX_LANES")) c.nlanes = std::min(3, std::max(1, atoi(v)));
   std::string out;
   TraceSink sink(&out);

@@ -42,6 +42,7 @@ struct fmx_comm {
   bool coarse = true;          // FMX_GRAIN=fine: per-piece waits instead of all-peer
   bool coarse_gather = true;   // FMX_GATHER_GRAIN=fine: per-owner gather waits only
   bool ramp = true;            // FMX_RAMP=0: equal rounds (no pipeline-fill ramp)
+  int min_rounds = 1;          // FMX_MIN_ROUNDS: shrink the slice so a chunk spans >= this many
   int nlanes = 3;              // FMX_LANES=1: one stream; 2: gather on the reduce lane
   // live kernel timing (fmx_comm_set_timing): event pairs around every reduce
   bool timing = false;
