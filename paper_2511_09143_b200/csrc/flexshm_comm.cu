@@ -548,7 +548,8 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
     return rc;  // message / dup pair already set
   }
 
-  c->transport = transport == FMX_TRANSPORT_AUTO ? FMX_TRANSPORT_CE : transport;
+  c->transport = transport;  // AUTO stays AUTO: chosen per collective by size (use_zc)
+  if (const char* v = getenv("FMX_ZC_MAX")) c->zc_max = strtoull(v, nullptr, 10);
   if (host_only) {
     *out = c;
     return FMX_OK;

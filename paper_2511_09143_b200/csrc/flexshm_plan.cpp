@@ -202,12 +202,12 @@ enum { kEvSlotFree = 0, kEvGathered = FMX_MAX_SLOTS };  // + R % K: W(R) and G(R
 int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
                    int op, float factor, bool aligned, int kind) {
   const int n = c->nranks, me = c->rank;
-  const bool zc = c->transport == FMX_TRANSPORT_ZC;
   const int LG = c->nlanes == 3 ? kLaneGather : kLaneMain;
   const int K = c->nslots;  // pipeline depth: slots per region
   const bool split = LG != kLaneMain;  // gather on its own lane: explicit W / G waits
   const bool ar = kind == kAllreduce, rs = kind == kReduceScatter, ag = kind == kAllgather;
   const Geometry g = allreduce_geometry(c, count, dtype, ar ? 0 : count);
+  const bool zc = c->use_zc(g.count * g.esz);  // every rank derives the same choice
   // where piece (me, j) of the result goes, and where my contribution / my
   // published chunk comes from (all-gather's send holds only my chunk)
   auto my_out = [&](uint32_t j) { return dst + (rs ? g.start[j] : g.lo(me, j)) * g.esz; };
@@ -497,8 +497,8 @@ int plan_broadcast(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
                    int root) {
   const int me = c->rank;
   const int L = kLaneMain;
-  const bool zc = c->transport == FMX_TRANSPORT_ZC;
   const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;
+  const bool zc = c->use_zc(count * esz);
   const size_t bslice = (size_t)c->nranks * c->slice_bytes / esz;
   const uint32_t rounds = (uint32_t)((count + bslice - 1) / bslice);
   std::vector<PlanSeg> segs(1);
@@ -545,7 +545,9 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   c.nranks = nranks;
   c.nslots = 2;
   if (const char* v = getenv("FMX_SLOTS")) c.nslots = std::min(FMX_MAX_SLOTS, std::max(2, atoi(v)));
-  c.transport = transport == FMX_TRANSPORT_ZC ? FMX_TRANSPORT_ZC : FMX_TRANSPORT_CE;
+  c.transport = (transport == FMX_TRANSPORT_ZC || transport == FMX_TRANSPORT_AUTO) ? transport
+                                                                                  : FMX_TRANSPORT_CE;
+  if (const char* v = getenv("FMX_ZC_MAX")) c.zc_max = strtoull(v, nullptr, 10);
   c.slice_bytes = slice_bytes;
   size_t max_bytes = 0;
   for (int i = 0; i < nops; ++i) max_bytes = std::max(max_bytes, counts[i] * (dtypes[i] ? 2 : 4));

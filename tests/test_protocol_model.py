@@ -362,3 +362,18 @@ def test_piece_starts_are_16_byte_aligned(monkeypatch, min_rounds, slice_bytes, 
             t = _lib.trace_plan(7, rank, [("allreduce", count, dtype)], slice_bytes)
             offs = [int(m.group(1)) for m in re.finditer(r"^\d UW (\d+) ", t, re.M)]
             assert offs and all(o % 16 == 0 for o in offs), (count, rank, offs[:8])
+
+
+@pytest.mark.parametrize("n", [2, 7])
+def test_auto_transport_mixes_zc_and_ce_calls(monkeypatch, n):
+    """AUTO picks ZC or CE per collective by size; consecutive calls of either
+    kind share slots and round counters, so mixed sequences must stay race- and
+    deadlock-free."""
+    monkeypatch.setenv("FMX_ZC_MAX", "100000")
+    for seq in ("mixed", "rs-ag", "host-buffer"):
+        progs = programs(n, SEQUENCES[seq], 4096, "auto")
+        for seed in range(6):
+            simulate(progs, seed)
+        merged = programs(n, SEQUENCES[seq], 4096, "auto", merged=True)
+        for seed in range(3):
+            simulate(merged, seed)
