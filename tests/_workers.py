@@ -113,7 +113,7 @@ def suite_worker(rank: int, job_key: str, n: int, transport: str, mode: str, sce
 
 
 def ddp_worker(rank: int, job_key: str, n: int, port: int, mode: str = "green",
-               overlap: bool = True):
+               overlap: bool = True, dtype: str = "f32"):
     """Tiny model: local gradients without DDP, then the same step under DDP
     with the flexshm comm hook; returns both (flattened fp32)."""
     import torch
@@ -133,8 +133,10 @@ def ddp_worker(rank: int, job_key: str, n: int, port: int, mode: str = "green",
         torch.manual_seed(1000 + rank)     # different init per rank: broadcast must fix it
         model = torch.nn.Sequential(torch.nn.Linear(64, 300), torch.nn.GELU(),
                                     torch.nn.Linear(300, 10)).cuda()
+        if dtype == "bf16":   # bf16 parameters -> bf16 gradient buckets (BERT leg's path)
+            model = model.to(torch.bfloat16)
         g = torch.Generator(device="cpu").manual_seed(7 + rank)
-        x = torch.randn(32, 64, generator=g).cuda()
+        x = torch.randn(32, 64, generator=g).cuda().to(next(model.parameters()).dtype)
         y = torch.randint(0, 10, (32,), generator=g).cuda()
         net = fddp.wrap(model, comm, control_group=dist.group.WORLD, bucket_cap_mb=0.05,
                         overlap=overlap)
@@ -150,4 +152,7 @@ def ddp_worker(rank: int, job_key: str, n: int, port: int, mode: str = "green",
     stream.synchronize()
     dist.destroy_process_group()
     comm.destroy()
-    return {"params0": params0.numpy(), "local": local.cpu().numpy(), "synced": synced.cpu().numpy()}
+    as_np = (lambda t: t.float().numpy()) if dtype == "f32" else \
+        (lambda t: t.cpu().view(torch.int16).numpy().view(np.uint16))
+    return {"params0": as_np(params0.cpu()), "local": as_np(local.cpu()),
+            "synced": as_np(synced.cpu())}

@@ -17,9 +17,10 @@ from tests import _workers
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n,overlap,mode", [(2, True, "green"), (3, True, "green"),
-                                            (2, False, "green"), (3, True, "mps")])
-def test_ddp_hook_matches_oracle(n, overlap, mode):
+@pytest.mark.parametrize("n,overlap,mode,dtype", [
+    (2, True, "green", "f32"), (3, True, "green", "f32"), (2, False, "green", "f32"),
+    (3, True, "mps", "f32"), (3, True, "green", "bf16"), (2, True, "mps", "bf16")])
+def test_ddp_hook_matches_oracle(n, overlap, mode, dtype):
     from paper_2511_09143_b200.launcher import launch, new_job_key
     from paper_2511_09143_b200.scheduler import fm_select, make_cluster
     from paper_2511_09143_b200.workload import Job
@@ -27,10 +28,12 @@ def test_ddp_hook_matches_oracle(n, overlap, mode):
     d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
     key = new_job_key("ddp")
     port = 20000 + os.getpid() % 20000
-    res = launch(_workers.ddp_worker, d, args=(key, n, port, mode, overlap), job_key=key,
+    res = launch(_workers.ddp_worker, d, args=(key, n, port, mode, overlap, dtype), job_key=key,
                  timeout_s=300, mode=mode)
     for r in res[1:]:
         assert np.array_equal(r["params0"], res[0]["params0"]), "parameter broadcast"
-    want = orc.allreduce_c([r["local"] for r in res], orc.F32, orc.OP_PREDIV_SUM, float(n))
+    dt = orc.F32 if dtype == "f32" else orc.BF16
+    want = orc.allreduce_c([r["local"] for r in res], dt, orc.OP_PREDIV_SUM, float(n))
+    bits = (lambda a: a.view(np.uint32)) if dtype == "f32" else (lambda a: a)
     for rank, r in enumerate(res):
-        assert np.array_equal(r["synced"].view(np.uint32), want.view(np.uint32)), rank
+        assert np.array_equal(bits(r["synced"]), bits(want)), rank
