@@ -493,10 +493,11 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
         continue;
       }
       if (h->nranks != nranks) {
+        const int theirs = h->nranks;  // read before the unmap
         munmap(p, (size_t)st.st_size);
         delete c;
         return fail(FMX_ERR_BAD_RANKS, "segment %s has %d ranks, caller says %d", name.c_str(),
-                    h->nranks, nranks);
+                    theirs, nranks);
       }
       c->base = (char*)p;
       c->total_bytes = (size_t)st.st_size;
