@@ -69,6 +69,9 @@ def parse_args(argv=None):
                    help="write a GPU-clock timeline of one allreduce (every op of every rank)")
     p.add_argument("--train-only", action="store_true")
     p.add_argument("--train-mode", choices=["green", "mps", "full"], default="mps")
+    p.add_argument("--nccl", action="store_true",
+                   help="N>1: also time stock NCCL over NVLink, one rank per GPU (comparison "
+                        "point; opt-in because NCCL inside MPS clients is untested here)")
     p.add_argument("--dry-run", action="store_true",
                    help="orchestration only (no CUDA): stub rank bodies; for the CPU tests of "
                         "the torchrun N>1 path")
@@ -785,6 +788,42 @@ def run_ours(args) -> dict | None:
     return line
 
 
+def run_nccl_point(args) -> dict:
+    """Comparison point (north_star): stock NCCL allreduce of the same gradient
+    bytes over NVLink, one rank per GPU (the torchrun ranks), CUDA events, max
+    over ranks.  Not the product path; never raises into the bench line."""
+    import torch
+    import torch.distributed as dist
+    try:
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        dev = torch.device("cuda", local)
+        torch.cuda.set_device(dev)
+        pg = dist.new_group(backend="nccl")
+        x = torch.randn(args.count, device=dev)
+        for _ in range(3):
+            dist.all_reduce(x, group=pg)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            dist.all_reduce(x, group=pg)
+        e1.record()
+        e1.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        n = dist.get_world_size()
+        s_bytes = args.count * 4
+        dist.destroy_process_group(pg)
+        return {"ms_per_step": ms, "algbw_gbs": s_bytes / ms / 1e6,
+                "busbw_gbs": s_bytes / ms / 1e6 * 2 * (n - 1) / n, "ranks": n,
+                "note": "stock NCCL over NVLink, one rank per GPU (this process is also an "
+                        "instance's MPS client, so NCCL runs on its SM share)"}
+    except Exception as exc:  # noqa: BLE001
+        return {"error": repr(exc)[:300]}
+
+
 def run_cpu_reference(count: int, n: int, dtype: str, steps: int, warmup: int,
                       nthreads: int | None = None, seconds: float | None = None) -> dict:
     """CPU restatement of the same algorithm (oracle/), all host threads."""
@@ -919,6 +958,10 @@ def _main(args, world, n, unit):
                 f.write(json.dumps(line) + "\n")
         return 0
     line = run_ours(args)
+    if world > 1 and not args.dry_run and args.nccl:
+        nccl = run_nccl_point(args)          # collective: every torchrun rank takes part
+        if line is not None:
+            line["nccl_nvlink"] = nccl
     if line is None:
         return 0
     if not args.no_train and args.gpus == 1 and world == 1:
