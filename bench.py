@@ -563,6 +563,20 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
         for _ in range(cfg["train_warmup"]):
             step()
     torch.cuda.synchronize()
+    stamps = None
+    if cfg.get("stamps"):
+        # one step on the GPU clock: markers 1/2 around it on the compute stream,
+        # every collective op of the hook's side stream in between
+        comm.barrier(300)
+        comm.set_stamps(1 << 15)
+        comm.barrier(300)
+        with torch.cuda.stream(stream):
+            comm.stamp(1, stream)
+            step()
+            comm.stamp(2, stream)
+        torch.cuda.synchronize()
+        stamps = comm.stamps(1 << 15)
+        comm.set_stamps(0)
     comm.barrier(300)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = comm.kernel_launches()
@@ -574,6 +588,7 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
     ev1.synchronize()
     comm.barrier(300)
     out = {"rank": rank, "ms_total": ev0.elapsed_time(ev1), "loss": float(loss.item()),
+           "stamps": stamps,
            "launches": comm.kernel_launches() - l0,
            "param_digest": float(sum(p.detach().double().sum().item() for p in model.parameters()))}
     dist.destroy_process_group()
@@ -636,12 +651,15 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
     cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
            "batch": args.batch, "train_steps": args.train_steps, "train_warmup": args.train_warmup,
            "port": 29000 + os.getpid() % 1000, "model": model, "no_sync": no_sync,
-           "bucket_mb": args.bucket_mb}
+           "bucket_mb": args.bucket_mb, "stamps": bool(args.stamps) and not no_sync}
     res = run_ranks(train_body, _spawned_train, list(range(n)), job_key + "-t", n, cfg,
                     args.train_mode, 0)
     t = max(r["ms_total"] for r in res.values()) / 1e3
     digests = {round(r["param_digest"], 3) for r in res.values()}
     desc, precision, unit = TRAIN_MODELS[model]
+    if cfg["stamps"]:
+        with open(args.stamps, "w") as f:
+            json.dump({"n": n, "model": model, "train": {r: v["stamps"] for r, v in res.items()}}, f)
     return {unit: n * args.batch * args.train_steps / t, "instances": n, "batch_per_instance":
             args.batch, "ms_per_step": t * 1e3 / args.train_steps, "steps": args.train_steps,
             "warmup": args.train_warmup, "instance_mode": args.train_mode,

@@ -206,6 +206,17 @@ int fmx_comm_flags(fmx_comm_t comm, uint32_t* out, int cap);
  * 8 + o STAGED_TO[o]. */
 int fmx_comm_monitor(fmx_comm_t comm, double seconds, uint64_t* out, size_t cap, size_t* n_out);
 
+/* Completion stream.  By default a collective forks from the stream it is
+ * called on and joins back into it.  With a join stream set (non-null), it
+ * still forks from the call's stream (its input is ready there) but joins into
+ * `stream`: the calling stream runs on, and consecutive device-buffer
+ * collectives (allreduce / reduce-scatter / all-gather on distinct buffers)
+ * overlap inside the library - the next call stages while the previous one
+ * gathers.  The caller orders reuse of a buffer after its completion (as DDP
+ * does by waiting on the bucket future).  Host-path calls and broadcasts wait
+ * for the previous collective.  NULL restores the default. */
+int fmx_comm_set_join_stream(fmx_comm_t comm, void* stream);
+
 /* Live timing of the reduction kernel: with timing on, every reduce launch
  * is bracketed by CUDA events on the lane stream it runs on; kernel_time
  * returns the summed device time and the number of timed launches since
@@ -223,6 +234,9 @@ int fmx_comm_kernel_time(fmx_comm_t comm, double* total_ms, uint64_t* count);
  * (info = value).  Stamp kernels are not counted by fmx_comm_kernel_launches. */
 int fmx_comm_set_stamps(fmx_comm_t comm, size_t capacity);
 int fmx_comm_stamps(fmx_comm_t comm, uint64_t* out, size_t cap, size_t* n_out);
+/* A caller's marker on the same timeline (op kind 7, lane 15): e.g. the start
+ * and end of a training step on the compute stream. */
+int fmx_comm_stamp(fmx_comm_t comm, void* stream, uint32_t info);
 /* Number of device kernels this communicator has launched so far. */
 int fmx_comm_kernel_launches(fmx_comm_t comm, uint64_t* launches);
 

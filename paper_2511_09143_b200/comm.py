@@ -236,6 +236,18 @@ class ShmCommunicator:
         """Timeline probe on (capacity entries) or off (0); see fmx_comm_set_stamps."""
         _lib.check(_lib.lib().fmx_comm_set_stamps(self._h, int(capacity)), "fmx_comm_set_stamps")
 
+    def set_join_stream(self, stream) -> None:
+        """Collectives join into `stream` instead of the calling stream (None:
+        back to the default); see fmx_comm_set_join_stream."""
+        h = 0 if stream is None else self._stream(stream)
+        _lib.check(_lib.lib().fmx_comm_set_join_stream(self._h, h or None),
+                   "fmx_comm_set_join_stream")
+
+    def stamp(self, info: int, stream=None) -> None:
+        """Caller's marker (op kind 7) on the timeline, enqueued on `stream`."""
+        _lib.check(_lib.lib().fmx_comm_stamp(self._h, self._stream(stream), int(info)),
+                   "fmx_comm_stamp")
+
     def stamps(self, cap: int = 1 << 16) -> list[tuple[int, int, int, int]]:
         """[(t_ns, lane, op kind, info)] of the stamps recorded so far."""
         buf = (ctypes.c_uint64 * (2 * cap))()

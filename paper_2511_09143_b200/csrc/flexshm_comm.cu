@@ -320,9 +320,13 @@ class CudaSink final : public Sink {
 // the caller's stream (a green context, an MPS client's, or the primary one),
 // so every lane object lives where the caller's work lives.
 int make_lane_objects(fmx_comm* c, CUcontext ctx) {
-  c->lane[0] = c->lane[1] = nullptr;  // objects of an earlier context are abandoned, not destroyed
-  for (int l = 0; l < 2; ++l) {
-    FMX_CUDA(cudaStreamCreateWithFlags(&c->lane[l], cudaStreamNonBlocking));
+  c->lane[0] = c->lane[1] = c->lane[2] = nullptr;  // an earlier context's objects are abandoned
+  // highest priority: a rank's collective work (copy kernels, reductions) is
+  // scheduled ahead of its compute kernels, because every peer waits on it
+  int lo_prio = 0, hi_prio = 0;
+  FMX_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  for (int l = 0; l < 3; ++l) {
+    FMX_CUDA(cudaStreamCreateWithPriority(&c->lane[l], cudaStreamNonBlocking, hi_prio));
     FMX_CUDA(cudaEventCreateWithFlags(&c->joined[l], cudaEventDisableTiming));
   }
   FMX_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
@@ -335,12 +339,19 @@ int make_lane_objects(fmx_comm* c, CUcontext ctx) {
   return FMX_OK;
 }
 
-// Run one collective: lane 1 is the caller's stream, lane 0 forks off it and
-// joins back.  Every runtime call happens with the caller's stream context
-// current (DDP calls hooks from autograd threads whose current context may be
-// another one).
+// Run one collective on the lane streams: they fork from the caller's stream
+// (the input is ready there) and join back into it - or, with a join stream
+// set (fmx_comm_set_join_stream), into that stream, so the caller's stream
+// runs on while the collective completes and consecutive device-buffer
+// collectives overlap on the lanes (stage of call k+1 while call k gathers;
+// slot reuse across calls is covered by the plan's W / G events, which count
+// rounds globally).  A host-path or broadcast call, or the first device call
+// after one, waits for the previous collective to complete.  Every runtime
+// call happens with the caller's stream context current (DDP calls hooks from
+// autograd threads whose current context may be another one).
+//   cls: 0 device-buffer allreduce / reduce-scatter / all-gather, 1 other.
 template <typename F>
-int on_lanes(fmx_comm* c, cudaStream_t user, F&& body) {
+int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
   CUcontext ctx = nullptr;
   if (g_stream_ctx((CUstream)user, &ctx) != CUDA_SUCCESS || !ctx)
     return fail(FMX_ERR_CUDA, "cannot resolve the context of the caller's stream");
@@ -354,17 +365,31 @@ int on_lanes(fmx_comm* c, cudaStream_t user, F&& body) {
   int rc;
   if (ctx != c->lane_ctx && (rc = make_lane_objects(c, ctx))) return rc;
   c->user = user;
-  const int forked = c->nlanes - 1;  // lane 0, then lane 2 (lane 1 is `user`)
-  if (forked > 0) FMX_CUDA(cudaEventRecord(c->fork, user));
-  for (int l = 0; l < forked; ++l) FMX_CUDA(cudaStreamWaitEvent(c->lane[l], c->fork, 0));
+  const int used = c->nlanes == 1 ? 0 : c->nlanes;  // lane streams in use (nlanes 1: `user`)
+  // host-path / broadcast calls (and the first device call after one) wait for
+  // the previous collective, whichever stream it joined (redundant, and free,
+  // when it joined the caller's stream)
+  const bool barrier = c->has_done && (cls != 0 || c->last_class != 0);
+  if (used) FMX_CUDA(cudaEventRecord(c->fork, user));
+  for (int l = 0; l < used; ++l) {
+    FMX_CUDA(cudaStreamWaitEvent(c->lane[l], c->fork, 0));
+    if (barrier) FMX_CUDA(cudaStreamWaitEvent(c->lane[l], c->done, 0));
+  }
+  if (!used && barrier) FMX_CUDA(cudaStreamWaitEvent(user, c->done, 0));
   rc = body();
-  for (int l = 0; l < forked; ++l) {
+  cudaStream_t target = c->join_stream ? c->join_stream : user;
+  for (int l = 0; l < used; ++l) {
     FMX_CUDA(cudaEventRecord(c->joined[l], c->lane[l]));
-    FMX_CUDA(cudaStreamWaitEvent(user, c->joined[l], 0));
+    FMX_CUDA(cudaStreamWaitEvent(target, c->joined[l], 0));
+  }
+  if (!used && target != user) {
+    FMX_CUDA(cudaEventRecord(c->joined[0], user));
+    FMX_CUDA(cudaStreamWaitEvent(target, c->joined[0], 0));
   }
   if (rc) return rc;
-  FMX_CUDA(cudaEventRecord(c->done, user));
+  FMX_CUDA(cudaEventRecord(c->done, target));
   c->has_done = true;
+  c->last_class = cls;
   return FMX_OK;
 }
 
@@ -635,7 +660,7 @@ int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int 
   const bool aligned = (((uintptr_t)send | (uintptr_t)recv) & 15) == 0;
   CudaSink sink(c);
   if (c->nranks == 1) {  // nothing to exchange: apply the scale convention locally
-    return on_lanes(c, s, [&]() -> int {
+    return on_lanes(c, s, 0, [&]() -> int {
       if (op == FMX_OP_SUM) {
         if (send != recv)
           FMX_CUDA(cudaMemcpyAsync(recv, send, count * esz, cudaMemcpyDeviceToDevice, lane_stream(c, kLaneMain)));
@@ -654,7 +679,7 @@ int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int 
       return sink.reduce(kLaneMain, pr);
     });
   }
-  return on_lanes(c, s, [&]() {
+  return on_lanes(c, s, 0, [&]() {
     return plan_allreduce(c, sink, (const char*)send, (char*)recv, count, dtype, op, factor,
                           aligned);
   });
@@ -679,7 +704,7 @@ int fmx_reduce_scatter(fmx_comm_t c, const void* send, void* recv, size_t recvco
   const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;
   const bool aligned = (((uintptr_t)send | (uintptr_t)recv) & 15) == 0 && (recvcount * esz) % 16 == 0;
   CudaSink sink(c);
-  return on_lanes(c, (cudaStream_t)stream, [&]() -> int {
+  return on_lanes(c, (cudaStream_t)stream, 0, [&]() -> int {
     if (c->nranks == 1) {  // my chunk is the whole buffer: apply the scale convention
       PlanReduce pr;
       memset(&pr.args, 0, sizeof pr.args);
@@ -708,7 +733,7 @@ int fmx_allgather(fmx_comm_t c, const void* send, void* recv, size_t sendcount, 
   if (!send || !recv) return fail(FMX_ERR_INVALID_ARG, "null buffer");
   const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;
   CudaSink sink(c);
-  return on_lanes(c, (cudaStream_t)stream, [&]() -> int {
+  return on_lanes(c, (cudaStream_t)stream, 0, [&]() -> int {
     if (c->nranks == 1) {
       if (send != recv)
         FMX_CUDA(cudaMemcpyAsync(recv, send, sendcount * esz, cudaMemcpyDeviceToDevice,
@@ -786,7 +811,7 @@ int fmx_allreduce_host(fmx_comm_t c, size_t offset, size_t count, int dtype, int
                 offset, count * esz, (size_t)c->L.user_bytes);
   if (count == 0) return FMX_OK;
   CudaSink sink(c);
-  return on_lanes(c, (cudaStream_t)stream, [&]() {
+  return on_lanes(c, (cudaStream_t)stream, 1, [&]() {
     return plan_allreduce_host(c, sink, offset, count, dtype, op, factor);
   });
 }
@@ -804,13 +829,13 @@ int fmx_broadcast(fmx_comm_t c, const void* send, void* recv, size_t count, int 
   cudaStream_t s = (cudaStream_t)stream;
   CudaSink sink(c);
   if (c->nranks == 1) {
-    return on_lanes(c, s, [&]() -> int {
+    return on_lanes(c, s, 1, [&]() -> int {
       if (send != recv)
         FMX_CUDA(cudaMemcpyAsync(recv, send, count * esz, cudaMemcpyDeviceToDevice, lane_stream(c, kLaneMain)));
       return FMX_OK;
     });
   }
-  return on_lanes(c, s, [&]() {
+  return on_lanes(c, s, 1, [&]() {
     return plan_broadcast(c, sink, (const char*)send, (char*)recv, count, dtype, root);
   });
 }
@@ -845,7 +870,7 @@ int fmx_comm_destroy(fmx_comm_t c) {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
   }
-  for (int l = 0; l < 2; ++l) {
+  for (int l = 0; l < 3; ++l) {
     if (c->lane[l]) cudaStreamDestroy(c->lane[l]);
     if (c->joined[l]) cudaEventDestroy(c->joined[l]);
   }
@@ -936,6 +961,12 @@ int fmx_comm_monitor(fmx_comm_t c, double seconds, uint64_t* out, size_t cap, si
   return FMX_OK;
 }
 
+int fmx_comm_set_join_stream(fmx_comm_t c, void* stream) {
+  if (!c) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
+  c->join_stream = (cudaStream_t)stream;
+  return FMX_OK;
+}
+
 int fmx_comm_set_timing(fmx_comm_t c, int on) {
   if (!c) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
   c->timing = on != 0;
@@ -985,6 +1016,15 @@ int fmx_comm_set_stamps(fmx_comm_t c, size_t capacity) {
     FMX_CUDA(cudaMalloc((void**)&c->stamps, capacity * sizeof(Stamp)));
     c->stamp_cap = capacity;
   }
+  return FMX_OK;
+}
+
+int fmx_comm_stamp(fmx_comm_t c, void* stream, uint32_t info) {
+  if (!c) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
+  if (!c->stamps || c->stamp_used >= c->stamp_cap) return FMX_OK;
+  fmx_stamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(c->stamps + c->stamp_used++,
+                                                       (uint32_t)(15u << 8 | 7u), info);
+  FMX_CUDA(cudaGetLastError());
   return FMX_OK;
 }
 

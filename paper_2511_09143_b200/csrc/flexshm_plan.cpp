@@ -72,6 +72,7 @@ class TraceSink final : public Sink {
   }
   int join() { return line("J\n"); }
   int nranks = 0;
+  int64_t user_base = 0;  // overlap traces: each collective's user buffer is a separate range
 
  private:
   void shm(int lane, const Annot& a, bool write) {
@@ -84,7 +85,7 @@ class TraceSink final : public Sink {
   void user(int lane, const Annot& a, bool write) {
     if (a.off < 0 || a.bytes == 0) return;
     const char* kind = a.scratch ? (write ? "SW" : "SR") : (write ? "UW" : "UR");
-    line("%d %s %lld %zu\n", lane, kind, (long long)a.off, a.bytes);
+    line("%d %s %lld %zu\n", lane, kind, (long long)(a.off + (a.scratch ? 0 : user_base)), a.bytes);
   }
   int line(const char* fmt, ...) __attribute__((format(printf, 2, 3))) {
     char buf[128];
@@ -178,8 +179,9 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t c
 //
 // Hazards and the wait that covers each:
 //  stage(R) into in[R%2][o][me], last read by owner o's fetch of round R-2:
-//      W(R-2) (every owner signalled REDUCED after its fetches of R-2); rounds
-//      of an earlier collective are covered by the fork.
+//      W(R-2) (every owner signalled REDUCED after its fetches of R-2).  Rounds
+//      are counted across collectives and so are the waits: consecutive calls
+//      may overlap on the lanes (join-stream mode, on_lanes).
 //  fetch(R) of in[R%2][me][q]              -> wait STAGED(_TO)[q] >= R+1
 //  reduce(R) writes out[R%2][me], last read by every q's gather(R-2):
 //      W(R-1): every q signalled REDUCED >= R, which q issued after G_q(R-2).
@@ -223,7 +225,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
     const uint32_t R = R0 + j;
     if (ag) return FMX_OK;  // nothing to reduce: no contributions to stage
     // slot R%K was read by round R-K's fetches: W(R-K)
-    if (j >= K && (rc = k.wait_event(kLaneStage, kEvSlotFree + R % K))) return rc;
+    if (R >= (uint32_t)K && (rc = k.wait_event(kLaneStage, kEvSlotFree + R % K))) return rc;
     if (c->coarse) {  // one batch of copies, one STAGED signal
       segs.clear();
       for (int o = 0; o < n; ++o) {
@@ -265,7 +267,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
     if (mylen && ag) {
       // publish: my piece into my result slot (and into my part of recv)
       const size_t out_off = c->out_off(R, me);
-      if (split && j + 1 >= K && (rc = k.wait_event(kLaneMain, kEvSlotFree + (R + 1 - K) % K)))
+      if (split && R + 1 >= (uint32_t)K && (rc = k.wait_event(kLaneMain, kEvSlotFree + (R + 1 - K) % K)))
         return rc;
       segs.clear();
       segs.push_back({my_in(j), c->at(zc, out_off), mylen * g.esz,
@@ -336,7 +338,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
         }
       }
       // out[R%K][me] is free once every peer gathered round R-K: W(R-K+1)
-      if (split && j + 1 >= K && (rc = k.wait_event(kLaneMain, kEvSlotFree + (R + 1 - K) % K)))
+      if (split && R + 1 >= (uint32_t)K && (rc = k.wait_event(kLaneMain, kEvSlotFree + (R + 1 - K) % K)))
         return rc;
       if ((rc = k.reduce(kLaneMain, pr))) return rc;
       if (via_ce) {  // result slot written by the copy engine from HBM
@@ -348,7 +350,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
       }
     }
     // REDUCED(R) also says "my gather(R-1) is done": G(R-1)
-    if (split && j >= 1 && (rc = k.wait_event(kLaneMain, kEvGathered + (R - 1) % K))) return rc;
+    if (split && R >= 1 && (rc = k.wait_event(kLaneMain, kEvGathered + (R - 1) % K))) return rc;
     if ((rc = k.signal(kLaneMain, kReduced, R + 1))) return rc;
     // all-gather (lane LG): each owner's result as soon as that owner has it
     if (c->coarse_gather) {
@@ -565,9 +567,15 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   sink.nranks = nranks;
   // fake user buffers: only their offsets matter and they never reach SHM
   static char dummy[16] __attribute__((aligned(16)));
+  // FMX_TRACE_OVERLAP=1: the join-stream mode - consecutive device-buffer
+  // collectives (distinct buffers) are not separated by a join on the lanes;
+  // host-path calls and broadcasts still are (on_lanes' barrier)
+  const bool overlap = getenv("FMX_TRACE_OVERLAP") && atoi(getenv("FMX_TRACE_OVERLAP"));
+  auto device_class = [&](int i) { return kinds[i] == 0 || kinds[i] == 3 || kinds[i] == 4; };
   for (int i = 0; i < nops; ++i) {
     int rc;
-    sink.join();
+    if (!overlap || i == 0 || !device_class(i) || !device_class(i - 1)) sink.join();
+    sink.user_base = overlap ? (int64_t)i << 40 : 0;
     if (kinds[i] == 1 && (!roots || roots[i] < 0 || roots[i] >= nranks))
       return fail(FMX_ERR_INVALID_ARG, "bad broadcast root");
     if (kinds[i] == 0)

@@ -32,11 +32,13 @@ struct fmx_comm {
   uint32_t ar_round = 0, bc_round = 0;
   int64_t barrier_gen = 0;
   char* scratch = nullptr;  // CE transport: n * slice_bytes of HBM
-  cudaStream_t lane[2] = {nullptr, nullptr};  // lane 0 (stage) and lane 2 (gather); lane 1 is the caller's stream
-  cudaStream_t user = nullptr;                 // caller's stream of the current collective
+  cudaStream_t lane[3] = {};       // lane streams: 0 stage (D2H), 1 fetch + reduce, 2 gather (H2D)
+  cudaStream_t user = nullptr;      // caller's stream of the current collective (its input is ready there)
+  cudaStream_t join_stream = nullptr;  // fmx_comm_set_join_stream: completion joins here, not `user`
+  int last_class = -1;              // 0 device-buffer collective, 1 host path / broadcast
   CUcontext lane_ctx = nullptr;                // context the lane objects were created in
   cudaEvent_t ev[fmx::kNumEvents] = {};  // intra-rank lane sync (see the kEv* ids)
-  cudaEvent_t fork = nullptr, joined[2] = {nullptr, nullptr};
+  cudaEvent_t fork = nullptr, joined[3] = {};
   bool result_via_ce = false;  // CE transport: result slot by copy engine, not SM stores
   bool copy2d = true;          // coalesce regular copy runs into cudaMemcpy2DAsync
   bool coarse = true;          // FMX_GRAIN=fine: per-piece waits instead of all-peer
@@ -90,9 +92,9 @@ struct fmx_comm {
 namespace fmx {
 
 inline cudaStream_t lane_stream(const fmx_comm* c, int lane) {
-  if (c->nlanes == 1 || lane == 1) return c->user;
-  if (lane == 0) return c->lane[0];
-  return c->nlanes == 3 ? c->lane[1] : c->user;
+  if (c->nlanes == 1) return c->user;
+  if (c->nlanes == 2) return lane == 0 ? c->lane[0] : c->lane[1];
+  return c->lane[lane];
 }
 
 

@@ -41,18 +41,21 @@ class HookState:
                 stream = s if isinstance(s, torch.cuda.Stream) else torch.cuda.ExternalStream(
                     s.cuda_stream, device=inst.device)
             else:
-                stream = torch.cuda.Stream()
+                # high priority: every peer's pipeline waits on this rank's reductions,
+                # so they must not queue behind the backward pass's kernels
+                stream = torch.cuda.Stream(priority=-1)
         self.stream = stream
 
 
 def flexshm_hook(state, bucket) -> torch.futures.Future[torch.Tensor]:
     """DDP communication hook: bucket.buffer() <- mean over ranks.
 
-    The bucket's producers ran on the current (autograd) stream; the side
-    stream waits for them, runs the allreduce, and the CUDA-aware future
-    records its completion there.  DDP's wait on the future makes the
+    The collective forks from the current (autograd) stream, where the
+    bucket's producers ran, and joins into the side stream; the CUDA-aware
+    future records its completion there.  DDP's wait on the future makes the
     consumer stream wait for that event, so later backward kernels are not
-    queued behind the collective's flag waits.  `state` may also be a bare
+    queued behind the collective's flag waits, and bucket k+1 stages while
+    bucket k is still being gathered.  `state` may also be a bare
     ShmCommunicator (collective on the current stream, no overlap).
     """
     buf = bucket.buffer()
@@ -62,9 +65,15 @@ def flexshm_hook(state, bucket) -> torch.futures.Future[torch.Tensor]:
         fut.set_result(buf)
         return fut
     cur = torch.cuda.current_stream(buf.device)
-    state.stream.wait_stream(cur)
+    # fork from the autograd stream (the bucket's producers), complete on the
+    # side stream: consecutive buckets overlap inside the library (join-stream
+    # mode) and the autograd stream never waits for a collective
+    state.comm.set_join_stream(state.stream)
+    try:
+        state.comm.allreduce(buf, op="avg", stream=cur)
+    finally:
+        state.comm.set_join_stream(None)
     with torch.cuda.stream(state.stream):
-        state.comm.allreduce(buf, op="avg", stream=state.stream)
         buf.record_stream(state.stream)
         fut = torch.futures.Future(devices=[buf.device])
         fut.set_result(buf)

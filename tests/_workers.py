@@ -156,3 +156,35 @@ def ddp_worker(rank: int, job_key: str, n: int, port: int, mode: str = "green",
         (lambda t: t.cpu().view(torch.int16).numpy().view(np.uint16))
     return {"params0": as_np(params0.cpu()), "local": as_np(local.cpu()),
             "synced": as_np(synced.cpu())}
+
+
+def overlap_worker(rank: int, job_key: str, n: int, counts: list, mode: str = "green"):
+    """Join-stream mode: several allreduces on distinct buffers issued back to
+    back on one stream, completing on a side stream (the DDP-bucket pattern);
+    returns every result."""
+    import torch
+
+    from oracle import oracle as orc
+    from paper_2511_09143_b200 import instance as inst_mod
+    from paper_2511_09143_b200.comm import init_process_group
+
+    inst = inst_mod.bind(0, rank + 1, mode=mode)
+    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n, timeout_s=120)
+    main = inst.stream
+    side = torch.cuda.Stream() if inst.green_ctx is None else torch.cuda.ExternalStream(
+        inst.green_ctx.Stream().cuda_stream)
+    bufs = []
+    with torch.cuda.stream(main):
+        for i, c in enumerate(counts):
+            x = orc.synthetic_gradient(rank, c, orc.F32, seed=500 + i)
+            bufs.append(torch.from_numpy(x).to("cuda"))
+    main.synchronize()
+    comm.set_join_stream(side)
+    for b in bufs:
+        comm.allreduce(b, op="avg", stream=main)
+    comm.set_join_stream(None)
+    side.synchronize()
+    out = [b.cpu().numpy() for b in bufs]
+    comm.barrier(60)
+    comm.destroy()
+    return {"results": out}

@@ -174,3 +174,24 @@ def rs_ag_scenarios(n: int) -> list:
 def test_reduce_scatter_and_allgather(n, transport):
     sc = rs_ag_scenarios(n)
     check_all(n, sc, run(n, sc, transport=transport, slice_bytes=1 << 18))
+
+
+@pytest.mark.parametrize("n,mode", [(2, "green"), (7, "green"), (7, "mps")])
+def test_join_stream_mode_overlapping_allreduces(n, mode):
+    """DDP-bucket pattern: back-to-back allreduces of distinct buffers that
+    overlap inside the library (fmx_comm_set_join_stream); every result is
+    bit-exact."""
+    from paper_2511_09143_b200.launcher import launch, new_job_key
+    from paper_2511_09143_b200.scheduler import fm_select, make_cluster
+    from paper_2511_09143_b200.workload import Job
+
+    counts = [2_000_003, 300_000, 1_000_000, 7, 2_500_000, 640_000, 1_048_576]
+    d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
+    key = new_job_key("ovl")
+    res = launch(_workers.overlap_worker, d, args=(key, n, counts, mode), job_key=key,
+                 timeout_s=300, mode=mode)
+    for i, c in enumerate(counts):
+        xs = [orc.synthetic_gradient(r, c, orc.F32, seed=500 + i) for r in range(n)]
+        want = orc.allreduce_c(xs, orc.F32, orc.OP_PREDIV_SUM, float(n))
+        for r, out in enumerate(res):
+            assert np.array_equal(out["results"][i].view(np.uint32), want.view(np.uint32)), (i, r)

@@ -377,3 +377,55 @@ def test_auto_transport_mixes_zc_and_ce_calls(monkeypatch, n):
         merged = programs(n, SEQUENCES[seq], 4096, "auto", merged=True)
         for seed in range(3):
             simulate(merged, seed)
+
+
+OVERLAP_SEQUENCES = {
+    "allreduces": [("allreduce", 30_001, 0), ("allreduce", 4_000, 1), ("allreduce", 50_000, 0),
+                   ("allreduce", 1, 0), ("allreduce", 77_777, 1), ("allreduce", 20_000, 0)],
+    "buckets+rs-ag": [("allreduce", 20_000, 0), ("reduce_scatter", 9_001, 0),
+                      ("allgather", 12_000, 1), ("allreduce", 60_000, 0),
+                      ("broadcast", 5_000, 0, 1), ("allreduce", 10_000, 0),
+                      ("allreduce_host", 30_000, 0), ("allreduce", 40_000, 1)],
+}
+
+
+@pytest.mark.parametrize("n", [2, 3, 7])
+@pytest.mark.parametrize("seq", sorted(OVERLAP_SEQUENCES))
+@pytest.mark.parametrize("slots,lanes,transport", [("2", "3", "ce"), ("3", "3", "ce"),
+                                                   ("2", "2", "ce"), ("2", "3", "zc"),
+                                                   ("2", "3", "auto")])
+def test_overlapping_collectives_join_stream_mode(monkeypatch, n, seq, slots, lanes, transport):
+    """Join-stream mode (DDP buckets): consecutive device collectives on
+    distinct buffers run on the lanes without a join in between, so call k+1
+    stages while call k still fetches and gathers.  Slot reuse across calls
+    rests on the global-round W / G events alone."""
+    monkeypatch.setenv("FMX_TRACE_OVERLAP", "1")
+    monkeypatch.setenv("FMX_SLOTS", slots)
+    monkeypatch.setenv("FMX_LANES", lanes)
+    monkeypatch.setenv("FMX_ZC_MAX", "100000")
+    progs = programs(n, OVERLAP_SEQUENCES[seq], 4096, transport)
+    for seed in range(10):
+        simulate(progs, seed, burst=4)
+    merged = programs(n, OVERLAP_SEQUENCES[seq], 4096, transport, merged=True)
+    for seed in range(3):
+        simulate(merged, seed)
+
+
+def test_overlap_mode_needs_the_cross_call_waits(monkeypatch):
+    """Drop the stage lane's W waits of the first K rounds of each later
+    collective (what the pre-overlap plan omitted, relying on the join) and
+    the checker must object in join-stream mode."""
+    monkeypatch.setenv("FMX_TRACE_OVERLAP", "1")
+    ops = [("allreduce", 3000, 0), ("allreduce", 3000, 0), ("allreduce", 3000, 0)]
+    progs = programs(3, ops, 4096, "ce")
+    lanes = progs[1]
+    broken0 = [op for op in lanes[0] if not (op[0] == "X" and op[1] < 4)]
+    assert broken0 != lanes[0]
+    broken = [[broken0, lanes[1], lanes[2]] if r == 1 else p for r, p in enumerate(progs)]
+    failures = 0
+    for seed in range(80):
+        try:
+            simulate(broken, seed, burst=4)
+        except AssertionError:
+            failures += 1
+    assert failures > 0
