@@ -328,7 +328,8 @@ def rank_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_lo
         torch.cuda.synchronize()
         comm.set_stamps(1 << 14)
         comm.barrier(300)
-        device_step()
+        for _ in range(int(os.environ.get("FMX_STAMP_STEPS", "1"))):
+            device_step()
         torch.cuda.synchronize()
         out["stamps_device"] = comm.stamps(1 << 14)
         comm.set_stamps(0)

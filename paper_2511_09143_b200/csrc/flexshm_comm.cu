@@ -320,13 +320,15 @@ class CudaSink final : public Sink {
 // the caller's stream (a green context, an MPS client's, or the primary one),
 // so every lane object lives where the caller's work lives.
 int make_lane_objects(fmx_comm* c, CUcontext ctx) {
-  c->lane[0] = c->lane[1] = c->lane[2] = nullptr;  // an earlier context's objects are abandoned
-  // highest priority: a rank's collective work (copy kernels, reductions) is
-  // scheduled ahead of its compute kernels, because every peer waits on it
-  int lo_prio = 0, hi_prio = 0;
+  c->lane[0] = c->lane[2] = nullptr;  // an earlier context's objects are abandoned
+  // lane priority (FMX_LANE_PRIORITY=1: highest) stays default: high-priority
+  // lanes made the device-buffer allreduce 1.4x slower on the B200 under MPS
+  // (profiles/r01/r2o) and did not help DP training (r2k)
+  int lo_prio = 0, hi_prio = 0, prio = 0;
   FMX_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  if (const char* v = getenv("FMX_LANE_PRIORITY")) prio = atoi(v) ? hi_prio : 0;
   for (int l = 0; l < 3; ++l) {
-    FMX_CUDA(cudaStreamCreateWithPriority(&c->lane[l], cudaStreamNonBlocking, hi_prio));
+    if (l != 1) FMX_CUDA(cudaStreamCreateWithPriority(&c->lane[l], cudaStreamNonBlocking, prio));
     FMX_CUDA(cudaEventCreateWithFlags(&c->joined[l], cudaEventDisableTiming));
   }
   FMX_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
@@ -339,13 +341,13 @@ int make_lane_objects(fmx_comm* c, CUcontext ctx) {
   return FMX_OK;
 }
 
-// Run one collective on the lane streams: they fork from the caller's stream
-// (the input is ready there) and join back into it - or, with a join stream
-// set (fmx_comm_set_join_stream), into that stream, so the caller's stream
-// runs on while the collective completes and consecutive device-buffer
-// collectives overlap on the lanes (stage of call k+1 while call k gathers;
-// slot reuse across calls is covered by the plan's W / G events, which count
-// rounds globally).  A host-path or broadcast call, or the first device call
+// Run one collective: lane 1 runs on the main stream (the join stream if one
+// is set, else the caller's), lanes 0 and 2 on two extra streams; all fork
+// from the caller's stream (the input is ready there) and join into the main
+// stream.  With a join stream (fmx_comm_set_join_stream) the caller's stream
+// runs on while the collective completes, and the next device-buffer call's
+// stage can overlap this call's gather (slot reuse across calls is covered by
+// the plan's W / G events, which count rounds globally).  A host-path or broadcast call, or the first device call
 // after one, waits for the previous collective to complete.  Every runtime
 // call happens with the caller's stream context current (DDP calls hooks from
 // autograd threads whose current context may be another one).
@@ -365,29 +367,30 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
   int rc;
   if (ctx != c->lane_ctx && (rc = make_lane_objects(c, ctx))) return rc;
   c->user = user;
-  const int used = c->nlanes == 1 ? 0 : c->nlanes;  // lane streams in use (nlanes 1: `user`)
+  cudaStream_t main = c->join_stream ? c->join_stream : user;  // lane 1 and the join target
+  // extra lane streams in use: lane 0, and lane 2 with three lanes
+  std::vector<cudaStream_t> extra;
+  if (c->nlanes >= 2) extra.push_back(c->lane[0]);
+  if (c->nlanes == 3) extra.push_back(c->lane[2]);
   // host-path / broadcast calls (and the first device call after one) wait for
   // the previous collective, whichever stream it joined (redundant, and free,
   // when it joined the caller's stream)
   const bool barrier = c->has_done && (cls != 0 || c->last_class != 0);
-  if (used) FMX_CUDA(cudaEventRecord(c->fork, user));
-  for (int l = 0; l < used; ++l) {
-    FMX_CUDA(cudaStreamWaitEvent(c->lane[l], c->fork, 0));
-    if (barrier) FMX_CUDA(cudaStreamWaitEvent(c->lane[l], c->done, 0));
+  std::vector<cudaStream_t> lanes_ = extra;
+  if (main != user) lanes_.push_back(main);
+  if (!lanes_.empty()) FMX_CUDA(cudaEventRecord(c->fork, user));
+  for (cudaStream_t s : lanes_) FMX_CUDA(cudaStreamWaitEvent(s, c->fork, 0));
+  if (barrier) {
+    for (cudaStream_t s : extra) FMX_CUDA(cudaStreamWaitEvent(s, c->done, 0));
+    FMX_CUDA(cudaStreamWaitEvent(main, c->done, 0));
   }
-  if (!used && barrier) FMX_CUDA(cudaStreamWaitEvent(user, c->done, 0));
   rc = body();
-  cudaStream_t target = c->join_stream ? c->join_stream : user;
-  for (int l = 0; l < used; ++l) {
-    FMX_CUDA(cudaEventRecord(c->joined[l], c->lane[l]));
-    FMX_CUDA(cudaStreamWaitEvent(target, c->joined[l], 0));
-  }
-  if (!used && target != user) {
-    FMX_CUDA(cudaEventRecord(c->joined[0], user));
-    FMX_CUDA(cudaStreamWaitEvent(target, c->joined[0], 0));
+  for (size_t l = 0; l < extra.size(); ++l) {
+    FMX_CUDA(cudaEventRecord(c->joined[l], extra[l]));
+    FMX_CUDA(cudaStreamWaitEvent(main, c->joined[l], 0));
   }
   if (rc) return rc;
-  FMX_CUDA(cudaEventRecord(c->done, target));
+  FMX_CUDA(cudaEventRecord(c->done, main));
   c->has_done = true;
   c->last_class = cls;
   return FMX_OK;
@@ -871,7 +874,7 @@ int fmx_comm_destroy(fmx_comm_t c) {
     cudaEventDestroy(pr.second);
   }
   for (int l = 0; l < 3; ++l) {
-    if (c->lane[l]) cudaStreamDestroy(c->lane[l]);
+    if (l != 1 && c->lane[l]) cudaStreamDestroy(c->lane[l]);
     if (c->joined[l]) cudaEventDestroy(c->joined[l]);
   }
   if (pushed) {

@@ -32,7 +32,7 @@ struct fmx_comm {
   uint32_t ar_round = 0, bc_round = 0;
   int64_t barrier_gen = 0;
   char* scratch = nullptr;  // CE transport: n * slice_bytes of HBM
-  cudaStream_t lane[3] = {};       // lane streams: 0 stage (D2H), 1 fetch + reduce, 2 gather (H2D)
+  cudaStream_t lane[3] = {};       // extra streams of lane 0 (stage, D2H) and lane 2 (gather, H2D); [1] unused
   cudaStream_t user = nullptr;      // caller's stream of the current collective (its input is ready there)
   cudaStream_t join_stream = nullptr;  // fmx_comm_set_join_stream: completion joins here, not `user`
   int last_class = -1;              // 0 device-buffer collective, 1 host path / broadcast
@@ -92,8 +92,13 @@ struct fmx_comm {
 namespace fmx {
 
 inline cudaStream_t lane_stream(const fmx_comm* c, int lane) {
-  if (c->nlanes == 1) return c->user;
-  if (c->nlanes == 2) return lane == 0 ? c->lane[0] : c->lane[1];
+  // lane 1 runs on the main stream: the join stream if one is set, else the
+  // caller's.  Only lanes 0 and 2 are extra streams: with 7 MPS clients per
+  // GPU, a third extra stream per client made the allreduce 1.5x slower
+  // (streams alias onto shared hardware queues; profiles/r01/r2q).
+  cudaStream_t main = c->join_stream ? c->join_stream : c->user;
+  if (c->nlanes == 1 || lane == 1) return main;
+  if (c->nlanes == 2) return lane == 0 ? c->lane[0] : main;
   return c->lane[lane];
 }
 
