@@ -659,7 +659,8 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
     digests = {round(r["param_digest"], 3) for r in res.values()}
     desc, precision, unit = TRAIN_MODELS[model]
     if cfg["stamps"]:
-        with open(args.stamps, "w") as f:
+        path = args.stamps if args.train_only else os.path.splitext(args.stamps)[0] + "_train.json"
+        with open(path, "w") as f:
             json.dump({"n": n, "model": model, "train": {r: v["stamps"] for r, v in res.items()}}, f)
     return {unit: n * args.batch * args.train_steps / t, "instances": n, "batch_per_instance":
             args.batch, "ms_per_step": t * 1e3 / args.train_steps, "steps": args.train_steps,
