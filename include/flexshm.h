@@ -216,6 +216,11 @@ int fmx_comm_monitor(fmx_comm_t comm, double seconds, uint64_t* out, size_t cap,
  * does by waiting on the bucket future).  Host-path calls and broadcasts wait
  * for the previous collective.  NULL restores the default. */
 int fmx_comm_set_join_stream(fmx_comm_t comm, void* stream);
+/* The stream the last collective completed on: the calling stream by default;
+ * in join-stream mode with three lanes, an internal stream (the gather lane),
+ * so the join stream is free for the next call's fetch.  Make consumers wait
+ * for an event recorded on it. */
+int fmx_comm_completion_stream(fmx_comm_t comm, void** stream);
 
 /* Live timing of the reduction kernel: with timing on, every reduce launch
  * is bracketed by CUDA events on the lane stream it runs on; kernel_time

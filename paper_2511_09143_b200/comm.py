@@ -243,6 +243,13 @@ class ShmCommunicator:
         _lib.check(_lib.lib().fmx_comm_set_join_stream(self._h, h or None),
                    "fmx_comm_set_join_stream")
 
+    def completion_stream(self) -> int:
+        """cudaStream_t (as int) the last collective completed on."""
+        s = ctypes.c_void_p()
+        _lib.check(_lib.lib().fmx_comm_completion_stream(self._h, ctypes.byref(s)),
+                   "fmx_comm_completion_stream")
+        return s.value or 0
+
     def stamp(self, info: int, stream=None) -> None:
         """Caller's marker (op kind 7) on the timeline, enqueued on `stream`."""
         _lib.check(_lib.lib().fmx_comm_stamp(self._h, self._stream(stream), int(info)),

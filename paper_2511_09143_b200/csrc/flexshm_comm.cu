@@ -375,7 +375,9 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
   // host-path / broadcast calls (and the first device call after one) wait for
   // the previous collective, whichever stream it joined (redundant, and free,
   // when it joined the caller's stream)
-  const bool barrier = c->has_done && (cls != 0 || c->last_class != 0);
+  // A change of main stream is a barrier too: lane 1 (HBM scratch slots) is
+  // ordered across calls only while it stays on one stream.
+  const bool barrier = c->has_done && (cls != 0 || c->last_class != 0 || main != c->last_main);
   std::vector<cudaStream_t> lanes_ = extra;
   if (main != user) lanes_.push_back(main);
   if (!lanes_.empty()) FMX_CUDA(cudaEventRecord(c->fork, user));
@@ -385,14 +387,27 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
     FMX_CUDA(cudaStreamWaitEvent(main, c->done, 0));
   }
   rc = body();
-  for (size_t l = 0; l < extra.size(); ++l) {
-    FMX_CUDA(cudaEventRecord(c->joined[l], extra[l]));
-    FMX_CUDA(cudaStreamWaitEvent(main, c->joined[l], 0));
+  // completion: by default every lane joins the caller's stream.  In
+  // join-stream mode with three lanes the call completes on lane 2 (the gather
+  // lane, last to finish): lanes 0 and 1 join it there and the join stream -
+  // lane 1 of the next call - does not wait for this call's gather, so bucket
+  // k+1 fetches while bucket k gathers.  fmx_comm_completion_stream names it.
+  cudaStream_t target = main;
+  if (c->join_stream && c->nlanes == 3) target = c->lane[2];
+  c->completion = target;
+  std::vector<cudaStream_t> into = extra;
+  if (target != main) {
+    into.assign({c->lane[0], main});
+  }
+  for (size_t l = 0; l < into.size(); ++l) {
+    FMX_CUDA(cudaEventRecord(c->joined[l], into[l]));
+    FMX_CUDA(cudaStreamWaitEvent(target, c->joined[l], 0));
   }
   if (rc) return rc;
-  FMX_CUDA(cudaEventRecord(c->done, main));
+  FMX_CUDA(cudaEventRecord(c->done, target));
   c->has_done = true;
   c->last_class = cls;
+  c->last_main = main;
   return FMX_OK;
 }
 
@@ -967,6 +982,12 @@ int fmx_comm_monitor(fmx_comm_t c, double seconds, uint64_t* out, size_t cap, si
 int fmx_comm_set_join_stream(fmx_comm_t c, void* stream) {
   if (!c) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
   c->join_stream = (cudaStream_t)stream;
+  return FMX_OK;
+}
+
+int fmx_comm_completion_stream(fmx_comm_t c, void** stream) {
+  if (!c || !stream) return fail(FMX_ERR_INVALID_ARG, "null argument");
+  *stream = (void*)c->completion;
   return FMX_OK;
 }
 

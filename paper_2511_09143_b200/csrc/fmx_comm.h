@@ -34,7 +34,9 @@ struct fmx_comm {
   char* scratch = nullptr;  // CE transport: n * slice_bytes of HBM
   cudaStream_t lane[3] = {};       // extra streams of lane 0 (stage, D2H) and lane 2 (gather, H2D); [1] unused
   cudaStream_t user = nullptr;      // caller's stream of the current collective (its input is ready there)
-  cudaStream_t join_stream = nullptr;  // fmx_comm_set_join_stream: completion joins here, not `user`
+  cudaStream_t join_stream = nullptr;  // fmx_comm_set_join_stream: lane 1 runs here, not on `user`
+  cudaStream_t completion = nullptr;   // stream the last collective completed on
+  cudaStream_t last_main = nullptr;    // lane-1 stream of the last collective
   int last_class = -1;              // 0 device-buffer collective, 1 host path / broadcast
   CUcontext lane_ctx = nullptr;                // context the lane objects were created in
   cudaEvent_t ev[fmx::kNumEvents] = {};  // intra-rank lane sync (see the kEv* ids)

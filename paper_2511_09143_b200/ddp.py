@@ -71,10 +71,17 @@ def flexshm_hook(state, bucket) -> torch.futures.Future[torch.Tensor]:
     state.comm.set_join_stream(state.stream)
     try:
         state.comm.allreduce(buf, op="avg", stream=cur)
+        done = state.comm.completion_stream()
     finally:
         state.comm.set_join_stream(None)
-    with torch.cuda.stream(state.stream):
-        buf.record_stream(state.stream)
+    # lane 1 ran on the side stream (tell the allocator); the call completes on
+    # the library's gather lane - the future's event is recorded there.  No
+    # record_stream on that library-owned stream: it may be destroyed (with the
+    # communicator) before DDP frees its bucket buffers.
+    buf.record_stream(state.stream)
+    done_stream = state.stream if done in (0, state.stream.cuda_stream) else \
+        torch.cuda.ExternalStream(done, device=buf.device)
+    with torch.cuda.stream(done_stream):
         fut = torch.futures.Future(devices=[buf.device])
         fut.set_result(buf)
     return fut

@@ -182,8 +182,10 @@ def overlap_worker(rank: int, job_key: str, n: int, counts: list, mode: str = "g
     comm.set_join_stream(side)
     for b in bufs:
         comm.allreduce(b, op="avg", stream=main)
+    done = comm.completion_stream()
     comm.set_join_stream(None)
-    side.synchronize()
+    torch.cuda.ExternalStream(done).synchronize()   # the last call completes there ...
+    side.synchronize()                              # ... and every call's lane 1 ran here
     out = [b.cpu().numpy() for b in bufs]
     comm.barrier(60)
     comm.destroy()
