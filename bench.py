@@ -72,6 +72,12 @@ def parse_args(argv=None):
     p.add_argument("--nccl", action="store_true",
                    help="N>1: also time stock NCCL over NVLink, one rank per GPU (comparison "
                         "point; opt-in because NCCL inside MPS clients is untested here)")
+    p.add_argument("--buckets", type=int, default=0,
+                   help="probe: allreduce the gradient as K back-to-back buckets (join-stream mode)")
+    p.add_argument("--bucket-serial", action="store_true",
+                   help="with --buckets: default completion (each bucket joins the caller's stream)")
+    p.add_argument("--load", type=int, default=0,
+                   help="interference probe: N bf16 GEMMs per instance during the timed loop")
     p.add_argument("--dry-run", action="store_true",
                    help="orchestration only (no CUDA): stub rank bodies; for the CPU tests of "
                         "the torchrun N>1 path")
@@ -292,12 +298,39 @@ def rank_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_lo
             comm.set_kernel_timing(False)
         return ev0.elapsed_time(ev1), comm.kernel_launches() - l0
 
-    def device_step():
-        comm.allreduce(buf, op="avg", stream=stream)
+    if cfg.get("buckets", 0) > 1:
+        # DDP-bucket pattern: the gradient as K back-to-back allreduces of distinct
+        # views, forked from `stream`, overlapping in join-stream mode; the step
+        # ends when the last completes (waited for on `stream`)
+        views = list(buf.chunk(cfg["buckets"]))
+        side = torch.cuda.Stream(device=gpu_local) if inst.green_ctx is None else \
+            torch.cuda.ExternalStream(inst.green_ctx.Stream().cuda_stream)
+        done_ev = torch.cuda.Event()
+
+        def device_step():
+            if cfg.get("bucket_join", True):
+                comm.set_join_stream(side)
+            for v in views:
+                comm.allreduce(v, op="avg", stream=stream)
+            done = comm.completion_stream()
+            comm.set_join_stream(None)
+            done_ev.record(torch.cuda.ExternalStream(done))
+            stream.wait_event(done_ev)
+    else:
+        def device_step():
+            comm.allreduce(buf, op="avg", stream=stream)
 
     for _ in range(cfg["warmup"]):
         device_step()
     torch.cuda.synchronize()
+    if cfg.get("load"):
+        # interference probe: keep this instance's SMs busy with bf16 GEMMs on
+        # another stream while the allreduces run (what DP training does)
+        load_stream = torch.cuda.Stream()
+        a = torch.randn(4096, 4096, device=f"cuda:{gpu_local}", dtype=torch.bfloat16)
+        with torch.cuda.stream(load_stream):
+            for _ in range(cfg["load"]):
+                a = (a @ a).clamp_(-1, 1)
     out["ms_total"], out["launches"] = timed(cfg["steps"], device_step, kernel_timing=True)
     if cfg.get("timeline"):
         # host-side flag timeline of 2 allreduces (rank 0 polls the segment)
@@ -683,7 +716,8 @@ def run_ours(args) -> dict | None:
     cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
            "slice_bytes": args.slice_bytes, "dtype": args.dtype, "count": args.count,
            "warmup": args.warmup, "steps": args.steps, "e2e": not args.no_e2e,
-           "timeline": args.timeline, "stamps": bool(args.stamps)}
+           "timeline": args.timeline, "stamps": bool(args.stamps), "load": args.load,
+           "buckets": args.buckets, "bucket_join": not args.bucket_serial}
     # one job key for all processes of all GPUs
     job_key = os.environ.get("FMX_BENCH_KEY") or f"bench-{os.environ.get('MASTER_PORT', '0')}-" \
         f"{os.environ.get('TORCHELASTIC_RUN_ID', str(os.getppid()))}"

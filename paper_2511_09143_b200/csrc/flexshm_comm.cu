@@ -269,7 +269,19 @@ class CudaSink final : public Sink {
     size_t bytes = 0;
     for (const PlanSeg& g : segs) bytes += g.bytes;
     int rc = copy_impl(lane, segs, src_sys, use_kernel);
-    return rc || segs.empty() ? rc : stamp(lane, kStCopy, (uint32_t)std::min<size_t>(bytes, ~0u));
+    if (rc || segs.empty()) return rc;
+    // Copy fence: a one-warp no-op kernel right after every copy-engine batch.
+    // A stream memory op (flag signal / wait) directly behind a copy-engine
+    // transfer takes a slow path on this B200 + MPS setup (13 back-to-back
+    // 8 MiB allreduces on one stream: 162 ms; with the fence 32 ms), and the
+    // fence also speeds up the plain allreduce (30.3 -> 28.1 ms) and the host
+    // path (17.7 -> 16.6 ms) (profiles/r01/r2z_r3a).  FMX_COPY_FENCE=0: off.
+    if (!use_kernel && c_->copy_fence) {
+      fmx_nop_kernel<<<1, 32, 0, lane_stream(c_, lane)>>>();
+      FMX_CUDA(cudaGetLastError());
+      c_->launches++;
+    }
+    return stamp(lane, kStCopy, (uint32_t)std::min<size_t>(bytes, ~0u));
   }
   int reduce(int lane, const PlanReduce& r) override {
     int rc = reduce_impl(lane, r);
@@ -370,8 +382,8 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
   cudaStream_t main = c->join_stream ? c->join_stream : user;  // lane 1 and the join target
   // extra lane streams in use: lane 0, and lane 2 with three lanes
   std::vector<cudaStream_t> extra;
-  if (c->nlanes >= 2) extra.push_back(c->lane[0]);
-  if (c->nlanes == 3) extra.push_back(c->lane[2]);
+  if (c->nlanes >= 2 && !c->join_stream) extra.push_back(c->lane[0]);
+  if (c->nlanes == 3 && !c->join_stream) extra.push_back(c->lane[2]);
   // host-path / broadcast calls (and the first device call after one) wait for
   // the previous collective, whichever stream it joined (redundant, and free,
   // when it joined the caller's stream)
@@ -387,20 +399,12 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
     FMX_CUDA(cudaStreamWaitEvent(main, c->done, 0));
   }
   rc = body();
-  // completion: by default every lane joins the caller's stream.  In
-  // join-stream mode with three lanes the call completes on lane 2 (the gather
-  // lane, last to finish): lanes 0 and 1 join it there and the join stream -
-  // lane 1 of the next call - does not wait for this call's gather, so bucket
-  // k+1 fetches while bucket k gathers.  fmx_comm_completion_stream names it.
+  // completion: the lanes join the main stream (the caller's, or the join
+  // stream, which then carries every lane); fmx_comm_completion_stream names it
   cudaStream_t target = main;
-  if (c->join_stream && c->nlanes == 3) target = c->lane[2];
   c->completion = target;
-  std::vector<cudaStream_t> into = extra;
-  if (target != main) {
-    into.assign({c->lane[0], main});
-  }
-  for (size_t l = 0; l < into.size(); ++l) {
-    FMX_CUDA(cudaEventRecord(c->joined[l], into[l]));
+  for (size_t l = 0; l < extra.size(); ++l) {
+    FMX_CUDA(cudaEventRecord(c->joined[l], extra[l]));
     FMX_CUDA(cudaStreamWaitEvent(target, c->joined[l], 0));
   }
   if (rc) return rc;
@@ -639,6 +643,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (const char* v = getenv("FMX_LANES")) c->nlanes = std::min(3, std::max(1, atoi(v)));
   if (const char* v = getenv("FMX_RAMP")) c->ramp = atoi(v) != 0;
   if (const char* v = getenv("FMX_MIN_ROUNDS")) c->min_rounds = atoi(v);
+  if (const char* v = getenv("FMX_COPY_FENCE")) c->copy_fence = atoi(v) != 0;
   if (e != cudaSuccess) {
     h->aborted.store(1);
     fail(FMX_ERR_CUDA, "device mapping of %zu-byte segment failed: %s", c->total_bytes,

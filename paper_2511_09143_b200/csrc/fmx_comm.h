@@ -37,6 +37,7 @@ struct fmx_comm {
   cudaStream_t join_stream = nullptr;  // fmx_comm_set_join_stream: lane 1 runs here, not on `user`
   cudaStream_t completion = nullptr;   // stream the last collective completed on
   cudaStream_t last_main = nullptr;    // lane-1 stream of the last collective
+  bool copy_fence = true;              // no-op kernel after every copy-engine batch (CudaSink::copy)
   int last_class = -1;              // 0 device-buffer collective, 1 host path / broadcast
   CUcontext lane_ctx = nullptr;                // context the lane objects were created in
   cudaEvent_t ev[fmx::kNumEvents] = {};  // intra-rank lane sync (see the kEv* ids)
@@ -99,7 +100,11 @@ inline cudaStream_t lane_stream(const fmx_comm* c, int lane) {
   // GPU, a third extra stream per client made the allreduce 1.5x slower
   // (streams alias onto shared hardware queues; profiles/r01/r2q).
   cudaStream_t main = c->join_stream ? c->join_stream : c->user;
-  if (c->nlanes == 1 || lane == 1) return main;
+  // join-stream mode runs every lane on the join stream: next to the caller's
+  // compute stream, two more extra streams per MPS client made bucketed
+  // allreduces 2.5x slower (hardware-queue aliasing, profiles/r01/r2w), and a
+  // single in-order stream per rank is as fast as three lanes on this box
+  if (c->nlanes == 1 || lane == 1 || c->join_stream) return main;
   if (c->nlanes == 2) return lane == 0 ? c->lane[0] : main;
   return c->lane[lane];
 }
