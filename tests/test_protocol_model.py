@@ -348,15 +348,17 @@ def test_model_catches_a_broken_host_push_lane():
     assert failures > 0
 
 
+@pytest.mark.parametrize("ramp", ["0", "1"])
 @pytest.mark.parametrize("min_rounds", ["1", "3", "4", "7"])
 @pytest.mark.parametrize("slice_bytes", [4096, 1 << 20, 4 << 20, 12288])
 @pytest.mark.parametrize("dtype", [0, 1])
-def test_piece_starts_are_16_byte_aligned(monkeypatch, min_rounds, slice_bytes, dtype):
+def test_piece_starts_are_16_byte_aligned(monkeypatch, ramp, min_rounds, slice_bytes, dtype):
     """The vector reduction needs every pipeline piece to start on 16 bytes:
     ramp pieces and the min-rounds slice are whole vectors for any slice size
     (a misaligned ramp piece once crashed the B200 with FMX_MIN_ROUNDS=4)."""
     import re
     monkeypatch.setenv("FMX_MIN_ROUNDS", min_rounds)
+    monkeypatch.setenv("FMX_RAMP", ramp)
     for count in (1_000_003, 2_000_000, 333_333, 64_001, 17):
         for rank in (0, 3, 6):
             t = _lib.trace_plan(7, rank, [("allreduce", count, dtype)], slice_bytes)
