@@ -190,3 +190,83 @@ def overlap_worker(rank: int, job_key: str, n: int, counts: list, mode: str = "g
     comm.barrier(60)
     comm.destroy()
     return {"results": out}
+
+
+def stress_ops(n: int, seed: int, nops: int) -> list:
+    """A seeded random program of collectives every rank runs in the same order."""
+    import random
+    rng = random.Random(seed)
+    ops = []
+    for i in range(nops):
+        kind = rng.choice(["allreduce"] * 4 + ["reduce_scatter", "allgather", "broadcast"])
+        dtype = rng.choice(["f32", "f32", "bf16"])
+        size = rng.choice([1, 7, 64, 4096, 100_003, 524_288, 1_000_001, 2_500_000])
+        op = rng.choice(["sum", "avg", "postscale"]) if kind in ("allreduce", "reduce_scatter") \
+            else "sum"
+        ops.append({"kind": kind, "dtype": dtype, "size": size, "op": op,
+                    "root": rng.randrange(n), "inplace": rng.random() < 0.5,
+                    "join": rng.random() < 0.3, "seed": 10_000 + i})
+    return ops
+
+
+def stress_input(rank: int, o: dict, n: int) -> np.ndarray:
+    from oracle import oracle as orc
+    dt = orc.F32 if o["dtype"] == "f32" else orc.BF16
+    count = o["size"] * (n if o["kind"] == "reduce_scatter" else 1)
+    return orc.synthetic_gradient(rank, count, dt, seed=o["seed"])
+
+
+def stress_worker(rank: int, job_key: str, n: int, seed: int, nops: int, mode: str = "mps"):
+    """Run the random program; return a sha256 per op of this rank's result."""
+    import torch
+
+    from paper_2511_09143_b200 import instance as inst_mod
+    from paper_2511_09143_b200.comm import init_process_group
+
+    inst = inst_mod.bind(0, rank + 1, mode=mode)
+    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n, timeout_s=120)
+    s = inst.stream
+    side = torch.cuda.Stream()
+    digests = []
+    for o in stress_ops(n, seed, nops):
+        x = stress_input(rank, o, n)
+        tdt = torch.float32 if o["dtype"] == "f32" else torch.bfloat16
+        host = torch.from_numpy(x.view(np.float32) if o["dtype"] == "f32" else x.view(np.int16))
+        with torch.cuda.stream(s):
+            t = host.to("cuda", non_blocking=False).view(tdt) if o["dtype"] != "f32" else \
+                host.to("cuda", non_blocking=False)
+        s.synchronize()
+        factor = 0.25 if o["op"] == "postscale" else None
+        if o["join"]:
+            comm.set_join_stream(side)
+        k = o["kind"]
+        if k == "allreduce":
+            res = t if o["inplace"] else torch.empty_like(t)
+            comm.allreduce(t, op=o["op"], factor=factor, out=None if o["inplace"] else res,
+                           stream=s)
+        elif k == "reduce_scatter":
+            c = o["size"]
+            res = t[rank * c:(rank + 1) * c] if o["inplace"] else torch.empty(c, dtype=tdt,
+                                                                              device="cuda")
+            comm.reduce_scatter(t, res, op=o["op"], factor=factor, stream=s)
+        elif k == "allgather":
+            c = o["size"]
+            res = torch.empty(n * c, dtype=tdt, device="cuda")
+            if o["inplace"]:
+                res[rank * c:(rank + 1) * c].copy_(t)
+                comm.allgather(res[rank * c:(rank + 1) * c], res, stream=s)
+            else:
+                comm.allgather(t, res, stream=s)
+        else:
+            comm.broadcast(t, root=o["root"], stream=s)
+            res = t
+        done = comm.completion_stream()
+        comm.set_join_stream(None)
+        torch.cuda.ExternalStream(done).synchronize()
+        s.synchronize()
+        r = res.cpu()
+        arr = r.numpy() if o["dtype"] == "f32" else r.view(torch.int16).numpy().view(np.uint16)
+        digests.append(digest(arr))
+    comm.barrier(120)
+    comm.destroy()
+    return {"digests": digests}

@@ -1,0 +1,52 @@
+"""Randomised soak test: a seeded program of allreduce / reduce-scatter /
+all-gather / broadcast calls (fp32 and bf16, all ops, ragged sizes, in and out
+of place, some in join-stream mode) run by 7 MPS ranks and 3 green-context
+ranks through one communicator each; every result is checked bit for bit
+against the oracle (sha256)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from tests import _workers
+
+pytestmark = pytest.mark.gpu
+
+OPS = {"sum": orc.OP_SUM, "postscale": orc.OP_SUM_POSTSCALE, "prediv": orc.OP_PREDIV_SUM}
+
+
+def expected_digest(o: dict, n: int, rank: int) -> str:
+    xs = [_workers.stress_input(r, o, n) for r in range(n)]
+    dt = orc.F32 if o["dtype"] == "f32" else orc.BF16
+    if o["kind"] == "broadcast":
+        return _workers.digest(xs[o["root"]])
+    if o["kind"] == "allgather":
+        return _workers.digest(np.concatenate(xs))
+    op, factor = o["op"], (0.25 if o["op"] == "postscale" else 1.0)
+    if op == "avg":
+        op, factor = "prediv", float(n)
+    full = orc.allreduce_c(xs, dt, OPS[op], factor)
+    if o["kind"] == "reduce_scatter":
+        c = o["size"]
+        return _workers.digest(full[rank * c:(rank + 1) * c])
+    return _workers.digest(full)
+
+
+@pytest.mark.parametrize("n,mode,seed", [(7, "mps", 1), (3, "green", 2)])
+def test_random_collective_program_is_bit_exact(n, mode, seed):
+    from paper_2511_09143_b200.launcher import launch, new_job_key
+    from paper_2511_09143_b200.scheduler import fm_select, make_cluster
+    from paper_2511_09143_b200.workload import Job
+
+    nops = 60
+    d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
+    key = new_job_key("stress")
+    res = launch(_workers.stress_worker, d, args=(key, n, seed, nops, mode), job_key=key,
+                 timeout_s=600, mode=mode)
+    ops = _workers.stress_ops(n, seed, nops)
+    for i, o in enumerate(ops):
+        for r in range(n):
+            want = expected_digest(o, n, r)
+            assert res[r]["digests"][i] == want, (i, o, r)
