@@ -8,12 +8,14 @@ fm_select, one process per instance).  N>1 (torchrun, one process per GPU):
 7 instances per GPU, 7N ranks in one communicator, rank order from fm_select
 over N GPUs (weak scaling: the per-rank gradient is fixed).
 
-A step = one allreduce of every rank's gradient.  `value` = algbw = gradient
-bytes / step time (device time, CUDA events on each rank's stream, max over
-ranks).  Inputs are device-resident and 7 x 102 MB per GPU of gradients plus
-the SHM slots exceed the 126 MB L2.  `e2e` = the same metric through the
-public API with host buffers: each step copies every rank's gradient from
-pinned host memory to the device, allreduces, and copies the result back.
+A step = one allreduce of every rank's gradient.  `value` = the whole job's
+aggregate: n_ranks x gradient bytes / step time (device time, CUDA events on
+each rank's stream, max over ranks); `algbw_gbs` = gradient bytes / step
+time, the usual per-buffer allreduce figure.  Inputs are device-resident and
+7 x 102 MB per GPU of gradients plus the SHM slots exceed the 126 MB L2.
+`e2e` = the same metric through the public API with host-resident data: every
+rank's gradient sits in its registered pinned host buffer, the GPUs read it
+and write the result back inside the timed region (fmx_allreduce_host).
 
 `--impl reference` times the CPU restatement of the same algorithm
 (oracle/flexshm_oracle.c: multi-threaded SHM reduce-scatter/all-gather,
@@ -42,6 +44,7 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # Host-link peaks measured on this pool's B200 box (profiles/r01_probe/bw.jsonl):
 # copy-engine pinned H2D / D2H / bidirectional, PCIe Gen5 x16.
 LINK_PEAK_FALLBACK = {"h2d": 55.61, "d2h": 56.77, "bidir": 100.21}
+UNIT = "GB/s (aggregate: all ranks' gradient bytes allreduced per second; algbw_gbs = per-buffer)"
 
 
 def parse_args(argv=None):
@@ -798,8 +801,11 @@ def run_ours(args) -> dict | None:
     peaks = dict(LINK_PEAK_FALLBACK)
     line = {
         "metric": "SHM allreduce GB/s vs host-link peak; ResNet-50 img/s on 1g slices",
-        "value": s_bytes / t_step / 1e9,
-        "unit": "GB/s (algbw: ResNet-50 gradient bytes allreduced per second)",
+        # whole-job aggregate: every rank's S-byte gradient is one unit of work
+        # (weak scaling: S per rank is fixed as ranks / GPUs grow); algbw = S / T
+        "value": n * s_bytes / t_step / 1e9,
+        "unit": UNIT,
+        "algbw_gbs": s_bytes / t_step / 1e9,
         "n_gpus": gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "float32" if args.dtype == "f32" else "bfloat16",
@@ -827,7 +833,8 @@ def run_ours(args) -> dict | None:
     if not args.no_e2e:
         t_e2e = local_max_e2e / 1e3 / args.steps
         t_dev = local_max_e2e_dev / 1e3 / args.steps
-        line["e2e"] = {"value": s_bytes / t_e2e / 1e9, "unit": line["unit"],
+        line["e2e"] = {"value": n * s_bytes / t_e2e / 1e9, "unit": line["unit"],
+                       "algbw_gbs": s_bytes / t_e2e / 1e9,
                        "ms_per_step": t_e2e * 1e3,
                        "api": "ShmCommunicator.allreduce_host -> fmx_allreduce_host (C ABI): "
                               "every rank's gradient in its registered pinned host buffer; the "
@@ -836,7 +843,7 @@ def run_ours(args) -> dict | None:
                        "h2d_bytes_per_step": n * s_bytes, "d2h_bytes_per_step": n * s_bytes,
                        "ranks_agree": len(digests) == 1}
         line["e2e_device_buffers"] = {
-            "value": s_bytes / t_dev / 1e9, "unit": line["unit"], "ms_per_step": t_dev * 1e3,
+            "value": n * s_bytes / t_dev / 1e9, "unit": line["unit"], "ms_per_step": t_dev * 1e3,
             "api": "pinned host -> device copy, ShmCommunicator.allreduce, device -> pinned host",
             "h2d_bytes_per_step": n * s_bytes, "d2h_bytes_per_step": n * s_bytes}
     return line
@@ -901,7 +908,8 @@ def run_cpu_reference(count: int, n: int, dtype: str, steps: int, warmup: int,
     t = sum(times) / len(times)
     esz = 4 if dtype == "f32" else 2
     del np
-    return {"value": count * esz / t / 1e9, "ms_per_step": t * 1e3, "iters": k,
+    return {"value": n * count * esz / t / 1e9, "algbw_gbs": count * esz / t / 1e9,
+            "ms_per_step": t * 1e3, "iters": k,
             "cores": nthreads}
 
 
@@ -909,7 +917,7 @@ def main(argv=None):
     args = parse_args(argv)
     grank, world, _ = dist_env()
     n = (args.gpus if world == 1 else world) * args.ranks_per_gpu
-    unit = "GB/s (algbw: ResNet-50 gradient bytes allreduced per second)"
+    unit = UNIT
     if args.impl == "reference":
         if grank != 0:
             return 0

@@ -43,6 +43,10 @@ def test_two_gpu_launch_reduces_over_ranks():
     assert abs(ln["ms_per_step"] - 10.0 * 14 / steps) < 1e-9
     assert abs(ln["e2e"]["ms_per_step"] - 5.0 * 14 / steps) < 1e-9
     assert ln["gpu_launches"] == 14          # summed over both GPUs' instances
+    # whole-job aggregate: all 14 ranks' gradients per second; algbw = one buffer's
+    s_bytes = ln["config"]["bytes"]
+    assert abs(ln["value"] - 14 * s_bytes / (ln["ms_per_step"] / 1e3) / 1e9) < 1e-6
+    assert abs(ln["algbw_gbs"] * 14 - ln["value"]) < 1e-6
     assert ln["scaling"] == "weak"
     assert ln["step_roofline"]["link_bytes_per_gpu"]["d2h"] == 7 * ln["config"]["bytes"]
 
@@ -52,4 +56,6 @@ def test_reference_arm_prints_once_under_torchrun():
                        "--count", "70000"])
     assert len(lines) == 1
     assert lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2
+    ln = lines[0]
+    assert abs(ln["value"] - 14 * 70000 * 4 / (ln["ms_per_step"] / 1e3) / 1e9) < 1e-6
     assert lines[0]["e2e"]["h2d_bytes_per_step"] == 0
