@@ -82,7 +82,7 @@ enum fmx_op {
 /* How host-link bytes move.  ZC: SM kernels store to / load from the mapped
  * SHM segment (128-bit, zero-copy).  CE: copy engines move the bytes, SM
  * kernels reduce out of HBM.  AUTO picks per collective by size: ZC up to
- * 4 MiB (no copy-engine launch latency), CE above (faster at bandwidth across
+ * 2 MiB (no copy-engine launch latency), CE above (faster at bandwidth across
  * processes on one GPU; env FMX_ZC_MAX overrides the cut).  HOST joins the bootstrap and host barrier without
  * touching CUDA (collectives then return FMX_ERR_UNSUPPORTED); it is how the
  * multi-process bootstrap is exercised on GPU-less machines. */

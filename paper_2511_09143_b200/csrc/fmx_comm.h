@@ -49,11 +49,11 @@ struct fmx_comm {
   bool ramp = false;           // FMX_RAMP=1: geometric s/8, s/4, s/2 fill / drain rounds (off:
                                // with the copy fence, equal rounds are 3-4% faster, r01/r3e)
   int min_rounds = 1;          // FMX_MIN_ROUNDS: shrink the slice so a chunk spans >= this many
-  size_t zc_max = 4u << 20;    // FMX_ZC_MAX: AUTO transport moves messages <= this with SM copies
+  size_t zc_max = 2u << 20;    // FMX_ZC_MAX: AUTO transport moves messages <= this with SM copies
 
   // transport of one collective of `bytes`: AUTO picks zero-copy SM transfers
-  // for small messages (no copy-engine launch latency: 0.12 vs 0.29 ms for
-  // 1 KiB at 7 ranks) and the copy engines above zc_max (profiles/r01/r2e)
+  // for small messages (no copy-engine launch latency: 0.12 vs 0.24 ms for
+  // 1 KiB at 7 ranks) and the copy engines above zc_max (crossover 1-4 MiB, r01/r3j)
   bool use_zc(size_t bytes) const {
     return transport == FMX_TRANSPORT_ZC || (transport == FMX_TRANSPORT_AUTO && bytes <= zc_max);
   }
