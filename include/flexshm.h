@@ -131,8 +131,9 @@ int fmx_restore_bus_id(const char* label, char* out);
  * the table is validated with the rules above (mig_aware), the segment is
  * pinned and device-mapped (cudaHostRegister Mapped|Portable) in the calling
  * thread's current CUDA context.  slice_bytes = bytes per (owner,
- * contributor) pipeline slot, 0 = default; nslots = pipeline depth, 2 (double
- * buffering) .. FMX_MAX_SLOTS, 0 = default (2, or env FMX_SLOTS).  host_bytes =
+ * contributor) pipeline slot, 0 = default (4 MiB; 16 MiB at two ranks);
+ * nslots = pipeline depth, 2 (double buffering) .. FMX_MAX_SLOTS, 0 = default
+ * (2; 4 at two ranks; env FMX_SLOTS overrides).  host_bytes =
  * size of every rank's registered host buffer (fmx_host_buffer), 0 = none.
  * Rank 0's slice_bytes / nslots / host_bytes win.  timeout_s bounds every bootstrap wait. */
 int fmx_comm_init(fmx_comm_t* comm, const char* job_key, int nranks, int rank,

@@ -90,7 +90,12 @@ int load_driver() {
                   __FILE__, __LINE__);                                                    \
   } while (0)
 
-constexpr size_t kDefaultSliceCap = 4u << 20;   // bytes per (owner, contributor) slot
+// Default slice (bytes per (owner, contributor) slot) and pipeline depth.  With
+// two ranks per communicator each round moves little, so rounds are longer and
+// the ring deeper: 16 MiB x 4 slots (n=2: 6.36 -> 5.88 ms for 102 MB,
+// profiles/r01/r3k); 4 MiB x 2 slots otherwise (n=7: 8 MiB and K=3 no better, r3g).
+inline size_t default_slice_cap(int nranks) { return nranks <= 2 ? (16u << 20) : (4u << 20); }
+inline int default_slots(int nranks) { return nranks <= 2 ? 4 : 2; }
 constexpr size_t kSegmentBudget = 1ull << 30;   // default cap on data-slot bytes
 constexpr int kBatchMax = 128;                  // memops per cuStreamBatchMemOp call
 
@@ -442,7 +447,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (klen == 0 || klen > 100 || strchr(job_key, '/'))
     return fail(FMX_ERR_INVALID_ARG, "job_key must be 1..100 chars without '/'");
   if (nslots == 0) {
-    nslots = 2;
+    nslots = default_slots(nranks);
     if (const char* v = getenv("FMX_SLOTS")) nslots = atoi(v);
   }
   if (nslots < 2 || nslots > FMX_MAX_SLOTS)
@@ -467,7 +472,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
     size_t sb = slice_bytes;
     if (sb == 0) {
       size_t per = (size_t)c->nslots * ((size_t)nranks * nranks + 2 * nranks);
-      sb = std::min(kDefaultSliceCap, kSegmentBudget / per);
+      sb = std::min(default_slice_cap(nranks), kSegmentBudget / per);
     }
     sb = std::max<size_t>(4096, sb / 4096 * 4096);
     Layout L = compute_layout(nranks, c->nslots, sb, host_bytes);
