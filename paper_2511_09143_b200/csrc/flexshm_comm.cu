@@ -159,11 +159,21 @@ class CudaSink final : public Sink {
       }
       return FMX_OK;
     }
+    return launch_copy(lane, segs, src_sys, nullptr, 0);
+  }
+
+  // zero-copy copy kernel(s); with `flag` (a single launch) the kernel releases it
+  int launch_copy(int lane, const std::vector<PlanSeg>& segs, bool src_sys, uint32_t* flag,
+                  uint32_t v) {
+    cudaStream_t s = lane_stream(c_, lane);
     for (size_t i0 = 0; i0 < segs.size(); i0 += kMaxSegs) {
       CopyArgs a;
       memset(&a, 0, sizeof a);
       a.nseg = (int)std::min<size_t>(kMaxSegs, segs.size() - i0);
       a.src_sys = src_sys ? 1 : 0;
+      a.flag = flag;
+      a.flag_value = v;
+      a.ctas_done = c_->ctas_done;
       size_t maxb = 0;
       for (int k = 0; k < a.nseg; ++k) {
         a.seg[k] = CopySeg{segs[i0 + k].src, segs[i0 + k].dst, segs[i0 + k].bytes};
@@ -288,6 +298,17 @@ class CudaSink final : public Sink {
     }
     return stamp(lane, kStCopy, (uint32_t)std::min<size_t>(bytes, ~0u));
   }
+  int copy_signal(int lane, const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel,
+                  int flag, uint32_t v) override {
+    // zero-copy copy kernel that releases the flag itself (one launch, no memop)
+    if (!use_kernel || !c_->fuse_signal || !c_->ctas_done || segs.empty() ||
+        segs.size() > (size_t)kMaxSegs || c_->stamps)
+      return Sink::copy_signal(lane, segs, src_sys, use_kernel, flag, v);
+    const uint32_t* fl = (const uint32_t*)c_->flag_dev(c_->rank, flag);
+    int rc = launch_copy(lane, segs, src_sys, (uint32_t*)fl, v);
+    return rc;
+  }
+
   int reduce(int lane, const PlanReduce& r) override {
     int rc = reduce_impl(lane, r);
     return rc || r.args.len == 0 ? rc : stamp(lane, kStReduce, (uint32_t)r.args.len);
@@ -638,6 +659,8 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   }
   // HBM scratch: CE contributions [n] (device path) / [2][n] fetch + [2][n] result replicas (host path)
   if (e == cudaSuccess) e = cudaMalloc((void**)&c->scratch, 4 * (size_t)nranks * c->slice_bytes);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&c->ctas_done, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(c->ctas_done, 0, sizeof(unsigned int));
 
 
   if (const char* v = getenv("FMX_RESULT_VIA_CE")) c->result_via_ce = atoi(v) != 0;
@@ -649,12 +672,14 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (const char* v = getenv("FMX_RAMP")) c->ramp = atoi(v) != 0;
   if (const char* v = getenv("FMX_MIN_ROUNDS")) c->min_rounds = atoi(v);
   if (const char* v = getenv("FMX_COPY_FENCE")) c->copy_fence = atoi(v) != 0;
+  if (const char* v = getenv("FMX_FUSE_SIGNAL")) c->fuse_signal = atoi(v) != 0;
   if (e != cudaSuccess) {
     h->aborted.store(1);
     fail(FMX_ERR_CUDA, "device mapping of %zu-byte segment failed: %s", c->total_bytes,
          cudaGetErrorString(e));
     if (c->registered) cudaHostUnregister(c->base);
     if (c->scratch) cudaFree(c->scratch);
+    if (c->ctas_done) cudaFree(c->ctas_done);
     unmap(c);
     delete c;
     return FMX_ERR_CUDA;
@@ -908,6 +933,7 @@ int fmx_comm_destroy(fmx_comm_t c) {
   }
   if (c->scratch) cudaFree(c->scratch);
   if (c->stamps) cudaFree(c->stamps);
+  if (c->ctas_done) cudaFree(c->ctas_done);
   if (c->registered) cudaHostUnregister(c->base);
   if (c->hdr) c->hdr->departed.fetch_add(1);
   unmap(c);

@@ -34,8 +34,28 @@ struct CopySeg {
 struct CopyArgs {
   CopySeg seg[kMaxSegs];
   int nseg;
-  int src_sys;  // 1: sources live in mapped host memory -> ld.cv
+  int src_sys;           // 1: sources live in mapped host memory -> ld.cv
+  uint32_t* flag;        // non-null: the last CTA to finish releases *flag = flag_value
+  uint32_t flag_value;   //   (system scope, after every CTA's stores) - a fused signal
+  unsigned int* ctas_done;  // device counter for the last-CTA election (reset by the winner)
 };
+
+// Fused signal: every CTA fences its stores at system scope and counts itself
+// done; the last one resets the counter and releases the flag, so a peer
+// that sees the flag (stream wait on host memory) sees every byte copied.
+__device__ __forceinline__ void release_flag_when_grid_done(const CopyArgs& a) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned int total = gridDim.x * gridDim.y;
+    if (atomicAdd(a.ctas_done, 1u) == total - 1) {
+      *a.ctas_done = 0;
+      __threadfence_system();
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.flag), "r"(a.flag_value)
+                   : "memory");
+    }
+  }
+}
 
 
 __device__ __forceinline__ uint4 ld_cv_v4(const void* p) {
@@ -86,6 +106,7 @@ __global__ void __launch_bounds__(512) fmx_copy_kernel(const __grid_constant__ C
   } else {
     for (; i < s.bytes; i += stride) s.dst[i] = ((volatile const char*)s.src)[i];
   }
+  if (a.flag) release_flag_when_grid_done(a);
 }
 
 // ---------------------------------------------------------------- reduce

@@ -236,8 +236,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
                         Annot{(int64_t)off, len * g.esz, me, R}, true,
                         ubuf(g.lo(o, j) * g.esz, len * g.esz)});
       }
-      if ((rc = k.copy(kLaneStage, segs, false, zc))) return rc;
-      return k.signal(kLaneStage, kStaged, R + 1);
+      return k.copy_signal(kLaneStage, segs, false, zc, kStaged, R + 1);
     }
     for (int i = 0; i < n - 1; ++i) {
       const int o = rot(i);

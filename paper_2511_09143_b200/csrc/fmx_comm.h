@@ -38,6 +38,9 @@ struct fmx_comm {
   cudaStream_t completion = nullptr;   // stream the last collective completed on
   cudaStream_t last_main = nullptr;    // lane-1 stream of the last collective
   bool copy_fence = true;              // no-op kernel after every copy-engine batch (CudaSink::copy)
+  bool fuse_signal = true;             // FMX_FUSE_SIGNAL=0: zero-copy stage + STAGED as two ops
+  unsigned int* ctas_done = nullptr;   // device counter of the fused signal (per comm; lanes
+                                       //   never run two fused copies at once: lane 0 only)
   int last_class = -1;              // 0 device-buffer collective, 1 host path / broadcast
   CUcontext lane_ctx = nullptr;                // context the lane objects were created in
   cudaEvent_t ev[fmx::kNumEvents] = {};  // intra-rank lane sync (see the kEv* ids)
@@ -163,6 +166,12 @@ struct Sink {
   virtual int copy(int lane, const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel) = 0;
   virtual int reduce(int lane, const PlanReduce& r) = 0;
   virtual int signal(int lane, int flag, uint32_t v) = 0;
+  // copy, then signal `flag` = v on the same lane (a sink may fuse the two)
+  virtual int copy_signal(int lane, const std::vector<PlanSeg>& segs, bool src_sys,
+                          bool use_kernel, int flag, uint32_t v) {
+    int rc = copy(lane, segs, src_sys, use_kernel);
+    return rc ? rc : signal(lane, flag, v);
+  }
   virtual int signal2(int lane, int f0, uint32_t v0, int f1, uint32_t v1) = 0;
   virtual int wait_peers(int lane, int flag, uint32_t v, int skip) = 0;
   virtual int wait_rank(int lane, int q, int flag, uint32_t v) = 0;
