@@ -133,6 +133,11 @@ def bind(gpu_id: int, instance_id: int, profile: str = "1g.5gb", mode: str = "gr
     inst.gpu_uuid = str(props.uuid)
     inst.bus_id = canonical_bus_id(
         f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0")
+    if os.environ.get("FMX_FAKE_BUS"):
+        # test only: several logical GPUs on one physical device get distinct bus
+        # ids (F0:00.0, F1:00.0, ...), so communicators wider than the
+        # reference's 10-ranks-per-bus rule (commsim.py:109-111) run on one B200
+        inst.bus_id = f"{0xF0 + gpu_id:02X}:00:00.0"
     if pin_cpus:
         cpus = gpu_cpus(f"{props.pci_domain_id:08X}:{props.pci_bus_id:02X}:"
                         f"{props.pci_device_id:02X}.0")

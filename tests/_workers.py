@@ -223,8 +223,10 @@ def stress_worker(rank: int, job_key: str, n: int, seed: int, nops: int, mode: s
     from paper_2511_09143_b200 import instance as inst_mod
     from paper_2511_09143_b200.comm import init_process_group
 
-    inst = inst_mod.bind(0, rank + 1, mode=mode)
-    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n, timeout_s=120)
+    # the launcher names this rank's instance (fm_select order over the GPUs)
+    inst = inst_mod.bind(int(os.environ.get("FMX_GPU_ID", "0")),
+                         int(os.environ.get("FMX_INSTANCE_ID", str(rank + 1))), mode=mode)
+    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n, timeout_s=300)
     s = inst.stream
     side = torch.cuda.Stream()
     digests = []

@@ -50,3 +50,26 @@ def test_random_collective_program_is_bit_exact(n, mode, seed):
         for r in range(n):
             want = expected_digest(o, n, r)
             assert res[r]["digests"][i] == want, (i, o, r)
+
+
+@pytest.mark.parametrize("n,gpus", [(14, 2), (28, 4)])
+def test_wide_communicators_on_logical_gpus(monkeypatch, n, gpus):
+    """The 2- and 4-GPU world sizes (14 and 28 ranks, fm_select round-robin
+    order over the GPUs) run on one B200: every logical GPU's seven instances
+    are MPS clients of the physical device, with distinct synthetic bus ids
+    (FMX_FAKE_BUS).  The random program must stay bit-exact."""
+    from paper_2511_09143_b200.launcher import launch, new_job_key
+    from paper_2511_09143_b200.scheduler import fm_select, make_cluster
+    from paper_2511_09143_b200.workload import Job
+
+    monkeypatch.setenv("FMX_FAKE_BUS", "1")
+    nops, seed = 16, 3 + n
+    d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", gpus))
+    assert len({g for g, _ in d.instances}) == gpus
+    key = new_job_key("wide")
+    res = launch(_workers.stress_worker, d, args=(key, n, seed, nops, "mps"), job_key=key,
+                 timeout_s=900, mode="mps", gpu_map={g: "0" for g in range(gpus)})
+    ops = _workers.stress_ops(n, seed, nops)
+    for i, o in enumerate(ops):
+        for r in range(n):
+            assert res[r]["digests"][i] == expected_digest(o, n, r), (i, o, r)
