@@ -669,7 +669,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   c->coarse_gather = c->coarse;
   if (const char* v = getenv("FMX_GATHER_GRAIN")) c->coarse_gather = strcmp(v, "fine") != 0;
   if (const char* v = getenv("FMX_LANES")) c->nlanes = std::min(3, std::max(1, atoi(v)));
-  if (const char* v = getenv("FMX_RAMP")) c->ramp = atoi(v) != 0;
+  if (const char* v = getenv("FMX_RAMP")) c->ramp = atoi(v);
   if (const char* v = getenv("FMX_MIN_ROUNDS")) c->min_rounds = atoi(v);
   if (const char* v = getenv("FMX_COPY_FENCE")) c->copy_fence = atoi(v) != 0;
   if (const char* v = getenv("FMX_FUSE_SIGNAL")) c->fuse_signal = atoi(v) != 0;

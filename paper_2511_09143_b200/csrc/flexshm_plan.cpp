@@ -136,14 +136,15 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t c
       up.push_back(x);
       ramp_sum += x;
     }
-    const size_t mid = g.chunk - 2 * ramp_sum;
+    const bool down = c->ramp != 2;  // FMX_RAMP=2: ramp up only (fill), no drain ramp
+    const size_t mid = g.chunk - (down ? 2 : 1) * ramp_sum;
     const size_t k = (mid + s - 1) / s;
     sizes = up;
     for (size_t i = 0; i < k; ++i) {  // equal split, multiples of the vector width
       const size_t lo = (mid * i / k) / vec * vec, hi = i + 1 == k ? mid : (mid * (i + 1) / k) / vec * vec;
       if (hi > lo) sizes.push_back(hi - lo);
     }
-    sizes.insert(sizes.end(), up.rbegin(), up.rend());
+    if (down) sizes.insert(sizes.end(), up.rbegin(), up.rend());
   } else {
     for (size_t left = g.chunk; left;) {
       const size_t y = std::min(s, left);
@@ -558,7 +559,7 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   if (const char* v = getenv("FMX_GRAIN")) c.coarse = strcmp(v, "fine") != 0;
   c.coarse_gather = c.coarse;
   if (const char* v = getenv("FMX_GATHER_GRAIN")) c.coarse_gather = strcmp(v, "fine") != 0;
-  if (const char* v = getenv("FMX_RAMP")) c.ramp = atoi(v) != 0;
+  if (const char* v = getenv("FMX_RAMP")) c.ramp = atoi(v);
   if (const char* v = getenv("FMX_MIN_ROUNDS")) c.min_rounds = atoi(v);
   if (const char* v = getenv("FMX_LANES")) c.nlanes = std::min(3, std::max(1, atoi(v)));
   std::string out;

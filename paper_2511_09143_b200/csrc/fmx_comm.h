@@ -49,7 +49,7 @@ struct fmx_comm {
   bool copy2d = true;          // coalesce regular copy runs into cudaMemcpy2DAsync
   bool coarse = true;          // FMX_GRAIN=fine: per-piece waits instead of all-peer
   bool coarse_gather = true;   // FMX_GATHER_GRAIN=fine: per-owner gather waits only
-  bool ramp = false;           // FMX_RAMP=1: geometric s/8, s/4, s/2 fill / drain rounds (off:
+  int ramp = 0;                // FMX_RAMP=1: geometric s/8, s/4, s/2 fill / drain rounds; 2: fill only (off:
                                // with the copy fence, equal rounds are 3-4% faster, r01/r3e)
   int min_rounds = 1;          // FMX_MIN_ROUNDS: shrink the slice so a chunk spans >= this many
   size_t zc_max = 2u << 20;    // FMX_ZC_MAX: AUTO transport moves messages <= this with SM copies

@@ -1,0 +1,9 @@
+#!/bin/bash
+# Fill-only ramp (FMX_RAMP=2) vs equal rounds, same lease, x3.
+OUT=gpurun_out/r3p; mkdir -p $OUT
+run() { tag=$1; shift; env $ENVS timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-train "$@" --out $OUT/bench_$tag.json > $OUT/bench_$tag.log 2>&1; echo "bench $tag rc=$?" >> $OUT/log.txt; }
+for rep in 1 2 3; do
+ENVS= run eq$rep
+ENVS=FMX_RAMP=2 run up$rep
+ENVS=FMX_RAMP=1 run updown$rep
+done
