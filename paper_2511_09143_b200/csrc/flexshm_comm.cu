@@ -13,7 +13,7 @@
 //  * Allreduce = reduce-scatter + all-gather through the segment.  Rank r owns
 //    chunk r of the flat buffer (16-byte aligned chunk boundaries).  Each
 //    chunk is pipelined in rounds of `slice` elements; round R uses slot
-//    R % 2 of every region (double buffering).  Per round a rank (1) stages
+//    R % K of every region (K = 2 by default).  Per round a rank (1) stages
 //    its pieces of the other owners' chunks into in-slot[owner][r], (2) after
 //    every peer signalled STAGED, reduces its own chunk in ascending rank
 //    order (own contribution read from HBM at its own rank position) into
@@ -24,8 +24,11 @@
 //    (system-scope fence before the write) and waited on with stream
 //    memory-op waits.  No SM ever spins: a wait parks the stream in the GPU
 //    front end, which matters because rank processes sharing one GPU without
-//    MPS are time-sliced.  Slot reuse needs no credit messages: the waits of
-//    round R already imply every peer finished round R-1.
+//    MPS are time-sliced.  Slot reuse needs no credit messages: events on the
+//    lanes carry "every peer is past round R-K".
+//  * The schedule itself (plans, trace for the model checker) lives in
+//    flexshm_plan.cpp; this file holds the CUDA half: CudaSink, the lanes,
+//    the segment, and the C API.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <errno.h>

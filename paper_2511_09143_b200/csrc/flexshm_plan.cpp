@@ -100,10 +100,11 @@ class TraceSink final : public Sink {
   int seq_[kNumEvents] = {};
 };
 
-// Round j of every chunk covers [prefix(j), prefix(j) + size(j)).  With the
-// ramp, the first rounds are slice/8, /4, /2 and the last ones /2, /4, /8: the
-// pipeline fills (round 0's stage is pure D2H, the H2D direction idle) and
-// drains (the last gather is pure H2D) in 1/8 of the time a full slice takes.
+// Round j of every chunk covers [prefix(j), prefix(j) + size(j)).  By default
+// the rounds are equal (at most one slice each).  FMX_RAMP=1 makes the first
+// rounds slice/8, /4, /2 and the last ones /2, /4, /8 (the pipeline fills and
+// drains in 1/8 of a full round), FMX_RAMP=2 ramps up only; both measured
+// slower once the copy fence was in.
 // chunk_elems = 0: allreduce chunking (16-byte aligned chunk starts over
 // `count`); otherwise every rank's chunk has exactly chunk_elems elements and
 // count = n * chunk_elems (reduce-scatter / all-gather, NCCL's layout).
@@ -162,9 +163,9 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t c
 
 // Reduce-scatter + all-gather through the segment, pipelined in rounds on three
 // lanes: lane 0 stages (D2H), lane 1 fetches and reduces (H2D + kernel), lane 2
-// gathers (H2D).  Round R uses slot R % 2.  With the gather on its own lane, a
-// rank fetches round R+1 while it still waits for the slowest owner of round R,
-// so the H2D direction never idles at a round boundary.
+// gathers (H2D).  Round R uses slot R % K (K = nslots, 2 by default; the
+// comments below write K = 2).  With the gather on its own lane, a rank fetches
+// round R+1 while it still waits for the slowest owner of round R.
 //
 // Enqueue order is itself a valid single-stream schedule: every wait (flag or
 // event) points at work enqueued earlier, by this rank or by peers that enqueue

@@ -117,10 +117,11 @@ inline cudaStream_t lane_stream(const fmx_comm* c, int lane) {
 // ---- the plan: what one rank enqueues for one collective -----------------------
 //
 // plan_allreduce / plan_broadcast describe the schedule once, against a Sink.
-// Work is issued on two lanes (CUDA streams) per rank so the two link
-// directions overlap inside a rank: lane 0 stages (HBM -> SHM, D2H), lane 1
-// fetches, reduces and gathers (SHM -> HBM, H2D).  Lanes fork from / join
-// back into the caller's stream at every collective.  CudaSink turns the
+// Work is issued on three lanes per rank so the link directions overlap inside
+// a rank: lane 0 stages (HBM -> SHM, D2H), lane 1 fetches and reduces
+// (SHM -> HBM, H2D; the caller's or the join stream), lane 2 gathers (H2D).
+// Lanes fork from / join back into the main stream at every collective
+// (on_lanes, flexshm_comm.cu).  CudaSink turns the
 // plan into stream operations; TraceSink records, per lane, every SHM and
 // user-buffer byte range touched and every flag signalled / waited on, so the
 // schedule of every rank of any world size can be model-checked on a CPU
