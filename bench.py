@@ -93,6 +93,8 @@ def parse_args(argv=None):
     p.add_argument("--train-no-sync", action="store_true",
                    help="--train-only: also time the step without gradient sync (compute bound)")
     p.add_argument("--bucket-mb", type=float, default=8.0, help="DDP bucket_cap_mb of the DP legs")
+    p.add_argument("--compress", choices=["bf16"], default=None,
+                   help="DP legs: exchange fp32 gradients in bf16 (flexshm_bf16_hook)")
     p.add_argument("--batch", type=int, default=32)
     p.add_argument("--train-steps", type=int, default=10)
     p.add_argument("--train-warmup", type=int, default=5)
@@ -573,7 +575,8 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
             x = torch.randn(cfg["batch"], 3, 224, 224, generator=g).cuda(gpu_local)
             x = x.to(memory_format=torch.channels_last)
             y = torch.randint(0, 1000, (cfg["batch"],), generator=g).cuda(gpu_local)
-        net = fddp.wrap(model, comm, control_group=pg, bucket_cap_mb=cfg.get("bucket_mb", 25.0))
+        net = fddp.wrap(model, comm, control_group=pg, bucket_cap_mb=cfg.get("bucket_mb", 25.0),
+                        compress=cfg.get("compress"))
         if name == "bert":
             opt = torch.optim.AdamW(net.parameters(), lr=2e-5)
         else:
@@ -688,7 +691,8 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
     cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
            "batch": args.batch, "train_steps": args.train_steps, "train_warmup": args.train_warmup,
            "port": 29000 + os.getpid() % 1000, "model": model, "no_sync": no_sync,
-           "bucket_mb": args.bucket_mb, "stamps": bool(args.stamps) and not no_sync}
+           "bucket_mb": args.bucket_mb, "stamps": bool(args.stamps) and not no_sync,
+           "compress": args.compress}
     res = run_ranks(train_body, _spawned_train, list(range(n)), job_key + "-t", n, cfg,
                     args.train_mode, 0)
     t = max(r["ms_total"] for r in res.values()) / 1e3
@@ -701,7 +705,10 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
     return {unit: n * args.batch * args.train_steps / t, "instances": n, "batch_per_instance":
             args.batch, "ms_per_step": t * 1e3 / args.train_steps, "steps": args.train_steps,
             "warmup": args.train_warmup, "instance_mode": args.train_mode,
-            "precision": precision, "replicas_agree": len(digests) == 1, "loss": res[0]["loss"],
+            "precision": (precision.replace("(fp32 SHM allreduce)",
+                                            "(bf16 SHM allreduce of the fp32 buckets)")
+                          if args.compress else precision),
+            "replicas_agree": len(digests) == 1, "loss": res[0]["loss"],
             "gpu_launches": sum(r["launches"] for r in res.values()), "model": desc}
 
 

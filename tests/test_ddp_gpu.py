@@ -37,3 +37,27 @@ def test_ddp_hook_matches_oracle(n, overlap, mode, dtype):
     bits = (lambda a: a.view(np.uint32)) if dtype == "f32" else (lambda a: a)
     for rank, r in enumerate(res):
         assert np.array_equal(bits(r["synced"]), bits(want)), rank
+
+
+def test_ddp_bf16_compressed_exchange_matches_oracle():
+    """flexshm_bf16_hook: fp32 buckets rounded to bf16, averaged over SHM with
+    the bf16 contract, widened back - bit-exact against the oracle applied to
+    the bf16-rounded local gradients."""
+    import torch
+
+    from paper_2511_09143_b200.launcher import launch, new_job_key
+    from paper_2511_09143_b200.scheduler import fm_select, make_cluster
+    from paper_2511_09143_b200.workload import Job
+
+    n = 3
+    d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
+    key = new_job_key("ddpc")
+    port = 21000 + os.getpid() % 20000
+    res = launch(_workers.ddp_worker, d, args=(key, n, port, "green", True, "f32", "bf16"),
+                 job_key=key, timeout_s=300)
+    locals_bf16 = [torch.from_numpy(r["local"]).to(torch.bfloat16).view(torch.int16).numpy()
+                   .view(np.uint16) for r in res]
+    want = orc.allreduce_c(locals_bf16, orc.BF16, orc.OP_PREDIV_SUM, float(n))
+    want_f32 = orc.bf16_to_f32(want)
+    for rank, r in enumerate(res):
+        assert np.array_equal(r["synced"].view(np.uint32), want_f32.view(np.uint32)), rank
