@@ -849,6 +849,12 @@ def run_ours(args) -> dict | None:
                               "timed region",
                        "h2d_bytes_per_step": n * s_bytes, "d2h_bytes_per_step": n * s_bytes,
                        "ranks_agree": len(digests) == 1}
+        # host path roofline: k*S each way per GPU, T* = max(one-way, bidirectional)
+        k_max = max(per_gpu)
+        t_star = max(k_max * s_bytes / (peaks["h2d"] * 1e9), k_max * s_bytes / (peaks["d2h"] * 1e9),
+                     2 * k_max * s_bytes / (peaks["bidir"] * 1e9))
+        line["e2e"]["step_roofline"] = {"bound": "host_link", "t_star_ms": t_star * 1e3,
+                                        "frac": t_star / t_e2e}
         line["e2e_device_buffers"] = {
             "value": n * s_bytes / t_dev / 1e9, "unit": line["unit"], "ms_per_step": t_dev * 1e3,
             "api": "pinned host -> device copy, ShmCommunicator.allreduce, device -> pinned host",

@@ -132,12 +132,15 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t c
     std::vector<size_t> up;
     size_t ramp_sum = 0;
     // ramp pieces are whole vectors so every piece start stays 16-byte aligned
-    for (size_t x = s / 8 / vec * vec; x < s && x > 0; x = x * 2 / vec * vec) {
+    // FMX_RAMP=3: one quarter-slice first round only (a short pipeline fill)
+    const size_t x0 = c->ramp == 3 ? s / 4 / vec * vec : s / 8 / vec * vec;
+    for (size_t x = x0; x < s && x > 0; x = x * 2 / vec * vec) {
       if (2 * (ramp_sum + x) > g.chunk) break;
       up.push_back(x);
       ramp_sum += x;
+      if (c->ramp == 3) break;
     }
-    const bool down = c->ramp != 2;  // FMX_RAMP=2: ramp up only (fill), no drain ramp
+    const bool down = c->ramp == 1;  // FMX_RAMP=2/3: fill only, no drain ramp
     const size_t mid = g.chunk - (down ? 2 : 1) * ramp_sum;
     const size_t k = (mid + s - 1) / s;
     sizes = up;
