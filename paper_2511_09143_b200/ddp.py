@@ -17,7 +17,9 @@ PAPER.md:264-271), so here:
   ascending-rank fp32 summation;
 * `ZeroShardBroadcast` re-broadcasts each owner's updated parameter shard
   after a sharded optimizer step (the ZeroRedundancyOptimizer pattern,
-  torch/distributed/optim/zero_redundancy_optimizer.py:785-801).
+  torch/distributed/optim/zero_redundancy_optimizer.py:785-801);
+  `ZeroShardAllgather` keeps the parameters in one flat buffer of equal
+  blocks and re-assembles it with a single in-place all-gather.
 """
 
 import torch
@@ -194,3 +196,41 @@ class ZeroShardBroadcast:
                 k = p.numel()
                 p.data.copy_(flat[off:off + k].view_as(p))
                 off += k
+
+
+class ZeroShardAllgather:
+    """ZeRO-style flat parameter shards re-assembled with ONE all-gather.
+
+    The parameters (one dtype) are moved into a flat buffer padded to
+    size * c elements and become views of it; rank r owns elements
+    [r*c, (r+1)*c) - its optimizer updates only `shard()` - and `sync()`
+    all-gathers every owner's block in place (NCCL in-place layout:
+    send = recv + rank*c).  One collective per step instead of one broadcast
+    per owner, and every byte crosses the host link once per reader."""
+
+    def __init__(self, params: list[torch.nn.Parameter], comm: ShmCommunicator):
+        self.comm = comm
+        self.params = list(params)
+        dtypes = {p.dtype for p in self.params}
+        if len(dtypes) != 1:
+            raise TypeError("ZeroShardAllgather needs parameters of one dtype")
+        total = sum(p.numel() for p in self.params)
+        n = comm.size
+        self.block = (total + n - 1) // n
+        dev = self.params[0].device
+        self.flat = torch.zeros(n * self.block, dtype=self.params[0].dtype, device=dev)
+        off = 0
+        with torch.no_grad():
+            for p in self.params:
+                k = p.numel()
+                self.flat[off:off + k].copy_(p.data.reshape(-1))
+                p.data = self.flat[off:off + k].view_as(p)
+                off += k
+
+    def shard(self, rank: int | None = None) -> torch.Tensor:
+        r = self.comm.rank if rank is None else rank
+        return self.flat[r * self.block:(r + 1) * self.block]
+
+    @torch.no_grad()
+    def sync(self, stream=None) -> None:
+        self.comm.allgather(self.shard(), self.flat, stream=stream)

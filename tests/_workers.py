@@ -272,3 +272,42 @@ def stress_worker(rank: int, job_key: str, n: int, seed: int, nops: int, mode: s
     comm.barrier(120)
     comm.destroy()
     return {"digests": digests}
+
+
+def zero_worker(rank: int, job_key: str, n: int, mode: str = "green"):
+    """Both ZeRO shard-sync flavours: every rank writes only what it owns, then
+    syncs; returns the parameters every rank ends up with."""
+    import torch
+
+    from paper_2511_09143_b200 import ddp as fddp
+    from paper_2511_09143_b200 import instance as inst_mod
+    from paper_2511_09143_b200.comm import init_process_group
+
+    inst = inst_mod.bind(0, rank + 1, mode=mode)
+    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n, timeout_s=120)
+    s = inst.stream
+    out = {}
+    with torch.cuda.stream(s):
+        torch.manual_seed(0)
+        shapes = [(300, 7), (11,), (64, 64), (5, 3, 3), (1000,)]
+        # broadcast flavour: parameter-granular owners
+        ps = [torch.nn.Parameter(torch.zeros(sh, device="cuda")) for sh in shapes]
+        zb = fddp.ZeroShardBroadcast(ps, comm)
+        for p, o in zip(ps, zb.owner):
+            if o == rank:
+                p.data.fill_(o + 1.0)
+        zb.sync()
+        out["bcast"] = torch.cat([p.detach().reshape(-1) for p in ps]).cpu().numpy()
+        out["owner"] = list(zb.owner)
+        # all-gather flavour: flat element blocks
+        qs = [torch.nn.Parameter(torch.zeros(sh, device="cuda")) for sh in shapes]
+        za = fddp.ZeroShardAllgather(qs, comm)
+        za.shard().fill_(rank + 1.0)
+        za.sync(stream=s)
+        out["flat"] = za.flat.cpu().numpy()
+        out["params"] = torch.cat([q.detach().reshape(-1) for q in qs]).cpu().numpy()
+        out["block"] = za.block
+    s.synchronize()
+    comm.barrier(60)
+    comm.destroy()
+    return out

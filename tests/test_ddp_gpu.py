@@ -61,3 +61,25 @@ def test_ddp_bf16_compressed_exchange_matches_oracle():
     want_f32 = orc.bf16_to_f32(want)
     for rank, r in enumerate(res):
         assert np.array_equal(r["synced"].view(np.uint32), want_f32.view(np.uint32)), rank
+
+
+@pytest.mark.parametrize("n", [2, 5])
+def test_zero_shard_sync_broadcast_and_allgather(n):
+    """ZeRO parameter re-sync: after each rank writes only the
+    shard it owns, both flavours leave every rank with every owner's values."""
+    from paper_2511_09143_b200.launcher import launch, new_job_key
+    from paper_2511_09143_b200.scheduler import fm_select, make_cluster
+    from paper_2511_09143_b200.workload import Job
+
+    d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
+    key = new_job_key("zero")
+    res = launch(_workers.zero_worker, d, args=(key, n), job_key=key, timeout_s=300)
+    sizes = [300 * 7, 11, 64 * 64, 5 * 3 * 3, 1000]
+    want_b = np.concatenate([np.full(k, o + 1.0, np.float32)
+                             for k, o in zip(sizes, res[0]["owner"])])
+    c = res[0]["block"]
+    want_flat = np.concatenate([np.full(c, q + 1.0, np.float32) for q in range(n)])
+    for r, out in enumerate(res):
+        assert np.array_equal(out["bcast"], want_b), r
+        assert np.array_equal(out["flat"], want_flat), r
+        assert np.array_equal(out["params"], want_flat[:sum(sizes)]), r
