@@ -671,7 +671,10 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
 
   if (const char* v = getenv("FMX_RESULT_VIA_CE")) c->result_via_ce = atoi(v) != 0;
   if (const char* v = getenv("FMX_COPY2D")) c->copy2d = atoi(v) != 0;
-  if (const char* v = getenv("FMX_GRAIN")) c->coarse = strcmp(v, "fine") != 0;
+  if (const char* v = getenv("FMX_GRAIN")) {
+    c->coarse = strcmp(v, "fine") != 0;
+    c->fine_first = strcmp(v, "first") == 0;
+  }
   c->coarse_gather = c->coarse;
   if (const char* v = getenv("FMX_GATHER_GRAIN")) c->coarse_gather = strcmp(v, "fine") != 0;
   if (const char* v = getenv("FMX_LANES")) c->nlanes = std::min(3, std::max(1, atoi(v)));

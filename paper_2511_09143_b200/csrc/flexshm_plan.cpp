@@ -225,13 +225,17 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
   // peers in rotated order starting after me, so that at any moment the
   // ranks work on different owners / contributors instead of all on one
   auto rot = [&](int i) { return (me + 1 + i) % n; };
+  // per-contributor STAGED_TO flags for this round?  FMX_GRAIN=fine: every
+  // round; FMX_GRAIN=first: the first round only, so owners start fetching as
+  // soon as their first contributors staged (a shorter pipeline fill)
+  auto coarse_round = [&](uint32_t j) { return c->coarse && !(c->fine_first && j == 0); };
 
   auto stage = [&](uint32_t j) -> int {
     const uint32_t R = R0 + j;
     if (ag) return FMX_OK;  // nothing to reduce: no contributions to stage
     // slot R%K was read by round R-K's fetches: W(R-K)
     if (R >= (uint32_t)K && (rc = k.wait_event(kLaneStage, kEvSlotFree + R % K))) return rc;
-    if (c->coarse) {  // one batch of copies, one STAGED signal
+    if (coarse_round(j)) {  // one batch of copies, one STAGED signal
       segs.clear();
       for (int o = 0; o < n; ++o) {
         const size_t len = o == me ? 0 : g.len(o, j);
@@ -302,7 +306,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
         pr.write = Annot{(int64_t)out_off, mylen * g.esz, me, R};
       }
       // each contribution is fetched as soon as its contributor staged it
-      if (c->coarse) {
+      if (coarse_round(j)) {
         if ((rc = k.wait_peers(kLaneMain, kStaged, R + 1, me))) return rc;
         if (!zc) {
           segs.clear();
@@ -316,7 +320,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
           if ((rc = k.copy(kLaneMain, segs, true, false))) return rc;
         }
       }
-      for (int i = 0; i < n - 1 && !c->coarse; ++i) {
+      for (int i = 0; i < n - 1 && !coarse_round(j); ++i) {
         const int q = rot(i);
         if ((rc = k.wait_rank(kLaneMain, q, kStagedTo + me, R + 1))) return rc;
         if (!zc) {
@@ -560,7 +564,10 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   c.L = compute_layout(nranks, c.nslots, slice_bytes, max_bytes);
   c.total_bytes = c.L.total;
   if (const char* v = getenv("FMX_RESULT_VIA_CE")) c.result_via_ce = atoi(v) != 0;
-  if (const char* v = getenv("FMX_GRAIN")) c.coarse = strcmp(v, "fine") != 0;
+  if (const char* v = getenv("FMX_GRAIN")) {
+    c.coarse = strcmp(v, "fine") != 0;
+    c.fine_first = strcmp(v, "first") == 0;
+  }
   c.coarse_gather = c.coarse;
   if (const char* v = getenv("FMX_GATHER_GRAIN")) c.coarse_gather = strcmp(v, "fine") != 0;
   if (const char* v = getenv("FMX_RAMP")) c.ramp = atoi(v);

@@ -48,6 +48,7 @@ struct fmx_comm {
   bool result_via_ce = false;  // CE transport: result slot by copy engine, not SM stores
   bool copy2d = true;          // coalesce regular copy runs into cudaMemcpy2DAsync
   bool coarse = true;          // FMX_GRAIN=fine: per-piece waits instead of all-peer
+  bool fine_first = false;     // FMX_GRAIN=first: per-contributor flags in round 0 only
   bool coarse_gather = true;   // FMX_GATHER_GRAIN=fine: per-owner gather waits only
   int ramp = 0;                // FMX_RAMP=1: geometric s/8, s/4, s/2 fill / drain rounds; 2: fill only (off:
                                // with the copy fence, equal rounds are 3-4% faster, r01/r3e)

@@ -269,7 +269,8 @@ def test_model_catches_a_broken_schedule(flag):
     ("coarse", "coarse", "1", "2", "2"), ("coarse", "fine", "1", "1", "2"),
     ("coarse", "coarse", "1", "3", "3"), ("fine", "fine", "1", "3", "4"),
     ("coarse", "coarse", "2", "3", "2"), ("coarse", "fine", "2", "2", "3"),
-    ("coarse", "coarse", "3", "3", "2"),
+    ("coarse", "coarse", "3", "3", "2"), ("first", "coarse", "0", "3", "2"),
+    ("first", "fine", "0", "2", "3"), ("first", "coarse", "1", "1", "2"),
     ("coarse", "coarse", "0", "2", "3"), ("coarse", "fine", "1", "3", "4")])
 def test_schedule_variants(monkeypatch, n, grain, gather, ramp, lanes, slots):
     monkeypatch.setenv("FMX_GRAIN", grain)
