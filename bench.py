@@ -576,7 +576,8 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
             x = x.to(memory_format=torch.channels_last)
             y = torch.randint(0, 1000, (cfg["batch"],), generator=g).cuda(gpu_local)
         net = fddp.wrap(model, comm, control_group=pg, bucket_cap_mb=cfg.get("bucket_mb", 25.0),
-                        compress=cfg.get("compress"))
+                        compress=cfg.get("compress"),
+                        threaded=bool(os.environ.get("FMX_HOOK_THREAD")))
         if name == "bert":
             opt = torch.optim.AdamW(net.parameters(), lr=2e-5)
         else:

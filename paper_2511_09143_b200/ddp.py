@@ -33,7 +33,7 @@ class HookState:
     context's stream in green mode), so bucket allreduces overlap the rest of
     the backward pass instead of queueing on the autograd stream."""
 
-    def __init__(self, comm: ShmCommunicator, stream=None):
+    def __init__(self, comm: ShmCommunicator, stream=None, threaded: bool = False):
         self.comm = comm
         if stream is None:
             inst = getattr(comm, "instance", None)
@@ -47,6 +47,42 @@ class HookState:
                 # so they must not queue behind the backward pass's kernels
                 stream = torch.cuda.Stream(priority=-1)
         self.stream = stream
+        self.threaded = threaded
+        self._queue = None
+        if threaded:
+            import queue
+            import threading
+            self._queue = queue.SimpleQueue()
+            self._device = torch.cuda.current_device()
+            self._thread = threading.Thread(target=self._run, name="flexshm-hook", daemon=True)
+            self._thread.start()
+
+    def _run(self):
+        """Enqueue thread: issues every bucket's collective (the ~30 driver calls
+        of a round) off the autograd thread, in hook order - the same order on
+        every rank.  ctypes releases the GIL inside the library."""
+        torch.cuda.set_device(self._device)
+        while True:
+            item = self._queue.get()
+            if item is None:
+                return
+            buf, ready, fut, op = item
+            try:
+                with torch.cuda.stream(self.stream):
+                    self.stream.wait_event(ready)          # the bucket's producers
+                    self.comm.set_join_stream(self.stream)
+                    try:
+                        self.comm.allreduce(buf, op=op, stream=self.stream)
+                    finally:
+                        self.comm.set_join_stream(None)
+                    fut.set_result(buf)                     # event on the side stream
+            except BaseException as exc:  # noqa: BLE001 - surface in DDP's wait
+                fut.set_exception(exc)
+
+    def close(self):
+        if self._queue is not None:
+            self._queue.put(None)
+            self._queue = None
 
 
 def flexshm_hook(state, bucket) -> torch.futures.Future[torch.Tensor]:
@@ -67,6 +103,15 @@ def flexshm_hook(state, bucket) -> torch.futures.Future[torch.Tensor]:
         fut.set_result(buf)
         return fut
     cur = torch.cuda.current_stream(buf.device)
+    if state.threaded:
+        # hand the bucket to the enqueue thread: the autograd thread only records
+        # an event and returns
+        ready = torch.cuda.Event()
+        ready.record(cur)
+        buf.record_stream(state.stream)
+        fut = torch.futures.Future(devices=[buf.device])
+        state._queue.put((buf, ready, fut, "avg"))
+        return fut
     # fork from the autograd stream (the bucket's producers), complete on the
     # side stream: consecutive buckets overlap inside the library (join-stream
     # mode) and the autograd stream never waits for a collective
@@ -137,7 +182,7 @@ def broadcast_parameters(module: torch.nn.Module, comm: ShmCommunicator, root: i
 
 def wrap(module: torch.nn.Module, comm: ShmCommunicator, control_group=None,
          bucket_cap_mb: float = 8.0, overlap: bool = True, compress: str | None = None,
-         **ddp_kwargs):
+         threaded: bool = False, **ddp_kwargs):
     """DistributedDataParallel over `control_group` (gloo) with gradients on
     the SHM path.  Parameters are synchronised from rank 0 first.  With
     `overlap` the bucket allreduces run on a side stream (HookState);
@@ -156,7 +201,8 @@ def wrap(module: torch.nn.Module, comm: ShmCommunicator, control_group=None,
     if compress == "bf16":
         ddp.register_comm_hook(HookState(comm), flexshm_bf16_hook)
     elif compress is None:
-        ddp.register_comm_hook(HookState(comm) if overlap else comm, flexshm_hook)
+        ddp.register_comm_hook(HookState(comm, threaded=threaded) if overlap else comm,
+                               flexshm_hook)
     else:
         raise ValueError(f"unknown gradient compression {compress!r}")
     return ddp

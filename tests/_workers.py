@@ -113,7 +113,8 @@ def suite_worker(rank: int, job_key: str, n: int, transport: str, mode: str, sce
 
 
 def ddp_worker(rank: int, job_key: str, n: int, port: int, mode: str = "green",
-               overlap: bool = True, dtype: str = "f32", compress: str | None = None):
+               overlap: bool = True, dtype: str = "f32", compress: str | None = None,
+               threaded: bool = False):
     """Tiny model: local gradients without DDP, then the same step under DDP
     with the flexshm comm hook; returns both (flattened fp32)."""
     import torch
@@ -139,7 +140,7 @@ def ddp_worker(rank: int, job_key: str, n: int, port: int, mode: str = "green",
         x = torch.randn(32, 64, generator=g).cuda().to(next(model.parameters()).dtype)
         y = torch.randint(0, 10, (32,), generator=g).cuda()
         net = fddp.wrap(model, comm, control_group=dist.group.WORLD, bucket_cap_mb=0.05,
-                        overlap=overlap, compress=compress)
+                        overlap=overlap, compress=compress, threaded=threaded)
         params0 = torch.cat([p.detach().reshape(-1) for p in model.parameters()]).cpu()
         # local gradient (no communication): no_sync skips the reducer
         with net.no_sync():

@@ -83,3 +83,22 @@ def test_zero_shard_sync_broadcast_and_allgather(n):
         assert np.array_equal(out["bcast"], want_b), r
         assert np.array_equal(out["flat"], want_flat), r
         assert np.array_equal(out["params"], want_flat[:sum(sizes)]), r
+
+
+@pytest.mark.parametrize("mode", ["green", "mps"])
+def test_ddp_threaded_hook_matches_oracle(mode):
+    """The enqueue-thread variant of the hook (collectives issued off the
+    autograd thread) is bit-exact too."""
+    from paper_2511_09143_b200.launcher import launch, new_job_key
+    from paper_2511_09143_b200.scheduler import fm_select, make_cluster
+    from paper_2511_09143_b200.workload import Job
+
+    n = 3
+    d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
+    key = new_job_key("ddpt")
+    port = 22000 + os.getpid() % 20000
+    res = launch(_workers.ddp_worker, d, args=(key, n, port, mode, True, "f32", None, True),
+                 job_key=key, timeout_s=300, mode=mode)
+    want = orc.allreduce_c([r["local"] for r in res], orc.F32, orc.OP_PREDIV_SUM, float(n))
+    for rank, r in enumerate(res):
+        assert np.array_equal(r["synced"].view(np.uint32), want.view(np.uint32)), rank
