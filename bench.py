@@ -63,8 +63,6 @@ def parse_args(argv=None):
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
-    p.add_argument("--inproc", action="store_true",
-                   help="ranks as threads of one process (for ncu); not the headline layout")
     p.add_argument("--out", default=None, help="also write the JSON line here")
     p.add_argument("--no-train", action="store_true", help="skip the ResNet-50 DP img/s leg")
     p.add_argument("--timeline", default=None, help="write a host-polled flag timeline here")
@@ -754,19 +752,6 @@ def run_ours(args) -> dict | None:
                        "kernel_count": 0, "ms_total_e2e": 5.0 * (r + 1),
                        "ms_total_e2e_dev": 6.0 * (r + 1), "e2e_digest": 0, "job_key": job_key}
                    for r in mine}
-    elif args.inproc:
-        # all ranks of this GPU as threads (ncu-friendly); primary context
-        def th(r):
-            try:
-                results[r] = rank_body(r, job_key, n, cfg, "full", gpu_local)
-            except BaseException as exc:  # noqa: BLE001
-                errors.append((r, exc))
-        ts = [threading.Thread(target=th, args=(r,)) for r in mine]
-        sampler.start()
-        for t in ts:
-            t.start()
-        for t in ts:
-            t.join()
     else:
         try:
             results = run_ranks(rank_body, _spawned_rank, mine, job_key, n, cfg, inst_mode,
@@ -823,7 +808,7 @@ def run_ours(args) -> dict | None:
                                f"{args.dtype}) across {args.ranks_per_gpu} 1g instances per "
                                f"B200 x {gpus} (BASELINE configs[1] comm step)",
                    "ranks": n, "ranks_per_gpu": per_gpu, "bytes": s_bytes,
-                   "instance_mode": "threads" if args.inproc else inst_mode,
+                   "instance_mode": inst_mode,
                    "transport": args.transport, "l2": "inputs > L2 (7 x 102 MB per GPU)",
                    "slots": int(os.environ.get("FMX_SLOTS", "2")),
                    "lanes": int(os.environ.get("FMX_LANES", "3")),
