@@ -5,7 +5,11 @@ New Python surface (the reference has none; shaped like torch / NCCL):
     comm = init_process_group(decision, rank, job_key, instance=inst)
     comm.allreduce(flat_grad)                 # fixed rank-order fp32 sum
     comm.allreduce(flat_grad, op="avg")       # DDP's divide-then-sum
+    comm.reduce_scatter(full, block)          # NCCL layouts
+    comm.allgather(block, full)
     comm.broadcast(flat_params, root=0)
+    comm.allreduce_host(comm.host_buffer()[:nbytes].view(torch.float32))  # host-resident data
+    comm.set_join_stream(side)                # complete on `side`, not the calling stream
     comm.destroy()
 
 `decision` is the `AllocationDecision` from `fm_select`; its `instances`
