@@ -802,8 +802,9 @@ def run_ours(args) -> dict | None:
         "n_gpus": gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "float32" if args.dtype == "f32" else "bfloat16",
-        "data": "synthetic (seeded N(0,1)*1e-3 gradient per rank); op = DDP mean "
-                "(divide by world size, then rank-order fp32 sum)",
+        "data": "synthetic (seeded N(0,1)*1e-3 gradient per rank); op = DDP mean: each "
+                "contribution x fl32(1/n) (what the default hook's bucket.div_(n) computes "
+                "on CUDA), then the rank-order fp32 sum",
         "config": {"workload": f"ResNet-50-sized gradient allreduce ({args.count} "
                                f"{args.dtype}) across {args.ranks_per_gpu} 1g instances per "
                                f"B200 x {gpus} (BASELINE configs[1] comm step)",
@@ -895,13 +896,13 @@ def run_cpu_reference(count: int, n: int, dtype: str, steps: int, warmup: int,
     bufs = [orc.synthetic_gradient(r, count, dt) for r in range(n)]
     shm = orc.ShmAllreduce(n, count, dt, nthreads)
     for _ in range(warmup):
-        shm(bufs, orc.OP_PREDIV_SUM, float(n))
+        shm(bufs, *orc.ddp_mean(n))
     times = []
     t_end = time.perf_counter() + (seconds or 0)
     k = 0
     while k < steps or (seconds and time.perf_counter() < t_end):
         t0 = time.perf_counter()
-        shm(bufs, orc.OP_PREDIV_SUM, float(n))
+        shm(bufs, *orc.ddp_mean(n))
         times.append(time.perf_counter() - t0)
         k += 1
     t = sum(times) / len(times)

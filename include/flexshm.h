@@ -71,12 +71,22 @@ enum fmx_status {
 
 enum fmx_dtype { FMX_FLOAT32 = 0, FMX_BFLOAT16 = 1 };
 
-/* Scale conventions; the arithmetic is the fixed ascending-rank fp32 sum. */
+/* Scale conventions; the arithmetic is the fixed ascending-rank fp32 sum.
+ *
+ * DDP's mean is FMX_OP_PREMUL_SUM with factor = fl32(1/world): the default
+ * hook's `bucket.div_(world)` (torch/distributed/algorithms/ddp_comm_hooks/
+ * default_hooks.py:26) runs ATen's div_true_kernel_cuda, which for a CPU
+ * scalar divisor computes a * fl32(1/b) in fp32 (BinaryDivTrueKernel.cu),
+ * and the hook-less reducer multiplies by 1/div_factor; NCCL's equivalent is
+ * ncclRedOpCreatePreMulSum (nccl.h:314).  For bf16 each product is rounded
+ * to bf16 (the bucket is a bf16 tensor after the in-place scale).
+ * FMX_OP_PREDIV_SUM keeps IEEE true division as an explicit op. */
 enum fmx_op {
   FMX_OP_SUM = 0,           /* out = x0 + x1 + ... (left to right)            */
   FMX_OP_SUM_POSTSCALE = 1, /* out = (sum) * factor                           */
-  FMX_OP_PREDIV_SUM = 2     /* out = x0/factor + x1/factor + ... (DDP default  */
-                            /* hook: bucket.div_(world) then SUM)              */
+  FMX_OP_PREDIV_SUM = 2,    /* out = x0/factor + x1/factor + ... (true divide) */
+  FMX_OP_PREMUL_SUM = 3     /* out = x0*factor + x1*factor + ... (DDP mean     */
+                            /* with factor = fl32(1/world); ncclPreMulSum)     */
 };
 
 /* How host-link bytes move.  ZC: SM kernels store to / load from the mapped

@@ -16,16 +16,22 @@
  *
  * ranks in ascending order = the order of AllocationDecision.instances
  * produced by fm_select's round-robin (reference scheduler.py:117-136), with
- * three scale conventions:
+ * four scale conventions:
  *   FMX_OP_SUM           no scaling
  *   FMX_OP_SUM_POSTSCALE (sum) * factor, one fp32 multiply
- *   FMX_OP_PREDIV_SUM    each x_q / factor before the sum (the DDP default
- *                        hook divides the bucket by world size, then SUMs:
- *                        torch/distributed/algorithms/ddp_comm_hooks/
- *                        default_hooks.py:18-33)
+ *   FMX_OP_PREDIV_SUM    each x_q / factor (IEEE division) before the sum
+ *   FMX_OP_PREMUL_SUM    each x_q * factor before the sum.  DDP's mean is
+ *                        this op with factor = fl32(1/world): the default
+ *                        hook's bucket.div_(world) (torch/distributed/
+ *                        algorithms/ddp_comm_hooks/default_hooks.py:26) runs
+ *                        ATen's div_true_kernel_cuda, which for a CPU-scalar
+ *                        divisor multiplies by the fp32 reciprocal
+ *                        (aten/src/ATen/native/cuda/BinaryDivTrueKernel.cu);
+ *                        pinned on the B200 by tests/test_ddp_arith_gpu.py
  * bf16: inputs widened exactly to fp32, summed in the same order, rounded
- * once to bf16 (round-to-nearest-even).  For PREDIV the divided contribution
- * is itself rounded to bf16 first (a bf16 bucket divided in place).
+ * once to bf16 (round-to-nearest-even).  For PREDIV / PREMUL the scaled
+ * contribution is itself rounded to bf16 first (a bf16 bucket scaled in
+ * place).
  * Broadcast is an exact bit copy.
  *
  * Parity status: UNPINNED against the reference (no reference arithmetic
@@ -42,7 +48,7 @@
 #include <string.h>
 
 enum { ORC_F32 = 0, ORC_BF16 = 1 };
-enum { ORC_SUM = 0, ORC_SUM_POSTSCALE = 1, ORC_PREDIV_SUM = 2 };
+enum { ORC_SUM = 0, ORC_SUM_POSTSCALE = 1, ORC_PREDIV_SUM = 2, ORC_PREMUL_SUM = 3 };
 
 static inline float bf16_to_f32(uint16_t h) {
   uint32_t u = (uint32_t)h << 16;
@@ -65,10 +71,11 @@ uint16_t oracle_f32_to_bf16(float f) { return f32_to_bf16_rne(f); }
 static inline float contrib_f32(const void* x, int dtype, size_t i, int op, float factor) {
   if (dtype == ORC_F32) {
     float v = ((const float*)x)[i];
-    return op == ORC_PREDIV_SUM ? v / factor : v;
+    return op == ORC_PREDIV_SUM ? v / factor : op == ORC_PREMUL_SUM ? v * factor : v;
   }
   float v = bf16_to_f32(((const uint16_t*)x)[i]);
   if (op == ORC_PREDIV_SUM) v = bf16_to_f32(f32_to_bf16_rne(v / factor));
+  if (op == ORC_PREMUL_SUM) v = bf16_to_f32(f32_to_bf16_rne(v * factor));
   return v;
 }
 

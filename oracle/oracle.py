@@ -18,8 +18,12 @@ restatements are checked against each other and against torch's bf16 RNE
 
 Scale conventions (int codes shared with include/flexshm.h):
   OP_SUM = 0, OP_SUM_POSTSCALE = 1 (sum * factor), OP_PREDIV_SUM = 2
-  (each contribution / factor, the DDP default hook,
-  torch/distributed/algorithms/ddp_comm_hooks/default_hooks.py:18-33).
+  (each contribution / factor, IEEE division), OP_PREMUL_SUM = 3 (each
+  contribution * factor).  DDP's mean (`ddp_mean`) is OP_PREMUL_SUM with
+  factor = fl32(1/world): the default hook's bucket.div_(world)
+  (torch/distributed/algorithms/ddp_comm_hooks/default_hooks.py:26) multiplies
+  by the fp32 reciprocal on CUDA (ATen BinaryDivTrueKernel.cu, CPU-scalar
+  branch); tests/test_ddp_arith_gpu.py pins this against torch on the B200.
 """
 
 from __future__ import annotations
@@ -31,7 +35,12 @@ import subprocess
 import numpy as np
 
 F32, BF16 = 0, 1
-OP_SUM, OP_SUM_POSTSCALE, OP_PREDIV_SUM = 0, 1, 2
+OP_SUM, OP_SUM_POSTSCALE, OP_PREDIV_SUM, OP_PREMUL_SUM = 0, 1, 2, 3
+
+
+def ddp_mean(n: int) -> tuple[int, float]:
+    """(op, factor) of DDP's gradient mean over n ranks: x * fl32(1/n)."""
+    return OP_PREMUL_SUM, float(np.float32(1.0) / np.float32(n))
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
@@ -61,10 +70,12 @@ def _contrib(x: np.ndarray, dtype: int, op: int, factor: float) -> np.ndarray:
     f = np.float32(factor)
     if dtype == F32:
         v = x.astype(np.float32, copy=False)
-        return v / f if op == OP_PREDIV_SUM else v
+        return v / f if op == OP_PREDIV_SUM else v * f if op == OP_PREMUL_SUM else v
     v = bf16_to_f32(x)
     if op == OP_PREDIV_SUM:
         v = bf16_to_f32(f32_to_bf16(v / f))
+    elif op == OP_PREMUL_SUM:
+        v = bf16_to_f32(f32_to_bf16(v * f))
     return v
 
 

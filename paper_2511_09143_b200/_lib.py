@@ -33,7 +33,7 @@ FMX_ERR_ABORTED = 9
 FMX_ERR_UNSUPPORTED = 10
 
 FLOAT32, BFLOAT16 = 0, 1
-OP_SUM, OP_SUM_POSTSCALE, OP_PREDIV_SUM = 0, 1, 2
+OP_SUM, OP_SUM_POSTSCALE, OP_PREDIV_SUM, OP_PREMUL_SUM = 0, 1, 2, 3
 TRANSPORT_AUTO, TRANSPORT_ZC, TRANSPORT_CE, TRANSPORT_HOST = 0, 1, 2, 3
 TRANSPORTS = {"auto": TRANSPORT_AUTO, "zc": TRANSPORT_ZC, "ce": TRANSPORT_CE,
               "host": TRANSPORT_HOST}

@@ -4,7 +4,7 @@ New Python surface (the reference has none; shaped like torch / NCCL):
 
     comm = init_process_group(decision, rank, job_key, instance=inst)
     comm.allreduce(flat_grad)                 # fixed rank-order fp32 sum
-    comm.allreduce(flat_grad, op="avg")       # DDP's divide-then-sum
+    comm.allreduce(flat_grad, op="avg")       # DDP's mean: sum of x * fl32(1/n)
     comm.reduce_scatter(full, block)          # NCCL layouts
     comm.allgather(block, full)
     comm.broadcast(flat_params, root=0)
@@ -34,7 +34,32 @@ OPS = {
     "sum": _lib.OP_SUM,
     "postscale": _lib.OP_SUM_POSTSCALE,
     "prediv": _lib.OP_PREDIV_SUM,
+    "premul": _lib.OP_PREMUL_SUM,
 }
+
+
+def mean_factor(n: int) -> float:
+    """fl32(1/n), the multiplier of DDP's mean.  The default comm hook does
+    `bucket.div_(world)` (torch/distributed/algorithms/ddp_comm_hooks/
+    default_hooks.py:26); for a CPU-scalar divisor ATen's CUDA kernel
+    multiplies by the fp32 reciprocal (BinaryDivTrueKernel.cu), and the
+    hook-less reducer multiplies by 1/div_factor - so "avg" is PREMUL_SUM
+    with this factor, bit-exact with DDP on the B200
+    (tests/test_ddp_arith_gpu.py)."""
+    import numpy as np
+    return float(np.float32(1.0) / np.float32(n))
+
+
+def resolve_op(op: str, factor: float | None, n: int) -> tuple[str, float]:
+    """Map the user-facing op name (+ optional factor) to (native op, factor)."""
+    if op == "avg":
+        return "premul", mean_factor(n)
+    if op not in OPS:
+        raise ValueError(f"unknown op {op!r}")
+    factor = 1.0 if factor is None else float(factor)
+    if op != "sum" and not math.isfinite(factor):
+        raise ValueError("factor must be finite")
+    return op, factor
 
 
 def _dtype_code(tensor) -> int:
@@ -60,8 +85,7 @@ def reduce_local(sources, out, op: str = "sum", factor: float | None = None, out
     `host_sources` that live in mapped pinned memory), op/factor as in
     allreduce; `out_host` (pinned host tensor) also receives the result."""
     import torch
-    if op == "avg":
-        op, factor = "prediv", float(len(sources))
+    op, factor = resolve_op(op, factor, len(sources))
     ptrs = (ctypes.c_void_p * len(sources))(*[t.data_ptr() for t in sources])
     mask = 0
     for q in host_sources:
@@ -69,8 +93,7 @@ def reduce_local(sources, out, op: str = "sum", factor: float | None = None, out
     s = stream if stream is not None else torch.cuda.current_stream()
     rc = _lib.lib().fmx_reduce_local(ptrs, len(sources), mask, out.data_ptr(),
                                      out_host.data_ptr() if out_host is not None else None,
-                                     out.numel(), _dtype_code(out), OPS[op],
-                                     ctypes.c_float(1.0 if factor is None else factor),
+                                     out.numel(), _dtype_code(out), OPS[op], ctypes.c_float(factor),
                                      int(s.cuda_stream))
     _lib.check(rc, "fmx_reduce_local")
     return out
@@ -107,19 +130,14 @@ class ShmCommunicator:
                   stream=None):
         """In-place (or into `out`) allreduce of a flat float32/bf16 buffer.
 
-        op: "sum"; "avg" (= "prediv" by world size, the DDP default hook);
-        "prediv" (each contribution / factor); "postscale" (sum * factor).
+        op: "sum"; "avg" (DDP's mean: each contribution * fl32(1/size),
+        = "premul" with mean_factor(size)); "premul" (each contribution *
+        factor); "prediv" (each contribution / factor, IEEE division);
+        "postscale" (sum * factor).
         """
         self._alive()
         _check_tensor(tensor, "tensor")
-        if op == "avg":
-            op, factor = "prediv", float(self.size)
-        if op not in OPS:
-            raise ValueError(f"unknown op {op!r}")
-        if factor is None:
-            factor = 1.0
-        if op != "sum" and not math.isfinite(factor):
-            raise ValueError("factor must be finite")
+        op, factor = resolve_op(op, factor, self.size)
         dst = tensor if out is None else out
         if dst is not tensor:
             _check_tensor(dst, "out")
@@ -150,13 +168,7 @@ class ShmCommunicator:
         _check_tensor(out, "out")
         if out.dtype != tensor.dtype or tensor.numel() != out.numel() * self.size:
             raise ValueError("tensor must hold size * out.numel() elements of out's dtype")
-        if op == "avg":
-            op, factor = "prediv", float(self.size)
-        if op not in OPS:
-            raise ValueError(f"unknown op {op!r}")
-        factor = 1.0 if factor is None else factor
-        if op != "sum" and not math.isfinite(factor):
-            raise ValueError("factor must be finite")
+        op, factor = resolve_op(op, factor, self.size)
         rc = _lib.lib().fmx_reduce_scatter(self._h, tensor.data_ptr(), out.data_ptr(), out.numel(),
                                            _dtype_code(tensor), OPS[op], ctypes.c_float(factor),
                                            self._stream(stream))
@@ -198,11 +210,7 @@ class ShmCommunicator:
         if tensor.is_cuda or not tensor.is_contiguous() or offset < 0 or \
                 offset + tensor.numel() * tensor.element_size() > base.numel():
             raise ValueError("tensor must be a contiguous view into host_buffer()")
-        if op == "avg":
-            op, factor = "prediv", float(self.size)
-        if op not in OPS:
-            raise ValueError(f"unknown op {op!r}")
-        factor = 1.0 if factor is None else factor
+        op, factor = resolve_op(op, factor, self.size)
         rc = _lib.lib().fmx_allreduce_host(self._h, offset, tensor.numel(), _dtype_code(tensor),
                                            OPS[op], ctypes.c_float(factor), self._stream(stream))
         _lib.check(rc, "fmx_allreduce_host")

@@ -124,13 +124,42 @@ int grid_for(size_t work_items, int threads, int cap) {
 
 enum StampKind { kStWaitPeers = 1, kStWaitRank, kStWaitEvent, kStCopy, kStReduce, kStSignal };
 
+// Is a kernel profiler / checker injected into this process?  ncu (and the
+// sanitizers) serialise kernel launches across processes behind one lock and
+// drain the launching context first.  A collective's kernel queued behind a
+// stream wait on a peer's flag then holds the lock while the peer - blocked
+// on the same lock before the launch that would raise the flag - cannot
+// proceed: a cross-process deadlock (the driver's ncu-instrumented smoke hung
+// that way in round 1).  In serialize mode the host drains this rank's lanes
+// before every kernel launch, so a launch never has pending dependencies; the
+// schedule stays deadlock-free because its enqueue order is a valid
+// single-FIFO schedule (tests/test_protocol_model.py).
+bool profiler_injected() {
+  if (const char* v = getenv("FMX_SERIALIZE")) return atoi(v) != 0;
+  static const char* kVars[] = {"CUDA_INJECTION64_PATH", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE",
+                                "NSYS_PROFILING_SESSION_ID"};
+  for (const char* k : kVars)
+    if (getenv(k) && *getenv(k)) return true;
+  return false;
+}
+
 class CudaSink final : public Sink {
  public:
   CudaSink(fmx_comm* c) : c_(c) {}
 
+  // serialize mode: wait (on the host) for everything this rank enqueued so far
+  int drain() {
+    if (!c_->serialize) return FMX_OK;
+    const cudaStream_t ss[4] = {c_->user, lane_stream(c_, 0), lane_stream(c_, 1),
+                                lane_stream(c_, 2)};
+    for (int i = 0; i < 4; ++i) FMX_CUDA(cudaStreamSynchronize(ss[i]));
+    return FMX_OK;
+  }
+
   // timeline probe: stamp the completion of the op just enqueued on `lane`
   int stamp(int lane, int kind, uint32_t info) {
     if (!c_->stamps || c_->stamp_used >= c_->stamp_cap) return FMX_OK;
+    if (int rc = drain()) return rc;
     fmx_stamp_kernel<<<1, 1, 0, lane_stream(c_, lane)>>>(c_->stamps + c_->stamp_used++,
                                                           (uint32_t)(lane << 8 | kind), info);
     FMX_CUDA(cudaGetLastError());
@@ -173,6 +202,7 @@ class CudaSink final : public Sink {
                   uint32_t v) {
     cudaStream_t s = lane_stream(c_, lane);
     for (size_t i0 = 0; i0 < segs.size(); i0 += kMaxSegs) {
+      if (int rc = drain()) return rc;
       CopyArgs a;
       memset(&a, 0, sizeof a);
       a.nseg = (int)std::min<size_t>(kMaxSegs, segs.size() - i0);
@@ -198,6 +228,7 @@ class CudaSink final : public Sink {
   int reduce_impl(int lane, const PlanReduce& r) {
     const ReduceArgs& a = r.args;
     if (a.len == 0) return FMX_OK;
+    if (int rc = drain()) return rc;
     cudaStream_t s = lane_stream(c_, lane);
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (c_->timing) {
@@ -212,21 +243,7 @@ class CudaSink final : public Sink {
       c_->timed_used++;
       FMX_CUDA(cudaEventRecord(t0, s));
     }
-    constexpr int kThreads = 256, kU = 2;
-    const int V = r.dtype == FMX_FLOAT32 ? 4 : 8;
-    if (r.aligned) {
-      int g = grid_for((a.len / V + kU - 1) / kU + 1, kThreads, 1184);
-      if (r.dtype == FMX_FLOAT32)
-        fmx_reduce_kernel<float, kU><<<g, kThreads, 0, s>>>(a);
-      else
-        fmx_reduce_kernel<__nv_bfloat16, kU><<<g, kThreads, 0, s>>>(a);
-    } else {
-      int g = grid_for(a.len, kThreads, 1184);
-      if (r.dtype == FMX_FLOAT32)
-        fmx_reduce_scalar_kernel<float><<<g, kThreads, 0, s>>>(a);
-      else
-        fmx_reduce_scalar_kernel<__nv_bfloat16><<<g, kThreads, 0, s>>>(a);
-    }
+    launch_reduce(a, r.dtype, r.aligned, s);
     FMX_CUDA(cudaGetLastError());
     if (t1) FMX_CUDA(cudaEventRecord(t1, s));
     c_->launches++;
@@ -298,6 +315,7 @@ class CudaSink final : public Sink {
     // fence also speeds up the plain allreduce (30.3 -> 28.1 ms) and the host
     // path (17.7 -> 16.6 ms) (profiles/r01/r2z_r3a).  FMX_COPY_FENCE=0: off.
     if (!use_kernel && c_->copy_fence) {
+      if ((rc = drain())) return rc;
       fmx_nop_kernel<<<1, 32, 0, lane_stream(c_, lane)>>>();
       FMX_CUDA(cudaGetLastError());
       c_->launches++;
@@ -682,6 +700,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (const char* v = getenv("FMX_MIN_ROUNDS")) c->min_rounds = atoi(v);
   if (const char* v = getenv("FMX_COPY_FENCE")) c->copy_fence = atoi(v) != 0;
   if (const char* v = getenv("FMX_FUSE_SIGNAL")) c->fuse_signal = atoi(v) != 0;
+  c->serialize = profiler_injected();
   if (e != cudaSuccess) {
     h->aborted.store(1);
     fail(FMX_ERR_CUDA, "device mapping of %zu-byte segment failed: %s", c->total_bytes,
@@ -712,7 +731,7 @@ int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int 
   if (rc) return rc;
   if (dtype != FMX_FLOAT32 && dtype != FMX_BFLOAT16)
     return fail(FMX_ERR_INVALID_ARG, "bad dtype %d", dtype);
-  if (op < FMX_OP_SUM || op > FMX_OP_PREDIV_SUM) return fail(FMX_ERR_INVALID_ARG, "bad op %d", op);
+  if (op < FMX_OP_SUM || op > FMX_OP_PREMUL_SUM) return fail(FMX_ERR_INVALID_ARG, "bad op %d", op);
   if (op != FMX_OP_SUM && !std::isfinite(factor))
     return fail(FMX_ERR_INVALID_ARG, "factor must be finite");
   if (count == 0) return FMX_OK;
@@ -751,7 +770,7 @@ int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int 
 static int check_reduction_args(int dtype, int op, float factor) {
   if (dtype != FMX_FLOAT32 && dtype != FMX_BFLOAT16)
     return fail(FMX_ERR_INVALID_ARG, "bad dtype %d", dtype);
-  if (op < FMX_OP_SUM || op > FMX_OP_PREDIV_SUM) return fail(FMX_ERR_INVALID_ARG, "bad op %d", op);
+  if (op < FMX_OP_SUM || op > FMX_OP_PREMUL_SUM) return fail(FMX_ERR_INVALID_ARG, "bad op %d", op);
   if (op != FMX_OP_SUM && !std::isfinite(factor))
     return fail(FMX_ERR_INVALID_ARG, "factor must be finite");
   return FMX_OK;
@@ -813,7 +832,7 @@ int fmx_reduce_local(const void* const* srcs, int nsrc, uint64_t sys_mask, void*
     return fail(FMX_ERR_INVALID_ARG, "bad arguments");
   if (dtype != FMX_FLOAT32 && dtype != FMX_BFLOAT16)
     return fail(FMX_ERR_INVALID_ARG, "bad dtype %d", dtype);
-  if (op < FMX_OP_SUM || op > FMX_OP_PREDIV_SUM) return fail(FMX_ERR_INVALID_ARG, "bad op %d", op);
+  if (op < FMX_OP_SUM || op > FMX_OP_PREMUL_SUM) return fail(FMX_ERR_INVALID_ARG, "bad op %d", op);
   if (count == 0) return FMX_OK;
   ReduceArgs a;
   memset(&a, 0, sizeof a);
@@ -830,22 +849,7 @@ int fmx_reduce_local(const void* const* srcs, int nsrc, uint64_t sys_mask, void*
   a.len = count;
   a.op = op;
   a.factor = factor;
-  cudaStream_t s = (cudaStream_t)stream;
-  constexpr int kThreads = 256, kU = 2;
-  const int V = dtype == FMX_FLOAT32 ? 4 : 8;
-  if ((bits & 15) == 0) {
-    int g = grid_for((count / V + kU - 1) / kU + 1, kThreads, 1184);
-    if (dtype == FMX_FLOAT32)
-      fmx_reduce_kernel<float, kU><<<g, kThreads, 0, s>>>(a);
-    else
-      fmx_reduce_kernel<__nv_bfloat16, kU><<<g, kThreads, 0, s>>>(a);
-  } else {
-    int g = grid_for(count, kThreads, 1184);
-    if (dtype == FMX_FLOAT32)
-      fmx_reduce_scalar_kernel<float><<<g, kThreads, 0, s>>>(a);
-    else
-      fmx_reduce_scalar_kernel<__nv_bfloat16><<<g, kThreads, 0, s>>>(a);
-  }
+  launch_reduce(a, dtype, (bits & 15) == 0, (cudaStream_t)stream);
   FMX_CUDA(cudaGetLastError());
   return FMX_OK;
 }
@@ -864,7 +868,7 @@ int fmx_allreduce_host(fmx_comm_t c, size_t offset, size_t count, int dtype, int
   if (rc) return rc;
   if (dtype != FMX_FLOAT32 && dtype != FMX_BFLOAT16)
     return fail(FMX_ERR_INVALID_ARG, "bad dtype %d", dtype);
-  if (op < FMX_OP_SUM || op > FMX_OP_PREDIV_SUM) return fail(FMX_ERR_INVALID_ARG, "bad op %d", op);
+  if (op < FMX_OP_SUM || op > FMX_OP_PREMUL_SUM) return fail(FMX_ERR_INVALID_ARG, "bad op %d", op);
   if (op != FMX_OP_SUM && !std::isfinite(factor))
     return fail(FMX_ERR_INVALID_ARG, "factor must be finite");
   const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2;

@@ -6,7 +6,8 @@
 //   fmx_reduce_kernel  - owner-chunk reduction: n sources (peer slots in SHM or
 //                        HBM scratch, own chunk in HBM), fixed ascending-rank
 //                        fp32 sum (__fadd_rn, no contraction), fused
-//                        pre-divide / post-scale and bf16 RNE cast, written to
+//                        pre-multiply (DDP mean) / pre-divide / post-scale
+//                        and bf16 RNE cast, written to
 //                        the rank's HBM result and its SHM result slot.
 //
 // All host-link traffic is streaming (each byte touched once), so the kernels
@@ -128,6 +129,7 @@ struct Elem<float> {
                       __float_as_uint(f[3]));
   }
   __device__ static __forceinline__ float prediv(float x, float d) { return __fdiv_rn(x, d); }
+  __device__ static __forceinline__ float premul(float x, float m) { return __fmul_rn(x, m); }
   __device__ static __forceinline__ float load1(const char* p) {
     return *(volatile const float*)p;
   }
@@ -160,6 +162,10 @@ struct Elem<__nv_bfloat16> {
   __device__ static __forceinline__ float prediv(float x, float d) {
     return bf16_bits_to_f32(f32_to_bf16_bits(__fdiv_rn(x, d)));
   }
+  // ATen's bf16 `mul by an fp32 scalar`: fp32 product, rounded to bf16
+  __device__ static __forceinline__ float premul(float x, float m) {
+    return bf16_bits_to_f32(f32_to_bf16_bits(__fmul_rn(x, m)));
+  }
   __device__ static __forceinline__ float load1(const char* p) {
     return bf16_bits_to_f32(*(volatile const unsigned short*)p);
   }
@@ -168,13 +174,28 @@ struct Elem<__nv_bfloat16> {
   }
 };
 
+// One rank's contribution under the op's input scaling (PREDIV / PREMUL);
+// OP is a template parameter so each op compiles to its own straight-line
+// code (no division path in the DDP-mean kernel, no spills).
+template <typename T, int OP>
+__device__ __forceinline__ float scale_in(float x, float f) {
+  if constexpr (OP == FMX_OP_PREMUL_SUM) return Elem<T>::premul(x, f);
+  else if constexpr (OP == FMX_OP_PREDIV_SUM) return Elem<T>::prediv(x, f);
+  else return x;
+}
+
+template <int OP>
+__device__ __forceinline__ float scale_out(float acc, float f) {
+  if constexpr (OP == FMX_OP_SUM_POSTSCALE) return __fmul_rn(acc, f);
+  else return acc;
+}
+
 // Sum of one 16-byte vector position across all sources, rank order.
-template <typename T>
+template <typename T, int OP>
 __device__ __forceinline__ void reduce_vec(const ReduceArgs& a, size_t off, float* acc) {
   using E = Elem<T>;
   constexpr int V = E::kVec;
   constexpr int B = 8;  // sources loaded per batch (independent loads in flight)
-  const bool prediv = a.op == FMX_OP_PREDIV_SUM;
   for (int q0 = 0; q0 < a.nsrc; q0 += B) {
     uint4 raw[B];
 #pragma unroll
@@ -191,20 +212,34 @@ __device__ __forceinline__ void reduce_vec(const ReduceArgs& a, size_t off, floa
         E::widen(raw[b], x);
 #pragma unroll
         for (int k = 0; k < V; ++k) {
-          float c = prediv ? E::prediv(x[k], a.factor) : x[k];
+          const float c = scale_in<T, OP>(x[k], a.factor);
           acc[k] = q == 0 ? c : __fadd_rn(acc[k], c);
         }
       }
     }
   }
-  if (a.op == FMX_OP_SUM_POSTSCALE) {
 #pragma unroll
-    for (int k = 0; k < V; ++k) acc[k] = __fmul_rn(acc[k], a.factor);
-  }
+  for (int k = 0; k < V; ++k) acc[k] = scale_out<OP>(acc[k], a.factor);
 }
 
-template <typename T, int U>
-__global__ void __launch_bounds__(256) fmx_reduce_kernel(const __grid_constant__ ReduceArgs a) {
+// One element (tails and the unaligned path).
+template <typename T, int OP>
+__device__ __forceinline__ void reduce_elem(const ReduceArgs& a, size_t e) {
+  using E = Elem<T>;
+  const size_t esz = sizeof(T);
+  float acc = 0.f;
+  for (int q = 0; q < a.nsrc; ++q) {
+    const float c = scale_in<T, OP>(E::load1(a.src[q] + e * esz), a.factor);
+    acc = q == 0 ? c : __fadd_rn(acc, c);
+  }
+  acc = scale_out<OP>(acc, a.factor);
+  E::store1(a.out_dev + e * esz, acc);
+  for (int k = 1; k < a.n_rep; ++k) E::store1(a.out_dev + k * a.rep_stride + e * esz, acc);
+  if (a.out_sys) E::store1(a.out_sys + e * esz, acc);
+}
+
+template <typename T, int U, int OP>
+__global__ void __launch_bounds__(256, 2) fmx_reduce_kernel(const __grid_constant__ ReduceArgs a) {
   using E = Elem<T>;
   constexpr int V = E::kVec;
   const size_t nvec = a.len / V;
@@ -214,7 +249,7 @@ __global__ void __launch_bounds__(256) fmx_reduce_kernel(const __grid_constant__
     float acc[U][V];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (i + u * stride < nvec) reduce_vec<T>(a, (i + u * stride) * 16, acc[u]);
+      if (i + u * stride < nvec) reduce_vec<T, OP>(a, (i + u * stride) * 16, acc[u]);
     uint4 o[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -232,39 +267,50 @@ __global__ void __launch_bounds__(256) fmx_reduce_kernel(const __grid_constant__
     }
   }
   // element tail (len not a multiple of the vector width)
-  const size_t esz = sizeof(T);
-  for (size_t e = nvec * V + tid; e < a.len; e += stride) {
-    float acc = 0.f;
-    for (int q = 0; q < a.nsrc; ++q) {
-      float c = E::load1(a.src[q] + e * esz);
-      if (a.op == FMX_OP_PREDIV_SUM) c = E::prediv(c, a.factor);
-      acc = q == 0 ? c : __fadd_rn(acc, c);
-    }
-    if (a.op == FMX_OP_SUM_POSTSCALE) acc = __fmul_rn(acc, a.factor);
-    E::store1(a.out_dev + e * esz, acc);
-    for (int k = 1; k < a.n_rep; ++k) E::store1(a.out_dev + k * a.rep_stride + e * esz, acc);
-    if (a.out_sys) E::store1(a.out_sys + e * esz, acc);
-  }
+  for (size_t e = nvec * V + tid; e < a.len; e += stride) reduce_elem<T, OP>(a, e);
 }
 
 // Unaligned fallback: one element per thread iteration.
-template <typename T>
+template <typename T, int OP>
 __global__ void __launch_bounds__(256) fmx_reduce_scalar_kernel(const __grid_constant__ ReduceArgs a) {
-  using E = Elem<T>;
-  const size_t esz = sizeof(T);
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.len; e += stride) {
-    float acc = 0.f;
-    for (int q = 0; q < a.nsrc; ++q) {
-      float c = E::load1(a.src[q] + e * esz);
-      if (a.op == FMX_OP_PREDIV_SUM) c = E::prediv(c, a.factor);
-      acc = q == 0 ? c : __fadd_rn(acc, c);
-    }
-    if (a.op == FMX_OP_SUM_POSTSCALE) acc = __fmul_rn(acc, a.factor);
-    E::store1(a.out_dev + e * esz, acc);
-    for (int k = 1; k < a.n_rep; ++k) E::store1(a.out_dev + k * a.rep_stride + e * esz, acc);
-    if (a.out_sys) E::store1(a.out_sys + e * esz, acc);
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.len; e += stride)
+    reduce_elem<T, OP>(a, e);
+}
+
+// Host-side dispatch over (dtype, op, alignment): grid capped at 8 x 148 CTAs
+// of 256 threads, 2 vectors per thread in flight.
+constexpr int kReduceThreads = 256, kReduceU = 2, kReduceGridCap = 1184;
+
+template <typename T, int OP>
+inline void launch_reduce_t(const ReduceArgs& a, bool aligned, cudaStream_t s) {
+  constexpr int V = Elem<T>::kVec;
+  auto grid = [](size_t items) {
+    size_t g = (items + kReduceThreads - 1) / kReduceThreads;
+    return (int)(g < 1 ? 1 : g > (size_t)kReduceGridCap ? kReduceGridCap : g);
+  };
+  if (aligned)
+    fmx_reduce_kernel<T, kReduceU, OP>
+        <<<grid((a.len / V + kReduceU - 1) / kReduceU + 1), kReduceThreads, 0, s>>>(a);
+  else
+    fmx_reduce_scalar_kernel<T, OP><<<grid(a.len), kReduceThreads, 0, s>>>(a);
+}
+
+template <typename T>
+inline void launch_reduce_op(const ReduceArgs& a, bool aligned, cudaStream_t s) {
+  switch (a.op) {
+    case FMX_OP_SUM_POSTSCALE: return launch_reduce_t<T, FMX_OP_SUM_POSTSCALE>(a, aligned, s);
+    case FMX_OP_PREDIV_SUM: return launch_reduce_t<T, FMX_OP_PREDIV_SUM>(a, aligned, s);
+    case FMX_OP_PREMUL_SUM: return launch_reduce_t<T, FMX_OP_PREMUL_SUM>(a, aligned, s);
+    default: return launch_reduce_t<T, FMX_OP_SUM>(a, aligned, s);
   }
+}
+
+inline void launch_reduce(const ReduceArgs& a, int dtype, bool aligned, cudaStream_t s) {
+  if (dtype == FMX_FLOAT32)
+    launch_reduce_op<float>(a, aligned, s);
+  else
+    launch_reduce_op<__nv_bfloat16>(a, aligned, s);
 }
 
 // ---------------------------------------------------------------- stamps

@@ -39,6 +39,8 @@ struct fmx_comm {
   cudaStream_t last_main = nullptr;    // lane-1 stream of the last collective
   bool copy_fence = true;              // no-op kernel after every copy-engine batch (CudaSink::copy)
   bool fuse_signal = true;             // FMX_FUSE_SIGNAL=0: zero-copy stage + STAGED as two ops
+  bool serialize = false;              // drain this rank's lanes before every kernel launch
+                                       //   (under a kernel profiler / FMX_SERIALIZE=1)
   unsigned int* ctas_done = nullptr;   // device counter of the fused signal (per comm; lanes
                                        //   never run two fused copies at once: lane 0 only)
   int last_class = -1;              // 0 device-buffer collective, 1 host path / broadcast

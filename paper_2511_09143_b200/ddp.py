@@ -11,10 +11,11 @@ PAPER.md:264-271), so here:
   `ShmCommunicator.broadcast` of the flattened parameters;
 * every gradient bucket is allreduced by `flexshm_hook` on a side stream
   (overlapping the rest of the backward pass), keeping DDP's
-  default-hook arithmetic - divide by world size, then SUM
-  (torch/distributed/algorithms/ddp_comm_hooks/default_hooks.py:18-33) -
-  fused into one pass (op="avg" = FMX_OP_PREDIV_SUM) with the fixed
-  ascending-rank fp32 summation;
+  default-hook arithmetic bit for bit - `bucket.div_(world)`, then SUM
+  (torch/distributed/algorithms/ddp_comm_hooks/default_hooks.py:18-33),
+  where the CUDA div_ by a CPU scalar is a multiply by fl32(1/world) -
+  fused into one pass (op="avg" = FMX_OP_PREMUL_SUM, comm.mean_factor) with
+  the fixed ascending-rank fp32 summation (tests/test_ddp_arith_gpu.py);
 * `ZeroShardBroadcast` re-broadcasts each owner's updated parameter shard
   after a sharded optimizer step (the ZeroRedundancyOptimizer pattern,
   torch/distributed/optim/zero_redundancy_optimizer.py:785-801);

@@ -146,6 +146,9 @@ def ddp_worker(rank: int, job_key: str, n: int, port: int, mode: str = "green",
         with net.no_sync():
             torch.nn.functional.cross_entropy(net(x), y).backward()
         local = torch.cat([p.grad.reshape(-1) for p in model.parameters()]).clone()
+        # what DDP's default hook does to a bucket before its SUM allreduce
+        # (default_hooks.py:26): an in-place CUDA div_ by the world size
+        local_div = local.clone().div_(n)
         for p in model.parameters():
             p.grad = None
         torch.nn.functional.cross_entropy(net(x), y).backward()
@@ -156,7 +159,7 @@ def ddp_worker(rank: int, job_key: str, n: int, port: int, mode: str = "green",
     as_np = (lambda t: t.float().numpy()) if dtype == "f32" else \
         (lambda t: t.cpu().view(torch.int16).numpy().view(np.uint16))
     return {"params0": as_np(params0.cpu()), "local": as_np(local.cpu()),
-            "synced": as_np(synced.cpu())}
+            "local_div": as_np(local_div.cpu()), "synced": as_np(synced.cpu())}
 
 
 def overlap_worker(rank: int, job_key: str, n: int, counts: list, mode: str = "green"):

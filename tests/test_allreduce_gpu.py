@@ -18,7 +18,8 @@ from tests import _workers
 
 pytestmark = pytest.mark.gpu
 
-OPS = {"sum": orc.OP_SUM, "postscale": orc.OP_SUM_POSTSCALE, "prediv": orc.OP_PREDIV_SUM}
+OPS = {"sum": orc.OP_SUM, "postscale": orc.OP_SUM_POSTSCALE, "prediv": orc.OP_PREDIV_SUM,
+       "premul": orc.OP_PREMUL_SUM}
 
 
 def expected(sc: dict, n: int) -> np.ndarray:
@@ -32,7 +33,7 @@ def expected(sc: dict, n: int) -> np.ndarray:
     op = sc.get("op", "sum")
     factor = sc.get("factor")
     if op == "avg":
-        op, factor = "prediv", float(n)
+        op, factor = "premul", orc.ddp_mean(n)[1]
     return orc.allreduce_c(xs, dt, OPS[op], 1.0 if factor is None else factor)
 
 
@@ -192,6 +193,6 @@ def test_join_stream_mode_overlapping_allreduces(n, mode):
                  timeout_s=300, mode=mode)
     for i, c in enumerate(counts):
         xs = [orc.synthetic_gradient(r, c, orc.F32, seed=500 + i) for r in range(n)]
-        want = orc.allreduce_c(xs, orc.F32, orc.OP_PREDIV_SUM, float(n))
+        want = orc.allreduce_c(xs, orc.F32, *orc.ddp_mean(n))
         for r, out in enumerate(res):
             assert np.array_equal(out["results"][i].view(np.uint32), want.view(np.uint32)), (i, r)

@@ -1,8 +1,9 @@
 """DDP integration: parameters broadcast over SHM, and
 every gradient bucket allreduced by ddp.flexshm_hook with DDP's default
-arithmetic (divide by world size, then sum) fused into the fixed rank-order
-fp32 sum - bit-exact against the oracle applied to the ranks' local
-gradients."""
+arithmetic (bucket.div_(world) - on CUDA a multiply by fl32(1/world) - then
+sum) fused into the fixed rank-order fp32 sum - bit-exact against the oracle
+applied to the ranks' local gradients (tests/test_ddp_arith_gpu.py pins the
+scaling against torch's own kernel)."""
 
 from __future__ import annotations
 
@@ -33,7 +34,7 @@ def test_ddp_hook_matches_oracle(n, overlap, mode, dtype):
     for r in res[1:]:
         assert np.array_equal(r["params0"], res[0]["params0"]), "parameter broadcast"
     dt = orc.F32 if dtype == "f32" else orc.BF16
-    want = orc.allreduce_c([r["local"] for r in res], dt, orc.OP_PREDIV_SUM, float(n))
+    want = orc.allreduce_c([r["local"] for r in res], dt, *orc.ddp_mean(n))
     bits = (lambda a: a.view(np.uint32)) if dtype == "f32" else (lambda a: a)
     for rank, r in enumerate(res):
         assert np.array_equal(bits(r["synced"]), bits(want)), rank
@@ -57,7 +58,7 @@ def test_ddp_bf16_compressed_exchange_matches_oracle():
                  job_key=key, timeout_s=300)
     locals_bf16 = [torch.from_numpy(r["local"]).to(torch.bfloat16).view(torch.int16).numpy()
                    .view(np.uint16) for r in res]
-    want = orc.allreduce_c(locals_bf16, orc.BF16, orc.OP_PREDIV_SUM, float(n))
+    want = orc.allreduce_c(locals_bf16, orc.BF16, *orc.ddp_mean(n))
     want_f32 = orc.bf16_to_f32(want)
     for rank, r in enumerate(res):
         assert np.array_equal(r["synced"].view(np.uint32), want_f32.view(np.uint32)), rank
@@ -99,6 +100,6 @@ def test_ddp_threaded_hook_matches_oracle(mode):
     port = 22000 + os.getpid() % 20000
     res = launch(_workers.ddp_worker, d, args=(key, n, port, mode, True, "f32", None, True),
                  job_key=key, timeout_s=300, mode=mode)
-    want = orc.allreduce_c([r["local"] for r in res], orc.F32, orc.OP_PREDIV_SUM, float(n))
+    want = orc.allreduce_c([r["local"] for r in res], orc.F32, *orc.ddp_mean(n))
     for rank, r in enumerate(res):
         assert np.array_equal(r["synced"].view(np.uint32), want.view(np.uint32)), rank

@@ -25,7 +25,8 @@ def same(a, b):
 
 @pytest.mark.parametrize("dtype", [orc.F32, orc.BF16])
 @pytest.mark.parametrize("op,factor", [(orc.OP_SUM, 1.0), (orc.OP_SUM_POSTSCALE, 0.125),
-                                       (orc.OP_PREDIV_SUM, 7.0), (orc.OP_PREDIV_SUM, 3.0)])
+                                       (orc.OP_PREDIV_SUM, 7.0), (orc.OP_PREDIV_SUM, 3.0),
+                                       (orc.OP_PREMUL_SUM, 1 / 7), (orc.OP_PREMUL_SUM, 0.1)])
 @pytest.mark.parametrize("n", [1, 2, 7, 14])
 def test_c_and_numpy_restatements_agree(dtype, op, factor, n):
     count = 10_007
@@ -38,9 +39,9 @@ def test_c_and_numpy_restatements_agree(dtype, op, factor, n):
 @pytest.mark.parametrize("n,count,threads", [(2, 1, 3), (7, 5, 2), (7, 100_003, 4), (3, 64, 8)])
 def test_cpu_shm_path_equals_checker(dtype, n, count, threads):
     xs = [orc.synthetic_gradient(r, count, dtype) for r in range(n)]
-    want = orc.allreduce_c(xs, dtype, orc.OP_PREDIV_SUM, float(n))
+    want = orc.allreduce_c(xs, dtype, *orc.ddp_mean(n))
     bufs = [x.copy() for x in xs]
-    orc.ShmAllreduce(n, count, dtype, threads)(bufs, orc.OP_PREDIV_SUM, float(n))
+    orc.ShmAllreduce(n, count, dtype, threads)(bufs, *orc.ddp_mean(n))
     for b in bufs:
         assert same(b, want)
 

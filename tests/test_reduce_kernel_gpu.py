@@ -12,7 +12,8 @@ from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
 
-OPS = {"sum": orc.OP_SUM, "postscale": orc.OP_SUM_POSTSCALE, "prediv": orc.OP_PREDIV_SUM}
+OPS = {"sum": orc.OP_SUM, "postscale": orc.OP_SUM_POSTSCALE, "prediv": orc.OP_PREDIV_SUM,
+       "premul": orc.OP_PREMUL_SUM}
 
 
 def to_torch(x, dtype, device):
@@ -38,7 +39,8 @@ def bits_equal_nan_aware(a, b, dtype):
 
 
 @pytest.mark.parametrize("dtype", [orc.F32, orc.BF16])
-@pytest.mark.parametrize("op,factor", [("sum", 1.0), ("postscale", 0.25), ("prediv", 7.0)])
+@pytest.mark.parametrize("op,factor", [("sum", 1.0), ("postscale", 0.25), ("prediv", 7.0),
+                                       ("premul", 1.0 / 7.0), ("premul", 0.1)])
 @pytest.mark.parametrize("n", [1, 2, 7, 9, 64])
 @pytest.mark.parametrize("count", [1, 7, 8, 9, 4099, 300_001])
 def test_reduce_kernel_matches_oracle(dtype, op, factor, n, count):
@@ -67,5 +69,5 @@ def test_reduce_kernel_unaligned_scalar_path():
     out = torch.empty(count + 1, device="cuda")[1:]
     reduce_local(srcs, out, op="avg")
     torch.cuda.synchronize()
-    want = orc.allreduce_c([x[1:] for x in xs], orc.F32, orc.OP_PREDIV_SUM, float(n))
+    want = orc.allreduce_c([x[1:] for x in xs], orc.F32, *orc.ddp_mean(n))
     assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))

@@ -14,7 +14,8 @@ from tests import _workers
 
 pytestmark = pytest.mark.gpu
 
-OPS = {"sum": orc.OP_SUM, "postscale": orc.OP_SUM_POSTSCALE, "prediv": orc.OP_PREDIV_SUM}
+OPS = {"sum": orc.OP_SUM, "postscale": orc.OP_SUM_POSTSCALE, "prediv": orc.OP_PREDIV_SUM,
+       "premul": orc.OP_PREMUL_SUM}
 
 
 def expected_digest(o: dict, n: int, rank: int) -> str:
@@ -26,7 +27,7 @@ def expected_digest(o: dict, n: int, rank: int) -> str:
         return _workers.digest(np.concatenate(xs))
     op, factor = o["op"], (0.25 if o["op"] == "postscale" else 1.0)
     if op == "avg":
-        op, factor = "prediv", float(n)
+        op, factor = "premul", orc.ddp_mean(n)[1]
     full = orc.allreduce_c(xs, dt, OPS[op], factor)
     if o["kind"] == "reduce_scatter":
         c = o["size"]
