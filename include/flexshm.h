@@ -145,7 +145,13 @@ int fmx_restore_bus_id(const char* label, char* out);
  * nslots = pipeline depth, 2 (double buffering) .. FMX_MAX_SLOTS, 0 = default
  * (2; 4 at two ranks; env FMX_SLOTS overrides).  host_bytes =
  * size of every rank's registered host buffer (fmx_host_buffer), 0 = none.
- * Rank 0's slice_bytes / nslots / host_bytes win.  timeout_s bounds every bootstrap wait. */
+ * Rank 0's slice_bytes / nslots / host_bytes win, and so do the schedule
+ * settings of rank 0's environment (FMX_RAMP, FMX_MIN_ROUNDS, FMX_GRAIN,
+ * FMX_GATHER_GRAIN, FMX_LANES, FMX_RESULT_VIA_CE, FMX_ZC_MAX), published in
+ * the segment header so every rank runs the same protocol.  Peers on another
+ * host (different host_hash: the reference's select_transport answers "NET",
+ * commsim.py:126-132) are refused with FMX_ERR_UNSUPPORTED: the transport is
+ * one host's shared memory.  timeout_s bounds every bootstrap wait. */
 int fmx_comm_init(fmx_comm_t* comm, const char* job_key, int nranks, int rank,
                   const fmx_peer_info* self, int mig_aware, size_t slice_bytes, int nslots,
                   size_t host_bytes, int transport, double timeout_s);
@@ -219,18 +225,18 @@ int fmx_comm_monitor(fmx_comm_t comm, double seconds, uint64_t* out, size_t cap,
 
 /* Completion stream.  By default a collective forks from the stream it is
  * called on and joins back into it.  With a join stream set (non-null), it
- * still forks from the call's stream (its input is ready there) but joins into
- * `stream`: the calling stream runs on, and consecutive device-buffer
- * collectives (allreduce / reduce-scatter / all-gather on distinct buffers)
- * overlap inside the library - the next call stages while the previous one
- * gathers.  The caller orders reuse of a buffer after its completion (as DDP
- * does by waiting on the bucket future).  Host-path calls and broadcasts wait
- * for the previous collective.  NULL restores the default. */
+ * still forks from the call's stream (its input is ready there) but runs ALL
+ * of its lanes, in order, on `stream` and completes there: the calling stream
+ * (e.g. DDP's autograd stream) runs on and never waits for a collective.
+ * Consecutive collectives are ordered on the join stream; they do not overlap
+ * inside the library (extra lane streams next to a compute stream aliased
+ * hardware queues under MPS and were slower).  The caller
+ * orders reuse of a buffer after its completion (as DDP does by waiting on the
+ * bucket future).  NULL restores the default. */
 int fmx_comm_set_join_stream(fmx_comm_t comm, void* stream);
-/* The stream the last collective completed on: the calling stream by default;
- * in join-stream mode with three lanes, an internal stream (the gather lane),
- * so the join stream is free for the next call's fetch.  Make consumers wait
- * for an event recorded on it. */
+/* The stream the last collective completed on: the calling stream by
+ * default, the join stream in join-stream mode.  Make consumers wait for an
+ * event recorded on it. */
 int fmx_comm_completion_stream(fmx_comm_t comm, void** stream);
 
 /* Live timing of the reduction kernel: with timing on, every reduce launch

@@ -16,6 +16,7 @@ from .errors import (
     FlexShmError,
     MalformedLabelError,
     ShmTimeoutError,
+    TransportUnavailableError,
 )
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libflexshm.so")
@@ -191,4 +192,6 @@ def check(rc: int, what: str = "") -> None:
         raise ShmTimeoutError(msg, rc)
     if rc == FMX_ERR_ABORTED:
         raise CommAbortedError(msg, rc)
+    if rc == FMX_ERR_UNSUPPORTED and "NET" in msg:
+        raise TransportUnavailableError(msg, rc)
     raise FlexShmError(f"{what}: {msg}" if what else msg, rc)

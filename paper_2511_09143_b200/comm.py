@@ -314,6 +314,8 @@ def init_process_group(decision: AllocationDecision | None, rank: int, job_key: 
     """
     from .instance import peer_info as _peer_info
 
+    if decision is None and nranks is None:
+        raise ValueError("need a decision or nranks")
     n = nranks if nranks is not None else len(decision.instances)
     if decision is not None and nranks is not None and nranks != len(decision.instances):
         raise ValueError("nranks disagrees with the decision")

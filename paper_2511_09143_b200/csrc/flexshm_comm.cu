@@ -377,12 +377,50 @@ class CudaSink final : public Sink {
   std::vector<CUstreamBatchMemOpParams> ops_;
 };
 
-// Fork the lanes off the caller's stream, run the plan, join them back.
-// (Re)create the lane-0 stream and the lane events in `ctx`, the context of
-// the caller's stream (a green context, an MPS client's, or the primary one),
-// so every lane object lives where the caller's work lives.
+// Lane objects (lane-0/2 streams, the lane events, the fork/join/done events,
+// the timing pairs) live in the context of the caller's stream - a green
+// context, an MPS client's, or the primary one - so every lane object lives
+// where the caller's work lives.  On a change of context the old objects are
+// destroyed in their own context after a host wait for the last collective
+// (its `done`), so ordering carries over: the new context's events start
+// unrecorded, and every wait on them is then rightly a no-op.
+int release_lane_objects(fmx_comm* c) {
+  if (!c->lane_ctx) return FMX_OK;
+  if (g_ctx_push(c->lane_ctx) != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "cuCtxPushCurrent failed");
+  int rc = FMX_OK;
+  if (c->has_done && cudaEventSynchronize(c->done) != cudaSuccess)
+    rc = fail(FMX_ERR_CUDA, "pending collective failed: %s", cudaGetErrorString(cudaGetLastError()));
+  if (c->done) cudaEventDestroy(c->done);
+  if (c->fork) cudaEventDestroy(c->fork);
+  c->done = c->fork = nullptr;
+  for (int i = 0; i < kNumEvents; ++i) {
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    c->ev[i] = nullptr;
+  }
+  for (auto& pr : c->timed) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  c->timed.clear();
+  c->timed_used = 0;
+  for (int l = 0; l < 3; ++l) {
+    if (l != 1 && c->lane[l]) cudaStreamDestroy(c->lane[l]);
+    if (c->joined[l]) cudaEventDestroy(c->joined[l]);
+    c->lane[l] = nullptr;
+    c->joined[l] = nullptr;
+  }
+  CUcontext dummy;
+  g_ctx_pop(&dummy);
+  c->has_done = false;
+  c->last_class = -1;
+  c->last_main = nullptr;
+  c->completion = nullptr;
+  c->lane_ctx = nullptr;
+  return rc;
+}
+
+// (Re)create the lane objects in `ctx` (pushed by the caller).
 int make_lane_objects(fmx_comm* c, CUcontext ctx) {
-  c->lane[0] = c->lane[2] = nullptr;  // an earlier context's objects are abandoned
   // lane priority (FMX_LANE_PRIORITY=1: highest) stays default: high-priority
   // lanes made the device-buffer allreduce 1.4x slower on the B200 under MPS
   // (profiles/r01/r2o) and did not help DP training (r2k)
@@ -396,9 +434,6 @@ int make_lane_objects(fmx_comm* c, CUcontext ctx) {
   FMX_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
   FMX_CUDA(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
   for (int i = 0; i < kNumEvents; ++i) FMX_CUDA(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
-  for (auto& pr : c->timed) pr = {nullptr, nullptr};
-  c->timed.clear();
-  c->timed_used = 0;
   c->lane_ctx = ctx;
   return FMX_OK;
 }
@@ -427,7 +462,9 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
     }
   } pop;
   int rc;
-  if (ctx != c->lane_ctx && (rc = make_lane_objects(c, ctx))) return rc;
+  if (ctx != c->lane_ctx) {
+    if ((rc = release_lane_objects(c)) || (rc = make_lane_objects(c, ctx))) return rc;
+  }
   c->user = user;
   cudaStream_t main = c->join_stream ? c->join_stream : user;  // lane 1 and the join target
   // extra lane streams in use: lane 0, and lane 2 with three lanes
@@ -558,6 +595,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
     h->creator_pid = (int32_t)getpid();
     h->mig_aware = mig_aware ? 1 : 0;
     snprintf(h->job_key, sizeof h->job_key, "%s", job_key);
+    h->proto = proto_from_env();  // every rank runs rank 0's schedule settings
     h->magic.store(kMagicReady, std::memory_order_release);
   } else {
     for (;;) {
@@ -584,7 +622,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
       }
       Header* h = (Header*)p;
       if (h->magic.load(std::memory_order_acquire) != kMagicReady || !pid_alive(h->creator_pid) ||
-          h->total_bytes != (uint64_t)st.st_size) {
+          h->total_bytes != (uint64_t)st.st_size || h->version != kVersion) {
         munmap(p, (size_t)st.st_size);
         usleep(1000);
         continue;
@@ -640,6 +678,14 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
     std::vector<char> labels((size_t)nranks * FMX_BUS_ID_LEN);
     rc = fmx_topology(c->peers.data(), nranks, labels.data(), nullptr, nullptr, nullptr);
   }
+  // One host only: peers on another host would need the NET transport
+  // (select_transport, reference commsim.py:126-132); every rank sees the same
+  // table, so every rank refuses the communicator the same way.
+  for (int r = 1; rc == FMX_OK && r < nranks; ++r)
+    if (c->peers[r].host_hash != c->peers[0].host_hash)
+      rc = fail(FMX_ERR_UNSUPPORTED,
+                "rank %d is on another host than rank 0 (host_hash differs): select_transport "
+                "answers NET, and this library provides only the SHM transport of one host", r);
   if (rc != FMX_OK) {
     unmap(c);
     delete c;
@@ -647,7 +693,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   }
 
   c->transport = transport;  // AUTO stays AUTO: chosen per collective by size (use_zc)
-  if (const char* v = getenv("FMX_ZC_MAX")) c->zc_max = strtoull(v, nullptr, 10);
+  apply_proto(c, h->proto);  // rank 0's schedule settings (never per-rank env)
   if (host_only) {
     *out = c;
     return FMX_OK;
@@ -687,17 +733,8 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (e == cudaSuccess) e = cudaMemset(c->ctas_done, 0, sizeof(unsigned int));
 
 
-  if (const char* v = getenv("FMX_RESULT_VIA_CE")) c->result_via_ce = atoi(v) != 0;
+  // local-only knobs (how this rank issues its copies; the protocol is unchanged)
   if (const char* v = getenv("FMX_COPY2D")) c->copy2d = atoi(v) != 0;
-  if (const char* v = getenv("FMX_GRAIN")) {
-    c->coarse = strcmp(v, "fine") != 0;
-    c->fine_first = strcmp(v, "first") == 0;
-  }
-  c->coarse_gather = c->coarse;
-  if (const char* v = getenv("FMX_GATHER_GRAIN")) c->coarse_gather = strcmp(v, "fine") != 0;
-  if (const char* v = getenv("FMX_LANES")) c->nlanes = std::min(3, std::max(1, atoi(v)));
-  if (const char* v = getenv("FMX_RAMP")) c->ramp = atoi(v);
-  if (const char* v = getenv("FMX_MIN_ROUNDS")) c->min_rounds = atoi(v);
   if (const char* v = getenv("FMX_COPY_FENCE")) c->copy_fence = atoi(v) != 0;
   if (const char* v = getenv("FMX_FUSE_SIGNAL")) c->fuse_signal = atoi(v) != 0;
   c->serialize = profiler_injected();
@@ -924,26 +961,7 @@ int fmx_barrier(fmx_comm_t c, double timeout_s) {
 
 int fmx_comm_destroy(fmx_comm_t c) {
   if (!c) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
-  int rc = FMX_OK;
-  const bool pushed = c->lane_ctx && g_ctx_push && g_ctx_push(c->lane_ctx) == CUDA_SUCCESS;
-  if (c->has_done && cudaEventSynchronize(c->done) != cudaSuccess)
-    rc = fail(FMX_ERR_CUDA, "pending collective failed: %s", cudaGetErrorString(cudaGetLastError()));
-  if (c->done) cudaEventDestroy(c->done);
-  if (c->fork) cudaEventDestroy(c->fork);
-  for (int i = 0; i < kNumEvents; ++i)
-    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
-  for (auto& pr : c->timed) {
-    cudaEventDestroy(pr.first);
-    cudaEventDestroy(pr.second);
-  }
-  for (int l = 0; l < 3; ++l) {
-    if (l != 1 && c->lane[l]) cudaStreamDestroy(c->lane[l]);
-    if (c->joined[l]) cudaEventDestroy(c->joined[l]);
-  }
-  if (pushed) {
-    CUcontext dummy;
-    g_ctx_pop(&dummy);
-  }
+  int rc = g_ctx_push ? release_lane_objects(c) : FMX_OK;
   if (c->scratch) cudaFree(c->scratch);
   if (c->stamps) cudaFree(c->stamps);
   if (c->ctas_done) cudaFree(c->ctas_done);
@@ -957,14 +975,35 @@ int fmx_comm_destroy(fmx_comm_t c) {
 int fmx_comm_abort(fmx_comm_t c) {
   if (!c || !c->hdr) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
   c->hdr->aborted.store(1, std::memory_order_release);
-  // Release every pending stream wait on every rank: push all counters far
-  // ahead (cyclic >= compares, so +2^29 satisfies any outstanding target).
-  for (int r = 0; r < c->nranks; ++r)
-    for (int f = 0; f < kFlagsPerRank; ++f) {
-      volatile uint32_t* p = c->flag_host(r, f);
-      *p = *p + (1u << 29);
-    }
-  __sync_synchronize();
+  // Release every pending stream wait of every rank: raise all counters far
+  // ahead (waits compare cyclic >=, so +2^29 satisfies any outstanding
+  // target).  A GPU that still has a queued flag signal can write a smaller,
+  // absolute value back after the raise and park a peer again, so the raise is
+  // re-asserted until every flag stayed up for a quiet period (bounded), and
+  // abort may be issued again at any time - e.g. after the local streams
+  // drained: the raised targets are remembered, so repeating it is idempotent.
+  const size_t nf = (size_t)c->nranks * kFlagsPerRank;
+  if (c->abort_target.size() != nf) {
+    c->abort_target.resize(nf);
+    for (int r = 0; r < c->nranks; ++r)
+      for (int f = 0; f < kFlagsPerRank; ++f)
+        c->abort_target[(size_t)r * kFlagsPerRank + f] = *c->flag_host(r, f) + (1u << 29);
+  }
+  const double t_end = now_s() + 0.5;
+  double quiet_since = now_s();
+  while (now_s() < t_end && now_s() - quiet_since < 0.05) {
+    for (int r = 0; r < c->nranks; ++r)
+      for (int f = 0; f < kFlagsPerRank; ++f) {
+        uint32_t* p = (uint32_t*)c->flag_host(r, f);
+        const uint32_t want = c->abort_target[(size_t)r * kFlagsPerRank + f];
+        const uint32_t v = __atomic_load_n(p, __ATOMIC_ACQUIRE);
+        if ((int32_t)(v - want) < 0) {
+          __atomic_store_n(p, want, __ATOMIC_RELEASE);
+          quiet_since = now_s();
+        }
+      }
+    std::this_thread::yield();
+  }
   return FMX_OK;
 }
 

@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "fmx_comm.h"
@@ -99,6 +100,40 @@ class TraceSink final : public Sink {
   std::string* out_;
   int seq_[kNumEvents] = {};
 };
+
+Proto proto_from_env() {
+  Proto p{};
+  p.ramp = 0;
+  p.min_rounds = 1;
+  p.coarse = 1;
+  p.fine_first = 0;
+  p.nlanes = 3;
+  p.result_via_ce = 0;
+  p.zc_max = 2u << 20;
+  if (const char* v = getenv("FMX_RESULT_VIA_CE")) p.result_via_ce = atoi(v) != 0;
+  if (const char* v = getenv("FMX_GRAIN")) {
+    p.coarse = strcmp(v, "fine") != 0;
+    p.fine_first = strcmp(v, "first") == 0;
+  }
+  p.coarse_gather = p.coarse;
+  if (const char* v = getenv("FMX_GATHER_GRAIN")) p.coarse_gather = strcmp(v, "fine") != 0;
+  if (const char* v = getenv("FMX_LANES")) p.nlanes = std::min(3, std::max(1, atoi(v)));
+  if (const char* v = getenv("FMX_RAMP")) p.ramp = atoi(v);
+  if (const char* v = getenv("FMX_MIN_ROUNDS")) p.min_rounds = atoi(v);
+  if (const char* v = getenv("FMX_ZC_MAX")) p.zc_max = strtoull(v, nullptr, 10);
+  return p;
+}
+
+void apply_proto(fmx_comm* c, const Proto& p) {
+  c->ramp = p.ramp;
+  c->min_rounds = p.min_rounds;
+  c->coarse = p.coarse != 0;
+  c->fine_first = p.fine_first != 0;
+  c->coarse_gather = p.coarse_gather != 0;
+  c->nlanes = p.nlanes;
+  c->result_via_ce = p.result_via_ce != 0;
+  c->zc_max = p.zc_max;
+}
 
 // Round j of every chunk covers [prefix(j), prefix(j) + size(j)).  By default
 // the rounds are equal (at most one slice each).  FMX_RAMP=1 makes the first
@@ -557,22 +592,12 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   if (const char* v = getenv("FMX_SLOTS")) c.nslots = std::min(FMX_MAX_SLOTS, std::max(2, atoi(v)));
   c.transport = (transport == FMX_TRANSPORT_ZC || transport == FMX_TRANSPORT_AUTO) ? transport
                                                                                   : FMX_TRANSPORT_CE;
-  if (const char* v = getenv("FMX_ZC_MAX")) c.zc_max = strtoull(v, nullptr, 10);
+  apply_proto(&c, proto_from_env());
   c.slice_bytes = slice_bytes;
   size_t max_bytes = 0;
   for (int i = 0; i < nops; ++i) max_bytes = std::max(max_bytes, counts[i] * (dtypes[i] ? 2 : 4));
   c.L = compute_layout(nranks, c.nslots, slice_bytes, max_bytes);
   c.total_bytes = c.L.total;
-  if (const char* v = getenv("FMX_RESULT_VIA_CE")) c.result_via_ce = atoi(v) != 0;
-  if (const char* v = getenv("FMX_GRAIN")) {
-    c.coarse = strcmp(v, "fine") != 0;
-    c.fine_first = strcmp(v, "first") == 0;
-  }
-  c.coarse_gather = c.coarse;
-  if (const char* v = getenv("FMX_GATHER_GRAIN")) c.coarse_gather = strcmp(v, "fine") != 0;
-  if (const char* v = getenv("FMX_RAMP")) c.ramp = atoi(v);
-  if (const char* v = getenv("FMX_MIN_ROUNDS")) c.min_rounds = atoi(v);
-  if (const char* v = getenv("FMX_LANES")) c.nlanes = std::min(3, std::max(1, atoi(v)));
   std::string out;
   TraceSink sink(&out);
   sink.nranks = nranks;

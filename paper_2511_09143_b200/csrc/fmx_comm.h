@@ -75,6 +75,7 @@ struct fmx_comm {
   fmx::Stamp* stamps = nullptr;
   size_t stamp_cap = 0, stamp_used = 0;
   std::vector<fmx_peer_info> peers;
+  std::vector<uint32_t> abort_target;  // fmx_comm_abort: raised flag values (re-asserted)
   std::vector<CUstreamBatchMemOpParams> ops;
 
   // byte offsets of the pipeline slots inside the segment
@@ -214,6 +215,11 @@ inline Annot sbuf(size_t off_bytes, size_t bytes) { return Annot{(int64_t)off_by
 
 // The three owner-chunk collectives of plan_allreduce.
 enum Kind { kAllreduce = 0, kReduceScatter = 1, kAllgather = 2 };
+
+// The schedule settings (Proto) from this process's environment, and their
+// application to a communicator (rank 0 publishes, every rank applies).
+Proto proto_from_env();
+void apply_proto(fmx_comm* c, const Proto& p);
 
 int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
                    int op, float factor, bool aligned, int kind = kAllreduce);

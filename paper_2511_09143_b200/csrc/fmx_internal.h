@@ -19,7 +19,7 @@ void set_dup(int a, int b);
 // [user region of rank 0] ... [user region of rank n-1]
 // Every region starts on a 4 KiB boundary; every flag owns a 64-byte line.
 constexpr uint32_t kMagicReady = 0x464D5831u;  // "FMX1"
-constexpr uint32_t kVersion = 1;
+constexpr uint32_t kVersion = 2;
 // Per rank: 8 scalar flags, then one STAGED_TO flag per destination owner.
 enum Flag { kStaged = 0, kReduced = 1, kBcStaged = 2, kBcDone = 3, kStagedTo = 8 };
 constexpr int kFlagsPerRank = kStagedTo + FMX_MAX_RANKS;
@@ -28,6 +28,17 @@ struct alignas(64) PeerSlot {
   std::atomic<int32_t> state;  // 0 empty, 1 published
   int32_t pid;
   fmx_peer_info info;
+};
+
+// Settings that change the schedule - piece boundaries, which flags are
+// signalled, which lane gathers, the transport of a collective.  Rank 0
+// publishes its own (read from its environment, FMX_RAMP, FMX_MIN_ROUNDS,
+// FMX_GRAIN, FMX_GATHER_GRAIN, FMX_LANES, FMX_RESULT_VIA_CE, FMX_ZC_MAX) in the
+// segment header and every rank adopts them, so ranks cannot disagree on the
+// protocol (a mismatch would give wrong results or park a stream forever).
+struct Proto {
+  int32_t ramp, min_rounds, coarse, fine_first, coarse_gather, nlanes, result_via_ce, pad;
+  uint64_t zc_max;
 };
 
 struct Header {
@@ -48,7 +59,10 @@ struct Header {
   alignas(64) std::atomic<int32_t> departed;
   alignas(64) std::atomic<int32_t> touched;  // ranks done first-touching their regions
   char job_key[128];
+  Proto proto;  // rank 0's schedule settings, adopted by every rank
 };
+
+static_assert(sizeof(Header) <= 4096, "the header owns the first page of the segment");
 
 struct Layout {
   size_t peers_off, flags_off, ar_in_off, ar_out_off, bc_off, user_off, user_bytes, total;

@@ -90,12 +90,13 @@ def flexshm_hook(state, bucket) -> torch.futures.Future[torch.Tensor]:
     """DDP communication hook: bucket.buffer() <- mean over ranks.
 
     The collective forks from the current (autograd) stream, where the
-    bucket's producers ran, and joins into the side stream; the CUDA-aware
-    future records its completion there.  DDP's wait on the future makes the
-    consumer stream wait for that event, so later backward kernels are not
-    queued behind the collective's flag waits, and bucket k+1 stages while
-    bucket k is still being gathered.  `state` may also be a bare
-    ShmCommunicator (collective on the current stream, no overlap).
+    bucket's producers ran, and runs in order on the side stream (join-stream
+    mode), where it completes; the CUDA-aware future records its completion
+    there.  DDP's wait on the future makes the consumer stream wait for that
+    event, so later backward kernels are not queued behind the collective's
+    flag waits.  Consecutive buckets are serialised on the side stream.
+    `state` may also be a bare ShmCommunicator (collective on the current
+    stream, no overlap).
     """
     buf = bucket.buffer()
     if isinstance(state, ShmCommunicator):
@@ -113,19 +114,18 @@ def flexshm_hook(state, bucket) -> torch.futures.Future[torch.Tensor]:
         fut = torch.futures.Future(devices=[buf.device])
         state._queue.put((buf, ready, fut, "avg"))
         return fut
-    # fork from the autograd stream (the bucket's producers), complete on the
-    # side stream: consecutive buckets overlap inside the library (join-stream
-    # mode) and the autograd stream never waits for a collective
+    # fork from the autograd stream (the bucket's producers), run and complete
+    # on the side stream (join-stream mode): the autograd stream never waits
+    # for a collective
     state.comm.set_join_stream(state.stream)
     try:
         state.comm.allreduce(buf, op="avg", stream=cur)
         done = state.comm.completion_stream()
     finally:
         state.comm.set_join_stream(None)
-    # lane 1 ran on the side stream (tell the allocator); the call completes on
-    # the library's gather lane - the future's event is recorded there.  No
-    # record_stream on that library-owned stream: it may be destroyed (with the
-    # communicator) before DDP frees its bucket buffers.
+    # the collective ran on the side stream (tell the allocator) and completed
+    # on the stream completion_stream() names - the future's event is recorded
+    # there (the side stream in join-stream mode).
     buf.record_stream(state.stream)
     done_stream = state.stream if done in (0, state.stream.cuda_stream) else \
         torch.cuda.ExternalStream(done, device=buf.device)

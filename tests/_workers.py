@@ -112,6 +112,14 @@ def suite_worker(rank: int, job_key: str, n: int, transport: str, mode: str, sce
     return {"results": out, "launches": launches, "pid": os.getpid()}
 
 
+def mixed_env_worker(rank: int, job_key: str, n: int, envs: dict, scenarios: list,
+                     slice_bytes: int = 0):
+    """suite_worker with per-rank schedule settings in the environment: every
+    rank must still run rank 0's (published in the segment header)."""
+    os.environ.update(envs.get(rank, {}))
+    return suite_worker(rank, job_key, n, "auto", "green", scenarios, slice_bytes)
+
+
 def ddp_worker(rank: int, job_key: str, n: int, port: int, mode: str = "green",
                overlap: bool = True, dtype: str = "f32", compress: str | None = None,
                threaded: bool = False):

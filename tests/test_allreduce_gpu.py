@@ -196,3 +196,25 @@ def test_join_stream_mode_overlapping_allreduces(n, mode):
         want = orc.allreduce_c(xs, orc.F32, *orc.ddp_mean(n))
         for r, out in enumerate(res):
             assert np.array_equal(out["results"][i].view(np.uint32), want.view(np.uint32)), (i, r)
+
+
+def test_schedule_settings_follow_rank0():
+    """Ranks whose environments ask for different schedules (ramp, grain,
+    lanes, transport cut) still run one protocol - rank 0's, published in the
+    segment header - and stay bit-exact (per-rank knobs used to
+    split pieces differently and could hang)."""
+    from paper_2511_09143_b200.launcher import launch, new_job_key
+    from paper_2511_09143_b200.scheduler import fm_select, make_cluster
+    from paper_2511_09143_b200.workload import Job
+
+    n = 3
+    envs = {1: {"FMX_RAMP": "1", "FMX_GRAIN": "fine", "FMX_ZC_MAX": "0"},
+            2: {"FMX_LANES": "2", "FMX_MIN_ROUNDS": "4", "FMX_GATHER_GRAIN": "fine"}}
+    scen = [dict(kind="allreduce", count=3_000_001, dtype="f32", op="avg"),
+            dict(kind="allreduce", count=1_000_003, dtype="bf16", op="sum"),
+            dict(kind="allreduce", count=700_001, dtype="f32", op="sum")]
+    d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
+    key = new_job_key("env")
+    res = launch(_workers.mixed_env_worker, d, args=(key, n, envs, scen, 262144), job_key=key,
+                 timeout_s=300)
+    check_all(n, scen, res)

@@ -102,11 +102,12 @@ def test_native_restore_bus_id_matches_reference_golden():
 # ---------------------------------------------------------------- multi-process
 
 
-def _host_rank(rank, n, key, mig_ids, q):
+def _host_rank(rank, n, key, mig_ids, q, hosts=None):
     from paper_2511_09143_b200.comm import init_process_group
     from paper_2511_09143_b200.commsim import PeerInfo
+    from paper_2511_09143_b200.errors import TransportUnavailableError
     try:
-        peer = PeerInfo(rank, "00:C0:00.0", mig_ids[rank], 7, 100 + rank)
+        peer = PeerInfo(rank, "00:C0:00.0", mig_ids[rank], hosts[rank] if hosts else 7, 100 + rank)
         comm = init_process_group(None, rank, key, peer=peer, nranks=n, transport="host",
                                   timeout_s=30)
         for _ in range(3):
@@ -116,15 +117,17 @@ def _host_rank(rank, n, key, mig_ids, q):
         q.put((rank, "ok", labels))
     except DuplicateDeviceError as exc:
         q.put((rank, "dup", (exc.rank_a, exc.rank_b)))
+    except TransportUnavailableError as exc:
+        q.put((rank, "net", str(exc)))
     except Exception as exc:  # noqa: BLE001
         q.put((rank, "err", repr(exc)))
 
 
-def run_host_world(n, mig_ids):
+def run_host_world(n, mig_ids, hosts=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     key = f"cpu-{uuid.uuid4().hex[:10]}"
-    ps = [ctx.Process(target=_host_rank, args=(r, n, key, mig_ids, q)) for r in range(n)]
+    ps = [ctx.Process(target=_host_rank, args=(r, n, key, mig_ids, q, hosts)) for r in range(n)]
     for p in ps:
         p.start()
     out = {}
@@ -149,3 +152,19 @@ def test_multiprocess_bootstrap_rejects_double_binding():
     out = run_host_world(3, ["MIG-a", "MIG-b", "MIG-a"])
     for r in range(3):
         assert out[r] == ("dup", (0, 2))
+
+
+def test_multiprocess_bootstrap_refuses_cross_host_peers():
+    """Peers on two hosts: select_transport answers NET for them (reference
+    commsim.py:126-132), which the SHM transport cannot serve - every rank
+    gets the same distinct error (FMX_ERR_UNSUPPORTED ->
+    TransportUnavailableError), and the reference's own rule agrees."""
+    from paper_2511_09143_b200.commsim import PeerInfo, select_transport
+    hosts = [7, 7, 8]
+    assert select_transport(PeerInfo(0, "00:C0:00.0", "a", 7, 1),
+                            PeerInfo(2, "00:C0:00.0", "c", 8, 3)) == "NET"
+    out = run_host_world(3, ["MIG-a", "MIG-b", "MIG-c"], hosts)
+    for r in range(3):
+        status, msg = out[r]
+        assert status == "net", out[r]
+        assert "rank 2" in msg and "NET" in msg
