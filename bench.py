@@ -121,18 +121,69 @@ def link_bytes(n: int, per_gpu: list[int], s_bytes: int):
     return [(k * s_bytes, 2 * k * (n - 1) * s_bytes / n) for k in per_gpu]
 
 
+# Host memory bandwidth (read + write bytes, all host threads), measured on the
+# GPU box (profiles/r01_probe/bw.jsonl "host_memcpy"); bench.py re-measures it
+# in the run (host_dram_gbs) and uses that when it can.
+HOST_DRAM_FALLBACK = 184.78
+
+
+def host_dram_gbs(nbytes: int = 1 << 30) -> float:
+    """Best-of-3 multithreaded host copy, read+write bytes per second (GB/s):
+    the B_dram of the roofline's host-memory term."""
+    import torch
+    torch.set_num_threads(os.cpu_count() or 1)
+    a = torch.ones(nbytes // 4)
+    b = torch.empty_like(a)
+    best = float("inf")
+    for _ in range(3):
+        t0 = time.perf_counter()
+        b.copy_(a)
+        best = min(best, time.perf_counter() - t0)
+    return 2 * nbytes / best / 1e9
+
+
 def step_roofline(n, per_gpu, s_bytes, t_s, peaks):
-    """T* = max_g max(D2H/B_d2h, H2D/B_h2d, (D2H+H2D)/B_bidir)."""
-    tstar = 0.0
-    for d2h, h2d in link_bytes(n, per_gpu, s_bytes):
+    """T* = max( max_g max(D2H_g/B_d2h, H2D_g/B_h2d, (D2H_g+H2D_g)/B_bidir),
+                 sum_g (D2H_g+H2D_g) / B_dram ).
+    per_gpu = ranks on each PHYSICAL GPU (logical GPUs sharing one device
+    share its link).  Every DMA byte is one host-memory access (D2H writes,
+    H2D reads), so the host-DRAM term binds once enough GPUs share the host."""
+    tstar, bound = 0.0, "host_link"
+    lb = link_bytes(n, per_gpu, s_bytes)
+    for d2h, h2d in lb:
         tstar = max(tstar, d2h / (peaks["d2h"] * 1e9), h2d / (peaks["h2d"] * 1e9),
                     (d2h + h2d) / (peaks["bidir"] * 1e9))
-    d2h0, h2d0 = link_bytes(n, per_gpu, s_bytes)[0]
-    return {"bound": "host_link", "t_star_ms": tstar * 1e3, "frac": tstar / t_s,
+    dram_bytes = sum(d + h for d, h in lb)
+    t_dram = dram_bytes / (peaks.get("dram", HOST_DRAM_FALLBACK) * 1e9)
+    if t_dram > tstar:
+        tstar, bound = t_dram, "host_dram"
+    d2h0, h2d0 = lb[0]
+    return {"bound": bound, "t_star_ms": tstar * 1e3, "frac": tstar / t_s,
             "achieved": (d2h0 + h2d0) / t_s / 1e9, "unit": "GB/s",
             "peak_bidir": peaks["bidir"], "peak_h2d": peaks["h2d"], "peak_d2h": peaks["d2h"],
-            "link_bytes_per_gpu": {"d2h": d2h0, "h2d": h2d0},
-            "peak_source": "profiles/r01_probe/bw.jsonl (cudaMemcpyAsync pinned, best of 5)"}
+            "peak_dram": peaks.get("dram", HOST_DRAM_FALLBACK),
+            "t_dram_ms": t_dram * 1e3, "host_dram_bytes": dram_bytes,
+            "link_bytes_per_gpu": {"d2h": d2h0, "h2d": h2d0}, "ranks_per_physical_gpu": per_gpu,
+            "peak_source": "host link: profiles/r01_probe/bw.jsonl (cudaMemcpyAsync pinned, "
+                           "best of 5); host DRAM: " + peaks.get("dram_source", "r01 probe")}
+
+
+def physical_split(d, gpus: int) -> list[int]:
+    """Ranks per physical GPU: the decision's per-GPU counts, merged where
+    FMX_DEVICE_MAP puts several logical GPUs on one device."""
+    per = [sum(1 for g, _ in d.instances if g == gg) for gg in range(gpus)]
+    dm = os.environ.get("FMX_DEVICE_MAP")
+    if not dm:
+        return per
+    phys: dict[str, int] = {}
+    for gg, dev in enumerate(dm.split(",")[:gpus]):
+        phys[dev] = phys.get(dev, 0) + per[gg]
+    return list(phys.values())
+
+
+def workload_name(count: int, dtype: str) -> str:
+    return {RESNET50_PARAMS: "ResNet-50", 3_504_872: "MobileNetV2",
+            109_483_778: "BERT-base"}.get(count, "synthetic") + f"-sized gradient ({count} {dtype})"
 
 
 # SM zero-copy store peak to mapped host memory (profiles/r01_probe/bw.jsonl, "zc"
@@ -514,9 +565,12 @@ def run_sweep(args) -> list[dict]:
     res = run_ranks(sweep_body, _spawned_sweep, list(range(n)), f"sweep-{os.getpid()}", n, cfg,
                     args.mode, 0)
     lines = []
+    # every sweep rank runs on device 0 of this node (gpus > 1: logical GPUs of
+    # one device), so all n ranks share one physical link
+    per_gpu = [n]
+    peaks = dict(LINK_PEAK_FALLBACK, dram=host_dram_gbs(), dram_source="measured in this run")
     for b in cfg["sizes"]:
         ms = max(r["ms"][b][0] for r in res.values())
-        per_gpu = [n]
         lines.append({"sweep": f"{args.sweep_op} size sweep (BASELINE configs[4])", "bytes": b,
                       "op": args.sweep_op,
                       "ranks": n, "instance_mode": args.mode, "dtype": args.dtype,
@@ -524,7 +578,7 @@ def run_sweep(args) -> list[dict]:
                       "busbw_gbs": b / ms / 1e6 * 2 * (n - 1) / n,
                       "iters": res[0]["ms"][b][1],
                       "step_roofline_frac": step_roofline(n, per_gpu, b, ms / 1e3,
-                                                          LINK_PEAK_FALLBACK)["frac"]
+                                                          peaks)["frac"]
                       if args.sweep_op == "allreduce" else None})
     return lines
 
@@ -791,7 +845,11 @@ def run_ours(args) -> dict | None:
     s_bytes = args.count * esz
     t_step = local_max / 1e3 / args.steps
     per_gpu = [sum(1 for g, _ in d.instances if g == gg) for gg in range(gpus)]
+    per_phys = physical_split(d, gpus)
     peaks = dict(LINK_PEAK_FALLBACK)
+    if not args.dry_run:
+        peaks.update(dram=host_dram_gbs(), dram_source="host copy measured in this run, all "
+                                                       "threads, read+write bytes")
     line = {
         "metric": "SHM allreduce GB/s vs host-link peak; ResNet-50 img/s on 1g slices",
         # whole-job aggregate: every rank's S-byte gradient is one unit of work
@@ -805,9 +863,10 @@ def run_ours(args) -> dict | None:
         "data": "synthetic (seeded N(0,1)*1e-3 gradient per rank); op = DDP mean: each "
                 "contribution x fl32(1/n) (what the default hook's bucket.div_(n) computes "
                 "on CUDA), then the rank-order fp32 sum",
-        "config": {"workload": f"ResNet-50-sized gradient allreduce ({args.count} "
-                               f"{args.dtype}) across {args.ranks_per_gpu} 1g instances per "
-                               f"B200 x {gpus} (BASELINE configs[1] comm step)",
+        "config": {"workload": f"{workload_name(args.count, args.dtype)} allreduce across "
+                               f"{args.ranks_per_gpu} 1g instances per B200 x {gpus}"
+                               + (" (BASELINE configs[1] comm step)"
+                                  if args.count == RESNET50_PARAMS and gpus == 1 else ""),
                    "ranks": n, "ranks_per_gpu": per_gpu, "bytes": s_bytes,
                    "instance_mode": inst_mode,
                    "transport": args.transport, "l2": "inputs > L2 (7 x 102 MB per GPU)",
@@ -818,12 +877,18 @@ def run_ours(args) -> dict | None:
         "roofline": kernel_roofline(args, n, s_bytes, kernel_ms, kernel_count,
                                     results.get(0, {}).get("iso_kernel_us"),
                                     results.get(0, {}).get("iso_piece_bytes")),
-        "step_roofline": step_roofline(n, per_gpu, s_bytes, t_step, peaks),
+        "step_roofline": step_roofline(n, per_phys, s_bytes, t_step, peaks),
         "gpu_launches": launches,
         "clocks": clocks,
     }
     if getattr(args, "mps_fallback", None):
         line["config"]["mps_fallback"] = args.mps_fallback
+    if os.environ.get("FMX_DEVICE_MAP"):
+        line["config"]["logical_gpus"] = (
+            f"{gpus} LOGICAL GPUs on {len(per_phys)} physical B200 (FMX_DEVICE_MAP="
+            f"{os.environ['FMX_DEVICE_MAP']}, synthetic bus ids FMX_FAKE_BUS): the communicator, "
+            "rank order and bootstrap are the multi-GPU ones, but all host-link traffic shares "
+            "one PCIe link - not a multi-GPU scaling number")
     if not args.no_e2e:
         t_e2e = local_max_e2e / 1e3 / args.steps
         t_dev = local_max_e2e_dev / 1e3 / args.steps
@@ -836,12 +901,16 @@ def run_ours(args) -> dict | None:
                               "timed region",
                        "h2d_bytes_per_step": n * s_bytes, "d2h_bytes_per_step": n * s_bytes,
                        "ranks_agree": len(digests) == 1}
-        # host path roofline: k*S each way per GPU, T* = max(one-way, bidirectional)
-        k_max = max(per_gpu)
-        t_star = max(k_max * s_bytes / (peaks["h2d"] * 1e9), k_max * s_bytes / (peaks["d2h"] * 1e9),
+        # host path roofline: k*S each way per GPU, T* = max(one-way, bidirectional,
+        # host DRAM over all GPUs)
+        k_max = max(per_phys)
+        t_link = max(k_max * s_bytes / (peaks["h2d"] * 1e9), k_max * s_bytes / (peaks["d2h"] * 1e9),
                      2 * k_max * s_bytes / (peaks["bidir"] * 1e9))
-        line["e2e"]["step_roofline"] = {"bound": "host_link", "t_star_ms": t_star * 1e3,
-                                        "frac": t_star / t_e2e}
+        t_dram = 2 * n * s_bytes / (peaks.get("dram", HOST_DRAM_FALLBACK) * 1e9)
+        t_star = max(t_link, t_dram)
+        line["e2e"]["step_roofline"] = {"bound": "host_link" if t_link >= t_dram else "host_dram",
+                                        "t_star_ms": t_star * 1e3, "frac": t_star / t_e2e,
+                                        "t_dram_ms": t_dram * 1e3}
         line["e2e_device_buffers"] = {
             "value": n * s_bytes / t_dev / 1e9, "unit": line["unit"], "ms_per_step": t_dev * 1e3,
             "api": "pinned host -> device copy, ShmCommunicator.allreduce, device -> pinned host",
@@ -886,31 +955,62 @@ def run_nccl_point(args) -> dict:
 
 
 def run_cpu_reference(count: int, n: int, dtype: str, steps: int, warmup: int,
-                      nthreads: int | None = None, seconds: float | None = None) -> dict:
-    """CPU restatement of the same algorithm (oracle/), all host threads."""
-    import numpy as np
-
+                      seconds: float | None = None, extras: bool = True) -> dict:
+    """The CPU reference path of BASELINE.md §3, timed on this box's cores:
+    oracle/shm_cpu_allreduce.c - one process per rank, each pinned to its own
+    host core, a real /dev/shm segment, the same reduce-scatter / all-gather
+    and rank-order fp32 sum (DDP mean), bit-identical to the GPU path.  At
+    least `steps` timed allreduces, more up to ~`seconds` of work.  With
+    `extras`, two more CPU figures on the same workload: the single-process
+    threaded port of the same algorithm (oracle ShmAllreduce, all threads)
+    and the in-place host-reduction bound (all buffers in one address space,
+    rank-order sum written back, no staging: n*S read + n*S written)."""
     from oracle import oracle as orc
     dt = orc.F32 if dtype == "f32" else orc.BF16
-    nthreads = nthreads or os.cpu_count() or 1
-    bufs = [orc.synthetic_gradient(r, count, dt) for r in range(n)]
-    shm = orc.ShmAllreduce(n, count, dt, nthreads)
-    for _ in range(warmup):
-        shm(bufs, *orc.ddp_mean(n))
-    times = []
-    t_end = time.perf_counter() + (seconds or 0)
-    k = 0
-    while k < steps or (seconds and time.perf_counter() < t_end):
-        t0 = time.perf_counter()
-        shm(bufs, *orc.ddp_mean(n))
-        times.append(time.perf_counter() - t0)
-        k += 1
-    t = sum(times) / len(times)
     esz = 4 if dtype == "f32" else 2
-    del np
-    return {"value": n * count * esz / t / 1e9, "algbw_gbs": count * esz / t / 1e9,
-            "ms_per_step": t * 1e3, "iters": k,
-            "cores": nthreads}
+    cores = orc.host_cores()
+    op, factor = orc.ddp_mean(n)
+    probe, _ = orc.mp_shm_allreduce(n, count, dt, op, factor, iters=1, warmup=max(warmup, 1),
+                                    cores=cores)
+    k = max(steps, min(500, int((seconds or 0) * 1e3 / max(probe["ms_per_step"], 1e-3))))
+    st, _ = orc.mp_shm_allreduce(n, count, dt, op, factor, iters=k, warmup=max(warmup, 1),
+                                 cores=cores)
+    t = st["ms_per_step"] / 1e3
+    out = {"value": n * count * esz / t / 1e9, "algbw_gbs": count * esz / t / 1e9,
+           "ms_per_step": t * 1e3, "iters": k, "cores": st["cores"], "processes": n,
+           "oversubscribed": st["oversubscribed"], "host_cpus": len(cores),
+           "kind": "port",
+           "sample": f"full workload: {n} rank processes x {count} {dtype}, one per host core "
+                     f"({st['cores']} of {len(cores)} cores"
+                     f"{', OVERSUBSCRIBED' if st['oversubscribed'] else ''}), POSIX SHM "
+                     f"reduce-scatter/all-gather, {k} timed allreduces "
+                     "(oracle/shm_cpu_allreduce.c)"}
+    if extras:
+        nthreads = len(cores)
+        bufs = [orc.synthetic_gradient(r, count, dt) for r in range(n)]
+        shm = orc.ShmAllreduce(n, count, dt, nthreads)
+        shm(bufs, op, factor)
+        reps = max(3, min(20, k // 4))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            shm(bufs, op, factor)
+        tp = (time.perf_counter() - t0) / reps
+        out["threaded_port"] = {"ms_per_step": tp * 1e3, "value": n * count * esz / tp / 1e9,
+                                "threads": nthreads,
+                                "what": "one process, n rank buffers, same staging RS/AG "
+                                        "(oracle ShmAllreduce)"}
+        orc.inplace_allreduce(bufs, dt, op, factor, nthreads)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            orc.inplace_allreduce(bufs, dt, op, factor, nthreads)
+        ti = (time.perf_counter() - t0) / reps
+        out["inplace_bound"] = {"ms_per_step": ti * 1e3, "value": n * count * esz / ti / 1e9,
+                                "threads": nthreads,
+                                "what": "in-place rank-order reduction of the n host buffers in "
+                                        "one address space (no staging; 2 n S bytes of host "
+                                        "memory traffic): the host's own floor for host-resident "
+                                        "gradients, to read the GPU e2e against"}
+    return out
 
 
 def main(argv=None):
@@ -921,23 +1021,28 @@ def main(argv=None):
     if args.impl == "reference":
         if grank != 0:
             return 0
-        r = run_cpu_reference(args.count, n, args.dtype, args.steps, args.warmup)
-        sample = (f"{n} rank buffers of {args.count} {args.dtype} in one process; "
-                  f"{r['iters']} full allreduces, {r['cores']} threads")
+        # bounded sample: at least --steps allreduces, at most ~20 s of work
+        r = run_cpu_reference(args.count, n, args.dtype, args.steps, args.warmup, seconds=20.0)
+        sample = r["sample"]
         line = {"impl": "reference", "metric": "SHM allreduce GB/s vs host-link peak; ResNet-50 "
                 "img/s on 1g slices", "value": r["value"], "unit": unit,
                 "n_gpus": args.gpus if world == 1 else world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None,
                 "dtype": "float32" if args.dtype == "f32" else "bfloat16", "data": "synthetic",
-                "config": {"workload": f"ResNet-50-sized gradient allreduce ({args.count} "
-                                       f"{args.dtype}) across {n} ranks", "ranks": n},
+                "config": {"workload": f"{workload_name(args.count, args.dtype)} allreduce "
+                                       f"across {n} ranks", "ranks": n},
                 "cpu_baseline": {"value": r["value"], "unit": unit, "cores": r["cores"],
-                                 "kind": "port", "sample": sample},
+                                 "kind": "port", "sample": sample,
+                                 "threaded_port": r.get("threaded_port"),
+                                 "inplace_bound": r.get("inplace_bound")},
                 "e2e": {"value": r["value"], "unit": unit, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0},
-                "note": "reference has no runnable allreduce (NCCL in the paper); CPU port of "
-                        "the same SHM RS/AG algorithm, oracle/flexshm_oracle.c"}
+                "note": "the reference has no runnable allreduce (its data path is NCCL, "
+                        "PAPER.md:353-354, 830); this arm is BASELINE.md §3's CPU reference "
+                        "path: one process per rank pinned to its own core, POSIX SHM "
+                        "reduce-scatter/all-gather, rank-order fp32 sum "
+                        "(oracle/shm_cpu_allreduce.c), bit-identical to the GPU path"}
         print(json.dumps(line))
         return 0
     mps = start_mps(args, world)
@@ -1033,12 +1138,12 @@ def _main(args, world, n, unit):
         except Exception as exc:  # noqa: BLE001 - report, keep the allreduce line
             line["resnet50"] = {"error": repr(exc)[:300]}
     if not args.no_cpu_baseline:
-        r = run_cpu_reference(args.count, n, args.dtype, 1, 1, seconds=args.cpu_seconds)
+        r = run_cpu_reference(args.count, n, args.dtype, 3, 1, seconds=args.cpu_seconds)
         line["cpu_baseline"] = {"value": r["value"], "unit": line["unit"], "cores": r["cores"],
-                                "kind": "port",
-                                "sample": f"full workload ({n} ranks x {args.count} {args.dtype}), "
-                                          f"{r['iters']} allreduces in ~{args.cpu_seconds:.0f} s, "
-                                          f"oracle/flexshm_oracle.c threads"}
+                                "kind": "port", "sample": r["sample"],
+                                "ms_per_step": r["ms_per_step"],
+                                "threaded_port": r.get("threaded_port"),
+                                "inplace_bound": r.get("inplace_bound")}
     print(json.dumps(line))
     if args.out:
         with open(args.out, "w") as f:

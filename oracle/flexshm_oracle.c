@@ -199,3 +199,49 @@ int oracle_shm_allreduce(int n, void** bufs, size_t count, int dtype, int op, fl
   }
   return 0;
 }
+
+/* ------------------------------------------------------------------------
+ * In-place host reduction (a bound, not an SHM path): every rank's buffer in
+ * one address space, each of `nthreads` threads takes an element range,
+ * sums it across the n buffers in rank order and writes the result back into
+ * all n buffers - read n*S + write n*S, no staging copies.  It is what a
+ * single host process could at best do with host-resident gradients, and is
+ * reported next to the GPU e2e figure (the GPU/CPU ratio must not
+ * be read as "GPU beats the host" without it).  Bit-identical results. */
+typedef struct {
+  int n, dtype, op;
+  float factor;
+  void** bufs;
+  size_t lo, hi;
+} inplace_job;
+
+static void* inplace_worker(void* arg) {
+  inplace_job* j = (inplace_job*)arg;
+  const size_t esz = j->dtype == ORC_F32 ? 4 : 2;
+  enum { B = 4096 };
+  union { float f[B]; uint16_t h[B]; } tmp;
+  for (size_t lo = j->lo; lo < j->hi; lo += B) {
+    const size_t len = j->hi - lo < B ? j->hi - lo : B;
+    const void* xs[1024];
+    for (int q = 0; q < j->n; ++q) xs[q] = (const char*)j->bufs[q] + lo * esz;
+    reduce_range(j->n, xs, &tmp, j->dtype, j->op, j->factor, 0, len);
+    for (int q = 0; q < j->n; ++q) memcpy((char*)j->bufs[q] + lo * esz, &tmp, len * esz);
+  }
+  return NULL;
+}
+
+int oracle_inplace_allreduce(int n, void** bufs, size_t count, int dtype, int op, float factor,
+                             int nthreads) {
+  if (n < 1 || n > 1024 || nthreads < 1 || nthreads > 256) return -1;
+  pthread_t th[256];
+  inplace_job jobs[256];
+  for (int t = 0; t < nthreads; ++t) {
+    inplace_job j = {n, dtype, op, factor, bufs, 0, 0};
+    split(count, t, nthreads, &j.lo, &j.hi);
+    jobs[t] = j;
+    if (t) pthread_create(&th[t], NULL, inplace_worker, &jobs[t]);
+  }
+  inplace_worker(&jobs[0]);
+  for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+  return 0;
+}

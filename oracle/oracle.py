@@ -98,10 +98,18 @@ def broadcast_np(xs: list[np.ndarray], root: int) -> np.ndarray:
 # ---------------------------------------------------------------- C oracle
 
 
+_MP_PATH = os.path.join(_HERE, "_build", "shm_cpu_allreduce")
+
+
 def build() -> str:
-    """Compile oracle/flexshm_oracle.c (TEST INFRASTRUCTURE) -> _build/liboracle.so."""
-    src = os.path.join(_HERE, "flexshm_oracle.c")
-    if not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+    """Compile oracle/flexshm_oracle.c -> _build/liboracle.so and
+    oracle/shm_cpu_allreduce.c -> _build/shm_cpu_allreduce (TEST / BASELINE
+    INFRASTRUCTURE)."""
+    stale = False
+    for out, src in ((_LIB_PATH, "flexshm_oracle.c"), (_MP_PATH, "shm_cpu_allreduce.c")):
+        src = os.path.join(_HERE, src)
+        stale |= not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src)
+    if stale:
         subprocess.check_call(["make", "-s", "-C", _HERE])
     return _LIB_PATH
 
@@ -122,6 +130,10 @@ def lib() -> ctypes.CDLL:
         _lib.oracle_shm_allreduce.restype = ctypes.c_int
         _lib.oracle_shm_scratch_bytes.argtypes = [ctypes.c_int, ctypes.c_size_t, ctypes.c_int]
         _lib.oracle_shm_scratch_bytes.restype = ctypes.c_size_t
+        _lib.oracle_inplace_allreduce.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
+                                                  ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
+                                                  ctypes.c_float, ctypes.c_int]
+        _lib.oracle_inplace_allreduce.restype = ctypes.c_int
     return _lib
 
 
@@ -152,6 +164,64 @@ class ShmAllreduce:
                                         self.nthreads, self.scratch.ctypes.data)
         if rc != 0:
             raise RuntimeError(f"oracle_shm_allreduce rc={rc}")
+
+
+def inplace_allreduce(bufs: list[np.ndarray], dtype: int = F32, op: int = OP_SUM,
+                      factor: float = 1.0, nthreads: int | None = None) -> None:
+    """In-place threaded rank-order reduction over n host buffers (one
+    address space, no staging): the host-memory bound next to the GPU e2e."""
+    ptrs = (ctypes.c_void_p * len(bufs))(*[b.ctypes.data for b in bufs])
+    rc = lib().oracle_inplace_allreduce(len(bufs), ptrs, bufs[0].size, dtype, op, factor,
+                                        nthreads or os.cpu_count() or 1)
+    if rc != 0:
+        raise RuntimeError(f"oracle_inplace_allreduce rc={rc}")
+
+
+def host_cores() -> list[int]:
+    """The host cores this process may run on."""
+    return sorted(os.sched_getaffinity(0))
+
+
+def mp_shm_allreduce(n: int, count: int, dtype: int = F32, op: int = OP_SUM,
+                     factor: float = 1.0, iters: int = 1, warmup: int = 0,
+                     cores: list[int] | None = None, xs: list[np.ndarray] | None = None,
+                     want_out: bool = False, timeout: float = 600.0):
+    """Run the multi-process POSIX-SHM CPU allreduce (oracle/shm_cpu_allreduce.c:
+    one process per rank pinned to its own core).  xs: the
+    ranks' inputs (default: the program's synthetic data).  Returns (stats
+    dict, outputs [n][count] or None)."""
+    import json
+    import tempfile
+    build()
+    cores = host_cores() if cores is None else cores
+    esz = 4 if dtype == F32 else 2
+    tmp = tempfile.mkdtemp(prefix="fmx-cpuref-", dir="/dev/shm" if os.path.isdir("/dev/shm")
+                           else None)
+    inp, outp = "-", "-"
+    try:
+        if xs is not None:
+            inp = os.path.join(tmp, "in")
+            np.concatenate([np.ascontiguousarray(x, _np_dtype(dtype)) for x in xs]).tofile(inp)
+        if want_out:
+            outp = os.path.join(tmp, "out")
+        r = subprocess.run([_MP_PATH, str(n), str(count), str(dtype), str(op), repr(float(factor)),
+                            str(iters), str(warmup), ",".join(map(str, cores)), inp, outp],
+                           capture_output=True, text=True, timeout=timeout)
+        if r.returncode != 0:
+            raise RuntimeError(f"shm_cpu_allreduce rc={r.returncode}: {r.stderr[-500:]}")
+        stats = json.loads(r.stdout.strip().splitlines()[-1])
+        outs = None
+        if want_out:
+            flat = np.fromfile(outp, dtype=_np_dtype(dtype))
+            outs = [flat[i * count:(i + 1) * count].copy() for i in range(n)]
+        return stats, outs
+    finally:
+        for f in ("in", "out"):
+            try:
+                os.unlink(os.path.join(tmp, f))
+            except OSError:
+                pass
+        os.rmdir(tmp)
 
 
 # ---------------------------------------------------------------- inputs

@@ -32,7 +32,9 @@ def suite_worker(rank: int, job_key: str, n: int, transport: str, mode: str, sce
     from paper_2511_09143_b200.comm import init_process_group
     from paper_2511_09143_b200.commsim import PeerInfo
 
-    inst = inst_mod.bind(0, rank + 1, mode=mode)
+    # the launcher names this rank's instance (fm_select order over the GPUs)
+    inst = inst_mod.bind(int(os.environ.get("FMX_GPU_ID", "0")),
+                         int(os.environ.get("FMX_INSTANCE_ID", str(rank + 1))), mode=mode)
     peer = inst_mod.peer_info(inst, rank)
     if peer_override and rank in peer_override:
         peer = PeerInfo(rank, peer.pcie_bus_id, peer_override[rank], peer.host_hash, peer.pid_hash)

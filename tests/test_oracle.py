@@ -84,3 +84,33 @@ def test_golden_allreduce_vectors():
         xs = [g[f"{stem}_in{r}"] for r in range(n)]
         assert same(orc.allreduce_c(xs, dtype, op, factor), g[key]), stem
         assert same(orc.allreduce_np(xs, dtype, op, factor), g[key]), stem
+
+
+@pytest.mark.parametrize("dtype", [orc.F32, orc.BF16])
+@pytest.mark.parametrize("n,count,cores", [(2, 1, None), (7, 100_003, None), (4, 3_504_872 // 64, [0]),
+                                           (14, 4099, [0, 1])])
+def test_multiprocess_shm_cpu_path_equals_checker(dtype, n, count, cores):
+    """BASELINE.md §3's CPU reference path - one process per rank over a POSIX
+    SHM segment (oracle/shm_cpu_allreduce.c) - is bit-identical to the
+    checker, also when ranks outnumber the cores it is given."""
+    xs = [orc.synthetic_gradient(r, count, dtype) for r in range(n)]
+    xs[0] = orc.adversarial(0, count, dtype)
+    for op, factor in (orc.ddp_mean(n), (orc.OP_SUM, 1.0)):
+        want = orc.allreduce_c(xs, dtype, op, factor)
+        stats, outs = orc.mp_shm_allreduce(n, count, dtype, op, factor, xs=xs, want_out=True,
+                                           cores=cores)
+        assert stats["processes"] == n
+        assert stats["oversubscribed"] == (cores is not None and len(cores) < n)
+        for r in range(n):
+            assert same(outs[r], want), r
+
+
+@pytest.mark.parametrize("dtype", [orc.F32, orc.BF16])
+def test_inplace_host_reduction_equals_checker(dtype):
+    n, count = 7, 50_001
+    xs = [orc.synthetic_gradient(r, count, dtype) for r in range(n)]
+    want = orc.allreduce_c(xs, dtype, *orc.ddp_mean(n))
+    bufs = [x.copy() for x in xs]
+    orc.inplace_allreduce(bufs, dtype, *orc.ddp_mean(n), nthreads=3)
+    for b in bufs:
+        assert same(b, want)

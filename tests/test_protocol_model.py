@@ -222,6 +222,35 @@ def test_protocol_multi_gpu_world_sizes(n):
         simulate(progs, seed, burst=8)
 
 
+def default_slice(n: int, slots: int = 2) -> int:
+    """fmx_comm_init's default slice (flexshm_comm.cu default_slice_cap /
+    segment_budget): min(cap, budget / (K (n^2 + 2n))), floored to 4 KiB."""
+    cap = (16 << 20) if n <= 2 else (4 << 20)
+    budget = (2 << 30) if n > 14 else (1 << 30)
+    sb = min(cap, budget // (slots * (n * n + 2 * n)))
+    return max(4096, sb // 4096 * 4096)
+
+
+@pytest.mark.parametrize("n,ops", [
+    # C4 at its own shape: BERT-base bf16 gradient over 14 ranks (2 GPUs, 7+7)
+    (14, [("allreduce", 109_483_778, 1), ("allreduce", 25_557_032, 0)]),
+    # C3: MobileNetV2 fp32 gradient over 4 ranks (2+2)
+    (4, [("allreduce", 3_504_872, 0), ("broadcast", 3_504_872, 0, 3)]),
+    # 8 GPUs x 7 instances: the north_star's top configuration, ResNet-50 and
+    # BERT-base gradients with the 56-rank default slice (320 KiB)
+    (56, [("allreduce", 25_557_032, 0), ("allreduce", 109_483_778, 1)]),
+])
+def test_protocol_at_baseline_config_shapes(n, ops):
+    """The BASELINE configs' own message sizes, world sizes and default slice
+    geometry (not a shrunken slice): race-, stale-read- and deadlock-free."""
+    sb = default_slice(n)
+    if n == 56:
+        assert sb == 320 << 10
+    progs = programs(n, ops, sb, "auto")
+    for seed in range(1 if n == 56 else 2):
+        simulate(progs, seed, burst=8)
+
+
 def test_model_catches_a_broken_host_schedule():
     """Drop the REDUCED wait at the end of a host-buffer allreduce: the next
     call's host write of the input races with a slow owner's result write."""
