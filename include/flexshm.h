@@ -147,7 +147,7 @@ int fmx_restore_bus_id(const char* label, char* out);
  * size of every rank's registered host buffer (fmx_host_buffer), 0 = none.
  * Rank 0's slice_bytes / nslots / host_bytes win, and so do the schedule
  * settings of rank 0's environment (FMX_RAMP, FMX_MIN_ROUNDS, FMX_GRAIN,
- * FMX_GATHER_GRAIN, FMX_LANES, FMX_RESULT_VIA_CE, FMX_ZC_MAX), published in
+ * FMX_GATHER_GRAIN, FMX_LANES, FMX_RESULT_VIA_CE, FMX_ZC_MAX, FMX_ONESHOT_MAX), published in
  * the segment header so every rank runs the same protocol.  Peers on another
  * host (different host_hash: the reference's select_transport answers "NET",
  * commsim.py:126-132) are refused with FMX_ERR_UNSUPPORTED: the transport is
@@ -157,7 +157,11 @@ int fmx_comm_init(fmx_comm_t* comm, const char* job_key, int nranks, int rank,
                   size_t host_bytes, int transport, double timeout_s);
 
 /* In-place allowed (send == recv).  count elements of dtype; op/factor per
- * enum fmx_op.  Enqueued on `stream` (a cudaStream_t); returns immediately. */
+ * enum fmx_op.  Enqueued on `stream` (a cudaStream_t); returns immediately.
+ * Messages up to FMX_ONESHOT_MAX bytes (64 KiB; AUTO / ZC transports) take the
+ * one-shot path: every rank publishes its buffer, one flag hop, every rank
+ * reduces all n contributions in rank order - same bits as the pipelined
+ * reduce-scatter / all-gather used above that size. */
 int fmx_allreduce(fmx_comm_t comm, const void* send, void* recv, size_t count, int dtype,
                   int op, float factor, void* stream);
 

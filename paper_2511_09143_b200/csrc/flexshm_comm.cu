@@ -194,12 +194,13 @@ class CudaSink final : public Sink {
       }
       return FMX_OK;
     }
-    return launch_copy(lane, segs, src_sys, nullptr, 0);
+    return launch_copy(lane, segs, src_sys, nullptr, 0, nullptr);
   }
 
-  // zero-copy copy kernel(s); with `flag` (a single launch) the kernel releases it
+  // zero-copy copy kernel(s); with `flag` (a single launch) the kernel releases it,
+  // electing the last CTA through the device counter `done`
   int launch_copy(int lane, const std::vector<PlanSeg>& segs, bool src_sys, uint32_t* flag,
-                  uint32_t v) {
+                  uint32_t v, unsigned int* done) {
     cudaStream_t s = lane_stream(c_, lane);
     for (size_t i0 = 0; i0 < segs.size(); i0 += kMaxSegs) {
       if (int rc = drain()) return rc;
@@ -209,7 +210,7 @@ class CudaSink final : public Sink {
       a.src_sys = src_sys ? 1 : 0;
       a.flag = flag;
       a.flag_value = v;
-      a.ctas_done = c_->ctas_done;
+      a.ctas_done = done;
       size_t maxb = 0;
       for (int k = 0; k < a.nseg; ++k) {
         a.seg[k] = CopySeg{segs[i0 + k].src, segs[i0 + k].dst, segs[i0 + k].bytes};
@@ -329,8 +330,9 @@ class CudaSink final : public Sink {
         segs.size() > (size_t)kMaxSegs || c_->stamps)
       return Sink::copy_signal(lane, segs, src_sys, use_kernel, flag, v);
     const uint32_t* fl = (const uint32_t*)c_->flag_dev(c_->rank, flag);
-    int rc = launch_copy(lane, segs, src_sys, (uint32_t*)fl, v);
-    return rc;
+    // one counter per lane that fuses signals (stage copies on lane 0, the
+    // one-shot publish on lane 1), so two fused copies never share a counter
+    return launch_copy(lane, segs, src_sys, (uint32_t*)fl, v, c_->ctas_done + (lane == kLaneMain));
   }
 
   int reduce(int lane, const PlanReduce& r) override {
@@ -448,7 +450,9 @@ int make_lane_objects(fmx_comm* c, CUcontext ctx) {
 // after one, waits for the previous collective to complete.  Every runtime
 // call happens with the caller's stream context current (DDP calls hooks from
 // autograd threads whose current context may be another one).
-//   cls: 0 device-buffer allreduce / reduce-scatter / all-gather, 1 other.
+//   cls: 0 device-buffer allreduce / reduce-scatter / all-gather, 1 other,
+//        2 device-buffer collective on lane 1 alone (the one-shot allreduce: no
+//        extra streams forked or joined).
 template <typename F>
 int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
   CUcontext ctx = nullptr;
@@ -468,9 +472,11 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
   c->user = user;
   cudaStream_t main = c->join_stream ? c->join_stream : user;  // lane 1 and the join target
   // extra lane streams in use: lane 0, and lane 2 with three lanes
+  const bool single = cls == 2;
+  if (single) cls = 0;
   std::vector<cudaStream_t> extra;
-  if (c->nlanes >= 2 && !c->join_stream) extra.push_back(c->lane[0]);
-  if (c->nlanes == 3 && !c->join_stream) extra.push_back(c->lane[2]);
+  if (c->nlanes >= 2 && !c->join_stream && !single) extra.push_back(c->lane[0]);
+  if (c->nlanes == 3 && !c->join_stream && !single) extra.push_back(c->lane[2]);
   // host-path / broadcast calls (and the first device call after one) wait for
   // the previous collective, whichever stream it joined (redundant, and free,
   // when it joined the caller's stream)
@@ -557,7 +563,8 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
       sb = std::min(default_slice_cap(nranks), segment_budget(nranks) / per);
     }
     sb = std::max<size_t>(4096, sb / 4096 * 4096);
-    Layout L = compute_layout(nranks, c->nslots, sb, host_bytes);
+    const Proto proto = proto_from_env();
+    Layout L = compute_layout(nranks, c->nslots, sb, host_bytes, (size_t)std::max(0, proto.oneshot_max));
     shm_unlink(name.c_str());  // stale segment of a crashed job with the same key
     int fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
     if (fd < 0) {
@@ -590,12 +597,14 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
     h->ar_in_off = L.ar_in_off;
     h->ar_out_off = L.ar_out_off;
     h->bc_off = L.bc_off;
+    h->os_off = L.os_off;
+    h->os_bytes = L.os_bytes;
     h->user_off = L.user_off;
     h->user_bytes = L.user_bytes;
     h->creator_pid = (int32_t)getpid();
     h->mig_aware = mig_aware ? 1 : 0;
     snprintf(h->job_key, sizeof h->job_key, "%s", job_key);
-    h->proto = proto_from_env();  // every rank runs rank 0's schedule settings
+    h->proto = proto;  // every rank runs rank 0's schedule settings
     h->magic.store(kMagicReady, std::memory_order_release);
   } else {
     for (;;) {
@@ -643,7 +652,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   c->slice_bytes = h->slice_bytes;
   c->nslots = h->nslots;  // rank 0's choice wins
   c->L = Layout{h->peers_off, h->flags_off, h->ar_in_off, h->ar_out_off, h->bc_off,
-                h->user_off, h->user_bytes, h->total_bytes};
+                h->os_off,    h->os_bytes,  h->user_off,   h->user_bytes, h->total_bytes};
   c->mig_aware = h->mig_aware;
 
   // publish this rank's PeerInfo
@@ -729,8 +738,8 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   }
   // HBM scratch: CE contributions [n] (device path) / [2][n] fetch + [2][n] result replicas (host path)
   if (e == cudaSuccess) e = cudaMalloc((void**)&c->scratch, 4 * (size_t)nranks * c->slice_bytes);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&c->ctas_done, sizeof(unsigned int));
-  if (e == cudaSuccess) e = cudaMemset(c->ctas_done, 0, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&c->ctas_done, 2 * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(c->ctas_done, 0, 2 * sizeof(unsigned int));
 
 
   // local-only knobs (how this rank issues its copies; the protocol is unchanged)
@@ -797,6 +806,11 @@ int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int 
       return sink.reduce(kLaneMain, pr);
     });
   }
+  if (c->use_oneshot(count * esz))
+    return on_lanes(c, s, 2, [&]() {
+      return plan_allreduce_oneshot(c, sink, (const char*)send, (char*)recv, count, dtype, op,
+                                    factor, aligned);
+    });
   return on_lanes(c, s, 0, [&]() {
     return plan_allreduce(c, sink, (const char*)send, (char*)recv, count, dtype, op, factor,
                           aligned);

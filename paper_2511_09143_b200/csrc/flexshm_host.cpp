@@ -43,7 +43,8 @@ double now_s() {
   return duration<double>(steady_clock::now().time_since_epoch()).count();
 }
 
-Layout compute_layout(int nranks, int nslots, size_t slice_bytes, size_t user_bytes) {
+Layout compute_layout(int nranks, int nslots, size_t slice_bytes, size_t user_bytes,
+                      size_t os_bytes) {
   Layout L;
   const size_t page = 4096;
   size_t off = page;  // header
@@ -57,6 +58,9 @@ Layout compute_layout(int nranks, int nslots, size_t slice_bytes, size_t user_by
   off += (size_t)nslots * nranks * slice_bytes;
   L.bc_off = off;
   off += (size_t)nslots * nranks * slice_bytes;
+  L.os_off = off = align_up(off, page);
+  L.os_bytes = align_up(os_bytes, page);
+  off += (size_t)kOsSlots * nranks * L.os_bytes;
   L.user_off = off = align_up(off, page);
   L.user_bytes = align_up(user_bytes, page);
   off += (size_t)nranks * L.user_bytes;

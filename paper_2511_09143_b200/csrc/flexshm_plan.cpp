@@ -110,6 +110,7 @@ Proto proto_from_env() {
   p.nlanes = 3;
   p.result_via_ce = 0;
   p.zc_max = 2u << 20;
+  p.oneshot_max = 64 << 10;
   if (const char* v = getenv("FMX_RESULT_VIA_CE")) p.result_via_ce = atoi(v) != 0;
   if (const char* v = getenv("FMX_GRAIN")) {
     p.coarse = strcmp(v, "fine") != 0;
@@ -121,6 +122,8 @@ Proto proto_from_env() {
   if (const char* v = getenv("FMX_RAMP")) p.ramp = atoi(v);
   if (const char* v = getenv("FMX_MIN_ROUNDS")) p.min_rounds = atoi(v);
   if (const char* v = getenv("FMX_ZC_MAX")) p.zc_max = strtoull(v, nullptr, 10);
+  if (const char* v = getenv("FMX_ONESHOT_MAX"))
+    p.oneshot_max = (int32_t)std::min<long long>(std::max(0ll, atoll(v)), (long long)kOneShotCap);
   return p;
 }
 
@@ -133,6 +136,7 @@ void apply_proto(fmx_comm* c, const Proto& p) {
   c->nlanes = p.nlanes;
   c->result_via_ce = p.result_via_ce != 0;
   c->zc_max = p.zc_max;
+  c->oneshot_max = (size_t)std::max(0, p.oneshot_max);
 }
 
 // Round j of every chunk covers [prefix(j), prefix(j) + size(j)).  By default
@@ -430,6 +434,59 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
   return FMX_OK;
 }
 
+// One-shot allreduce for small messages (AUTO / ZC, bytes <= oneshot_max): the
+// two-hop reduce-scatter / all-gather above pays STAGED -> REDUCED -> gather,
+// three flag hops and five launches, for a message the link moves in a few
+// microseconds.  Here every rank publishes its whole buffer into its one-shot
+// slot with one zero-copy kernel that releases OS_READY itself, waits for every
+// peer's OS_READY, and reduces all n contributions in ascending rank order
+// straight out of the segment (its own from HBM) into its buffer: one flag hop,
+// two launches, one flag write, and every rank computes the same bits as the owner of that
+// chunk would (same kernel, same order).  Single lane (lane 1), no HBM scratch.
+// Slots alternate (kOsSlots = 2) and need no credit flag: slot J % 2 is next
+// written at call J + 2, after this rank's wait of call J + 1 saw every peer's
+// OS_READY >= J + 2 - and each peer publishes call J + 1 only after its reduce
+// of call J (which read my slot) in its stream order.  The model checker
+// confirms it (tests/test_protocol_model.py).  Own round counter and flag:
+// mixing with the pipelined collectives shares nothing but the stream.
+constexpr uint32_t kOsTag = 1u << 30;  // trace: one-shot rounds, apart from pipeline rounds
+
+int plan_allreduce_oneshot(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count,
+                           int dtype, int op, float factor, bool aligned) {
+  const int n = c->nranks, me = c->rank;
+  const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2, bytes = count * esz;
+  const uint32_t J = c->os_round;
+  int rc;
+  const size_t mine = c->os_slot_off(J, me);
+  std::vector<PlanSeg> segs{{src, c->at(true, mine), bytes, Annot{(int64_t)mine, bytes, me, J | kOsTag},
+                             true, ubuf(0, bytes)}};
+  if ((rc = k.copy_signal(kLaneMain, segs, false, true, kOsReady, J + 1))) return rc;
+  if ((rc = k.wait_peers(kLaneMain, kOsReady, J + 1, me))) return rc;
+  PlanReduce pr;
+  memset(&pr.args, 0, sizeof pr.args);
+  pr.dtype = dtype;
+  pr.aligned = aligned;
+  pr.args.nsrc = n;
+  pr.args.len = count;
+  pr.args.op = op;
+  pr.args.factor = factor;
+  pr.args.out_dev = dst;
+  pr.user_rw = ubuf(0, bytes);
+  for (int q = 0; q < n; ++q) {
+    if (q == me) {
+      pr.args.src[q] = src;
+      continue;
+    }
+    const size_t off = c->os_slot_off(J, q);
+    pr.args.src[q] = c->at(true, off);
+    pr.args.sys_mask |= 1ull << q;
+    pr.reads.push_back(Annot{(int64_t)off, bytes, q, J | kOsTag});
+  }
+  if ((rc = k.reduce(kLaneMain, pr))) return rc;
+  c->os_round = J + 1;
+  return FMX_OK;
+}
+
 // Allreduce over the ranks' registered host buffers (the regions at the end of
 // the segment): in place, no staging and no all-gather.  Every input already
 // sits in host memory, so owner r copy-engines piece j of chunk r out of all n
@@ -596,7 +653,7 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   c.slice_bytes = slice_bytes;
   size_t max_bytes = 0;
   for (int i = 0; i < nops; ++i) max_bytes = std::max(max_bytes, counts[i] * (dtypes[i] ? 2 : 4));
-  c.L = compute_layout(nranks, c.nslots, slice_bytes, max_bytes);
+  c.L = compute_layout(nranks, c.nslots, slice_bytes, max_bytes, c.oneshot_max);
   c.total_bytes = c.L.total;
   std::string out;
   TraceSink sink(&out);
@@ -614,7 +671,10 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
     sink.user_base = overlap ? (int64_t)i << 40 : 0;
     if (kinds[i] == 1 && (!roots || roots[i] < 0 || roots[i] >= nranks))
       return fail(FMX_ERR_INVALID_ARG, "bad broadcast root");
-    if (kinds[i] == 0)
+    const size_t esz = dtypes[i] ? 2 : 4;
+    if (kinds[i] == 0 && c.use_oneshot(counts[i] * esz))
+      rc = plan_allreduce_oneshot(&c, sink, dummy, dummy, counts[i], dtypes[i], FMX_OP_SUM, 1.0f, true);
+    else if (kinds[i] == 0)
       rc = plan_allreduce(&c, sink, dummy, dummy, counts[i], dtypes[i], FMX_OP_SUM, 1.0f, true);
     else if (kinds[i] == 3 || kinds[i] == 4)  // reduce-scatter / all-gather, in place
       rc = plan_allreduce(&c, sink, dummy, dummy, counts[i], dtypes[i], FMX_OP_SUM, 1.0f, true,

@@ -29,7 +29,7 @@ struct fmx_comm {
   char* dbase = nullptr;  // device VA of the same bytes
   Header* hdr = nullptr;
   bool registered = false;
-  uint32_t ar_round = 0, bc_round = 0;
+  uint32_t ar_round = 0, bc_round = 0, os_round = 0;
   int64_t barrier_gen = 0;
   char* scratch = nullptr;  // CE transport: n * slice_bytes of HBM
   cudaStream_t lane[3] = {};       // extra streams of lane 0 (stage, D2H) and lane 2 (gather, H2D); [1] unused
@@ -41,8 +41,8 @@ struct fmx_comm {
   bool fuse_signal = true;             // FMX_FUSE_SIGNAL=0: zero-copy stage + STAGED as two ops
   bool serialize = false;              // drain this rank's lanes before every kernel launch
                                        //   (under a kernel profiler / FMX_SERIALIZE=1)
-  unsigned int* ctas_done = nullptr;   // device counter of the fused signal (per comm; lanes
-                                       //   never run two fused copies at once: lane 0 only)
+  unsigned int* ctas_done = nullptr;   // device counters of the fused signal: [0] lane 0's
+                                       //   stage copies, [1] the one-shot publish (lane 1)
   int last_class = -1;              // 0 device-buffer collective, 1 host path / broadcast
   CUcontext lane_ctx = nullptr;                // context the lane objects were created in
   cudaEvent_t ev[fmx::kNumEvents] = {};  // intra-rank lane sync (see the kEv* ids)
@@ -62,6 +62,14 @@ struct fmx_comm {
   // 1 KiB at 7 ranks) and the copy engines above zc_max (crossover 1-4 MiB, r01/r3j)
   bool use_zc(size_t bytes) const {
     return transport == FMX_TRANSPORT_ZC || (transport == FMX_TRANSPORT_AUTO && bytes <= zc_max);
+  }
+  // One-shot small-message allreduce (plan_allreduce_oneshot): every rank
+  // publishes its whole buffer, one flag hop, every rank reduces all n in rank
+  // order.  Taken by AUTO / ZC for messages up to oneshot_max bytes.
+  size_t oneshot_max = 64u << 10;
+  bool use_oneshot(size_t bytes) const {
+    return transport != FMX_TRANSPORT_CE && transport != FMX_TRANSPORT_HOST && nranks > 1 &&
+           bytes <= oneshot_max && bytes <= L.os_bytes;
   }
   int nlanes = 3;              // FMX_LANES=1: one stream; 2: gather on the reduce lane
   // live kernel timing (fmx_comm_set_timing): event pairs around every reduce
@@ -87,6 +95,9 @@ struct fmx_comm {
   }
   size_t bc_slot_off(uint32_t R) const {
     return L.bc_off + (size_t)(R % nslots) * nranks * slice_bytes;
+  }
+  size_t os_slot_off(uint32_t J, int r) const {
+    return L.os_off + ((size_t)(J % fmx::kOsSlots) * nranks + r) * L.os_bytes;
   }
   size_t user_region_off(int r) const { return L.user_off + (size_t)r * L.user_bytes; }
   // host (dev=false) or device (dev=true) address of a segment offset
@@ -223,6 +234,8 @@ void apply_proto(fmx_comm* c, const Proto& p);
 
 int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
                    int op, float factor, bool aligned, int kind = kAllreduce);
+int plan_allreduce_oneshot(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count,
+                           int dtype, int op, float factor, bool aligned);
 int plan_allreduce_host(fmx_comm* c, Sink& k, size_t off_bytes, size_t count, int dtype, int op,
                         float factor);
 int plan_broadcast(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,

@@ -16,12 +16,17 @@ void set_dup(int a, int b);
 
 // ---- SHM segment layout ----------------------------------------------------
 // [header 4 KiB][peer table][flag lines][AR in-slots][AR out-slots][BC slots]
-// [user region of rank 0] ... [user region of rank n-1]
+// [one-shot slots][user region of rank 0] ... [user region of rank n-1]
 // Every region starts on a 4 KiB boundary; every flag owns a 64-byte line.
 constexpr uint32_t kMagicReady = 0x464D5831u;  // "FMX1"
-constexpr uint32_t kVersion = 2;
+constexpr uint32_t kVersion = 3;
 // Per rank: 8 scalar flags, then one STAGED_TO flag per destination owner.
-enum Flag { kStaged = 0, kReduced = 1, kBcStaged = 2, kBcDone = 3, kStagedTo = 8 };
+// OS_READY is the one-shot small-message allreduce's own round counter
+// (plan_allreduce_oneshot, flexshm_plan.cpp).
+enum Flag { kStaged = 0, kReduced = 1, kBcStaged = 2, kBcDone = 3, kOsReady = 4, kStagedTo = 8 };
+// One-shot slots: [kOsSlots][rank][os_bytes], alternating between calls.
+constexpr int kOsSlots = 2;
+constexpr size_t kOneShotCap = 1u << 20;  // largest one-shot message (FMX_ONESHOT_MAX is clamped)
 constexpr int kFlagsPerRank = kStagedTo + FMX_MAX_RANKS;
 
 struct alignas(64) PeerSlot {
@@ -33,11 +38,13 @@ struct alignas(64) PeerSlot {
 // Settings that change the schedule - piece boundaries, which flags are
 // signalled, which lane gathers, the transport of a collective.  Rank 0
 // publishes its own (read from its environment, FMX_RAMP, FMX_MIN_ROUNDS,
-// FMX_GRAIN, FMX_GATHER_GRAIN, FMX_LANES, FMX_RESULT_VIA_CE, FMX_ZC_MAX) in the
+// FMX_GRAIN, FMX_GATHER_GRAIN, FMX_LANES, FMX_RESULT_VIA_CE, FMX_ZC_MAX,
+// FMX_ONESHOT_MAX) in the
 // segment header and every rank adopts them, so ranks cannot disagree on the
 // protocol (a mismatch would give wrong results or park a stream forever).
 struct Proto {
-  int32_t ramp, min_rounds, coarse, fine_first, coarse_gather, nlanes, result_via_ce, pad;
+  int32_t ramp, min_rounds, coarse, fine_first, coarse_gather, nlanes, result_via_ce;
+  int32_t oneshot_max;  // bytes; allreduces up to this size take the one-shot path (0: off)
   uint64_t zc_max;
 };
 
@@ -48,7 +55,7 @@ struct Header {
   int32_t nslots;
   uint64_t slice_bytes;
   uint64_t total_bytes;
-  uint64_t peers_off, flags_off, ar_in_off, ar_out_off, bc_off;
+  uint64_t peers_off, flags_off, ar_in_off, ar_out_off, bc_off, os_off, os_bytes;
   uint64_t user_off, user_bytes;  // per-rank registered host buffers
   int32_t creator_pid;
   int32_t mig_aware;
@@ -65,9 +72,11 @@ struct Header {
 static_assert(sizeof(Header) <= 4096, "the header owns the first page of the segment");
 
 struct Layout {
-  size_t peers_off, flags_off, ar_in_off, ar_out_off, bc_off, user_off, user_bytes, total;
+  size_t peers_off, flags_off, ar_in_off, ar_out_off, bc_off, os_off, os_bytes, user_off, user_bytes,
+      total;
 };
-Layout compute_layout(int nranks, int nslots, size_t slice_bytes, size_t user_bytes);
+Layout compute_layout(int nranks, int nslots, size_t slice_bytes, size_t user_bytes,
+                      size_t os_bytes);
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 

@@ -463,3 +463,70 @@ def test_overlap_mode_needs_the_cross_call_waits(monkeypatch):
         except AssertionError:
             failures += 1
     assert failures > 0
+
+
+# ---- one-shot small-message allreduce (plan_allreduce_oneshot) ----------------
+
+OS_READY = 4  # kOsReady
+ONESHOT_SEQ = ([("allreduce", 1 + 37 * i, i % 2) for i in range(9)]
+               + [("allreduce", 60_000, 0), ("allreduce", 5, 1), ("broadcast", 300, 0, 1),
+                  ("allreduce", 16_384, 0), ("reduce_scatter", 11, 0), ("allreduce", 3, 0),
+                  ("allreduce_host", 700, 0), ("allreduce", 32_768, 1)])
+
+
+def test_oneshot_is_selected_by_size():
+    """AUTO takes the one-shot path up to FMX_ONESHOT_MAX bytes (64 KiB): one
+    publish + OS_READY, one wait, one reduce - no pipeline flags."""
+    small = _lib.trace_plan(7, 3, [("allreduce", 16_384, 0)], 4096, "auto")
+    assert f" S {OS_READY} 1" in small and small.count(" S ") == 1
+    assert " S 0 " not in small and " S 1 " not in small  # no STAGED / REDUCED
+    big = _lib.trace_plan(7, 3, [("allreduce", 16_385, 0)], 4096, "auto")
+    assert f" S {OS_READY} " not in big
+    ce = _lib.trace_plan(7, 3, [("allreduce", 5, 0)], 4096, "ce")
+    assert f" S {OS_READY} " not in ce
+
+
+@pytest.mark.parametrize("n", [2, 3, 7])
+def test_oneshot_mixed_with_pipelined_collectives(n):
+    """More one-shot calls than slots (slot reuse), interleaved with pipelined
+    allreduces, broadcasts, reduce-scatters and host-path calls."""
+    progs = programs(n, ONESHOT_SEQ, 4096, "auto")
+    for seed in range(10):
+        simulate(progs, seed)
+    merged = programs(n, ONESHOT_SEQ, 4096, "auto", merged=True)
+    for seed in range(4):
+        simulate(merged, seed)
+
+
+def test_oneshot_at_56_ranks():
+    ops = [("allreduce", 256, 0)] * 6 + [("allreduce", 32_768, 1)]
+    progs = programs(56, ops, 320 << 10, "auto")
+    simulate(progs, 0, burst=8)
+
+
+def test_model_catches_a_broken_oneshot():
+    """Drop one rank's OS_READY waits: it reduces peer slots before they were
+    published (and overwrites its own slot while a slow peer still reads it)."""
+    ops = [("allreduce", 1000, 0)] * 5
+    progs = programs(3, ops, 4096, "auto")
+    lanes = progs[1]
+    broken_lanes = [[op for op in lane if not (op[0] == "A" and op[2] == OS_READY)] for lane in lanes]
+    assert broken_lanes != lanes
+    broken = [broken_lanes if r == 1 else p for r, p in enumerate(progs)]
+    failures = 0
+    for seed in range(100):
+        try:
+            simulate(broken, seed)
+        except AssertionError:
+            failures += 1
+    assert failures > 0
+
+
+def test_oneshot_slot_reuse_needs_no_credit_flag():
+    """Twelve back-to-back one-shot calls reuse the two slots six times each:
+    race-free without a credit flag, because a peer publishes call J+1 only
+    after its reduce of call J read my slot."""
+    ops = [("allreduce", 64, 0)] * 12
+    progs = programs(4, ops, 4096, "auto")
+    for seed in range(20):
+        simulate(progs, seed, burst=1)
