@@ -73,6 +73,11 @@ def parse_args(argv=None):
     p.add_argument("--nccl", action="store_true",
                    help="N>1: also time stock NCCL over NVLink, one rank per GPU (comparison "
                         "point; opt-in because NCCL inside MPS clients is untested here)")
+    p.add_argument("--nccl-shm", action="store_true",
+                   help="N>1: the NCCL comparison point over NCCL's own SHM transport "
+                        "(NCCL_P2P_DISABLE=1, NCCL_NVLS_ENABLE=0: the paper's SHM-vs-NET "
+                        "setting, PAPER.md:750-770); a separate run from --nccl, because NCCL "
+                        "reads these variables once per process")
     p.add_argument("--buckets", type=int, default=0,
                    help="probe: allreduce the gradient as K back-to-back buckets (join-stream mode)")
     p.add_argument("--bucket-serial", action="store_true",
@@ -765,6 +770,53 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
             "gpu_launches": sum(r["launches"] for r in res.values()), "model": desc}
 
 
+def dry_exchange(d, mine: list[int], job_key: str, m: int = 4099) -> dict[int, int]:
+    """--dry-run data path without CUDA: this process's instance ranks, one
+    thread each, join the job's FMX_TRANSPORT_HOST communicator (the real SHM
+    bootstrap, peer table and MIG-aware checks, across every torchrun process),
+    each writes m seeded fp32 values into its registered host region, and after
+    a barrier reads every rank's region and sums them in rank order.  Returns
+    rank -> crc32 of that sum; all ranks of all processes must agree."""
+    import threading
+    import zlib
+
+    import numpy as np
+
+    from paper_2511_09143_b200.comm import init_process_group
+    from paper_2511_09143_b200.commsim import PeerInfo
+
+    n = len(d.instances)
+    host = zlib.crc32(os.uname().nodename.encode())
+    out, errs = {}, []
+
+    def one(r):
+        try:
+            g, i = d.instances[r]
+            peer = PeerInfo(r, f"{0x1B + g:02X}:00:00.0", f"MIG-dry-{g}-{i}", host, os.getpid())
+            comm = init_process_group(None, r, job_key + "-dry", peer=peer, nranks=n,
+                                      transport="host", host_bytes=4 * m, timeout_s=120)
+            x = np.random.default_rng(1000 + r).standard_normal(m).astype(np.float32)
+            comm.host_buffer()[:4 * m].numpy()[:] = x.view(np.uint8)
+            comm.barrier(120)
+            acc = np.zeros(m, np.float32)
+            for q in range(n):
+                acc = acc + comm.host_buffer(q)[:4 * m].numpy().view(np.float32)
+            comm.barrier(120)  # nobody leaves while a peer still reads its region
+            out[r] = zlib.crc32(acc.tobytes())
+            comm.destroy()
+        except BaseException as exc:  # noqa: BLE001
+            errs.append((r, exc))
+
+    ths = [threading.Thread(target=one, args=(r,)) for r in mine]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    if errs:
+        raise RuntimeError(f"dry-run rank {errs[0][0]} failed: {errs[0][1]!r}") from errs[0][1]
+    return out
+
+
 def run_ours(args) -> dict | None:
     import torch
 
@@ -791,7 +843,7 @@ def run_ours(args) -> dict | None:
         job_key = obj[0]
     my_gpu = grank if world > 1 else 0
     mine = [r for r, (g, _) in enumerate(d.instances) if g == my_gpu] if world > 1 else list(range(n))
-    gpu_local = local if world > 1 else 0
+    gpu_local = local if world > 1 and not os.environ.get("FMX_ONE_GPU_VISIBLE") else 0
     if os.environ.get("FMX_DEVICE_MAP"):
         # e.g. "0,0": run the N>1 orchestration with several logical GPUs on one device
         gpu_local = int(os.environ["FMX_DEVICE_MAP"].split(",")[local])
@@ -801,10 +853,15 @@ def run_ours(args) -> dict | None:
     errors = []
 
     if args.dry_run:
-        # stub ranks: distinct, known timings so the MAX-over-ranks reduction is checkable
+        # no CUDA: every instance rank joins ONE host-transport communicator across
+        # all torchrun processes and exchanges data through the registered host
+        # regions of the shared segment (dry_exchange); stub timings, distinct and
+        # known, so the MAX-over-ranks reduction is checkable
+        digests_dry = dry_exchange(d, mine, job_key)
         results = {r: {"rank": r, "ms_total": 10.0 * (r + 1), "launches": 1, "kernel_ms": 0.0,
                        "kernel_count": 0, "ms_total_e2e": 5.0 * (r + 1),
-                       "ms_total_e2e_dev": 6.0 * (r + 1), "e2e_digest": 0, "job_key": job_key}
+                       "ms_total_e2e_dev": 6.0 * (r + 1), "e2e_digest": digests_dry[r],
+                       "job_key": job_key}
                    for r in mine}
     else:
         try:
@@ -831,6 +888,10 @@ def run_ours(args) -> dict | None:
     digests = {r.get("e2e_digest") for r in results.values()}
     if world > 1:
         import torch.distributed as dist
+        every = [None] * world
+        dist.all_gather_object(every, {r: v.get("e2e_digest") for r, v in results.items()})
+        all_digests = {k: v for part in every for k, v in part.items()}
+        digests = set(all_digests.values())
         t = torch.tensor([local_max, local_max_e2e, float(launches), kernel_ms, float(kernel_count),
                           local_max_e2e_dev], dtype=torch.float64)
         mx = t.clone()
@@ -881,6 +942,13 @@ def run_ours(args) -> dict | None:
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    if args.dry_run:
+        line["dry_exchange"] = {
+            "ranks": len(all_digests) if world > 1 else len(results), "agree": len(digests) == 1,
+            "what": "no CUDA: every instance rank (threads of its GPU's torchrun process) joined "
+                    "one FMX_TRANSPORT_HOST communicator, wrote seeded fp32 values into its "
+                    "registered host region of the shared segment and rank-order summed every "
+                    "rank's region after a barrier; crc32 of the sums agree across processes"}
     if getattr(args, "mps_fallback", None):
         line["config"]["mps_fallback"] = args.mps_fallback
     if os.environ.get("FMX_DEVICE_MAP"):
@@ -918,12 +986,18 @@ def run_ours(args) -> dict | None:
     return line
 
 
-def run_nccl_point(args) -> dict:
+def run_nccl_point(args, transport: str = "nvlink") -> dict:
     """Comparison point (north_star): stock NCCL allreduce of the same gradient
-    bytes over NVLink, one rank per GPU (the torchrun ranks), CUDA events, max
-    over ranks.  Not the product path; never raises into the bench line."""
+    bytes, one rank per GPU (the torchrun ranks), CUDA events, max over ranks;
+    transport "nvlink" (NCCL's default P2P / NVLS over NVSwitch) or "shm"
+    (P2P and NVLS off: NCCL's host shared-memory transport, the stock
+    equivalent of this repo's path).  Not the product path; never raises into
+    the bench line."""
     import torch
     import torch.distributed as dist
+    if transport == "shm":
+        os.environ.update(NCCL_P2P_DISABLE="1", NCCL_NVLS_ENABLE="0", NCCL_SHM_DISABLE="0",
+                          NCCL_IB_DISABLE="1")
     try:
         local = int(os.environ.get("LOCAL_RANK", "0"))
         dev = torch.device("cuda", local)
@@ -948,8 +1022,11 @@ def run_nccl_point(args) -> dict:
         dist.destroy_process_group(pg)
         return {"ms_per_step": ms, "algbw_gbs": s_bytes / ms / 1e6,
                 "busbw_gbs": s_bytes / ms / 1e6 * 2 * (n - 1) / n, "ranks": n,
-                "note": "stock NCCL over NVLink, one rank per GPU (this process is also an "
-                        "instance's MPS client, so NCCL runs on its SM share)"}
+                "transport": transport,
+                "note": f"stock NCCL ({'NVLink/NVSwitch' if transport == 'nvlink' else 'SHM: '
+                                      'NCCL_P2P_DISABLE=1 NCCL_NVLS_ENABLE=0'}), one rank per "
+                        "GPU (this process is also an instance's MPS client, so NCCL runs on "
+                        "its SM share)"}
     except Exception as exc:  # noqa: BLE001
         return {"error": repr(exc)[:300]}
 
@@ -1046,6 +1123,17 @@ def main(argv=None):
         print(json.dumps(line))
         return 0
     mps = start_mps(args, world)
+    if args.nccl and args.nccl_shm:
+        raise SystemExit("--nccl and --nccl-shm are separate runs (NCCL caches its env per process)")
+    if world > 1 and not args.dry_run and not (args.nccl or args.nccl_shm) and \
+            not os.environ.get("FMX_DEVICE_MAP"):
+        # one GPU per torchrun process and its instance processes (they inherit
+        # the variable): no peer device is even visible, so P2P / NVLink cannot
+        # be used - the transport is what MIG allows.  After the
+        # MPS daemon started (it must see every GPU); --nccl keeps every GPU
+        # visible for the NVLink comparison point.
+        os.environ["CUDA_VISIBLE_DEVICES"] = os.environ.get("LOCAL_RANK", "0")
+        os.environ["FMX_ONE_GPU_VISIBLE"] = "1"
     try:
         return _main(args, world, n, unit)
     finally:
@@ -1125,10 +1213,11 @@ def _main(args, world, n, unit):
                 f.write(json.dumps(line) + "\n")
         return 0
     line = run_ours(args)
-    if world > 1 and not args.dry_run and args.nccl:
-        nccl = run_nccl_point(args)          # collective: every torchrun rank takes part
+    if world > 1 and not args.dry_run and (args.nccl or args.nccl_shm):
+        tr = "shm" if args.nccl_shm else "nvlink"
+        nccl = run_nccl_point(args, tr)      # collective: every torchrun rank takes part
         if line is not None:
-            line["nccl_nvlink"] = nccl
+            line[f"nccl_{tr}"] = nccl
     if line is None:
         return 0
     if not args.no_train and args.gpus == 1 and world == 1:

@@ -165,7 +165,20 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t c
   }
   std::vector<size_t> sizes;
   const size_t s = g.slice;
-  if (c->ramp && g.chunk > s) {
+  if (c->ramp == 4 && g.chunk > s) {
+    // FMX_RAMP=4: as many rounds as equal ones would take, all full slices but
+    // the FIRST, which takes the remainder: the pipeline fill (every rank's
+    // round-0 staging, H2D idle) shrinks without adding a round
+    const size_t k = (g.chunk + s - 1) / s;
+    size_t first = (g.chunk - (k - 1) * s) / vec * vec;
+    if (first == 0) first = s;  // remainder under one vector: a full first round instead
+    sizes.push_back(first);
+    for (size_t left = g.chunk - first; left;) {
+      const size_t y = std::min(s, left);
+      sizes.push_back(y);
+      left -= y;
+    }
+  } else if (c->ramp && g.chunk > s) {
     // geometric ramp s/8, s/4, s/2 up and down (as much of it as fits in half
     // the chunk each way), the middle in equal rounds of at most s
     std::vector<size_t> up;

@@ -52,7 +52,8 @@ struct fmx_comm {
   bool coarse = true;          // FMX_GRAIN=fine: per-piece waits instead of all-peer
   bool fine_first = false;     // FMX_GRAIN=first: per-contributor flags in round 0 only
   bool coarse_gather = true;   // FMX_GATHER_GRAIN=fine: per-owner gather waits only
-  int ramp = 0;                // FMX_RAMP=1: geometric s/8, s/4, s/2 fill / drain rounds; 2: fill only (off:
+  int ramp = 0;                // FMX_RAMP=1: geometric s/8, s/4, s/2 fill / drain rounds; 2: fill only;
+                               // 4: remainder-sized first round, no extra round (off:
                                // with the copy fence, equal rounds are 3-4% faster, r01/r3e)
   int min_rounds = 1;          // FMX_MIN_ROUNDS: shrink the slice so a chunk spans >= this many
   size_t zc_max = 2u << 20;    // FMX_ZC_MAX: AUTO transport moves messages <= this with SM copies

@@ -1,8 +1,11 @@
 """The torchrun N>1 path of bench.py on CPU (gloo, world size 2): rank ->
 GPU -> instance partition from fm_select, one job key for all ranks, MAX
 over ranks of the step time, SUM of launches, a single JSON line from rank 0,
-and the reference arm printing from rank 0 only.  Rank bodies are stubs
-(--dry-run): the CUDA data path is covered by the -m gpu tests."""
+and the reference arm printing from rank 0 only.  --dry-run rank bodies make
+no CUDA call: the 14 instance ranks of both torchrun processes join one
+host-transport communicator (the real SHM bootstrap across processes) and
+exchange data through their registered host regions; timings are stubs.  The
+CUDA data path is covered by the -m gpu tests."""
 
 from __future__ import annotations
 
@@ -49,6 +52,8 @@ def test_two_gpu_launch_reduces_over_ranks():
     assert abs(ln["algbw_gbs"] * 14 - ln["value"]) < 1e-6
     assert ln["scaling"] == "weak"
     assert ln["step_roofline"]["link_bytes_per_gpu"]["d2h"] == 7 * ln["config"]["bytes"]
+    # the cross-process exchange over the shared segment: 14 ranks, one answer
+    assert ln["dry_exchange"]["ranks"] == 14 and ln["dry_exchange"]["agree"]
 
 
 def test_reference_arm_prints_once_under_torchrun():

@@ -85,6 +85,27 @@ def test_perf_model_calibration():
         PerfModel.from_measurement(0.0, 1.0)
 
 
+def test_perf_model_one_to_one_calibration():
+    """tools/calibrate_perfmodel.py: multi_overhead = T(k x 1g, batch b each) /
+    T(1 instance of the combined size, batch k*b) - the reference's
+    one-to-many over one-to-one (simcore.py:46-51)."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "calib", os.path.join(os.path.dirname(__file__), "..", "tools", "calibrate_perfmodel.py"))
+    calib = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(calib)
+    many = {"resnet50": {"instances": 7, "batch_per_instance": 32, "ms_per_step": 70.0,
+                         "no_sync": {"ms_per_step": 56.0}}}
+    one = {"resnet50": {"instances": 1, "batch_per_instance": 224, "ms_per_step": 50.0}}
+    res = calib.calibrate(many, one)["resnet50"]
+    assert res["perf_model"]["multi_overhead"] == pytest.approx(1.4)
+    assert res["sync_overhead"] == pytest.approx(1.25)
+    with pytest.raises(ValueError):
+        calib.calibrate(many, {"resnet50": {"instances": 1, "batch_per_instance": 32,
+                                            "ms_per_step": 9.0}})
+
+
 def test_cli_select_prints_rank_order():
     out = subprocess.run([sys.executable, "-m", "paper_2511_09143_b200.cli", "select", "--gpus", "2",
                           "--size", "4"], capture_output=True, text=True, check=True).stdout

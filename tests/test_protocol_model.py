@@ -300,7 +300,8 @@ def test_model_catches_a_broken_schedule(flag):
     ("coarse", "coarse", "2", "3", "2"), ("coarse", "fine", "2", "2", "3"),
     ("coarse", "coarse", "3", "3", "2"), ("first", "coarse", "0", "3", "2"),
     ("first", "fine", "0", "2", "3"), ("first", "coarse", "1", "1", "2"),
-    ("coarse", "coarse", "0", "2", "3"), ("coarse", "fine", "1", "3", "4")])
+    ("coarse", "coarse", "0", "2", "3"), ("coarse", "fine", "1", "3", "4"),
+    ("coarse", "coarse", "4", "3", "2"), ("fine", "fine", "4", "2", "3")])
 def test_schedule_variants(monkeypatch, n, grain, gather, ramp, lanes, slots):
     monkeypatch.setenv("FMX_GRAIN", grain)
     monkeypatch.setenv("FMX_GATHER_GRAIN", gather)
@@ -380,7 +381,7 @@ def test_model_catches_a_broken_host_push_lane():
     assert failures > 0
 
 
-@pytest.mark.parametrize("ramp", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("ramp", ["0", "1", "2", "3", "4"])
 @pytest.mark.parametrize("min_rounds", ["1", "3", "4", "7"])
 @pytest.mark.parametrize("slice_bytes", [4096, 1 << 20, 4 << 20, 12288])
 @pytest.mark.parametrize("dtype", [0, 1])

@@ -3,6 +3,11 @@
 // barrier), fmx_barrier and fmx_comm_abort, with every rank a thread of one
 // process (TSAN sees threads, not processes).  FMX_TRANSPORT_HOST makes no CUDA
 // call, so this runs without a GPU.  Build + run: tools/sanitize/run_tsan.sh.
+// Scope: every rank maps the segment itself (its own virtual addresses), so
+// TSAN checks the process-wide state (call_once driver loading, thread-local
+// error state, the communicator objects) and each rank's own accesses, not
+// cross-rank accesses to the segment - those are the protocol the model
+// checker covers (tests/test_protocol_model.py) and the atomics of Header.
 #include <cstdio>
 #include <cstring>
 #include <string>
