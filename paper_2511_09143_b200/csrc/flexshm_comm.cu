@@ -477,6 +477,13 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
   std::vector<cudaStream_t> extra;
   if (c->nlanes >= 2 && !c->join_stream && !single) extra.push_back(c->lane[0]);
   if (c->nlanes == 3 && !c->join_stream && !single) extra.push_back(c->lane[2]);
+  // join-stream mode with a stage lane (FMX_JOIN_LANES=2): lane 0 forks from the
+  // caller's stream like every lane but never joins back - the next bucket's
+  // stage (D2H) runs while this one fetches and gathers (H2D) on the join
+  // stream.  Completion on the join stream still covers it: my last gather
+  // waited every peer's REDUCED, and each peer reduced only after my STAGED.
+  const bool stage_lane = c->join_stream && c->join_lanes == 2 && !single;
+  if (stage_lane) extra.push_back(c->lane[0]);
   // host-path / broadcast calls (and the first device call after one) wait for
   // the previous collective, whichever stream it joined (redundant, and free,
   // when it joined the caller's stream)
@@ -496,7 +503,7 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
   // stream, which then carries every lane); fmx_comm_completion_stream names it
   cudaStream_t target = main;
   c->completion = target;
-  for (size_t l = 0; l < extra.size(); ++l) {
+  for (size_t l = 0; l < extra.size() && !stage_lane; ++l) {
     FMX_CUDA(cudaEventRecord(c->joined[l], extra[l]));
     FMX_CUDA(cudaStreamWaitEvent(target, c->joined[l], 0));
   }
@@ -746,6 +753,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (const char* v = getenv("FMX_COPY2D")) c->copy2d = atoi(v) != 0;
   if (const char* v = getenv("FMX_COPY_FENCE")) c->copy_fence = atoi(v) != 0;
   if (const char* v = getenv("FMX_FUSE_SIGNAL")) c->fuse_signal = atoi(v) != 0;
+  if (const char* v = getenv("FMX_JOIN_LANES")) c->join_lanes = atoi(v) == 2 ? 2 : 1;
   c->serialize = profiler_injected();
   if (e != cudaSuccess) {
     h->aborted.store(1);

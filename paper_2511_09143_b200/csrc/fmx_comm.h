@@ -37,6 +37,8 @@ struct fmx_comm {
   cudaStream_t join_stream = nullptr;  // fmx_comm_set_join_stream: lane 1 runs here, not on `user`
   cudaStream_t completion = nullptr;   // stream the last collective completed on
   cudaStream_t last_main = nullptr;    // lane-1 stream of the last collective
+  int join_lanes = 1;                  // join-stream mode: 1 every lane on the join stream;
+                                       //   2 (FMX_JOIN_LANES=2) the stage lane on its own stream
   bool copy_fence = true;              // no-op kernel after every copy-engine batch (CudaSink::copy)
   bool fuse_signal = true;             // FMX_FUSE_SIGNAL=0: zero-copy stage + STAGED as two ops
   bool serialize = false;              // drain this rank's lanes before every kernel launch
@@ -52,9 +54,8 @@ struct fmx_comm {
   bool coarse = true;          // FMX_GRAIN=fine: per-piece waits instead of all-peer
   bool fine_first = false;     // FMX_GRAIN=first: per-contributor flags in round 0 only
   bool coarse_gather = true;   // FMX_GATHER_GRAIN=fine: per-owner gather waits only
-  int ramp = 0;                // FMX_RAMP=1: geometric s/8, s/4, s/2 fill / drain rounds; 2: fill only;
-                               // 4: remainder-sized first round, no extra round (off:
-                               // with the copy fence, equal rounds are 3-4% faster, r01/r3e)
+  int ramp = 4;                // round geometry (allreduce_geometry): 4 remainder-sized first
+                               // round (default); 0 equal rounds; 1/2/3 geometric ramps (slower)
   int min_rounds = 1;          // FMX_MIN_ROUNDS: shrink the slice so a chunk spans >= this many
   size_t zc_max = 2u << 20;    // FMX_ZC_MAX: AUTO transport moves messages <= this with SM copies
 
@@ -124,7 +125,8 @@ inline cudaStream_t lane_stream(const fmx_comm* c, int lane) {
   // compute stream, two more extra streams per MPS client made bucketed
   // allreduces 2.5x slower (hardware-queue aliasing, profiles/r01/r2w), and a
   // single in-order stream per rank is as fast as three lanes on this box
-  if (c->nlanes == 1 || lane == 1 || c->join_stream) return main;
+  if (c->join_stream) return lane == 0 && c->join_lanes == 2 && c->nlanes >= 2 ? c->lane[0] : main;
+  if (c->nlanes == 1 || lane == 1) return main;
   if (c->nlanes == 2) return lane == 0 ? c->lane[0] : main;
   return c->lane[lane];
 }
