@@ -483,7 +483,20 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
   // stream.  Completion on the join stream still covers it: my last gather
   // waited every peer's REDUCED, and each peer reduced only after my STAGED.
   const bool stage_lane = c->join_stream && c->join_lanes == 2 && !single;
-  if (stage_lane) extra.push_back(c->lane[0]);
+  if (stage_lane) {
+    // the stage lane runs at the join stream's priority: its copy fences and
+    // signals must not queue behind the caller's compute kernels for SM slots
+    // (a DDP side stream is high priority, the autograd stream is not)
+    int jp = 0, lp = 0;
+    FMX_CUDA(cudaStreamGetPriority(c->join_stream, &jp));
+    FMX_CUDA(cudaStreamGetPriority(c->lane[0], &lp));
+    if (jp != lp) {
+      FMX_CUDA(cudaStreamSynchronize(c->lane[0]));  // once: flags stay monotone
+      FMX_CUDA(cudaStreamDestroy(c->lane[0]));
+      FMX_CUDA(cudaStreamCreateWithPriority(&c->lane[0], cudaStreamNonBlocking, jp));
+    }
+    extra.push_back(c->lane[0]);
+  }
   // host-path / broadcast calls (and the first device call after one) wait for
   // the previous collective, whichever stream it joined (redundant, and free,
   // when it joined the caller's stream)
