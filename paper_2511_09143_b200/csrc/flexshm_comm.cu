@@ -252,6 +252,7 @@ class CudaSink final : public Sink {
   }
 
   int signal_impl(int lane, int flag, uint32_t v) {
+    if (c_->kernel_sync) return signal_kernel(lane, flag, v, -1, 0);
     CUstreamBatchMemOpParams op;
     memset(&op, 0, sizeof op);
     op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
@@ -262,6 +263,7 @@ class CudaSink final : public Sink {
   }
 
   int signal2_impl(int lane, int f0, uint32_t v0, int f1, uint32_t v1) {
+    if (c_->kernel_sync) return signal_kernel(lane, f0, v0, f1, v1);
     CUstreamBatchMemOpParams op[2];
     memset(op, 0, sizeof op);
     op[0].writeValue.operation = op[1].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
@@ -273,6 +275,7 @@ class CudaSink final : public Sink {
   }
 
   int wait_peers_impl(int lane, int flag, uint32_t v, int skip) {
+    if (c_->kernel_sync) return wait_kernel(lane, flag, v, 0, c_->nranks, skip);
     ops_.clear();
     for (int q = 0; q < c_->nranks; ++q)
       if (q != skip) ops_.push_back(wait_op(q, flag, v));
@@ -284,6 +287,7 @@ class CudaSink final : public Sink {
   }
 
   int wait_rank_impl(int lane, int q, int flag, uint32_t v) {
+    if (c_->kernel_sync) return wait_kernel(lane, flag, v, q, q + 1, -1);
     CUstreamBatchMemOpParams op = wait_op(q, flag, v);
     return batch(lane, &op, 1);
   }
@@ -315,7 +319,7 @@ class CudaSink final : public Sink {
     // 8 MiB allreduces on one stream: 162 ms; with the fence 32 ms), and the
     // fence also speeds up the plain allreduce (30.3 -> 28.1 ms) and the host
     // path (17.7 -> 16.6 ms) (profiles/r01/r2z_r3a).  FMX_COPY_FENCE=0: off.
-    if (!use_kernel && c_->copy_fence) {
+    if (!use_kernel && c_->copy_fence && !c_->kernel_sync) {
       if ((rc = drain())) return rc;
       fmx_nop_kernel<<<1, 32, 0, lane_stream(c_, lane)>>>();
       FMX_CUDA(cudaGetLastError());
@@ -361,6 +365,26 @@ class CudaSink final : public Sink {
   }
 
  private:
+  // FMX_SYNC=kernel (flexshm_kernels.cuh): one-warp signal / wait kernels
+  int signal_kernel(int lane, int f0, uint32_t v0, int f1, uint32_t v1) {
+    if (int rc = drain()) return rc;
+    fmx_signal_kernel<<<1, 32, 0, lane_stream(c_, lane)>>>(
+        (uint32_t*)c_->flag_dev(c_->rank, f0), v0,
+        f1 >= 0 ? (uint32_t*)c_->flag_dev(c_->rank, f1) : nullptr, v1);
+    FMX_CUDA(cudaGetLastError());
+    c_->launches++;
+    return FMX_OK;
+  }
+  int wait_kernel(int lane, int flag, uint32_t v, int lo, int hi, int skip) {
+    if (int rc = drain()) return rc;
+    const char* base = (const char*)c_->flag_dev(0, flag);
+    fmx_wait_kernel<<<1, 64, 0, lane_stream(c_, lane)>>>(base, (size_t)kFlagsPerRank * 64, lo, hi,
+                                                         skip, v);
+    FMX_CUDA(cudaGetLastError());
+    c_->launches++;
+    return FMX_OK;
+  }
+
   CUstreamBatchMemOpParams wait_op(int q, int flag, uint32_t v) {
     CUstreamBatchMemOpParams op;
     memset(&op, 0, sizeof op);
@@ -477,26 +501,6 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
   std::vector<cudaStream_t> extra;
   if (c->nlanes >= 2 && !c->join_stream && !single) extra.push_back(c->lane[0]);
   if (c->nlanes == 3 && !c->join_stream && !single) extra.push_back(c->lane[2]);
-  // join-stream mode with a stage lane (FMX_JOIN_LANES=2): lane 0 forks from the
-  // caller's stream like every lane but never joins back - the next bucket's
-  // stage (D2H) runs while this one fetches and gathers (H2D) on the join
-  // stream.  Completion on the join stream still covers it: my last gather
-  // waited every peer's REDUCED, and each peer reduced only after my STAGED.
-  const bool stage_lane = c->join_stream && c->join_lanes == 2 && !single;
-  if (stage_lane) {
-    // the stage lane runs at the join stream's priority: its copy fences and
-    // signals must not queue behind the caller's compute kernels for SM slots
-    // (a DDP side stream is high priority, the autograd stream is not)
-    int jp = 0, lp = 0;
-    FMX_CUDA(cudaStreamGetPriority(c->join_stream, &jp));
-    FMX_CUDA(cudaStreamGetPriority(c->lane[0], &lp));
-    if (jp != lp) {
-      FMX_CUDA(cudaStreamSynchronize(c->lane[0]));  // once: flags stay monotone
-      FMX_CUDA(cudaStreamDestroy(c->lane[0]));
-      FMX_CUDA(cudaStreamCreateWithPriority(&c->lane[0], cudaStreamNonBlocking, jp));
-    }
-    extra.push_back(c->lane[0]);
-  }
   // host-path / broadcast calls (and the first device call after one) wait for
   // the previous collective, whichever stream it joined (redundant, and free,
   // when it joined the caller's stream)
@@ -516,7 +520,7 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
   // stream, which then carries every lane); fmx_comm_completion_stream names it
   cudaStream_t target = main;
   c->completion = target;
-  for (size_t l = 0; l < extra.size() && !stage_lane; ++l) {
+  for (size_t l = 0; l < extra.size(); ++l) {
     FMX_CUDA(cudaEventRecord(c->joined[l], extra[l]));
     FMX_CUDA(cudaStreamWaitEvent(target, c->joined[l], 0));
   }
@@ -766,8 +770,10 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (const char* v = getenv("FMX_COPY2D")) c->copy2d = atoi(v) != 0;
   if (const char* v = getenv("FMX_COPY_FENCE")) c->copy_fence = atoi(v) != 0;
   if (const char* v = getenv("FMX_FUSE_SIGNAL")) c->fuse_signal = atoi(v) != 0;
-  if (const char* v = getenv("FMX_JOIN_LANES")) c->join_lanes = atoi(v) == 2 ? 2 : 1;
   c->serialize = profiler_injected();
+  // flag sync by kernels (FMX_SYNC=kernel) spins an SM warp per wait: never
+  // under a kernel profiler, whose serialised launches would deadlock on it
+  if (const char* v = getenv("FMX_SYNC")) c->kernel_sync = strcmp(v, "kernel") == 0 && !c->serialize;
   if (e != cudaSuccess) {
     h->aborted.store(1);
     fail(FMX_ERR_CUDA, "device mapping of %zu-byte segment failed: %s", c->total_bytes,

@@ -313,6 +313,42 @@ inline void launch_reduce(const ReduceArgs& a, int dtype, bool aligned, cudaStre
     launch_reduce_op<__nv_bfloat16>(a, aligned, s);
 }
 
+// ---------------------------------------------------------------- flag sync kernels
+//
+// FMX_SYNC=kernel: flag signals and waits as one-warp kernels instead of stream
+// memory operations (which park the stream in the GPU front end).  Same flags,
+// same values, same enqueue order: the protocol is unchanged.
+//   fmx_signal_kernel: system fence (everything earlier in the stream - copy
+//     engine transfers included - completed before the kernel started), then
+//     release-store up to two flags.
+//   fmx_wait_kernel:   thread q polls rank q's flag (acquire, system scope)
+//     until it is cyclically >= v; a raised flag (fmx_comm_abort) releases it.
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void fmx_signal_kernel(uint32_t* f0, uint32_t v0, uint32_t* f1, uint32_t v1) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f0), "r"(v0) : "memory");
+  if (f1) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f1), "r"(v1) : "memory");
+}
+
+// flags of rank q live at base + q * stride (bytes); ranks [lo, hi) except skip
+__global__ void __launch_bounds__(64) fmx_wait_kernel(const char* base, size_t stride, int lo,
+                                                      int hi, int skip, uint32_t v) {
+  const int q = lo + (int)threadIdx.x;
+  if (q < hi && q != skip) {
+    const uint32_t* f = (const uint32_t*)(base + (size_t)q * stride);
+    while ((int32_t)(ld_acquire_sys(f) - v) < 0) __nanosleep(256);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+}
+
 // ---------------------------------------------------------------- stamps
 
 // Pipeline timeline probe (fmx_comm_set_stamps): one thread writes the GPU's

@@ -37,8 +37,8 @@ struct fmx_comm {
   cudaStream_t join_stream = nullptr;  // fmx_comm_set_join_stream: lane 1 runs here, not on `user`
   cudaStream_t completion = nullptr;   // stream the last collective completed on
   cudaStream_t last_main = nullptr;    // lane-1 stream of the last collective
-  int join_lanes = 1;                  // join-stream mode: 1 every lane on the join stream;
-                                       //   2 (FMX_JOIN_LANES=2) the stage lane on its own stream
+  bool kernel_sync = false;            // FMX_SYNC=kernel: flag signals / waits as one-warp kernels
+                                       //   (fmx_signal_kernel / fmx_wait_kernel), not stream memops
   bool copy_fence = true;              // no-op kernel after every copy-engine batch (CudaSink::copy)
   bool fuse_signal = true;             // FMX_FUSE_SIGNAL=0: zero-copy stage + STAGED as two ops
   bool serialize = false;              // drain this rank's lanes before every kernel launch
@@ -125,8 +125,7 @@ inline cudaStream_t lane_stream(const fmx_comm* c, int lane) {
   // compute stream, two more extra streams per MPS client made bucketed
   // allreduces 2.5x slower (hardware-queue aliasing, profiles/r01/r2w), and a
   // single in-order stream per rank is as fast as three lanes on this box
-  if (c->join_stream) return lane == 0 && c->join_lanes == 2 && c->nlanes >= 2 ? c->lane[0] : main;
-  if (c->nlanes == 1 || lane == 1) return main;
+  if (c->nlanes == 1 || lane == 1 || c->join_stream) return main;
   if (c->nlanes == 2) return lane == 0 ? c->lane[0] : main;
   return c->lane[lane];
 }

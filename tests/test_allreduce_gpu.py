@@ -177,15 +177,10 @@ def test_reduce_scatter_and_allgather(n, transport):
     check_all(n, sc, run(n, sc, transport=transport, slice_bytes=1 << 18))
 
 
-@pytest.mark.parametrize("n,mode,join_lanes", [(2, "green", "1"), (7, "green", "1"),
-                                                (7, "mps", "1"), (2, "green", "2"),
-                                                (7, "mps", "2")])
-def test_join_stream_mode_overlapping_allreduces(monkeypatch, n, mode, join_lanes):
-    """DDP-bucket pattern: back-to-back allreduces of distinct buffers that
-    overlap inside the library (fmx_comm_set_join_stream); every result is
-    bit-exact.  FMX_JOIN_LANES=2: each bucket's stage runs on its own stream,
-    overlapping the previous bucket's fetch and gather."""
-    monkeypatch.setenv("FMX_JOIN_LANES", join_lanes)
+@pytest.mark.parametrize("n,mode", [(2, "green"), (7, "green"), (7, "mps")])
+def test_join_stream_mode_overlapping_allreduces(n, mode):
+    """DDP-bucket pattern: back-to-back allreduces of distinct buffers in
+    join-stream mode (fmx_comm_set_join_stream); every result is bit-exact."""
     from paper_2511_09143_b200.launcher import launch, new_job_key
     from paper_2511_09143_b200.scheduler import fm_select, make_cluster
     from paper_2511_09143_b200.workload import Job
