@@ -252,7 +252,6 @@ class CudaSink final : public Sink {
   }
 
   int signal_impl(int lane, int flag, uint32_t v) {
-    if (c_->kernel_sync) return signal_kernel(lane, flag, v, -1, 0);
     CUstreamBatchMemOpParams op;
     memset(&op, 0, sizeof op);
     op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
@@ -263,7 +262,6 @@ class CudaSink final : public Sink {
   }
 
   int signal2_impl(int lane, int f0, uint32_t v0, int f1, uint32_t v1) {
-    if (c_->kernel_sync) return signal_kernel(lane, f0, v0, f1, v1);
     CUstreamBatchMemOpParams op[2];
     memset(op, 0, sizeof op);
     op[0].writeValue.operation = op[1].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
@@ -275,7 +273,6 @@ class CudaSink final : public Sink {
   }
 
   int wait_peers_impl(int lane, int flag, uint32_t v, int skip) {
-    if (c_->kernel_sync) return wait_kernel(lane, flag, v, 0, c_->nranks, skip);
     ops_.clear();
     for (int q = 0; q < c_->nranks; ++q)
       if (q != skip) ops_.push_back(wait_op(q, flag, v));
@@ -287,7 +284,6 @@ class CudaSink final : public Sink {
   }
 
   int wait_rank_impl(int lane, int q, int flag, uint32_t v) {
-    if (c_->kernel_sync) return wait_kernel(lane, flag, v, q, q + 1, -1);
     CUstreamBatchMemOpParams op = wait_op(q, flag, v);
     return batch(lane, &op, 1);
   }
@@ -319,7 +315,7 @@ class CudaSink final : public Sink {
     // 8 MiB allreduces on one stream: 162 ms; with the fence 32 ms), and the
     // fence also speeds up the plain allreduce (30.3 -> 28.1 ms) and the host
     // path (17.7 -> 16.6 ms) (profiles/r01/r2z_r3a).  FMX_COPY_FENCE=0: off.
-    if (!use_kernel && c_->copy_fence && !c_->kernel_sync) {
+    if (!use_kernel && c_->copy_fence) {
       if ((rc = drain())) return rc;
       fmx_nop_kernel<<<1, 32, 0, lane_stream(c_, lane)>>>();
       FMX_CUDA(cudaGetLastError());
@@ -337,6 +333,17 @@ class CudaSink final : public Sink {
     // one counter per lane that fuses signals (stage copies on lane 0, the
     // one-shot publish on lane 1), so two fused copies never share a counter
     return launch_copy(lane, segs, src_sys, (uint32_t*)fl, v, c_->ctas_done + (lane == kLaneMain));
+  }
+
+  // the one-shot's OS_READY wait fused into its reduction (MPS ranks only)
+  int wait_reduce(int lane, const PlanReduce& r, int flag, uint32_t v, int skip) override {
+    if (!c_->spin_wait || c_->stamps || r.args.len == 0) return Sink::wait_reduce(lane, r, flag, v, skip);
+    PlanReduce f = r;
+    f.args.wait_flags = (const char*)c_->flag_dev(0, flag);
+    f.args.wait_stride = (size_t)kFlagsPerRank * 64;
+    f.args.wait_value = v;
+    f.args.wait_skip = skip;
+    return reduce(lane, f);
   }
 
   int reduce(int lane, const PlanReduce& r) override {
@@ -365,26 +372,6 @@ class CudaSink final : public Sink {
   }
 
  private:
-  // FMX_SYNC=kernel (flexshm_kernels.cuh): one-warp signal / wait kernels
-  int signal_kernel(int lane, int f0, uint32_t v0, int f1, uint32_t v1) {
-    if (int rc = drain()) return rc;
-    fmx_signal_kernel<<<1, 32, 0, lane_stream(c_, lane)>>>(
-        (uint32_t*)c_->flag_dev(c_->rank, f0), v0,
-        f1 >= 0 ? (uint32_t*)c_->flag_dev(c_->rank, f1) : nullptr, v1);
-    FMX_CUDA(cudaGetLastError());
-    c_->launches++;
-    return FMX_OK;
-  }
-  int wait_kernel(int lane, int flag, uint32_t v, int lo, int hi, int skip) {
-    if (int rc = drain()) return rc;
-    const char* base = (const char*)c_->flag_dev(0, flag);
-    fmx_wait_kernel<<<1, 64, 0, lane_stream(c_, lane)>>>(base, (size_t)kFlagsPerRank * 64, lo, hi,
-                                                         skip, v);
-    FMX_CUDA(cudaGetLastError());
-    c_->launches++;
-    return FMX_OK;
-  }
-
   CUstreamBatchMemOpParams wait_op(int q, int flag, uint32_t v) {
     CUstreamBatchMemOpParams op;
     memset(&op, 0, sizeof op);
@@ -771,9 +758,18 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (const char* v = getenv("FMX_COPY_FENCE")) c->copy_fence = atoi(v) != 0;
   if (const char* v = getenv("FMX_FUSE_SIGNAL")) c->fuse_signal = atoi(v) != 0;
   c->serialize = profiler_injected();
-  // flag sync by kernels (FMX_SYNC=kernel) spins an SM warp per wait: never
-  // under a kernel profiler, whose serialised launches would deadlock on it
-  if (const char* v = getenv("FMX_SYNC")) c->kernel_sync = strcmp(v, "kernel") == 0 && !c->serialize;
+  // The one-shot may fuse its flag wait into the reduction (spinning CTAs) only
+  // where ranks run concurrently - MPS clients; never time-sliced contexts
+  // (green / plain processes), and never under a kernel profiler, whose
+  // serialised launches would deadlock on a spinning kernel.
+  {
+    int dev = 0, mps = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&mps, cudaDevAttrMpsEnabled, dev) == cudaSuccess)
+      c->spin_wait = mps != 0 && !c->serialize;
+    cudaGetLastError();
+    if (const char* v = getenv("FMX_SPIN_WAIT")) c->spin_wait = atoi(v) != 0 && !c->serialize;
+  }
   if (e != cudaSuccess) {
     h->aborted.store(1);
     fail(FMX_ERR_CUDA, "device mapping of %zu-byte segment failed: %s", c->total_bytes,

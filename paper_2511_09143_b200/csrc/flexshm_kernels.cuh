@@ -59,6 +59,26 @@ __device__ __forceinline__ void release_flag_when_grid_done(const CopyArgs& a) {
 }
 
 
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Fused flag wait (ReduceArgs::wait_flags): thread q of the CTA polls rank q's
+// flag with acquire loads at system scope; the CTA barrier then orders every
+// thread's source loads after the peers' releases.  Only for MPS-concurrent
+// ranks (the caller checks): a spinning CTA must not hold a time slice.
+__device__ __forceinline__ void wait_flags_cta(const char* base, size_t stride, int n, int skip,
+                                               uint32_t v) {
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
+    if (q == skip) continue;
+    const uint32_t* f = (const uint32_t*)(base + (size_t)q * stride);
+    while ((int32_t)(ld_acquire_sys(f) - v) < 0) __nanosleep(64);
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ uint4 ld_cv_v4(const void* p) {
   uint4 v;
   asm volatile("ld.global.cv.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -242,6 +262,7 @@ template <typename T, int U, int OP>
 __global__ void __launch_bounds__(256, 2) fmx_reduce_kernel(const __grid_constant__ ReduceArgs a) {
   using E = Elem<T>;
   constexpr int V = E::kVec;
+  if (a.wait_flags) wait_flags_cta(a.wait_flags, a.wait_stride, a.nsrc, a.wait_skip, a.wait_value);
   const size_t nvec = a.len / V;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -273,6 +294,7 @@ __global__ void __launch_bounds__(256, 2) fmx_reduce_kernel(const __grid_constan
 // Unaligned fallback: one element per thread iteration.
 template <typename T, int OP>
 __global__ void __launch_bounds__(256) fmx_reduce_scalar_kernel(const __grid_constant__ ReduceArgs a) {
+  if (a.wait_flags) wait_flags_cta(a.wait_flags, a.wait_stride, a.nsrc, a.wait_skip, a.wait_value);
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.len; e += stride)
     reduce_elem<T, OP>(a, e);
@@ -311,42 +333,6 @@ inline void launch_reduce(const ReduceArgs& a, int dtype, bool aligned, cudaStre
     launch_reduce_op<float>(a, aligned, s);
   else
     launch_reduce_op<__nv_bfloat16>(a, aligned, s);
-}
-
-// ---------------------------------------------------------------- flag sync kernels
-//
-// FMX_SYNC=kernel: flag signals and waits as one-warp kernels instead of stream
-// memory operations (which park the stream in the GPU front end).  Same flags,
-// same values, same enqueue order: the protocol is unchanged.
-//   fmx_signal_kernel: system fence (everything earlier in the stream - copy
-//     engine transfers included - completed before the kernel started), then
-//     release-store up to two flags.
-//   fmx_wait_kernel:   thread q polls rank q's flag (acquire, system scope)
-//     until it is cyclically >= v; a raised flag (fmx_comm_abort) releases it.
-
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__global__ void fmx_signal_kernel(uint32_t* f0, uint32_t v0, uint32_t* f1, uint32_t v1) {
-  if (threadIdx.x != 0) return;
-  __threadfence_system();
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f0), "r"(v0) : "memory");
-  if (f1) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f1), "r"(v1) : "memory");
-}
-
-// flags of rank q live at base + q * stride (bytes); ranks [lo, hi) except skip
-__global__ void __launch_bounds__(64) fmx_wait_kernel(const char* base, size_t stride, int lo,
-                                                      int hi, int skip, uint32_t v) {
-  const int q = lo + (int)threadIdx.x;
-  if (q < hi && q != skip) {
-    const uint32_t* f = (const uint32_t*)(base + (size_t)q * stride);
-    while ((int32_t)(ld_acquire_sys(f) - v) < 0) __nanosleep(256);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) __threadfence_system();
 }
 
 // ---------------------------------------------------------------- stamps

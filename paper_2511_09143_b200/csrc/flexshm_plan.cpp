@@ -477,7 +477,6 @@ int plan_allreduce_oneshot(fmx_comm* c, Sink& k, const char* src, char* dst, siz
   std::vector<PlanSeg> segs{{src, c->at(true, mine), bytes, Annot{(int64_t)mine, bytes, me, J | kOsTag},
                              true, ubuf(0, bytes)}};
   if ((rc = k.copy_signal(kLaneMain, segs, false, true, kOsReady, J + 1))) return rc;
-  if ((rc = k.wait_peers(kLaneMain, kOsReady, J + 1, me))) return rc;
   PlanReduce pr;
   memset(&pr.args, 0, sizeof pr.args);
   pr.dtype = dtype;
@@ -498,7 +497,8 @@ int plan_allreduce_oneshot(fmx_comm* c, Sink& k, const char* src, char* dst, siz
     pr.args.sys_mask |= 1ull << q;
     pr.reads.push_back(Annot{(int64_t)off, bytes, q, J | kOsTag});
   }
-  if ((rc = k.reduce(kLaneMain, pr))) return rc;
+  // wait for every peer's publish, then reduce (fused into one kernel for MPS ranks)
+  if ((rc = k.wait_reduce(kLaneMain, pr, kOsReady, J + 1, me))) return rc;
   c->os_round = J + 1;
   return FMX_OK;
 }

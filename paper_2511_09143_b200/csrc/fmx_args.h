@@ -20,6 +20,13 @@ struct ReduceArgs {
   int nsrc;
   int op;
   float factor;
+  // non-null: before reading any source, every CTA waits until the flag of
+  // each rank q != wait_skip (at wait_flags + q * wait_stride) is cyclically
+  // >= wait_value - the one-shot's OS_READY wait fused into its reduction
+  const char* wait_flags;
+  size_t wait_stride;
+  uint32_t wait_value;
+  int wait_skip;
 };
 
 // Pipeline timeline probe entry (fmx_comm_set_stamps).

@@ -37,8 +37,8 @@ struct fmx_comm {
   cudaStream_t join_stream = nullptr;  // fmx_comm_set_join_stream: lane 1 runs here, not on `user`
   cudaStream_t completion = nullptr;   // stream the last collective completed on
   cudaStream_t last_main = nullptr;    // lane-1 stream of the last collective
-  bool kernel_sync = false;            // FMX_SYNC=kernel: flag signals / waits as one-warp kernels
-                                       //   (fmx_signal_kernel / fmx_wait_kernel), not stream memops
+  bool spin_wait = false;              // one-shot: OS_READY wait fused into the reduce kernel
+                                       //   (MPS-concurrent ranks only; FMX_SPIN_WAIT=0/1 overrides)
   bool copy_fence = true;              // no-op kernel after every copy-engine batch (CudaSink::copy)
   bool fuse_signal = true;             // FMX_FUSE_SIGNAL=0: zero-copy stage + STAGED as two ops
   bool serialize = false;              // drain this rank's lanes before every kernel launch
@@ -183,6 +183,11 @@ struct Sink {
   virtual ~Sink() {}
   virtual int copy(int lane, const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel) = 0;
   virtual int reduce(int lane, const PlanReduce& r) = 0;
+  // wait until every peer's `flag` >= v, then reduce (a sink may fuse the two)
+  virtual int wait_reduce(int lane, const PlanReduce& r, int flag, uint32_t v, int skip) {
+    int rc = wait_peers(lane, flag, v, skip);
+    return rc ? rc : reduce(lane, r);
+  }
   virtual int signal(int lane, int flag, uint32_t v) = 0;
   // copy, then signal `flag` = v on the same lane (a sink may fuse the two)
   virtual int copy_signal(int lane, const std::vector<PlanSeg>& segs, bool src_sys,
