@@ -244,7 +244,7 @@ class CudaSink final : public Sink {
       c_->timed_used++;
       FMX_CUDA(cudaEventRecord(t0, s));
     }
-    launch_reduce(a, r.dtype, r.aligned, s);
+    launch_reduce(a, r.dtype, r.aligned, s, c_->reduce_ctas);
     FMX_CUDA(cudaGetLastError());
     if (t1) FMX_CUDA(cudaEventRecord(t1, s));
     c_->launches++;
@@ -757,6 +757,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (const char* v = getenv("FMX_COPY2D")) c->copy2d = atoi(v) != 0;
   if (const char* v = getenv("FMX_COPY_FENCE")) c->copy_fence = atoi(v) != 0;
   if (const char* v = getenv("FMX_FUSE_SIGNAL")) c->fuse_signal = atoi(v) != 0;
+  if (const char* v = getenv("FMX_REDUCE_CTAS")) c->reduce_ctas = std::max(1, std::min(atoi(v), kReduceGridCap));
   c->serialize = profiler_injected();
   // The one-shot may fuse its flag wait into the reduction (spinning CTAs) only
   // where ranks run concurrently - MPS clients; never time-sliced contexts

@@ -305,11 +305,11 @@ __global__ void __launch_bounds__(256) fmx_reduce_scalar_kernel(const __grid_con
 constexpr int kReduceThreads = 256, kReduceU = 2, kReduceGridCap = 1184;
 
 template <typename T, int OP>
-inline void launch_reduce_t(const ReduceArgs& a, bool aligned, cudaStream_t s) {
+inline void launch_reduce_t(const ReduceArgs& a, bool aligned, cudaStream_t s, int cap) {
   constexpr int V = Elem<T>::kVec;
-  auto grid = [](size_t items) {
+  auto grid = [cap](size_t items) {
     size_t g = (items + kReduceThreads - 1) / kReduceThreads;
-    return (int)(g < 1 ? 1 : g > (size_t)kReduceGridCap ? kReduceGridCap : g);
+    return (int)(g < 1 ? 1 : g > (size_t)cap ? cap : g);
   };
   if (aligned)
     fmx_reduce_kernel<T, kReduceU, OP>
@@ -319,20 +319,22 @@ inline void launch_reduce_t(const ReduceArgs& a, bool aligned, cudaStream_t s) {
 }
 
 template <typename T>
-inline void launch_reduce_op(const ReduceArgs& a, bool aligned, cudaStream_t s) {
+inline void launch_reduce_op(const ReduceArgs& a, bool aligned, cudaStream_t s, int cap) {
   switch (a.op) {
-    case FMX_OP_SUM_POSTSCALE: return launch_reduce_t<T, FMX_OP_SUM_POSTSCALE>(a, aligned, s);
-    case FMX_OP_PREDIV_SUM: return launch_reduce_t<T, FMX_OP_PREDIV_SUM>(a, aligned, s);
-    case FMX_OP_PREMUL_SUM: return launch_reduce_t<T, FMX_OP_PREMUL_SUM>(a, aligned, s);
-    default: return launch_reduce_t<T, FMX_OP_SUM>(a, aligned, s);
+    case FMX_OP_SUM_POSTSCALE: return launch_reduce_t<T, FMX_OP_SUM_POSTSCALE>(a, aligned, s, cap);
+    case FMX_OP_PREDIV_SUM: return launch_reduce_t<T, FMX_OP_PREDIV_SUM>(a, aligned, s, cap);
+    case FMX_OP_PREMUL_SUM: return launch_reduce_t<T, FMX_OP_PREMUL_SUM>(a, aligned, s, cap);
+    default: return launch_reduce_t<T, FMX_OP_SUM>(a, aligned, s, cap);
   }
 }
 
-inline void launch_reduce(const ReduceArgs& a, int dtype, bool aligned, cudaStream_t s) {
+// cap: most CTAs per launch (kReduceGridCap; FMX_REDUCE_CTAS lowers it per communicator)
+inline void launch_reduce(const ReduceArgs& a, int dtype, bool aligned, cudaStream_t s,
+                          int cap = kReduceGridCap) {
   if (dtype == FMX_FLOAT32)
-    launch_reduce_op<float>(a, aligned, s);
+    launch_reduce_op<float>(a, aligned, s, cap);
   else
-    launch_reduce_op<__nv_bfloat16>(a, aligned, s);
+    launch_reduce_op<__nv_bfloat16>(a, aligned, s, cap);
 }
 
 // ---------------------------------------------------------------- stamps

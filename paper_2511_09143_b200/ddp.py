@@ -46,7 +46,9 @@ class HookState:
             else:
                 # high priority: every peer's pipeline waits on this rank's reductions,
                 # so they must not queue behind the backward pass's kernels
-                stream = torch.cuda.Stream(priority=-1)
+                # (FMX_HOOK_PRIORITY overrides, for measurements)
+                import os
+                stream = torch.cuda.Stream(priority=int(os.environ.get("FMX_HOOK_PRIORITY", "-1")))
         self.stream = stream
         self.threaded = threaded
         self._queue = None
