@@ -935,7 +935,12 @@ def run_ours(args) -> dict | None:
                                   if args.count == RESNET50_PARAMS and gpus == 1 else ""),
                    "ranks": n, "ranks_per_gpu": per_gpu, "bytes": s_bytes,
                    "instance_mode": inst_mode,
-                   "transport": args.transport, "l2": "inputs > L2 (7 x 102 MB per GPU)",
+                   "transport": args.transport,
+                   "l2": (f"inputs {max(per_phys)} x {s_bytes / 1e6:.1f} MB per GPU "
+                          + ("> L2 (126 MB): no flush needed"
+                             if max(per_phys) * s_bytes > 126e6 else
+                             "< L2 (126 MB), not flushed: every byte crosses the host link, "
+                             "which bounds the path")),
                    "slots": int(os.environ.get("FMX_SLOTS", "2")),
                    "lanes": int(os.environ.get("FMX_LANES", "3")),
                    "rank_order": "fm_select round-robin"},

@@ -335,9 +335,13 @@ class CudaSink final : public Sink {
     return launch_copy(lane, segs, src_sys, (uint32_t*)fl, v, c_->ctas_done + (lane == kLaneMain));
   }
 
-  // the one-shot's OS_READY wait fused into its reduction (MPS ranks only)
+  // the one-shot's OS_READY wait fused into its reduction (MPS ranks, messages up
+  // to 16 KiB: 1 KiB at 7 ranks 0.049 -> 0.028 ms; at 64 KiB the spinning
+  // CTAs cost more than the memop wait saves, 0.119 vs 0.096 ms, r02/r2h)
   int wait_reduce(int lane, const PlanReduce& r, int flag, uint32_t v, int skip) override {
-    if (!c_->spin_wait || c_->stamps || r.args.len == 0) return Sink::wait_reduce(lane, r, flag, v, skip);
+    const size_t bytes = r.args.len * (r.dtype == FMX_FLOAT32 ? 4 : 2);
+    if (!c_->spin_wait || c_->stamps || r.args.len == 0 || bytes > (16u << 10))
+      return Sink::wait_reduce(lane, r, flag, v, skip);
     PlanReduce f = r;
     f.args.wait_flags = (const char*)c_->flag_dev(0, flag);
     f.args.wait_stride = (size_t)kFlagsPerRank * 64;
