@@ -445,7 +445,9 @@ int make_lane_objects(fmx_comm* c, CUcontext ctx) {
   FMX_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
   if (const char* v = getenv("FMX_LANE_PRIORITY")) prio = atoi(v) ? hi_prio : 0;
   for (int l = 0; l < 3; ++l) {
-    if (l != 1) FMX_CUDA(cudaStreamCreateWithPriority(&c->lane[l], cudaStreamNonBlocking, prio));
+    // extra lane streams only where the schedule uses them (FMX_LANES=1: none)
+    const bool used = (l == 0 && c->nlanes >= 2) || (l == 2 && c->nlanes == 3);
+    if (used) FMX_CUDA(cudaStreamCreateWithPriority(&c->lane[l], cudaStreamNonBlocking, prio));
     FMX_CUDA(cudaEventCreateWithFlags(&c->joined[l], cudaEventDisableTiming));
   }
   FMX_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));

@@ -103,6 +103,27 @@ def analyse(path, per_rank, esz=4, show_ops=None):
     big = [(a, b) for a, b in gaps if b - a > 50_000]
     print(f"  h2d idle gaps > 50 us: {len(big)}, total {sum(b - a for a, b in big) / 1e6:.2f} ms: " +
           ", ".join(f"{(a - t0) / 1e6:.2f}+{(b - a) / 1e3:.0f}us" for a, b in big[:30]))
+    # the link around the dominant kernel: all ranks' D2H traffic (stage copies +
+    # result stores, each spread evenly over its interval) that overlaps each
+    # reduce launch, over the launch's duration - is the D2H direction saturated
+    # while the reduce kernel stores its result slot?
+    if path == "device":
+        d2h_ops = []
+        for r, st in per_rank.items():
+            for lane, kind, info, s, e in intervals(st):
+                if direction(path, lane, kind) == "d2h" and e > s:
+                    d2h_ops.append((s, e, info * esz if kind == 5 else info))
+        tot_t = tot_b = 0.0
+        for r, st in per_rank.items():
+            for lane, kind, info, s, e in intervals(st):
+                if kind != 5 or e <= s:
+                    continue
+                ov = sum(b * max(0, min(e, e2) - max(s, s2)) / (e2 - s2) for s2, e2, b in d2h_ops)
+                tot_t += e - s
+                tot_b += ov
+        if tot_t:
+            print(f"  d2h link while a reduce kernel runs: {tot_b / tot_t:.1f} GB/s of all ranks' "
+                  f"traffic (time-weighted over {tot_t / 1e6:.2f} ms of reduce launches)")
     print("  lane-time in waits per rank (ms): " +
           " ".join(f"{r}:{w:.2f}" for r, w in sorted(waits.items(), key=lambda kv: int(kv[0]))))
 
