@@ -683,14 +683,19 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
     comm.barrier(300)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = comm.kernel_launches()
+    h0 = list(fddp.HOOK_HOST)
+    t_host = time.perf_counter()
     ev0.record(stream)
     with torch.cuda.stream(stream):
         for _ in range(cfg["train_steps"]):
             loss = step()
     ev1.record(stream)
+    t_host = time.perf_counter() - t_host  # enqueue time of the timed steps (no sync inside)
     ev1.synchronize()
     comm.barrier(300)
     out = {"rank": rank, "ms_total": ev0.elapsed_time(ev1), "loss": float(loss.item()),
+           "host_enqueue_ms": t_host * 1e3,
+           "hook_host_ms": (fddp.HOOK_HOST[0] - h0[0]) * 1e3, "hook_calls": fddp.HOOK_HOST[1] - h0[1],
            "stamps": stamps,
            "launches": comm.kernel_launches() - l0,
            "param_digest": float(sum(p.detach().double().sum().item() for p in model.parameters()))}
@@ -772,6 +777,14 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
                                             "(bf16 SHM allreduce of the fp32 buckets)")
                           if args.compress else precision),
             "replicas_agree": len(digests) == 1, "loss": res[0]["loss"],
+            "host": {"enqueue_ms_per_step": max(r["host_enqueue_ms"] for r in res.values())
+                     / args.train_steps,
+                     "hook_ms_per_step": max(r["hook_host_ms"] for r in res.values())
+                     / args.train_steps,
+                     "hooks_per_step": res[0]["hook_calls"] / args.train_steps,
+                     "what": "host time to enqueue the timed steps (max over ranks; loss.item() "
+                             "syncs once per step only in the last one) and the part spent "
+                             "inside flexshm_hook's collective calls"},
             "gpu_launches": sum(r["launches"] for r in res.values()), "model": desc}
 
 

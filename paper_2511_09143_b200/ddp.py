@@ -23,9 +23,20 @@ PAPER.md:264-271), so here:
   blocks and re-assembles it with a single in-place all-gather.
 """
 
+import os
+import time
+
 import torch
 
 from .comm import ShmCommunicator
+
+# host seconds spent inside flexshm_hook's collective enqueue, and calls (a
+# measurement aid: is the autograd thread held up by the driver calls?)
+HOOK_HOST = [0.0, 0]
+# FMX_HOOK_STAMP=1: stamp each bucket's readiness on the GPU timeline;
+# FMX_HOOK_NOOP=1: skip the exchange (measurement of the bare backward pass)
+_MEASURE = {"stamp": os.environ.get("FMX_HOOK_STAMP") == "1",
+            "noop": os.environ.get("FMX_HOOK_NOOP") == "1"}
 
 
 class HookState:
@@ -47,7 +58,6 @@ class HookState:
                 # high priority: every peer's pipeline waits on this rank's reductions,
                 # so they must not queue behind the backward pass's kernels
                 # (FMX_HOOK_PRIORITY overrides, for measurements)
-                import os
                 stream = torch.cuda.Stream(priority=int(os.environ.get("FMX_HOOK_PRIORITY", "-1")))
         self.stream = stream
         self.threaded = threaded
@@ -107,6 +117,15 @@ def flexshm_hook(state, bucket) -> torch.futures.Future[torch.Tensor]:
         fut.set_result(buf)
         return fut
     cur = torch.cuda.current_stream(buf.device)
+    if _MEASURE["stamp"]:
+        # timeline probe: when this bucket's gradient is ready on the GPU
+        state.comm.stamp(100 + bucket.index(), stream=cur)
+    if _MEASURE["noop"]:
+        # measurement only: no exchange at all (replicas diverge) - the backward
+        # pass's own progress, for comparison with the exchanging step
+        fut = torch.futures.Future(devices=[buf.device])
+        fut.set_result(buf)
+        return fut
     if state.threaded:
         # hand the bucket to the enqueue thread: the autograd thread only records
         # an event and returns
@@ -119,12 +138,15 @@ def flexshm_hook(state, bucket) -> torch.futures.Future[torch.Tensor]:
     # fork from the autograd stream (the bucket's producers), run and complete
     # on the side stream (join-stream mode): the autograd stream never waits
     # for a collective
+    t0 = time.perf_counter()
     state.comm.set_join_stream(state.stream)
     try:
         state.comm.allreduce(buf, op="avg", stream=cur)
         done = state.comm.completion_stream()
     finally:
         state.comm.set_join_stream(None)
+    HOOK_HOST[0] += time.perf_counter() - t0
+    HOOK_HOST[1] += 1
     # the collective ran on the side stream (tell the allocator) and completed
     # on the stream completion_stream() names - the future's event is recorded
     # there (the side stream in join-stream mode).
