@@ -199,6 +199,9 @@ def workload_name(count: int, dtype: str) -> str:
 # SM zero-copy store peak to mapped host memory (profiles/r01_probe/bw.jsonl, "zc"
 # write_gbs, any grid >= 8 CTAs) - the bound of the reduce kernel's result store.
 ZC_WRITE_PEAK = 52.7
+# ... and the same store while copy engines stream H2D and D2H concurrently
+# (profiles/r02/r2k/probe_zc_*.jsonl, load=both, mean of full-GPU and 14 % MPS)
+ZC_WRITE_UNDER_LOAD = 21.1
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
 
@@ -249,8 +252,17 @@ def kernel_roofline(args, n, s_bytes, kernel_ms, kernel_count, iso_us=None, iso_
                                  "hbm_write": link},
             "launch_us": t_launch * 1e6, "launches": kernel_count,
             "timing": "CUDA events around every reduce launch on its lane stream, inside the "
-                      "timed region; includes time-slice waits behind the other 6 processes",
-            "peak_source": "measured SM zero-copy store peak (profiles/r01_probe/bw.jsonl)"}
+                      "timed region",
+            "peak_source": "measured SM zero-copy store peak (profiles/r01_probe/bw.jsonl)",
+            # the same store while copy engines stream both directions, as they do
+            # throughout the pipeline (other ranks' stages / fetches / gathers):
+            # the contended ceiling the live launches run against
+            "under_link_load": {"peak": ZC_WRITE_UNDER_LOAD,
+                                "frac": link / t_launch / 1e9 / ZC_WRITE_UNDER_LOAD,
+                                "peak_source": "tools/probe_zc_contention.py, load=both: the "
+                                               "same kernel and piece alone 48 GB/s, with "
+                                               "concurrent CE H2D + D2H 20.4-21.7 GB/s "
+                                               "(profiles/r02/r2k)"}}
     if iso_us:
         line["isolated"] = {"launch_us": iso_us, "piece_bytes": iso_piece,
                             "achieved": iso_piece / (iso_us * 1e-6) / 1e9,
@@ -651,15 +663,24 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
         with (net.no_sync() if cfg.get("no_sync") else nullcontext()):
             return _step()
 
+    host_phase = {"fwd": 0.0, "bwd": 0.0, "opt": 0.0}  # host enqueue seconds per phase
+
     def _step():
+        t0 = time.perf_counter()
         if name == "bert":
             loss = F.cross_entropy(net(input_ids=x).logits.float(), y)
         else:
             with torch.autocast("cuda", dtype=torch.bfloat16):
                 loss = F.cross_entropy(net(x), y)
         opt.zero_grad(set_to_none=True)
+        t1 = time.perf_counter()
         loss.backward()
+        t2 = time.perf_counter()
         opt.step()
+        t3 = time.perf_counter()
+        host_phase["fwd"] += t1 - t0
+        host_phase["bwd"] += t2 - t1
+        host_phase["opt"] += t3 - t2
         return loss
 
     with torch.cuda.stream(stream):
@@ -684,6 +705,8 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = comm.kernel_launches()
     h0 = list(fddp.HOOK_HOST)
+    for k in host_phase:
+        host_phase[k] = 0.0
     t_host = time.perf_counter()
     ev0.record(stream)
     with torch.cuda.stream(stream):
@@ -696,6 +719,7 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
     out = {"rank": rank, "ms_total": ev0.elapsed_time(ev1), "loss": float(loss.item()),
            "host_enqueue_ms": t_host * 1e3,
            "hook_host_ms": (fddp.HOOK_HOST[0] - h0[0]) * 1e3, "hook_calls": fddp.HOOK_HOST[1] - h0[1],
+           "host_phase_ms": {k: v * 1e3 for k, v in host_phase.items()},
            "stamps": stamps,
            "launches": comm.kernel_launches() - l0,
            "param_digest": float(sum(p.detach().double().sum().item() for p in model.parameters()))}
@@ -782,6 +806,8 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
                      "hook_ms_per_step": max(r["hook_host_ms"] for r in res.values())
                      / args.train_steps,
                      "hooks_per_step": res[0]["hook_calls"] / args.train_steps,
+                     "phase_ms_per_step_rank0": {k: v / args.train_steps for k, v in
+                                                 res[0]["host_phase_ms"].items()},
                      "what": "host time to enqueue the timed steps (max over ranks; loss.item() "
                              "syncs once per step only in the last one) and the part spent "
                              "inside flexshm_hook's collective calls"},

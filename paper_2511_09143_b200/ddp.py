@@ -34,9 +34,10 @@ from .comm import ShmCommunicator
 # measurement aid: is the autograd thread held up by the driver calls?)
 HOOK_HOST = [0.0, 0]
 # FMX_HOOK_STAMP=1: stamp each bucket's readiness on the GPU timeline;
-# FMX_HOOK_NOOP=1: skip the exchange (measurement of the bare backward pass)
+# FMX_HOOK_NOOP=1: skip the exchange (measurement of the bare backward pass);
+# FMX_HOOK_NOOP=2: skip it but keep the side-stream future plumbing
 _MEASURE = {"stamp": os.environ.get("FMX_HOOK_STAMP") == "1",
-            "noop": os.environ.get("FMX_HOOK_NOOP") == "1"}
+            "noop": os.environ.get("FMX_HOOK_NOOP", "0")}
 
 
 class HookState:
@@ -120,11 +121,19 @@ def flexshm_hook(state, bucket) -> torch.futures.Future[torch.Tensor]:
     if _MEASURE["stamp"]:
         # timeline probe: when this bucket's gradient is ready on the GPU
         state.comm.stamp(100 + bucket.index(), stream=cur)
-    if _MEASURE["noop"]:
+    if _MEASURE["noop"] == "1":
         # measurement only: no exchange at all (replicas diverge) - the backward
         # pass's own progress, for comparison with the exchanging step
         fut = torch.futures.Future(devices=[buf.device])
         fut.set_result(buf)
+        return fut
+    if _MEASURE["noop"] == "2":
+        # measurement only: the hook's stream / future plumbing without the exchange
+        state.stream.wait_stream(cur)
+        buf.record_stream(state.stream)
+        with torch.cuda.stream(state.stream):
+            fut = torch.futures.Future(devices=[buf.device])
+            fut.set_result(buf)
         return fut
     if state.threaded:
         # hand the bucket to the enqueue thread: the autograd thread only records

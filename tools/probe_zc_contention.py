@@ -1,5 +1,6 @@
-"""Probe: the reduce kernel's zero-copy result store (SM stores to mapped host
-memory) alone and while copy engines stream host->device (H2D) and/or
+"""Probe: the reduce kernel's zero-copy traffic - its result store (SM stores
+to mapped host memory), or in the ZC flavour its n-1 source reads (SM loads
+from mapped host memory) - alone and while copy engines stream host->device (H2D) and/or
 device->host (D2H) on other streams - the live conditions of the pipeline,
 where every rank's fetch / gather (H2D) and stage (D2H) copies run while an
 owner reduces.  One process, one full 4 MiB piece of 7 sources, CUDA events
@@ -26,20 +27,32 @@ ks = torch.cuda.Stream()
 s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
 
 
-def time_kernel(iters=20):
+# the ZC-transport flavour: n-1 contributions read zero-copy from mapped host
+# memory (the fetch fused into the reduction), result to HBM only
+host_srcs = [srcs[0]] + [torch.randn(piece).pin_memory() for _ in range(n - 1)]
+
+
+def run_once(kind):
+    if kind == "store":
+        reduce_local(srcs, out, op="avg", out_host=out_host, stream=ks)
+    else:
+        reduce_local(host_srcs, out, op="avg", host_sources=range(1, n), stream=ks)
+
+
+def time_kernel(kind, iters=20):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(ks):
         for _ in range(3):
-            reduce_local(srcs, out, op="avg", out_host=out_host, stream=ks)
+            run_once(kind)
         e0.record(ks)
         for _ in range(iters):
-            reduce_local(srcs, out, op="avg", out_host=out_host, stream=ks)
+            run_once(kind)
         e1.record(ks)
     e1.synchronize()
     return e0.elapsed_time(e1) / iters * 1e3  # us
 
 
-for load in ("none", "h2d", "d2h", "both"):
+for kind, load in [(k, ld) for k in ("store", "load") for ld in ("none", "h2d", "d2h", "both")]:
     torch.cuda.synchronize()
     if load in ("h2d", "both"):
         with torch.cuda.stream(s_h2d):
@@ -49,7 +62,9 @@ for load in ("none", "h2d", "d2h", "both"):
         with torch.cuda.stream(s_d2h):
             for _ in range(8):
                 h_dst.copy_(d_buf2, non_blocking=True)
-    us = time_kernel()
+    us = time_kernel(kind)
     torch.cuda.synchronize()
-    print(json.dumps({"probe": "reduce_zc_store_under_load", "load": load, "kernel_us": round(us, 1),
-                      "store_gbs": round(piece * 4 / us / 1e3, 2)}), flush=True)
+    moved = piece * 4 * (1 if kind == "store" else n - 1)
+    print(json.dumps({"probe": f"reduce_zc_{kind}_under_load", "load": load,
+                      "kernel_us": round(us, 1), "link_gbs": round(moved / us / 1e3, 2)}),
+          flush=True)
