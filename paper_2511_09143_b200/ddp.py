@@ -36,6 +36,7 @@ HOOK_HOST = [0.0, 0]
 # FMX_HOOK_STAMP=1: stamp each bucket's readiness on the GPU timeline;
 # FMX_HOOK_NOOP=1: skip the exchange (measurement of the bare backward pass);
 # FMX_HOOK_NOOP=2: skip it but keep the side-stream future plumbing
+_SCRATCH = {}
 _MEASURE = {"stamp": os.environ.get("FMX_HOOK_STAMP") == "1",
             "noop": os.environ.get("FMX_HOOK_NOOP", "0")}
 
@@ -126,6 +127,28 @@ def flexshm_hook(state, bucket) -> torch.futures.Future[torch.Tensor]:
         # pass's own progress, for comparison with the exchanging step
         fut = torch.futures.Future(devices=[buf.device])
         fut.set_result(buf)
+        return fut
+    if _MEASURE["noop"] in ("3", "4"):
+        # measurement only, no exchange: "3" the exchange's copy-engine traffic
+        # alone (bucket D2H to pinned host memory, twice H2D back into scratch);
+        # "4" its reduction kernel alone (7 HBM sources, result to HBM)
+        from .comm import reduce_local
+        state.stream.wait_stream(cur)
+        buf.record_stream(state.stream)
+        with torch.cuda.stream(state.stream):
+            key = (buf.numel(), buf.dtype)
+            if key not in _SCRATCH:
+                _SCRATCH[key] = (torch.empty(buf.numel(), dtype=buf.dtype).pin_memory(),
+                                 torch.empty_like(buf))
+            host, dev = _SCRATCH[key]
+            if _MEASURE["noop"] == "3":
+                host.copy_(buf, non_blocking=True)
+                dev.copy_(host, non_blocking=True)
+                dev.copy_(host, non_blocking=True)
+            else:
+                reduce_local([buf] * 7, dev, op="avg", stream=state.stream)
+            fut = torch.futures.Future(devices=[buf.device])
+            fut.set_result(buf)
         return fut
     if _MEASURE["noop"] == "2":
         # measurement only: the hook's stream / future plumbing without the exchange
