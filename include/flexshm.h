@@ -266,6 +266,35 @@ int fmx_comm_stamp(fmx_comm_t comm, void* stream, uint32_t info);
 /* Number of device kernels this communicator has launched so far. */
 int fmx_comm_kernel_launches(fmx_comm_t comm, uint64_t* launches);
 
+/* ---- fences and CUDA graphs ------------------------------------------------ */
+
+/* Fence: enqueued on `stream` after every earlier collective of this rank; it
+ * completes once every rank reached its own fence (signal FENCE, wait for
+ * every peer's).  After it, no peer touches any SHM slot of an earlier
+ * collective. */
+int fmx_comm_fence(fmx_comm_t comm, void* stream);
+
+/* Capture collectives into a CUDA graph (a whole DP training step, replayed
+ * as one launch: ddp.ShmDataParallel).  No reference interface: NCCL
+ * collectives are capturable (ncclGroup under cudaStreamBeginCapture), and
+ * this is how the SHM path is.
+ *   capture_begin  before the caller begins the stream capture;
+ *   capture_end    after it ended, with the captured cudaGraph_t, BEFORE it
+ *                  is instantiated: appends the end-of-replay fence after every
+ *                  leaf and records the graph's flag operations -> *handle
+ *                  (graph NULL: abandon a failed capture);
+ *   launch_prepare before EVERY launch of an instance (cudaGraphExec_t) of
+ *                  that graph on `stream`: re-bases the instance's flag values
+ *                  to the communicator's round counters (and fences first if
+ *                  collectives ran since the last replay).
+ * Replays of one communicator's graphs and its eager calls are ordered by the
+ * streams they are issued on (a replay on another stream than the previous
+ * one waits for it).  Every rank must capture and replay the same sequence. */
+int fmx_graph_capture_begin(fmx_comm_t comm);
+int fmx_graph_capture_end(fmx_comm_t comm, void* graph, int* handle);
+int fmx_graph_launch_prepare(fmx_comm_t comm, int handle, void* graph_exec, void* stream);
+int fmx_graph_release(fmx_comm_t comm, int handle);
+
 /* ---- schedule introspection (no GPU, no segment) ---------------------------- */
 
 /* Write the schedule `rank` of an `nranks` communicator would enqueue for a

@@ -53,6 +53,8 @@ EXPORTS = (
     "fmx_comm_kernel_launches", "fmx_comm_flags", "fmx_comm_set_timing", "fmx_comm_kernel_time",
     "fmx_comm_monitor", "fmx_comm_set_stamps", "fmx_comm_stamps",
     "fmx_comm_stamp", "fmx_comm_set_join_stream", "fmx_comm_completion_stream",
+    "fmx_comm_fence", "fmx_graph_capture_begin", "fmx_graph_capture_end",
+    "fmx_graph_launch_prepare", "fmx_graph_release",
     "fmx_trace_plan", "fmx_last_error", "fmx_dup_ranks",
     "fmx_abi_version",
 )
@@ -130,6 +132,11 @@ def lib() -> ctypes.CDLL:
         "fmx_comm_stamp": [c_void, c_void, ctypes.c_uint32],
         "fmx_comm_set_join_stream": [c_void, c_void],
         "fmx_comm_completion_stream": [c_void, P(c_void)],
+        "fmx_comm_fence": [c_void, c_void],
+        "fmx_graph_capture_begin": [c_void],
+        "fmx_graph_capture_end": [c_void, c_void, P(c_int)],
+        "fmx_graph_launch_prepare": [c_void, c_int, c_void, c_void],
+        "fmx_graph_release": [c_void, c_int],
         "fmx_trace_plan": [c_int, c_int, c_int, c_size, c_int, P(c_int), P(c_size), P(c_int),
                            P(c_int), ctypes.c_char_p, c_size, P(c_size)],
         "fmx_dup_ranks": [P(c_int), P(c_int)],

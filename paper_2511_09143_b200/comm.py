@@ -280,6 +280,42 @@ class ShmCommunicator:
             out.append((t, tag >> 8, tag & 0xFF, info))
         return out
 
+    # -- fences and CUDA graphs (fmx_comm_fence, fmx_graph_*) ------------------
+    def fence(self, stream=None) -> None:
+        """Every rank reached this point of its stream (after its earlier
+        collectives); see fmx_comm_fence."""
+        self._alive()
+        _lib.check(_lib.lib().fmx_comm_fence(self._h, self._stream(stream)), "fmx_comm_fence")
+
+    def capture_begin(self) -> None:
+        """Announce a stream capture of collectives (before cudaStreamBeginCapture
+        / torch.cuda.graph)."""
+        self._alive()
+        _lib.check(_lib.lib().fmx_graph_capture_begin(self._h), "fmx_graph_capture_begin")
+
+    def capture_end(self, graph) -> int:
+        """After the capture ended, before instantiation: `graph` is the captured
+        cudaGraph_t (int, e.g. torch CUDAGraph(keep_graph=True).raw_cuda_graph()).
+        Appends the end-of-replay fence; returns the graph handle."""
+        self._alive()
+        h = ctypes.c_int()
+        _lib.check(_lib.lib().fmx_graph_capture_end(self._h, ctypes.c_void_p(int(graph) or None),
+                                                    ctypes.byref(h)), "fmx_graph_capture_end")
+        return h.value
+
+    def launch_prepare(self, handle: int, graph_exec, stream=None) -> None:
+        """Before every launch of an instance (cudaGraphExec_t as int) of
+        captured graph `handle` on `stream`."""
+        self._alive()
+        _lib.check(_lib.lib().fmx_graph_launch_prepare(self._h, int(handle),
+                                                       ctypes.c_void_p(int(graph_exec)),
+                                                       self._stream(stream)),
+                   "fmx_graph_launch_prepare")
+
+    def graph_release(self, handle: int) -> None:
+        self._alive()
+        _lib.check(_lib.lib().fmx_graph_release(self._h, int(handle)), "fmx_graph_release")
+
     def flags(self) -> list[list[int]]:
         """Every rank's [STAGED, REDUCED, BC_STAGED, BC_DONE] counters."""
         buf = (ctypes.c_uint32 * (4 * self.size))()

@@ -85,6 +85,44 @@ int load_driver() {
   return FMX_OK;
 }
 
+// Graph entry points (fmx_graph_*), loaded on first use.
+typedef CUresult (*PFN_graphGetNodes)(CUgraph, CUgraphNode*, size_t*);
+typedef CUresult (*PFN_nodeGetType)(CUgraphNode, CUgraphNodeType*);
+typedef CUresult (*PFN_memopGet)(CUgraphNode, CUDA_BATCH_MEM_OP_NODE_PARAMS*);
+typedef CUresult (*PFN_execMemopSet)(CUgraphExec, CUgraphNode, const CUDA_BATCH_MEM_OP_NODE_PARAMS*);
+typedef CUresult (*PFN_addMemop)(CUgraphNode*, CUgraph, const CUgraphNode*, size_t,
+                                 const CUDA_BATCH_MEM_OP_NODE_PARAMS*);
+typedef CUresult (*PFN_nodeDeps)(CUgraphNode, CUgraphNode*, size_t*);
+PFN_graphGetNodes g_graph_nodes = nullptr;
+PFN_nodeGetType g_node_type = nullptr;
+PFN_memopGet g_memop_get = nullptr;
+PFN_execMemopSet g_exec_memop_set = nullptr;
+PFN_addMemop g_add_memop = nullptr;
+PFN_nodeDeps g_node_dependents = nullptr;
+std::once_flag g_graph_once;
+int g_graph_status = FMX_OK;
+
+int load_graph_driver() {
+  if (int rc = load_driver()) return rc;
+  std::call_once(g_graph_once, [] {
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      cudaError_t e = cudaGetDriverEntryPointByVersion(name, fn, 12000, cudaEnableDefault, &q);
+      if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !*fn)
+        g_graph_status = FMX_ERR_UNSUPPORTED;
+    };
+    get("cuGraphGetNodes", (void**)&g_graph_nodes);
+    get("cuGraphNodeGetType", (void**)&g_node_type);
+    get("cuGraphBatchMemOpNodeGetParams", (void**)&g_memop_get);
+    get("cuGraphExecBatchMemOpNodeSetParams", (void**)&g_exec_memop_set);
+    get("cuGraphAddBatchMemOpNode", (void**)&g_add_memop);
+    get("cuGraphNodeGetDependentNodes", (void**)&g_node_dependents);
+  });
+  if (g_graph_status != FMX_OK)
+    return fail(FMX_ERR_UNSUPPORTED, "driver graph entry points (batch memop nodes) unavailable");
+  return FMX_OK;
+}
+
 #define FMX_CUDA(call)                                                                    \
   do {                                                                                    \
     cudaError_t _e = (call);                                                              \
@@ -148,8 +186,9 @@ class CudaSink final : public Sink {
   CudaSink(fmx_comm* c) : c_(c) {}
 
   // serialize mode: wait (on the host) for everything this rank enqueued so far
+  // (not while capturing: nothing runs during a capture)
   int drain() {
-    if (!c_->serialize) return FMX_OK;
+    if (!c_->serialize || c_->cap_active) return FMX_OK;
     const cudaStream_t ss[4] = {c_->user, lane_stream(c_, 0), lane_stream(c_, 1),
                                 lane_stream(c_, 2)};
     for (int i = 0; i < 4; ++i) FMX_CUDA(cudaStreamSynchronize(ss[i]));
@@ -158,7 +197,7 @@ class CudaSink final : public Sink {
 
   // timeline probe: stamp the completion of the op just enqueued on `lane`
   int stamp(int lane, int kind, uint32_t info) {
-    if (!c_->stamps || c_->stamp_used >= c_->stamp_cap) return FMX_OK;
+    if (!c_->stamps || c_->stamp_used >= c_->stamp_cap || c_->cap_active) return FMX_OK;
     if (int rc = drain()) return rc;
     fmx_stamp_kernel<<<1, 1, 0, lane_stream(c_, lane)>>>(c_->stamps + c_->stamp_used++,
                                                           (uint32_t)(lane << 8 | kind), info);
@@ -232,7 +271,7 @@ class CudaSink final : public Sink {
     if (int rc = drain()) return rc;
     cudaStream_t s = lane_stream(c_, lane);
     cudaEvent_t t0 = nullptr, t1 = nullptr;
-    if (c_->timing) {
+    if (c_->timing && !c_->cap_active) {
       if (c_->timed_used == c_->timed.size()) {
         cudaEvent_t x, y;
         FMX_CUDA(cudaEventCreate(&x));
@@ -295,10 +334,15 @@ class CudaSink final : public Sink {
 
   int record(int lane, int ev) override {
     FMX_CUDA(cudaEventRecord(c_->ev[ev], lane_stream(c_, lane)));
+    c_->ev_cap[ev] = c_->cap_active;
     return FMX_OK;
   }
 
+  // A wait on an event last recorded in another capture or on the eager
+  // timeline is dropped (it cannot be captured, and is covered by the stream
+  // order of graph launches plus the fence every replay ends with).
   int wait_event_impl(int lane, int ev) {
+    if (c_->ev_cap[ev] != c_->cap_active) return FMX_OK;
     FMX_CUDA(cudaStreamWaitEvent(lane_stream(c_, lane), c_->ev[ev], 0));
     return FMX_OK;
   }
@@ -326,8 +370,10 @@ class CudaSink final : public Sink {
   int copy_signal(int lane, const std::vector<PlanSeg>& segs, bool src_sys, bool use_kernel,
                   int flag, uint32_t v) override {
     // zero-copy copy kernel that releases the flag itself (one launch, no memop)
+    // (not in a captured graph: every flag value must sit in a memop node that
+    // fmx_graph_launch_prepare can re-base)
     if (!use_kernel || !c_->fuse_signal || !c_->ctas_done || segs.empty() ||
-        segs.size() > (size_t)kMaxSegs || c_->stamps)
+        segs.size() > (size_t)kMaxSegs || c_->stamps || c_->cap_active)
       return Sink::copy_signal(lane, segs, src_sys, use_kernel, flag, v);
     const uint32_t* fl = (const uint32_t*)c_->flag_dev(c_->rank, flag);
     // one counter per lane that fuses signals (stage copies on lane 0, the
@@ -340,7 +386,7 @@ class CudaSink final : public Sink {
   // CTAs cost more than the memop wait saves, 0.119 vs 0.096 ms, r02/r2h)
   int wait_reduce(int lane, const PlanReduce& r, int flag, uint32_t v, int skip) override {
     const size_t bytes = r.args.len * (r.dtype == FMX_FLOAT32 ? 4 : 2);
-    if (!c_->spin_wait || c_->stamps || r.args.len == 0 || bytes > (16u << 10))
+    if (!c_->spin_wait || c_->stamps || c_->cap_active || r.args.len == 0 || bytes > (16u << 10))
       return Sink::wait_reduce(lane, r, flag, v, skip);
     PlanReduce f = r;
     f.args.wait_flags = (const char*)c_->flag_dev(0, flag);
@@ -405,11 +451,15 @@ int release_lane_objects(fmx_comm* c) {
   if (!c->lane_ctx) return FMX_OK;
   if (g_ctx_push(c->lane_ctx) != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "cuCtxPushCurrent failed");
   int rc = FMX_OK;
-  if (c->has_done && cudaEventSynchronize(c->done) != cudaSuccess)
+  if (c->has_done && c->done_cap == 0 && cudaEventSynchronize(c->done) != cudaSuccess)
     rc = fail(FMX_ERR_CUDA, "pending collective failed: %s", cudaGetErrorString(cudaGetLastError()));
+  if (c->graph_stream && cudaStreamSynchronize(c->graph_stream) != cudaSuccess && rc == FMX_OK)
+    rc = fail(FMX_ERR_CUDA, "pending graph replay failed: %s", cudaGetErrorString(cudaGetLastError()));
   if (c->done) cudaEventDestroy(c->done);
   if (c->fork) cudaEventDestroy(c->fork);
-  c->done = c->fork = nullptr;
+  if (c->graph_ev) cudaEventDestroy(c->graph_ev);
+  c->done = c->fork = c->graph_ev = nullptr;
+  c->graph_stream = nullptr;
   for (int i = 0; i < kNumEvents; ++i) {
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     c->ev[i] = nullptr;
@@ -452,6 +502,7 @@ int make_lane_objects(fmx_comm* c, CUcontext ctx) {
   }
   FMX_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
   FMX_CUDA(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
+  FMX_CUDA(cudaEventCreateWithFlags(&c->graph_ev, cudaEventDisableTiming));
   for (int i = 0; i < kNumEvents; ++i) FMX_CUDA(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
   c->lane_ctx = ctx;
   return FMX_OK;
@@ -483,8 +534,25 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
     }
   } pop;
   int rc;
+  // capture discipline: a captured collective must be announced
+  // (fmx_graph_capture_begin) so its flag values can be re-based per replay
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  FMX_CUDA(cudaStreamIsCapturing(user, &cs));
+  if (cs == cudaStreamCaptureStatusActive && !c->cap_active)
+    return fail(FMX_ERR_INVALID_ARG, "collective on a capturing stream: call fmx_graph_capture_begin first");
+  if (cs != cudaStreamCaptureStatusActive && c->cap_active)
+    return fail(FMX_ERR_INVALID_ARG, "capture mode is on but the stream is not capturing");
   if (ctx != c->lane_ctx) {
+    if (c->cap_active) return fail(FMX_ERR_INVALID_ARG, "context change inside a capture");
     if ((rc = release_lane_objects(c)) || (rc = make_lane_objects(c, ctx))) return rc;
+  }
+  // the first eager call after a graph replay on another stream is ordered after it
+  if (!c->cap_active && c->graph_stream) {
+    if (c->graph_stream != user) {
+      FMX_CUDA(cudaEventRecord(c->graph_ev, c->graph_stream));
+      FMX_CUDA(cudaStreamWaitEvent(user, c->graph_ev, 0));
+    }
+    c->graph_stream = nullptr;
   }
   c->user = user;
   cudaStream_t main = c->join_stream ? c->join_stream : user;  // lane 1 and the join target
@@ -499,7 +567,8 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
   // when it joined the caller's stream)
   // A change of main stream is a barrier too: lane 1 (HBM scratch slots) is
   // ordered across calls only while it stays on one stream.
-  const bool barrier = c->has_done && (cls != 0 || c->last_class != 0 || main != c->last_main);
+  const bool barrier = c->has_done && c->done_cap == c->cap_active &&
+                       (cls != 0 || c->last_class != 0 || main != c->last_main);
   std::vector<cudaStream_t> lanes_ = extra;
   if (main != user) lanes_.push_back(main);
   if (!lanes_.empty()) FMX_CUDA(cudaEventRecord(c->fork, user));
@@ -519,6 +588,8 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
   }
   if (rc) return rc;
   FMX_CUDA(cudaEventRecord(c->done, target));
+  c->done_cap = c->cap_active;
+  c->fenced = false;
   c->has_done = true;
   c->last_class = cls;
   c->last_main = main;
@@ -1204,6 +1275,268 @@ int fmx_comm_stamps(fmx_comm_t c, uint64_t* out, size_t cap, size_t* n_out) {
     out[2 * i] = h[i].t_ns;
     out[2 * i + 1] = ((uint64_t)h[i].tag << 32) | h[i].info;
   }
+  return FMX_OK;
+}
+
+// ---- CUDA graphs ---------------------------------------------------------------
+//
+// A training step that contains collectives can be captured into one CUDA
+// graph and replayed (ddp.ShmDataParallel).  Eager launches make the GPU read
+// every launch's work from host memory, and those reads queue behind the
+// exchange's own host-link traffic: ResNet-50 fwd+bwd 10.7 -> 18.2 ms under
+// D2H copy traffic eager, 8.5 -> 8.7 ms as a graph (profiles/r02/r2o).
+//
+// Graph nodes bake their parameters, and a collective's flag values are round
+// counters.  So: capture_begin snapshots the counters; every captured signal /
+// wait is a batch-memop node; capture_end appends a fence (signal FENCE, wait
+// for every peer's FENCE) after every leaf, finds the memop nodes on this
+// communicator's flags and rolls the counters back (nothing ran);
+// launch_prepare re-bases each node's values by how far its counter moved since
+// the capture and advances the counters by one replay.  Slot addresses stay as
+// captured: every replay starts with no peer touching any slot (the previous
+// replay's fence; an eager fence first if collectives ran since), so the
+// schedule inside a replay is the model-checked one, shifted in round numbers
+// only.  Replays (and eager calls after them) are ordered by stream order.
+
+namespace {
+
+int flag_counter(const fmx_comm* c, CUdeviceptr addr) {
+  const CUdeviceptr base = c->flag_dev(0, 0);
+  const CUdeviceptr end = base + (CUdeviceptr)c->nranks * kFlagsPerRank * 64;
+  if (addr < base || addr >= end) return -1;
+  const int f = (int)(((addr - base) / 64) % kFlagsPerRank);
+  if (f == kStaged || f == kReduced || f >= kStagedTo) return kCtrAr;
+  if (f == kOsReady) return kCtrOs;
+  if (f == kBcStaged || f == kBcDone) return kCtrBc;
+  if (f == kFence) return kCtrFence;
+  return -2;
+}
+
+struct CtxPush {
+  bool on = false;
+  explicit CtxPush(CUcontext ctx) { on = ctx && g_ctx_push && g_ctx_push(ctx) == CUDA_SUCCESS; }
+  ~CtxPush() {
+    CUcontext d;
+    if (on) g_ctx_pop(&d);
+  }
+};
+
+}  // namespace
+
+int fmx_comm_fence(fmx_comm_t c, void* stream) {
+  int rc = check_comm(c);
+  if (rc) return rc;
+  CudaSink sink(c);
+  const uint32_t v = c->fence_round + 1;
+  rc = on_lanes(c, (cudaStream_t)stream, 1, [&]() -> int {
+    if (c->nranks == 1) return FMX_OK;
+    int r = sink.signal(kLaneMain, kFence, v);
+    return r ? r : sink.wait_peers(kLaneMain, kFence, v, c->rank);
+  });
+  if (rc) return rc;
+  c->fence_round = v;
+  if (!c->cap_active) c->fenced = true;
+  return FMX_OK;
+}
+
+int fmx_graph_capture_begin(fmx_comm_t c) {
+  int rc = check_comm(c);
+  if (rc) return rc;
+  if (c->cap_active) return fail(FMX_ERR_INVALID_ARG, "a capture is already active");
+  if ((rc = load_graph_driver())) return rc;
+  if (c->has_done && c->done_cap == 0 && c->lane_ctx) {
+    // eager work still in flight: the captured collectives drop their waits
+    // on eager events, and a replay is ordered after it by launch_prepare
+    CtxPush push(c->lane_ctx);
+    FMX_CUDA(cudaEventSynchronize(c->done));
+  }
+  for (int k = 0; k < kNumCounters; ++k) c->cap_c0[k] = *c->counter(k);
+  c->cap_launches0 = c->launches;
+  c->cap_active = ++c->cap_next;
+  return FMX_OK;
+}
+
+int fmx_graph_capture_end(fmx_comm_t c, void* graph, int* handle) {
+  if (!c || !c->hdr || (graph && !handle)) return fail(FMX_ERR_INVALID_ARG, "null argument");
+  if (!c->cap_active) return fail(FMX_ERR_INVALID_ARG, "no capture is active");
+  c->cap_active = 0;
+  if (!graph) {  // the capture failed: abandon it (nothing was enqueued that will run)
+    for (int k = 0; k < kNumCounters; ++k) *c->counter(k) = c->cap_c0[k];
+    c->launches = c->cap_launches0;
+    return FMX_OK;
+  }
+  CUgraph g = (CUgraph)graph;
+  GraphRec rec;
+  for (int k = 0; k < kNumCounters; ++k) {
+    rec.c0[k] = c->cap_c0[k];
+    rec.delta[k] = *c->counter(k) - c->cap_c0[k];
+  }
+  rec.launches = c->launches - c->cap_launches0;
+  auto rollback = [&] {
+    for (int k = 0; k < kNumCounters; ++k) *c->counter(k) = c->cap_c0[k];
+    c->launches = c->cap_launches0;
+  };
+  if (!c->lane_ctx) {
+    rollback();
+    return fail(FMX_ERR_INVALID_ARG, "no collective was captured");
+  }
+  CtxPush push(c->lane_ctx);
+  auto nodes_of = [&](std::vector<CUgraphNode>& v) -> int {
+    size_t n = 0;
+    if (g_graph_nodes(g, nullptr, &n) != CUDA_SUCCESS) return fail(FMX_ERR_CUDA, "cuGraphGetNodes failed");
+    v.resize(n);
+    if (n && g_graph_nodes(g, v.data(), &n) != CUDA_SUCCESS)
+      return fail(FMX_ERR_CUDA, "cuGraphGetNodes failed");
+    v.resize(n);
+    return FMX_OK;
+  };
+  std::vector<CUgraphNode> nodes;
+  int rc = nodes_of(nodes);
+  // the end-of-replay fence, after every leaf of the captured graph
+  if (rc == FMX_OK && c->nranks > 1) {
+    std::vector<CUgraphNode> leaves;
+    for (CUgraphNode nd : nodes) {
+      size_t k = 0;
+      if (g_node_dependents(nd, nullptr, &k) != CUDA_SUCCESS) {
+        rc = fail(FMX_ERR_CUDA, "cuGraphNodeGetDependentNodes failed");
+        break;
+      }
+      if (k == 0) leaves.push_back(nd);
+    }
+    const uint32_t v = c->fence_round + 1;
+    CUstreamBatchMemOpParams sig;
+    memset(&sig, 0, sizeof sig);
+    sig.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+    sig.writeValue.address = c->flag_dev(c->rank, kFence);
+    sig.writeValue.value = v;
+    sig.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+    std::vector<CUstreamBatchMemOpParams> waits;
+    for (int q = 0; q < c->nranks; ++q) {
+      if (q == c->rank) continue;
+      CUstreamBatchMemOpParams w;
+      memset(&w, 0, sizeof w);
+      w.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+      w.waitValue.address = c->flag_dev(q, kFence);
+      w.waitValue.value = v;
+      w.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+      waits.push_back(w);
+    }
+    CUDA_BATCH_MEM_OP_NODE_PARAMS p;
+    memset(&p, 0, sizeof p);
+    p.ctx = c->lane_ctx;
+    p.count = 1;
+    p.paramArray = &sig;
+    CUgraphNode sn = nullptr, wn = nullptr;
+    if (rc == FMX_OK && g_add_memop(&sn, g, leaves.data(), leaves.size(), &p) != CUDA_SUCCESS)
+      rc = fail(FMX_ERR_CUDA, "adding the fence signal node failed");
+    p.count = (unsigned)waits.size();
+    p.paramArray = waits.data();
+    if (rc == FMX_OK && g_add_memop(&wn, g, &sn, 1, &p) != CUDA_SUCCESS)
+      rc = fail(FMX_ERR_CUDA, "adding the fence wait node failed");
+    rec.delta[kCtrFence] += 1;
+    if (rc == FMX_OK) rc = nodes_of(nodes);
+  }
+  // every memop node on this communicator's flags
+  for (size_t i = 0; rc == FMX_OK && i < nodes.size(); ++i) {
+    CUgraphNodeType t;
+    if (g_node_type(nodes[i], &t) != CUDA_SUCCESS) {
+      rc = fail(FMX_ERR_CUDA, "cuGraphNodeGetType failed");
+      break;
+    }
+    if (t != CU_GRAPH_NODE_TYPE_BATCH_MEM_OP) continue;
+    CUDA_BATCH_MEM_OP_NODE_PARAMS p;
+    if (g_memop_get(nodes[i], &p) != CUDA_SUCCESS) {
+      rc = fail(FMX_ERR_CUDA, "cuGraphBatchMemOpNodeGetParams failed");
+      break;
+    }
+    GraphMemop m;
+    m.node = nodes[i];
+    m.ctx = p.ctx;
+    m.flags = p.flags;
+    m.ops.assign(p.paramArray, p.paramArray + p.count);
+    bool mine = false;
+    for (const CUstreamBatchMemOpParams& op : m.ops) {
+      CUdeviceptr a = 0;
+      if (op.operation == CU_STREAM_MEM_OP_WRITE_VALUE_32) a = op.writeValue.address;
+      else if (op.operation == CU_STREAM_MEM_OP_WAIT_VALUE_32) a = op.waitValue.address;
+      const int k = a ? flag_counter(c, a) : -1;
+      if (k == -2) {
+        rc = fail(FMX_ERR_UNSUPPORTED, "captured memop on an unexpected flag");
+        break;
+      }
+      m.ctr.push_back((int8_t)k);
+      mine |= k >= 0;
+    }
+    if (mine) rec.memops.push_back(std::move(m));
+  }
+  rollback();
+  if (rc) return rc;
+  c->graphs.push_back(std::move(rec));
+  *handle = (int)c->graphs.size() - 1;
+  return FMX_OK;
+}
+
+int fmx_graph_launch_prepare(fmx_comm_t c, int handle, void* graph_exec, void* stream) {
+  int rc = check_comm(c);
+  if (rc) return rc;
+  if (handle < 0 || handle >= (int)c->graphs.size() || !c->graphs[handle].live || !graph_exec)
+    return fail(FMX_ERR_INVALID_ARG, "bad graph handle");
+  if (c->cap_active) return fail(FMX_ERR_INVALID_ARG, "launch_prepare inside a capture");
+  GraphRec& rec = c->graphs[handle];
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!c->fenced && c->nranks > 1) {
+    // collectives ran since the last replay: fence first, on the launch stream
+    cudaStream_t js = c->join_stream;
+    c->join_stream = nullptr;
+    rc = fmx_comm_fence(c, stream);
+    c->join_stream = js;
+    if (rc) return rc;
+  }
+  CtxPush push(c->lane_ctx);
+  if (c->graph_stream && c->graph_stream != s) {  // previous replay on another stream
+    FMX_CUDA(cudaEventRecord(c->graph_ev, c->graph_stream));
+    FMX_CUDA(cudaStreamWaitEvent(s, c->graph_ev, 0));
+  }
+  if (c->has_done && c->done_cap == 0) FMX_CUDA(cudaStreamWaitEvent(s, c->done, 0));
+  uint32_t off[kNumCounters];
+  for (int k = 0; k < kNumCounters; ++k) off[k] = *c->counter(k) - rec.c0[k];
+  if (rec.exec != (CUgraphExec)graph_exec || memcmp(off, rec.applied, sizeof off) != 0) {
+    std::vector<CUstreamBatchMemOpParams> ops;
+    for (const GraphMemop& m : rec.memops) {
+      ops = m.ops;
+      for (size_t i = 0; i < ops.size(); ++i) {
+        if (m.ctr[i] < 0) continue;
+        if (ops[i].operation == CU_STREAM_MEM_OP_WRITE_VALUE_32) ops[i].writeValue.value += off[m.ctr[i]];
+        else ops[i].waitValue.value += off[m.ctr[i]];
+      }
+      CUDA_BATCH_MEM_OP_NODE_PARAMS p;
+      memset(&p, 0, sizeof p);
+      p.ctx = m.ctx;
+      p.count = (unsigned)ops.size();
+      p.paramArray = ops.data();
+      p.flags = m.flags;
+      CUresult r = g_exec_memop_set((CUgraphExec)graph_exec, m.node, &p);
+      if (r != CUDA_SUCCESS) {
+        rec.exec = nullptr;
+        return fail(FMX_ERR_CUDA, "cuGraphExecBatchMemOpNodeSetParams failed (%d)", (int)r);
+      }
+    }
+    rec.exec = (CUgraphExec)graph_exec;
+    memcpy(rec.applied, off, sizeof off);
+  }
+  for (int k = 0; k < kNumCounters; ++k) *c->counter(k) += rec.delta[k];
+  c->fenced = true;
+  c->graph_stream = s;
+  c->launches += rec.launches;
+  return FMX_OK;
+}
+
+int fmx_graph_release(fmx_comm_t c, int handle) {
+  if (!c || handle < 0 || handle >= (int)c->graphs.size())
+    return fail(FMX_ERR_INVALID_ARG, "bad graph handle");
+  c->graphs[handle].live = false;
+  c->graphs[handle].memops.clear();
+  c->graphs[handle].exec = nullptr;
   return FMX_OK;
 }
 

@@ -15,6 +15,32 @@
 
 namespace fmx {
 constexpr int kNumEvents = 2 * FMX_MAX_SLOTS + 7;  // W[K], G[K]; host path F[2], C[2], inputs, P[2]
+
+// Round counters a flag's values follow (fmx_graph_*: baked flag values of a
+// captured graph are re-based per replay by their counter's advance).
+enum Counter { kCtrAr = 0, kCtrOs = 1, kCtrBc = 2, kCtrFence = 3, kNumCounters = 4 };
+
+// One batch-memop node of a captured graph that signals / waits on this
+// communicator's flags, with its parameters as captured.
+struct GraphMemop {
+  CUgraphNode node;
+  CUcontext ctx;
+  unsigned int flags;
+  std::vector<CUstreamBatchMemOpParams> ops;
+  std::vector<int8_t> ctr;  // Counter of each op's flag (-1: not this communicator's)
+};
+
+// A captured graph (fmx_graph_capture_end): flag values as captured against
+// counters c0, the counters' advance per replay, and the values last written
+// into an instantiated graph.
+struct GraphRec {
+  uint32_t c0[kNumCounters] = {}, delta[kNumCounters] = {};
+  uint64_t launches = 0;  // kernels per replay
+  std::vector<GraphMemop> memops;
+  CUgraphExec exec = nullptr;  // exec the `applied` offsets were written into
+  uint32_t applied[kNumCounters] = {};
+  bool live = true;
+};
 }  // namespace fmx
 
 using fmx::Header;
@@ -88,6 +114,27 @@ struct fmx_comm {
   std::vector<fmx_peer_info> peers;
   std::vector<uint32_t> abort_target;  // fmx_comm_abort: raised flag values (re-asserted)
   std::vector<CUstreamBatchMemOpParams> ops;
+
+  // CUDA-graph capture (fmx_graph_*).  While a capture is active (cap_active =
+  // its id) every collective is recorded into the caller's stream capture with
+  // flag values from the counters; events remember the capture they were last
+  // recorded in (0: eager) and a wait on an event of another capture / of the
+  // eager timeline is dropped: that ordering comes from the stream order of
+  // graph launches and the fence every replay ends with.
+  uint32_t fence_round = 0;
+  int cap_active = 0, cap_next = 0;
+  uint32_t cap_c0[fmx::kNumCounters] = {};
+  uint64_t cap_launches0 = 0;
+  int ev_cap[fmx::kNumEvents] = {};
+  int done_cap = 0;
+  bool fenced = true;                    // no collective since the last fence / replay
+  cudaStream_t graph_stream = nullptr;   // stream of the last replay (ordering of the next call)
+  cudaEvent_t graph_ev = nullptr;
+  std::vector<fmx::GraphRec> graphs;
+  uint32_t* counter(int k) {
+    return k == fmx::kCtrAr ? &ar_round : k == fmx::kCtrOs ? &os_round
+                                        : k == fmx::kCtrBc ? &bc_round : &fence_round;
+  }
 
   // byte offsets of the pipeline slots inside the segment
   size_t in_off(uint32_t R, int owner, int contrib) const {

@@ -22,8 +22,10 @@ constexpr uint32_t kMagicReady = 0x464D5831u;  // "FMX1"
 constexpr uint32_t kVersion = 3;
 // Per rank: 8 scalar flags, then one STAGED_TO flag per destination owner.
 // OS_READY is the one-shot small-message allreduce's own round counter
-// (plan_allreduce_oneshot, flexshm_plan.cpp).
-enum Flag { kStaged = 0, kReduced = 1, kBcStaged = 2, kBcDone = 3, kOsReady = 4, kStagedTo = 8 };
+// (plan_allreduce_oneshot, flexshm_plan.cpp); FENCE the end-of-replay fence of
+// captured graphs (fmx_graph_*, flexshm_comm.cu).
+enum Flag { kStaged = 0, kReduced = 1, kBcStaged = 2, kBcDone = 3, kOsReady = 4, kFence = 5,
+            kStagedTo = 8 };
 // One-shot slots: [kOsSlots][rank][os_bytes], alternating between calls.
 constexpr int kOsSlots = 2;
 constexpr size_t kOneShotCap = 1u << 20;  // largest one-shot message (FMX_ONESHOT_MAX is clamped)

@@ -265,6 +265,193 @@ def wrap(module: torch.nn.Module, comm: ShmCommunicator, control_group=None,
     return ddp
 
 
+class ShmDataParallel(torch.nn.Module):
+    """Data parallelism over the SHM communicator whose whole training step
+    can be captured into ONE CUDA graph (`graphed_step`).
+
+    Same contract as DDP + flexshm_hook - parameters broadcast from rank 0,
+    gradients averaged bucket by bucket while the backward pass runs, DDP's
+    default-hook arithmetic (x * fl32(1/n), rank-order fp32 sum) - re-expressed
+    without torch's C++ Reducer, whose futures and host callbacks cannot live
+    in a graph:
+
+    * buckets follow DDP's rebuilt assignment: the order gradients became
+      ready in the first backward pass (reducer.cpp rebuild_buckets), a
+      first bucket of `first_bucket_mb` (dist._DEFAULT_FIRST_BUCKET_BYTES),
+      the rest up to `bucket_cap_mb`; one flat buffer per bucket, each
+      parameter's .grad a view of it (gradient_as_bucket_view);
+    * a post-accumulate-grad hook counts each bucket's gradients; a complete
+      bucket - and every complete one after it, in index order, the same on
+      every rank - is allreduced (op="avg") forking from the autograd stream
+      onto a side stream (join-stream mode); an autograd final callback
+      launches any bucket left and joins the side stream back.
+
+    Why a graph: eager kernel launches make the GPU fetch each launch's work
+    from host memory, and those reads queue behind the exchange's own PCIe
+    traffic - ResNet-50 fwd+bwd 10.7 -> 18.2 ms under D2H copy traffic eager,
+    8.5 -> 8.7 ms replayed as a graph (profiles/r02/r2o).  The collectives
+    inside are re-based per replay by the library (fmx_graph_*).
+
+    Call `zero_grad()` (in-place zeroing of the buckets) instead of the
+    optimizer's set_to_none; gradients that arrive detached from their bucket
+    view are copied into it.
+    """
+
+    def __init__(self, module: torch.nn.Module, comm: ShmCommunicator, bucket_cap_mb: float = 8.0,
+                 first_bucket_mb: float = 1.0, stream=None):
+        super().__init__()
+        self.module = module
+        self.comm = comm
+        broadcast_parameters(module, comm, root=0)
+        self.params = [p for p in module.parameters() if p.requires_grad]
+        self.cap = int(bucket_cap_mb * (1 << 20))
+        self.first_cap = int(first_bucket_mb * (1 << 20))
+        self.hook_state = HookState(comm, stream)
+        self.stream = self.hook_state.stream
+        self.buckets = None          # [(flat tensor, [param index])]
+        self.bucket_of = None        # param index -> bucket index
+        self._order = []             # first backward: gradient-ready order
+        self._pending = []
+        self._next = 0
+        self._armed = False
+        index = {id(p): i for i, p in enumerate(self.params)}
+        self._hooks = [p.register_post_accumulate_grad_hook(
+            lambda p, i=index[id(p)]: self._on_grad(i)) for p in self.params]
+
+    def forward(self, *args, **kwargs):
+        return self.module(*args, **kwargs)
+
+    # -- buckets -------------------------------------------------------------
+    def _build(self):
+        seen = set(self._order)
+        order = self._order + [i for i in range(len(self.params)) if i not in seen]
+        groups, cur, cur_bytes, cur_dtype = [], [], 0, None
+        for i in order:
+            p = self.params[i]
+            nb = p.numel() * p.element_size()
+            cap = self.first_cap if not groups else self.cap
+            if cur and (p.dtype != cur_dtype or cur_bytes + nb > cap):
+                groups.append(cur)
+                cur, cur_bytes = [], 0
+            cur.append(i)
+            cur_bytes += nb
+            cur_dtype = p.dtype
+        if cur:
+            groups.append(cur)
+        self.buckets, self.bucket_of, self._views = [], {}, {}
+        for b, idx in enumerate(groups):
+            p0 = self.params[idx[0]]
+            flat = torch.zeros(sum(self.params[i].numel() for i in idx), dtype=p0.dtype,
+                               device=p0.device)
+            off = 0
+            for i in idx:
+                p = self.params[i]
+                view = flat[off:off + p.numel()].view_as(p)
+                if p.grad is not None:
+                    view.copy_(p.grad)
+                p.grad = view
+                off += p.numel()
+                self.bucket_of[i] = b
+                self._views[i] = view
+            self.buckets.append((flat, idx))
+
+    def zero_grad(self, set_to_none: bool = False):  # noqa: ARG002 - buckets are persistent
+        if self.buckets is None:
+            for p in self.params:
+                p.grad = None
+            return
+        for flat, _ in self.buckets:
+            flat.zero_()
+
+    # -- hooks ---------------------------------------------------------------
+    def _arm(self):
+        if not self._armed:
+            self._armed = True
+            if self.buckets is not None:
+                self._pending = [len(idx) for _, idx in self.buckets]
+                self._next = 0
+            torch.autograd.Variable._execution_engine.queue_callback(self._finish)
+
+    def _on_grad(self, i):
+        self._arm()
+        if self.buckets is None:
+            self._order.append(i)
+            return
+        p, view = self.params[i], self._views[i]
+        if p.grad is None or p.grad.data_ptr() != view.data_ptr():
+            # the gradient left its bucket view (set_to_none): move it back
+            if p.grad is None:
+                view.zero_()
+            else:
+                view.copy_(p.grad)
+            p.grad = view
+        b = self.bucket_of[i]
+        self._pending[b] -= 1
+        while self._next < len(self.buckets) and self._pending[self._next] == 0:
+            self._launch(self._next)
+            self._next += 1
+
+    def _launch(self, b):
+        flat, _ = self.buckets[b]
+        cur = torch.cuda.current_stream(flat.device)
+        self.comm.set_join_stream(self.stream)
+        try:
+            self.comm.allreduce(flat, op="avg", stream=cur)
+        finally:
+            self.comm.set_join_stream(None)
+
+    def _finish(self):
+        self._armed = False
+        if self.buckets is None:
+            self._build()          # first backward: buckets in gradient-ready order
+            self._pending = [0] * len(self.buckets)
+            self._next = 0
+        while self._next < len(self.buckets):
+            self._launch(self._next)
+            self._next += 1
+        torch.cuda.current_stream(self.params[0].device).wait_stream(self.stream)
+
+    # -- CUDA graph ----------------------------------------------------------
+    def graphed_step(self, step_fn, warmup: int = 3):
+        """Capture `step_fn` - forward, backward and optimizer step on static
+        input tensors, returning its outputs - into one CUDA graph; returns
+        `replay()`, which runs one training step and returns the same (static)
+        outputs.  Runs `warmup` eager steps first (bucket assignment,
+        optimizer state, cuDNN plans).  Every rank must capture the same step."""
+        dev = self.params[0].device
+        # capture on the caller's stream (an instance's stream lives in its
+        # green / MPS context) unless that is the legacy default stream
+        cur = torch.cuda.current_stream(dev)
+        s = cur if cur.cuda_stream != 0 else torch.cuda.Stream(device=dev)
+        s.wait_stream(cur)
+        with torch.cuda.stream(s):
+            for _ in range(max(1, warmup)):
+                step_fn()
+        cur.wait_stream(s)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph(keep_graph=True)
+        self.comm.capture_begin()
+        try:
+            with torch.cuda.graph(g, stream=s):
+                out = step_fn()
+        except BaseException:
+            self.comm.capture_end(0)       # abandon the capture (counters roll back)
+            raise
+        handle = self.comm.capture_end(g.raw_cuda_graph())
+        g.instantiate()
+        exec_ = g.raw_cuda_graph_exec()
+        comm = self.comm
+
+        def replay():
+            comm.launch_prepare(handle, exec_, torch.cuda.current_stream(dev))
+            g.replay()
+            return out
+
+        replay.graph = g
+        replay.handle = handle
+        return replay
+
+
 class ZeroShardBroadcast:
     """After a sharded optimizer step, rank r owns parameter shard r; every
     shard is broadcast from its owner so all replicas agree again."""

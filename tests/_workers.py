@@ -325,3 +325,73 @@ def zero_worker(rank: int, job_key: str, n: int, mode: str = "green"):
     comm.barrier(60)
     comm.destroy()
     return out
+
+
+def graph_dp_worker(rank: int, job_key: str, n: int, mode: str = "mps", steps: int = 5,
+                    warmup: int = 2):
+    """ddp.ShmDataParallel on a small MLP: (1) the first step's averaged
+    gradient next to this rank's local gradient (oracle check in the test);
+    (2) `steps` eager training steps; (3) the same from the same start as a
+    captured CUDA graph (warmup eager steps, then replays), with an eager
+    allreduce between two replays.  Returns flattened fp32 arrays."""
+    import torch
+    import torch.nn.functional as F
+
+    from paper_2511_09143_b200 import ddp as fddp
+    from paper_2511_09143_b200 import instance as inst_mod
+    from paper_2511_09143_b200.comm import init_process_group
+
+    inst = inst_mod.bind(0, rank + 1, mode=mode)
+    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n, timeout_s=120)
+    stream = inst.stream
+    out = {}
+
+    def build():
+        torch.manual_seed(1000 + rank)   # different init per rank: the broadcast must fix it
+        return torch.nn.Sequential(torch.nn.Linear(64, 300), torch.nn.GELU(),
+                                   torch.nn.Linear(300, 10)).cuda()
+
+    flat = lambda ts: torch.cat([t.detach().reshape(-1) for t in ts]).float().cpu().numpy()
+    with torch.cuda.stream(stream):
+        g = torch.Generator(device="cpu").manual_seed(7 + rank)
+        x = torch.randn(32, 64, generator=g).cuda()
+        y = torch.randint(0, 10, (32,), generator=g).cuda()
+        # local gradient from the broadcast start (no exchange)
+        ref = build()
+        fddp.broadcast_parameters(ref, comm)
+        F.cross_entropy(ref(x), y).backward()
+        out["local"] = flat([p.grad for p in ref.parameters()])
+
+        runs = {}
+        for kind in ("eager", "graph"):
+            model = build()
+            net = fddp.ShmDataParallel(model, comm, bucket_cap_mb=0.05, first_bucket_mb=0.01)
+            opt = torch.optim.SGD(net.parameters(), lr=0.05, momentum=0.9)
+
+            def step():
+                net.zero_grad()
+                loss = F.cross_entropy(net(x), y)
+                loss.backward()
+                opt.step()
+                return loss
+
+            if kind == "eager":
+                for k in range(steps):
+                    step()
+                    if k == 0:
+                        out["synced"] = flat([p.grad for p in model.parameters()])
+                out["buckets"] = len(net.buckets)
+            else:
+                replay = net.graphed_step(step, warmup=warmup)
+                extra = torch.arange(1000, dtype=torch.float32, device="cuda") * (rank + 1)
+                for k in range(steps - warmup):
+                    replay()
+                    if k == 0:       # an eager collective between two replays
+                        comm.allreduce(extra, op="sum")
+                out["extra"] = extra.cpu().numpy()
+                out["launches_per_replay"] = comm.kernel_launches()
+            runs[kind] = flat(model.parameters())
+    stream.synchronize()
+    out.update(params_eager=runs["eager"], params_graph=runs["graph"])
+    comm.destroy()
+    return out
