@@ -93,9 +93,14 @@ def parse_args(argv=None):
                    default="allreduce", help="collective of the --sweep (bytes = full buffer)")
     p.add_argument("--train-model", choices=["resnet50", "mobilenet_v2", "bert"],
                    default="resnet50", help="model of the --train-only leg")
+    p.add_argument("--train-engine", choices=["graph", "ddp"], default="graph",
+                   help="graph: ddp.ShmDataParallel, whole step captured as one CUDA graph "
+                        "(default); ddp: torch DDP + flexshm_hook, eager")
     p.add_argument("--train-no-sync", action="store_true",
                    help="--train-only: also time the step without gradient sync (compute bound)")
     p.add_argument("--bucket-mb", type=float, default=8.0, help="DDP bucket_cap_mb of the DP legs")
+    p.add_argument("--first-bucket-mb", type=float, default=1.0,
+                   help="first bucket cap of the graph engine (DDP's first_bucket_bytes)")
     p.add_argument("--compress", choices=["bf16"], default=None,
                    help="DP legs: exchange fp32 gradients in bf16 (flexshm_bf16_hook)")
     p.add_argument("--batch", type=int, default=32)
@@ -649,30 +654,42 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
             x = torch.randn(cfg["batch"], 3, 224, 224, generator=g).cuda(gpu_local)
             x = x.to(memory_format=torch.channels_last)
             y = torch.randint(0, 1000, (cfg["batch"],), generator=g).cuda(gpu_local)
-        net = fddp.wrap(model, comm, control_group=pg, bucket_cap_mb=cfg.get("bucket_mb", 25.0),
-                        compress=cfg.get("compress"),
-                        threaded=bool(os.environ.get("FMX_HOOK_THREAD")))
+        graph = cfg.get("engine", "graph") == "graph"
+        if not graph:
+            net = fddp.wrap(model, comm, control_group=pg, bucket_cap_mb=cfg.get("bucket_mb", 25.0),
+                            compress=cfg.get("compress"),
+                            threaded=bool(os.environ.get("FMX_HOOK_THREAD")))
+        elif cfg.get("no_sync"):
+            fddp.broadcast_parameters(model, comm)   # same start, no exchange in the step
+            net = model
+        else:
+            net = fddp.ShmDataParallel(model, comm, bucket_cap_mb=cfg.get("bucket_mb", 8.0),
+                                       first_bucket_mb=cfg.get("first_bucket_mb", 1.0))
         if name == "bert":
-            opt = torch.optim.AdamW(net.parameters(), lr=2e-5)
+            opt = torch.optim.AdamW(net.parameters(), lr=2e-5, capturable=graph)
         else:
             opt = torch.optim.SGD(net.parameters(), lr=0.01, momentum=0.9)
 
     from contextlib import nullcontext
 
     def step():
-        with (net.no_sync() if cfg.get("no_sync") else nullcontext()):
+        with (net.no_sync() if cfg.get("no_sync") and not graph else nullcontext()):
             return _step()
 
     host_phase = {"fwd": 0.0, "bwd": 0.0, "opt": 0.0}  # host enqueue seconds per phase
 
     def _step():
         t0 = time.perf_counter()
+        if graph:   # the buckets (or .grad) stay in place: zero them, do not drop them
+            net.zero_grad(set_to_none=False)
         if name == "bert":
             loss = F.cross_entropy(net(input_ids=x).logits.float(), y)
         else:
-            with torch.autocast("cuda", dtype=torch.bfloat16):
+            # (no autocast weight cache: a graph replays the casts every step)
+            with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=not graph):
                 loss = F.cross_entropy(net(x), y)
-        opt.zero_grad(set_to_none=True)
+        if not graph:
+            opt.zero_grad(set_to_none=True)
         t1 = time.perf_counter()
         loss.backward()
         t2 = time.perf_counter()
@@ -683,24 +700,35 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
         host_phase["opt"] += t3 - t2
         return loss
 
+    replay = None
     with torch.cuda.stream(stream):
-        for _ in range(cfg["train_warmup"]):
-            step()
+        if graph and not cfg.get("no_sync"):
+            # warmup eager steps, then the whole step as one CUDA graph (with
+            # --stamps: stamp slots baked into it, rewritten by every replay)
+            replay = net.graphed_step(step, warmup=cfg["train_warmup"], before_capture=(
+                (lambda: comm.set_stamps(1 << 15)) if cfg.get("stamps") else None))
+        elif graph:
+            replay = graphed_plain(step, cfg["train_warmup"])
+        else:
+            for _ in range(cfg["train_warmup"]):
+                step()
     torch.cuda.synchronize()
     stamps = None
-    if cfg.get("stamps"):
+    if cfg.get("stamps") and (not graph or replay is not None and not cfg.get("no_sync")):
         # one step on the GPU clock: markers 1/2 around it on the compute stream,
         # every collective op of the hook's side stream in between
         comm.barrier(300)
-        comm.set_stamps(1 << 15)
+        if not graph:
+            comm.set_stamps(1 << 15)
         comm.barrier(300)
         with torch.cuda.stream(stream):
             comm.stamp(1, stream)
-            step()
+            replay() if replay is not None else step()
             comm.stamp(2, stream)
         torch.cuda.synchronize()
         stamps = comm.stamps(1 << 15)
-        comm.set_stamps(0)
+        if replay is None:   # a captured graph keeps writing its baked stamp slots
+            comm.set_stamps(0)
     comm.barrier(300)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = comm.kernel_launches()
@@ -711,7 +739,7 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
     ev0.record(stream)
     with torch.cuda.stream(stream):
         for _ in range(cfg["train_steps"]):
-            loss = step()
+            loss = replay() if replay is not None else step()
     ev1.record(stream)
     t_host = time.perf_counter() - t_host  # enqueue time of the timed steps (no sync inside)
     ev1.synchronize()
@@ -726,6 +754,24 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
     dist.destroy_process_group()
     comm.destroy()
     return out
+
+
+def graphed_plain(step, warmup: int):
+    """A step without collectives as one CUDA graph (the no-sync bound of the
+    graph engine): `warmup` eager steps on the current stream, then capture."""
+    import torch
+    s = torch.cuda.current_stream()
+    for _ in range(max(1, warmup)):
+        step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        out = step()
+
+    def replay():
+        g.replay()
+        return out
+    return replay
 
 
 def _spawned_train(rank, job_key, n, cfg, inst_mode, gpu_local):
@@ -783,7 +829,10 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
     cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
            "batch": args.batch, "train_steps": args.train_steps, "train_warmup": args.train_warmup,
            "port": 29000 + os.getpid() % 1000, "model": model, "no_sync": no_sync,
-           "bucket_mb": args.bucket_mb, "stamps": bool(args.stamps) and not no_sync,
+           "bucket_mb": args.bucket_mb, "first_bucket_mb": args.first_bucket_mb,
+           "stamps": bool(args.stamps) and not no_sync,
+           # the bf16-compressed exchange exists as a DDP comm hook only
+           "engine": "ddp" if args.compress else args.train_engine,
            "compress": args.compress}
     res = run_ranks(train_body, _spawned_train, list(range(n)), job_key + "-t", n, cfg,
                     args.train_mode, 0)
@@ -811,7 +860,10 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
                      "what": "host time to enqueue the timed steps (max over ranks; loss.item() "
                              "syncs once per step only in the last one) and the part spent "
                              "inside flexshm_hook's collective calls"},
-            "gpu_launches": sum(r["launches"] for r in res.values()), "model": desc}
+            "gpu_launches": sum(r["launches"] for r in res.values()), "model": desc,
+            "engine": ("ddp.ShmDataParallel: whole step (fwd, bwd with bucket allreduces, "
+                       "optimizer) replayed as one CUDA graph" if cfg["engine"] == "graph" else
+                       "torch DDP + ddp.flexshm_hook, eager")}
 
 
 def dry_exchange(d, mine: list[int], job_key: str, m: int = 4099) -> dict[int, int]:

@@ -274,6 +274,16 @@ int fmx_comm_kernel_launches(fmx_comm_t comm, uint64_t* launches);
  * collective. */
 int fmx_comm_fence(fmx_comm_t comm, void* stream);
 
+/* Deferred gather (set_defer on): an allreduce's last all-gather round is
+ * enqueued by this rank's NEXT collective, right after that one's first stage,
+ * or by fmx_comm_flush - so on one in-order stream (join-stream mode) the
+ * stage of bucket b+1 fills the wait for peers to finish reducing bucket b.
+ * An allreduce's result is complete only after the next collective / flush
+ * (on the stream that one runs on).  Off by default; turning it off needs no
+ * pending gather. */
+int fmx_comm_set_defer(fmx_comm_t comm, int on);
+int fmx_comm_flush(fmx_comm_t comm, void* stream);
+
 /* Capture collectives into a CUDA graph (a whole DP training step, replayed
  * as one launch: ddp.ShmDataParallel).  No reference interface: NCCL
  * collectives are capturable (ncclGroup under cudaStreamBeginCapture), and

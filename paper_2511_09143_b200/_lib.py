@@ -53,7 +53,7 @@ EXPORTS = (
     "fmx_comm_kernel_launches", "fmx_comm_flags", "fmx_comm_set_timing", "fmx_comm_kernel_time",
     "fmx_comm_monitor", "fmx_comm_set_stamps", "fmx_comm_stamps",
     "fmx_comm_stamp", "fmx_comm_set_join_stream", "fmx_comm_completion_stream",
-    "fmx_comm_fence", "fmx_graph_capture_begin", "fmx_graph_capture_end",
+    "fmx_comm_fence", "fmx_comm_set_defer", "fmx_comm_flush", "fmx_graph_capture_begin", "fmx_graph_capture_end",
     "fmx_graph_launch_prepare", "fmx_graph_release",
     "fmx_trace_plan", "fmx_last_error", "fmx_dup_ranks",
     "fmx_abi_version",
@@ -133,6 +133,8 @@ def lib() -> ctypes.CDLL:
         "fmx_comm_set_join_stream": [c_void, c_void],
         "fmx_comm_completion_stream": [c_void, P(c_void)],
         "fmx_comm_fence": [c_void, c_void],
+        "fmx_comm_set_defer": [c_void, c_int],
+        "fmx_comm_flush": [c_void, c_void],
         "fmx_graph_capture_begin": [c_void],
         "fmx_graph_capture_end": [c_void, c_void, P(c_int)],
         "fmx_graph_launch_prepare": [c_void, c_int, c_void, c_void],
@@ -162,7 +164,7 @@ def trace_plan(nranks: int, rank: int, ops: list[tuple], slice_bytes: int = 4096
     per rank)."""
     n = len(ops)
     code = {"allreduce": 0, "broadcast": 1, "allreduce_host": 2, "reduce_scatter": 3,
-            "allgather": 4}
+            "allgather": 4, "flush": 5}
     kinds = (ctypes.c_int * max(1, n))(*[code[o[0]] for o in ops])
     counts = (ctypes.c_size_t * max(1, n))(*[o[1] for o in ops])
     dtypes = (ctypes.c_int * max(1, n))(*[o[2] for o in ops])

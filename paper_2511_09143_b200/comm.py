@@ -280,6 +280,17 @@ class ShmCommunicator:
             out.append((t, tag >> 8, tag & 0xFF, info))
         return out
 
+    def set_defer(self, on: bool) -> None:
+        """Deferred gather (fmx_comm_set_defer): an allreduce's last gather is
+        enqueued by the next collective / flush()."""
+        self._alive()
+        _lib.check(_lib.lib().fmx_comm_set_defer(self._h, int(bool(on))), "fmx_comm_set_defer")
+
+    def flush(self, stream=None) -> None:
+        """Enqueue a deferred gather, if any, on `stream` (or the join stream)."""
+        self._alive()
+        _lib.check(_lib.lib().fmx_comm_flush(self._h, self._stream(stream)), "fmx_comm_flush")
+
     # -- fences and CUDA graphs (fmx_comm_fence, fmx_graph_*) ------------------
     def fence(self, stream=None) -> None:
         """Every rank reached this point of its stream (after its earlier

@@ -197,7 +197,8 @@ class CudaSink final : public Sink {
 
   // timeline probe: stamp the completion of the op just enqueued on `lane`
   int stamp(int lane, int kind, uint32_t info) {
-    if (!c_->stamps || c_->stamp_used >= c_->stamp_cap || c_->cap_active) return FMX_OK;
+    // (in a capture the stamp slots are baked: each replay rewrites them)
+    if (!c_->stamps || c_->stamp_used >= c_->stamp_cap) return FMX_OK;
     if (int rc = drain()) return rc;
     fmx_stamp_kernel<<<1, 1, 0, lane_stream(c_, lane)>>>(c_->stamps + c_->stamp_used++,
                                                           (uint32_t)(lane << 8 | kind), info);
@@ -560,8 +561,11 @@ int on_lanes(fmx_comm* c, cudaStream_t user, int cls, F&& body) {
   const bool single = cls == 2;
   if (single) cls = 0;
   std::vector<cudaStream_t> extra;
-  if (c->nlanes >= 2 && !c->join_stream && !single) extra.push_back(c->lane[0]);
-  if (c->nlanes == 3 && !c->join_stream && !single) extra.push_back(c->lane[2]);
+  // (join-stream mode: FMX_JOIN_LANES=2/3 keep the stage / gather lanes as
+  // extra streams too - in a captured graph, parallel branches)
+  const int jl = c->join_stream ? std::min(c->join_lanes, c->nlanes) : c->nlanes;
+  if (jl >= 2 && c->nlanes >= 2 && !single) extra.push_back(c->lane[0]);
+  if (jl == 3 && c->nlanes == 3 && !single) extra.push_back(c->lane[2]);
   // host-path / broadcast calls (and the first device call after one) wait for
   // the previous collective, whichever stream it joined (redundant, and free,
   // when it joined the caller's stream)
@@ -833,6 +837,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   // local-only knobs (how this rank issues its copies; the protocol is unchanged)
   if (const char* v = getenv("FMX_COPY2D")) c->copy2d = atoi(v) != 0;
   if (const char* v = getenv("FMX_COPY_FENCE")) c->copy_fence = atoi(v) != 0;
+  if (const char* v = getenv("FMX_JOIN_LANES")) c->join_lanes = std::max(1, std::min(3, atoi(v)));
   if (const char* v = getenv("FMX_FUSE_SIGNAL")) c->fuse_signal = atoi(v) != 0;
   if (const char* v = getenv("FMX_REDUCE_CTAS")) c->reduce_ctas = std::max(1, std::min(atoi(v), kReduceGridCap));
   c->serialize = profiler_injected();
@@ -1077,6 +1082,7 @@ int fmx_barrier(fmx_comm_t c, double timeout_s) {
 int fmx_comm_destroy(fmx_comm_t c) {
   if (!c) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
   int rc = g_ctx_push ? release_lane_objects(c) : FMX_OK;
+  drop_pending(c);
   if (c->scratch) cudaFree(c->scratch);
   if (c->stamps) cudaFree(c->stamps);
   if (c->ctas_done) cudaFree(c->ctas_done);
@@ -1330,7 +1336,8 @@ int fmx_comm_fence(fmx_comm_t c, void* stream) {
   const uint32_t v = c->fence_round + 1;
   rc = on_lanes(c, (cudaStream_t)stream, 1, [&]() -> int {
     if (c->nranks == 1) return FMX_OK;
-    int r = sink.signal(kLaneMain, kFence, v);
+    int r = plan_flush(c, sink);
+    if (r == FMX_OK) r = sink.signal(kLaneMain, kFence, v);
     return r ? r : sink.wait_peers(kLaneMain, kFence, v, c->rank);
   });
   if (rc) return rc;
@@ -1339,10 +1346,25 @@ int fmx_comm_fence(fmx_comm_t c, void* stream) {
   return FMX_OK;
 }
 
+int fmx_comm_set_defer(fmx_comm_t c, int on) {
+  if (!c) return fail(FMX_ERR_INVALID_ARG, "invalid communicator");
+  if (!on && c->pending) return fail(FMX_ERR_INVALID_ARG, "flush the deferred gather first");
+  c->defer_gather = on != 0;
+  return FMX_OK;
+}
+
+int fmx_comm_flush(fmx_comm_t c, void* stream) {
+  int rc = check_comm(c);
+  if (rc || !c->pending) return rc;
+  CudaSink sink(c);
+  return on_lanes(c, (cudaStream_t)stream, 0, [&]() { return plan_flush(c, sink); });
+}
+
 int fmx_graph_capture_begin(fmx_comm_t c) {
   int rc = check_comm(c);
   if (rc) return rc;
   if (c->cap_active) return fail(FMX_ERR_INVALID_ARG, "a capture is already active");
+  if (c->pending) return fail(FMX_ERR_INVALID_ARG, "flush the deferred gather before a capture");
   if ((rc = load_graph_driver())) return rc;
   if (c->has_done && c->done_cap == 0 && c->lane_ctx) {
     // eager work still in flight: the captured collectives drop their waits
@@ -1360,6 +1382,12 @@ int fmx_graph_capture_end(fmx_comm_t c, void* graph, int* handle) {
   if (!c || !c->hdr || (graph && !handle)) return fail(FMX_ERR_INVALID_ARG, "null argument");
   if (!c->cap_active) return fail(FMX_ERR_INVALID_ARG, "no capture is active");
   c->cap_active = 0;
+  if (c->pending) {  // a gather deferred inside the capture would never run
+    drop_pending(c);
+    for (int k = 0; k < kNumCounters; ++k) *c->counter(k) = c->cap_c0[k];
+    c->launches = c->cap_launches0;
+    return fail(FMX_ERR_INVALID_ARG, "the capture ended with a deferred gather: flush inside it");
+  }
   if (!graph) {  // the capture failed: abandon it (nothing was enqueued that will run)
     for (int k = 0; k < kNumCounters; ++k) *c->counter(k) = c->cap_c0[k];
     c->launches = c->cap_launches0;

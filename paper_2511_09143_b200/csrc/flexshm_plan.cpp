@@ -72,6 +72,8 @@ class TraceSink final : public Sink {
     return FMX_OK;
   }
   int join() { return line("J\n"); }
+  int64_t scope() const override { return user_base; }
+  void set_scope(int64_t b) override { user_base = b; }
   int nranks = 0;
   int64_t user_base = 0;  // overlap traces: each collective's user buffer is a separate range
 
@@ -252,6 +254,69 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t c
 // stream order (the schedule of the first B200 runs).
 enum { kEvSlotFree = 0, kEvGathered = FMX_MAX_SLOTS };  // + R % K: W(R) and G(R) above
 
+// The all-gather of one round: wait for the owners' REDUCED, record W(R), copy
+// their results out of the out-slots, record G(R).  Built per round; with
+// fmx_comm_set_defer the last round's is kept (c->pending) and enqueued by the
+// next collective right after its first stage, so one in-order stream stages
+// bucket b+1 while peers are still reducing bucket b.  That order is valid:
+// the deferred gather waits only on REDUCED flags peers signalled before their
+// own next stage, and it still precedes this rank's next REDUCED signal (the
+// G(R-1) wait) - the model checker runs it (FMX_TRACE_DEFER).
+}  // namespace fmx
+struct fmx::PendingGather {
+  uint32_t R = 0;
+  int LG = 0, K = 2;
+  bool zc = false, coarse = true, split = false;
+  int64_t scope = 0;
+  std::vector<int> q;           // owners, in wait order
+  std::vector<PlanSeg> segs;    // their result pieces (bytes 0: wait only)
+};
+namespace fmx {
+
+static int emit_gather(fmx_comm* c, Sink& k, const PendingGather& p) {
+  const int me = c->rank;
+  int rc;
+  const int64_t scope = k.scope();
+  k.set_scope(p.scope);
+  struct Restore {
+    Sink& k;
+    int64_t s;
+    ~Restore() { k.set_scope(s); }
+  } restore{k, scope};
+  std::vector<PlanSeg> segs;
+  if (p.coarse) {
+    if ((rc = k.wait_peers(p.LG, kReduced, p.R + 1, me))) return rc;
+    if ((rc = k.record(p.LG, kEvSlotFree + p.R % p.K))) return rc;  // W(R)
+    for (const PlanSeg& g : p.segs)
+      if (g.bytes) segs.push_back(g);
+    if ((rc = k.copy(p.LG, segs, true, p.zc))) return rc;
+  } else {
+    for (size_t i = 0; i < p.q.size(); ++i) {
+      if ((rc = k.wait_rank(p.LG, p.q[i], kReduced, p.R + 1))) return rc;
+      if (!p.segs[i].bytes) continue;
+      segs.assign(1, p.segs[i]);
+      if ((rc = k.copy(p.LG, segs, true, p.zc))) return rc;
+    }
+    if ((rc = k.record(p.LG, kEvSlotFree + p.R % p.K))) return rc;  // W(R)
+  }
+  if (p.split && (rc = k.record(p.LG, kEvGathered + p.R % p.K))) return rc;  // G(R)
+  return FMX_OK;
+}
+
+void drop_pending(fmx_comm* c) {
+  delete c->pending;
+  c->pending = nullptr;
+}
+
+int plan_flush(fmx_comm* c, Sink& k) {
+  if (!c->pending) return FMX_OK;
+  PendingGather* p = c->pending;
+  c->pending = nullptr;
+  const int rc = emit_gather(c, k, *p);
+  delete p;
+  return rc;
+}
+
 // The three owner-chunk collectives share one schedule:
 //   kAllreduce     stage -> fetch -> reduce (HBM + result slot) -> gather
 //   kReduceScatter stage -> fetch -> reduce into recv (no result slot, no gather copies)
@@ -318,10 +383,14 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
     return FMX_OK;
   };
 
+  // a deferred gather of the previous allreduce goes after this call's first
+  // stage(s) (allreduce) or first of all (reduce-scatter / all-gather)
+  if (!ar && (rc = plan_flush(c, k))) return rc;
   // lane 0 stages K-1 rounds ahead of the reduction
   const uint32_t ahead = (uint32_t)K - 1;
   for (uint32_t j = 0; j < ahead && j < g.rounds; ++j)
     if ((rc = stage(j))) return rc;
+  if ((rc = plan_flush(c, k))) return rc;
   for (uint32_t j = 0; j < g.rounds; ++j) {
     const uint32_t R = R0 + j;
     if (j + ahead < g.rounds && (rc = stage(j + ahead))) return rc;
@@ -416,35 +485,29 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
     if (split && R >= 1 && (rc = k.wait_event(kLaneMain, kEvGathered + (R - 1) % K))) return rc;
     if ((rc = k.signal(kLaneMain, kReduced, R + 1))) return rc;
     // all-gather (lane LG): each owner's result as soon as that owner has it
-    if (c->coarse_gather) {
-      if ((rc = k.wait_peers(LG, kReduced, R + 1, me))) return rc;
-      if ((rc = k.record(LG, kEvSlotFree + R % K))) return rc;  // W(R)
-      segs.clear();
-      for (int q = 0; q < n && !rs; ++q) {
-        const size_t len = q == me ? 0 : g.len(q, j);
-        if (!len) continue;
-        const size_t off = c->out_off(R, q);
-        segs.push_back({c->at(zc, off), dst + g.lo(q, j) * g.esz, len * g.esz,
-                        Annot{(int64_t)off, len * g.esz, q, R}, false,
-                        ubuf(g.lo(q, j) * g.esz, len * g.esz)});
-      }
-      if ((rc = k.copy(LG, segs, true, zc))) return rc;
-    } else {
-      for (int i = 0; i < n - 1; ++i) {
-        const int q = rot(i);
-        if ((rc = k.wait_rank(LG, q, kReduced, R + 1))) return rc;
-        const size_t len = rs ? 0 : g.len(q, j);
-        if (!len) continue;
-        const size_t off = c->out_off(R, q);
-        segs.clear();
-        segs.push_back({c->at(zc, off), dst + g.lo(q, j) * g.esz, len * g.esz,
-                        Annot{(int64_t)off, len * g.esz, q, R}, false,
-                        ubuf(g.lo(q, j) * g.esz, len * g.esz)});
-        if ((rc = k.copy(LG, segs, true, zc))) return rc;
-      }
-      if ((rc = k.record(LG, kEvSlotFree + R % K))) return rc;  // W(R)
+    PendingGather pg;
+    pg.R = R;
+    pg.LG = LG;
+    pg.K = K;
+    pg.zc = zc;
+    pg.coarse = c->coarse_gather;
+    pg.split = split;
+    pg.scope = k.scope();
+    for (int i = 0; i < n - 1; ++i) {
+      // coarse: ascending owners, one copy batch; fine: rotated, a wait per owner
+      const int q = pg.coarse ? (i < me ? i : i + 1) : rot(i);
+      const size_t len = rs ? 0 : g.len(q, j);
+      const size_t off = c->out_off(R, q);
+      pg.q.push_back(q);
+      pg.segs.push_back({c->at(zc, off), dst + g.lo(q, j) * g.esz, len * g.esz,
+                         Annot{(int64_t)off, len * g.esz, q, R}, false,
+                         ubuf(g.lo(q, j) * g.esz, len * g.esz)});
     }
-    if (split && (rc = k.record(LG, kEvGathered + R % K))) return rc;  // G(R)
+    if (ar && c->defer_gather && j + 1 == g.rounds) {
+      c->pending = new PendingGather(std::move(pg));  // enqueued by the next call / fmx_comm_flush
+    } else if ((rc = emit_gather(c, k, pg))) {
+      return rc;
+    }
   }
   c->ar_round += g.rounds;
   return FMX_OK;
@@ -473,6 +536,7 @@ int plan_allreduce_oneshot(fmx_comm* c, Sink& k, const char* src, char* dst, siz
   const size_t esz = dtype == FMX_FLOAT32 ? 4 : 2, bytes = count * esz;
   const uint32_t J = c->os_round;
   int rc;
+  if ((rc = plan_flush(c, k))) return rc;
   const size_t mine = c->os_slot_off(J, me);
   std::vector<PlanSeg> segs{{src, c->at(true, mine), bytes, Annot{(int64_t)mine, bytes, me, J | kOsTag},
                              true, ubuf(0, bytes)}};
@@ -526,6 +590,7 @@ int plan_allreduce_host(fmx_comm* c, Sink& k, size_t off_bytes, size_t count, in
   };
   std::vector<PlanSeg> segs;
   int rc;
+  if ((rc = plan_flush(c, k))) return rc;
   // the caller wrote its whole input before the call (host program order)
   for (int o = 0; o < n; ++o)
     for (uint32_t j = 0; j < P; ++j)
@@ -621,6 +686,7 @@ int plan_broadcast(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
   const uint32_t rounds = (uint32_t)((count + bslice - 1) / bslice);
   std::vector<PlanSeg> segs(1);
   int rc;
+  if ((rc = plan_flush(c, k))) return rc;
   for (uint32_t j = 0; j < rounds; ++j) {
     const uint32_t R = c->bc_round + j;
     const size_t lo = (size_t)j * bslice, len = std::min(bslice, count - lo);
@@ -666,6 +732,8 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   c.transport = (transport == FMX_TRANSPORT_ZC || transport == FMX_TRANSPORT_AUTO) ? transport
                                                                                   : FMX_TRANSPORT_CE;
   apply_proto(&c, proto_from_env());
+  // FMX_TRACE_DEFER=1: fmx_comm_set_defer (an allreduce's last gather deferred)
+  c.defer_gather = getenv("FMX_TRACE_DEFER") && atoi(getenv("FMX_TRACE_DEFER"));
   c.slice_bytes = slice_bytes;
   size_t max_bytes = 0;
   for (int i = 0; i < nops; ++i) max_bytes = std::max(max_bytes, counts[i] * (dtypes[i] ? 2 : 4));
@@ -680,7 +748,9 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   // collectives (distinct buffers) are not separated by a join on the lanes;
   // host-path calls and broadcasts still are (on_lanes' barrier)
   const bool overlap = getenv("FMX_TRACE_OVERLAP") && atoi(getenv("FMX_TRACE_OVERLAP"));
-  auto device_class = [&](int i) { return kinds[i] == 0 || kinds[i] == 3 || kinds[i] == 4; };
+  auto device_class = [&](int i) {
+    return kinds[i] == 0 || kinds[i] == 3 || kinds[i] == 4 || kinds[i] == 5;
+  };
   for (int i = 0; i < nops; ++i) {
     int rc;
     if (!overlap || i == 0 || !device_class(i) || !device_class(i - 1)) sink.join();
@@ -688,7 +758,9 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
     if (kinds[i] == 1 && (!roots || roots[i] < 0 || roots[i] >= nranks))
       return fail(FMX_ERR_INVALID_ARG, "bad broadcast root");
     const size_t esz = dtypes[i] ? 2 : 4;
-    if (kinds[i] == 0 && c.use_oneshot(counts[i] * esz))
+    if (kinds[i] == 5)  // fmx_comm_flush
+      rc = plan_flush(&c, sink);
+    else if (kinds[i] == 0 && c.use_oneshot(counts[i] * esz))
       rc = plan_allreduce_oneshot(&c, sink, dummy, dummy, counts[i], dtypes[i], FMX_OP_SUM, 1.0f, true);
     else if (kinds[i] == 0)
       rc = plan_allreduce(&c, sink, dummy, dummy, counts[i], dtypes[i], FMX_OP_SUM, 1.0f, true);
@@ -699,7 +771,14 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
       rc = plan_allreduce_host(&c, sink, 0, counts[i], dtypes[i], FMX_OP_SUM, 1.0f);
     else
       rc = plan_broadcast(&c, sink, dummy, dummy, counts[i], dtypes[i], roots ? roots[i] : 0);
-    if (rc) return rc;
+    if (rc) {
+      drop_pending(&c);
+      return rc;
+    }
+  }
+  if (c.pending) {  // an unflushed deferred gather: the sequence must end with a flush
+    drop_pending(&c);
+    return fail(FMX_ERR_INVALID_ARG, "deferred gather not flushed (end the sequence with kind 5)");
   }
   sink.join();
   if (used) *used = out.size() + 1;

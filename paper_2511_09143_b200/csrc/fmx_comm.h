@@ -20,6 +20,8 @@ constexpr int kNumEvents = 2 * FMX_MAX_SLOTS + 7;  // W[K], G[K]; host path F[2]
 // captured graph are re-based per replay by their counter's advance).
 enum Counter { kCtrAr = 0, kCtrOs = 1, kCtrBc = 2, kCtrFence = 3, kNumCounters = 4 };
 
+struct PendingGather;  // an allreduce's deferred last gather (flexshm_plan.cpp)
+
 // One batch-memop node of a captured graph that signals / waits on this
 // communicator's flags, with its parameters as captured.
 struct GraphMemop {
@@ -100,7 +102,15 @@ struct fmx_comm {
     return transport != FMX_TRANSPORT_CE && transport != FMX_TRANSPORT_HOST && nranks > 1 &&
            bytes <= oneshot_max && bytes <= L.os_bytes;
   }
+  // fmx_comm_set_defer: an allreduce's LAST gather is enqueued by the next
+  // collective, after that one's first stage (or by fmx_comm_flush), so a
+  // single in-order stream stages bucket b+1 while peers finish reducing b
+  bool defer_gather = false;
+  fmx::PendingGather* pending = nullptr;
   int nlanes = 3;              // FMX_LANES=1: one stream; 2: gather on the reduce lane
+  int join_lanes = 1;          // join-stream mode: 1 every lane on the join stream; 2 stage on
+                               // its own stream; 3 stage and gather on their own (FMX_JOIN_LANES,
+                               // local knob: stream mapping only, the schedule is the same)
   // live kernel timing (fmx_comm_set_timing): event pairs around every reduce
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
@@ -173,7 +183,12 @@ inline cudaStream_t lane_stream(const fmx_comm* c, int lane) {
   // compute stream, two more extra streams per MPS client made bucketed
   // allreduces 2.5x slower (hardware-queue aliasing, profiles/r01/r2w), and a
   // single in-order stream per rank is as fast as three lanes on this box
-  if (c->nlanes == 1 || lane == 1 || c->join_stream) return main;
+  if (c->nlanes == 1 || lane == 1) return main;
+  if (c->join_stream) {
+    const int jl = std::min(c->join_lanes, c->nlanes);
+    if (jl <= 1 || (lane == 2 && jl < 3)) return main;
+    return c->lane[lane];
+  }
   if (c->nlanes == 2) return lane == 0 ? c->lane[0] : main;
   return c->lane[lane];
 }
@@ -252,6 +267,10 @@ struct Sink {
   virtual int wait_event(int lane, int ev) = 0;
   // host-program accesses to SHM around a collective (trace only)
   virtual int host_access(int lane, const Annot& a, bool write) { return FMX_OK; }
+  // user-buffer scope of the collective being planned (TraceSink: each
+  // collective's buffer is a separate range); a deferred gather keeps its own
+  virtual int64_t scope() const { return 0; }
+  virtual void set_scope(int64_t) {}
 };
 
 
@@ -295,5 +314,8 @@ int plan_allreduce_host(fmx_comm* c, Sink& k, size_t off_bytes, size_t count, in
                         float factor);
 int plan_broadcast(fmx_comm* c, Sink& k, const char* src, char* dst, size_t count, int dtype,
                    int root);
+// enqueue the pending deferred gather, if any (every plan does this first)
+int plan_flush(fmx_comm* c, Sink& k);
+void drop_pending(fmx_comm* c);
 
 }  // namespace fmx

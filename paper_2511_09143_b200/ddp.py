@@ -265,6 +265,17 @@ def wrap(module: torch.nn.Module, comm: ShmCommunicator, control_group=None,
     return ddp
 
 
+def _dense(t: torch.Tensor) -> bool:
+    """Strides that cover exactly numel() elements with no overlap."""
+    dims = sorted((st, sz) for st, sz in zip(t.stride(), t.size()) if sz > 1)
+    expect = 1
+    for st, sz in dims:
+        if st != expect:
+            return False
+        expect *= sz
+    return True
+
+
 class ShmDataParallel(torch.nn.Module):
     """Data parallelism over the SHM communicator whose whole training step
     can be captured into ONE CUDA graph (`graphed_step`).
@@ -298,7 +309,7 @@ class ShmDataParallel(torch.nn.Module):
     """
 
     def __init__(self, module: torch.nn.Module, comm: ShmCommunicator, bucket_cap_mb: float = 8.0,
-                 first_bucket_mb: float = 1.0, stream=None):
+                 first_bucket_mb: float = 1.0, stream=None, defer_gather: bool | None = None):
         super().__init__()
         self.module = module
         self.comm = comm
@@ -306,6 +317,9 @@ class ShmDataParallel(torch.nn.Module):
         self.params = [p for p in module.parameters() if p.requires_grad]
         self.cap = int(bucket_cap_mb * (1 << 20))
         self.first_cap = int(first_bucket_mb * (1 << 20))
+        # each bucket's last gather is enqueued after the next bucket's stage
+        # (fmx_comm_set_defer) while the backward pass runs; flushed at its end
+        self.defer = os.environ.get("FMX_DEFER", "1") != "0" if defer_gather is None else defer_gather
         self.hook_state = HookState(comm, stream)
         self.stream = self.hook_state.stream
         self.buckets = None          # [(flat tensor, [param index])]
@@ -346,7 +360,10 @@ class ShmDataParallel(torch.nn.Module):
             off = 0
             for i in idx:
                 p = self.params[i]
-                view = flat[off:off + p.numel()].view_as(p)
+                # the view takes the parameter's strides (channels_last convs): the
+                # gradient layout contract of AccumulateGrad, as DDP's bucket views do
+                view = flat.as_strided(p.size(), p.stride(), off) if _dense(p) else \
+                    flat[off:off + p.numel()].view_as(p)
                 if p.grad is not None:
                     view.copy_(p.grad)
                 p.grad = view
@@ -394,8 +411,12 @@ class ShmDataParallel(torch.nn.Module):
     def _launch(self, b):
         flat, _ = self.buckets[b]
         cur = torch.cuda.current_stream(flat.device)
+        if _MEASURE["stamp"]:     # timeline probe: when this bucket is ready on the GPU
+            self.comm.stamp(100 + b, stream=cur)
         self.comm.set_join_stream(self.stream)
         try:
+            if self.defer:
+                self.comm.set_defer(True)
             self.comm.allreduce(flat, op="avg", stream=cur)
         finally:
             self.comm.set_join_stream(None)
@@ -409,10 +430,18 @@ class ShmDataParallel(torch.nn.Module):
         while self._next < len(self.buckets):
             self._launch(self._next)
             self._next += 1
-        torch.cuda.current_stream(self.params[0].device).wait_stream(self.stream)
+        cur = torch.cuda.current_stream(self.params[0].device)
+        if self.defer:   # the last bucket's gather, then back to immediate completion
+            self.comm.set_join_stream(self.stream)
+            try:
+                self.comm.flush(stream=cur)
+            finally:
+                self.comm.set_join_stream(None)
+                self.comm.set_defer(False)
+        cur.wait_stream(self.stream)
 
     # -- CUDA graph ----------------------------------------------------------
-    def graphed_step(self, step_fn, warmup: int = 3):
+    def graphed_step(self, step_fn, warmup: int = 3, before_capture=None):
         """Capture `step_fn` - forward, backward and optimizer step on static
         input tensors, returning its outputs - into one CUDA graph; returns
         `replay()`, which runs one training step and returns the same (static)
@@ -429,6 +458,8 @@ class ShmDataParallel(torch.nn.Module):
                 step_fn()
         cur.wait_stream(s)
         torch.cuda.synchronize(dev)
+        if before_capture is not None:
+            before_capture()
         g = torch.cuda.CUDAGraph(keep_graph=True)
         self.comm.capture_begin()
         try:

@@ -18,15 +18,16 @@ from tests import _workers
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n,mode", [(2, "mps"), (3, "mps"), (3, "green")])
-def test_graphed_dp_matches_eager_and_oracle(n, mode):
+@pytest.mark.parametrize("n,mode,defer", [(2, "mps", True), (3, "mps", True), (3, "green", True),
+                                          (3, "mps", False)])
+def test_graphed_dp_matches_eager_and_oracle(n, mode, defer):
     from paper_2511_09143_b200.launcher import launch, new_job_key
     from paper_2511_09143_b200.scheduler import fm_select, make_cluster
     from paper_2511_09143_b200.workload import Job
 
     d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
     key = new_job_key("gdp")
-    res = launch(_workers.graph_dp_worker, d, args=(key, n, mode), job_key=key, timeout_s=300,
+    res = launch(_workers.graph_dp_worker, d, args=(key, n, mode, defer), job_key=key, timeout_s=300,
                  mode=mode)
     assert res[0]["buckets"] >= 3
     want = orc.allreduce_c([r["local"] for r in res], orc.F32, *orc.ddp_mean(n))

@@ -531,3 +531,58 @@ def test_oneshot_slot_reuse_needs_no_credit_flag():
     progs = programs(4, ops, 4096, "auto")
     for seed in range(20):
         simulate(progs, seed, burst=1)
+
+
+# ---- deferred gather (fmx_comm_set_defer, the DP bucket order) ----------------
+
+DEFER_SEQUENCES = {
+    "buckets": [("allreduce", 30_001, 0), ("allreduce", 50_000, 0), ("allreduce", 200_003, 0),
+                ("allreduce", 7, 0), ("allreduce", 77_777, 1), ("allreduce", 20_000, 0),
+                ("flush", 0, 0)],
+    "mixed": [("allreduce", 20_000, 0), ("allreduce", 60_000, 1), ("reduce_scatter", 9_001, 0),
+              ("allreduce", 40_000, 0), ("broadcast", 5_000, 0, 1), ("allreduce", 10_000, 0),
+              ("allreduce_host", 30_000, 0), ("allreduce", 300, 0), ("allreduce", 40_000, 1),
+              ("allgather", 12_000, 1), ("allreduce", 90_000, 0), ("flush", 0, 0)],
+}
+
+
+@pytest.mark.parametrize("n", [2, 3, 7])
+@pytest.mark.parametrize("seq", sorted(DEFER_SEQUENCES))
+@pytest.mark.parametrize("slots,lanes,transport", [("2", "3", "ce"), ("3", "3", "ce"),
+                                                   ("2", "1", "ce"), ("2", "3", "zc"),
+                                                   ("2", "3", "auto")])
+def test_deferred_gather(monkeypatch, n, seq, slots, lanes, transport):
+    """An allreduce's last gather enqueued after the next collective's first
+    stage (or by the flush / any other collective first): race-, stale-read-
+    and deadlock-free in join-stream mode, on the lanes and as one FIFO."""
+    monkeypatch.setenv("FMX_TRACE_OVERLAP", "1")
+    monkeypatch.setenv("FMX_TRACE_DEFER", "1")
+    monkeypatch.setenv("FMX_SLOTS", slots)
+    monkeypatch.setenv("FMX_LANES", lanes)
+    monkeypatch.setenv("FMX_ZC_MAX", "100000")
+    progs = programs(n, DEFER_SEQUENCES[seq], 4096, transport)
+    for seed in range(10):
+        simulate(progs, seed, burst=4)
+    merged = programs(n, DEFER_SEQUENCES[seq], 4096, transport, merged=True)
+    for seed in range(6):
+        simulate(merged, seed)
+
+
+def test_deferred_gather_order(monkeypatch):
+    """The deferred gather of call k sits after call k+1's first stage and
+    before call k+1's REDUCED signal (merged enqueue order of one rank)."""
+    monkeypatch.setenv("FMX_TRACE_DEFER", "1")
+    text = _lib.trace_plan(3, 0, [("allreduce", 30_000, 0), ("allreduce", 30_000, 0),
+                                  ("flush", 0, 0)], 1 << 20, "ce")
+    ops = [ln.split()[1:] for ln in text.splitlines() if ln and ln != "J"]
+    reduced_waits = [i for i, o in enumerate(ops) if o[0] == "A" and o[2] == str(REDUCED)]
+    staged = [i for i, o in enumerate(ops) if o[0] == "S" and o[1] == "0"]
+    reduced = [i for i, o in enumerate(ops) if o[0] == "S" and o[1] == str(REDUCED)]
+    # call 0's gather waits come after call 1's STAGED signal, before its REDUCED
+    assert staged[1] < reduced_waits[0] < reduced[1]
+
+
+def test_deferred_gather_must_be_flushed(monkeypatch):
+    monkeypatch.setenv("FMX_TRACE_DEFER", "1")
+    with pytest.raises(ValueError):
+        _lib.trace_plan(2, 0, [("allreduce", 30_000, 0)], 4096, "ce")
