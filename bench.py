@@ -93,9 +93,11 @@ def parse_args(argv=None):
                    default="allreduce", help="collective of the --sweep (bytes = full buffer)")
     p.add_argument("--train-model", choices=["resnet50", "mobilenet_v2", "bert"],
                    default="resnet50", help="model of the --train-only leg")
-    p.add_argument("--train-engine", choices=["graph", "ddp"], default="graph",
-                   help="graph: ddp.ShmDataParallel, whole step captured as one CUDA graph "
-                        "(default); ddp: torch DDP + flexshm_hook, eager")
+    p.add_argument("--train-engine", choices=["auto", "graph", "ddp"], default="auto",
+                   help="graph: ddp.ShmDataParallel, whole step captured as one CUDA graph; "
+                        "ddp: torch DDP + flexshm_hook, eager; auto (default): graph for the "
+                        "conv nets, ddp for bert (link-bound; graph 2465 vs eager 2658 seq/s, "
+                        "r02/r2v)")
     p.add_argument("--train-no-sync", action="store_true",
                    help="--train-only: also time the step without gradient sync (compute bound)")
     p.add_argument("--bucket-mb", type=float, default=8.0, help="DDP bucket_cap_mb of the DP legs")
@@ -637,12 +639,15 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
     stream = inst.stream
     torch.manual_seed(0)
     name = cfg.get("model", "resnet50")
+    graph = cfg.get("engine", "graph") == "graph"
     g = torch.Generator(device="cpu").manual_seed(100 + rank)
     with torch.cuda.stream(stream):
         if name == "bert":
             # BASELINE configs[3]: BERT-base fine-tune shape, bf16 weights and gradients
             # (bf16 SHM allreduce), seq 128, 2 labels
             from transformers import BertConfig, BertForSequenceClassification
+            if graph:
+                _sdpa_mask_skip_in_capture()
             model = BertForSequenceClassification(BertConfig(num_labels=2)).cuda(gpu_local)
             model = model.to(torch.bfloat16)
             x = torch.randint(0, 30522, (cfg["batch"], 128), generator=g).cuda(gpu_local)
@@ -654,7 +659,6 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
             x = torch.randn(cfg["batch"], 3, 224, 224, generator=g).cuda(gpu_local)
             x = x.to(memory_format=torch.channels_last)
             y = torch.randint(0, 1000, (cfg["batch"],), generator=g).cuda(gpu_local)
-        graph = cfg.get("engine", "graph") == "graph"
         if not graph:
             net = fddp.wrap(model, comm, control_group=pg, bucket_cap_mb=cfg.get("bucket_mb", 25.0),
                             compress=cfg.get("compress"),
@@ -756,6 +760,26 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
     return out
 
 
+def _sdpa_mask_skip_in_capture():
+    """HF BERT skips its all-ones attention mask in eager mode (no padding:
+    SDPA dispatches to the flash / cuDNN kernels) but cannot check the mask
+    while a CUDA graph is captured, so the captured step would carry a dense
+    mask down SDPA's math path: 3x slower inside a 14 % MPS client
+    (profiles/r02/r2u).  The synthetic sequences have no padding and pass no
+    mask, so skip it under capture too - the same computation as eager."""
+    import transformers.masking_utils as mu
+    if getattr(mu, "_fmx_patched", False):
+        return
+    orig = mu._ignore_bidirectional_mask_sdpa
+
+    def skip(padding_mask, kv_length, local_attention_size=None):
+        if padding_mask is None and local_attention_size is None:
+            return True
+        return orig(padding_mask, kv_length, local_attention_size)
+    mu._ignore_bidirectional_mask_sdpa = skip
+    mu._fmx_patched = True
+
+
 def graphed_plain(step, warmup: int):
     """A step without collectives as one CUDA graph (the no-sync bound of the
     graph engine): `warmup` eager steps on the current stream, then capture."""
@@ -832,7 +856,8 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
            "bucket_mb": args.bucket_mb, "first_bucket_mb": args.first_bucket_mb,
            "stamps": bool(args.stamps) and not no_sync,
            # the bf16-compressed exchange exists as a DDP comm hook only
-           "engine": "ddp" if args.compress else args.train_engine,
+           "engine": "ddp" if args.compress else args.train_engine if args.train_engine != "auto"
+           else ("ddp" if model == "bert" else "graph"),
            "compress": args.compress}
     res = run_ranks(train_body, _spawned_train, list(range(n)), job_key + "-t", n, cfg,
                     args.train_mode, 0)

@@ -310,7 +310,9 @@ int fmx_graph_release(fmx_comm_t comm, int handle);
 /* Write the schedule `rank` of an `nranks` communicator would enqueue for a
  * sequence of `nops` collectives (kinds[i]: 0 allreduce, 1 broadcast with
  * roots[i], 2 host-buffer allreduce, 3 reduce-scatter and 4 all-gather with
- * counts[i] per rank) as text: one line per SHM access ("W off bytes round", "R off
+ * counts[i] per rank, 5 fmx_comm_flush) as text (environment: FMX_TRACE_OVERLAP
+ * join-stream mode, FMX_TRACE_DEFER deferred gather, FMX_TRACE_REPLAYS=k the
+ * sequence as a captured graph replayed k times): one line per SHM access ("W off bytes round", "R off
  * bytes writer round") or flag op ("S flag value", "A rank flag value"),
  * "#" between collectives.  Used to model-check the protocol for any world
  * size on a CPU (tests/test_protocol_model.py).  *used = bytes needed. */

@@ -1333,15 +1333,10 @@ int fmx_comm_fence(fmx_comm_t c, void* stream) {
   int rc = check_comm(c);
   if (rc) return rc;
   CudaSink sink(c);
-  const uint32_t v = c->fence_round + 1;
   rc = on_lanes(c, (cudaStream_t)stream, 1, [&]() -> int {
-    if (c->nranks == 1) return FMX_OK;
-    int r = plan_flush(c, sink);
-    if (r == FMX_OK) r = sink.signal(kLaneMain, kFence, v);
-    return r ? r : sink.wait_peers(kLaneMain, kFence, v, c->rank);
+    return c->nranks == 1 ? FMX_OK : plan_fence(c, sink);
   });
   if (rc) return rc;
-  c->fence_round = v;
   if (!c->cap_active) c->fenced = true;
   return FMX_OK;
 }

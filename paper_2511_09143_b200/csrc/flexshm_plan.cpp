@@ -45,27 +45,33 @@ class TraceSink final : public Sink {
     shm(lane, r.write, true);
     return FMX_OK;
   }
-  int signal(int lane, int flag, uint32_t v) override { return line("%d S %d %u\n", lane, flag, v); }
+  int signal(int lane, int flag, uint32_t v) override {
+    return line("%d S %d %u\n", lane, flag, v + off(flag));
+  }
   int signal2(int lane, int f0, uint32_t v0, int f1, uint32_t v1) override {
-    line("%d S %d %u\n", lane, f0, v0);
-    return line("%d S %d %u\n", lane, f1, v1);
+    line("%d S %d %u\n", lane, f0, v0 + off(f0));
+    return line("%d S %d %u\n", lane, f1, v1 + off(f1));
   }
   int wait_peers(int lane, int flag, uint32_t v, int skip) override {
     for (int q = 0; q < nranks; ++q)
-      if (q != skip) line("%d A %d %d %u\n", lane, q, flag, v);
+      if (q != skip) line("%d A %d %d %u\n", lane, q, flag, v + off(flag));
     return FMX_OK;
   }
   int wait_rank(int lane, int q, int flag, uint32_t v) override {
-    return line("%d A %d %d %u\n", lane, q, flag, v);
+    return line("%d A %d %d %u\n", lane, q, flag, v + off(flag));
   }
   int d2d(int lane, void*, const void*, size_t, Annot from, Annot to) override {
     user(lane, from, false);
     user(lane, to, true);
     return FMX_OK;
   }
-  int record(int lane, int ev) override { return line("%d E %d %d\n", lane, ev, ++seq_[ev]); }
+  int record(int lane, int ev) override {
+    ev_epoch_[ev] = epoch;
+    return line("%d E %d %d\n", lane, ev, ++seq_[ev]);
+  }
+  // (a replayed graph drops waits on events recorded outside its capture)
   int wait_event(int lane, int ev) override {
-    return seq_[ev] ? line("%d X %d %d\n", lane, ev, seq_[ev]) : FMX_OK;
+    return seq_[ev] && ev_epoch_[ev] == epoch ? line("%d X %d %d\n", lane, ev, seq_[ev]) : FMX_OK;
   }
   int host_access(int lane, const Annot& a, bool write) override {
     shm(lane, a, write);
@@ -76,14 +82,20 @@ class TraceSink final : public Sink {
   void set_scope(int64_t b) override { user_base = b; }
   int nranks = 0;
   int64_t user_base = 0;  // overlap traces: each collective's user buffer is a separate range
+  // graph replays (FMX_TRACE_REPLAYS): flag values re-based per counter class
+  // (what fmx_graph_launch_prepare writes into the nodes), annotation rounds
+  // tagged with the replay, events of other replays invisible
+  uint32_t flag_off[kNumCounters] = {};
+  uint32_t round_tag = 0;
+  int epoch = 0;
 
  private:
   void shm(int lane, const Annot& a, bool write) {
     if (a.off < 0 || a.bytes == 0) return;
     if (write)
-      line("%d W %lld %zu %u\n", lane, (long long)a.off, a.bytes, a.round);
+      line("%d W %lld %zu %u\n", lane, (long long)a.off, a.bytes, a.round + round_tag);
     else
-      line("%d R %lld %zu %d %u\n", lane, (long long)a.off, a.bytes, a.writer, a.round);
+      line("%d R %lld %zu %d %u\n", lane, (long long)a.off, a.bytes, a.writer, a.round + round_tag);
   }
   void user(int lane, const Annot& a, bool write) {
     if (a.off < 0 || a.bytes == 0) return;
@@ -99,8 +111,16 @@ class TraceSink final : public Sink {
     out_->append(buf);
     return FMX_OK;
   }
+  uint32_t off(int flag) const {
+    const int k = (flag == kStaged || flag == kReduced || flag >= kStagedTo) ? kCtrAr
+                  : flag == kOsReady                                      ? kCtrOs
+                  : flag == kFence                                        ? kCtrFence
+                                                                          : kCtrBc;
+    return flag_off[k];
+  }
   std::string* out_;
   int seq_[kNumEvents] = {};
+  int ev_epoch_[kNumEvents] = {};
 };
 
 Proto proto_from_env() {
@@ -300,6 +320,16 @@ static int emit_gather(fmx_comm* c, Sink& k, const PendingGather& p) {
     if ((rc = k.record(p.LG, kEvSlotFree + p.R % p.K))) return rc;  // W(R)
   }
   if (p.split && (rc = k.record(p.LG, kEvGathered + p.R % p.K))) return rc;  // G(R)
+  return FMX_OK;
+}
+
+int plan_fence(fmx_comm* c, Sink& k) {
+  int rc = plan_flush(c, k);
+  if (rc) return rc;
+  const uint32_t v = c->fence_round + 1;
+  if ((rc = k.signal(kLaneMain, kFence, v)) || (rc = k.wait_peers(kLaneMain, kFence, v, c->rank)))
+    return rc;
+  c->fence_round = v;
   return FMX_OK;
 }
 
@@ -751,6 +781,24 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   auto device_class = [&](int i) {
     return kinds[i] == 0 || kinds[i] == 3 || kinds[i] == 4 || kinds[i] == 5;
   };
+  // FMX_TRACE_REPLAYS=k: the op list is a captured graph, launched k times
+  // (fmx_graph_*): every replay runs the captured schedule - same slots, same
+  // rounds - with flag values re-based by the counters' advance, ends with the
+  // fence capture_end appends (FMX_TRACE_REPLAY_FENCE=0 drops it: the checker
+  // must then object), and sees no event of another replay
+  const int replays = getenv("FMX_TRACE_REPLAYS") ? std::max(1, atoi(getenv("FMX_TRACE_REPLAYS"))) : 0;
+  const bool replay_fence = !getenv("FMX_TRACE_REPLAY_FENCE") || atoi(getenv("FMX_TRACE_REPLAY_FENCE"));
+  uint32_t c0[kNumCounters], delta[kNumCounters] = {};
+  for (int k = 0; k < kNumCounters; ++k) c0[k] = *c.counter(k);
+  for (int rep = 0; rep < std::max(1, replays); ++rep) {
+  if (replays && rep > 0) {
+    for (int k = 0; k < kNumCounters; ++k) {
+      *c.counter(k) = c0[k];
+      sink.flag_off[k] = (uint32_t)rep * delta[k];
+    }
+    sink.round_tag = (uint32_t)rep << 24;
+    sink.epoch = rep;
+  }
   for (int i = 0; i < nops; ++i) {
     int rc;
     if (!overlap || i == 0 || !device_class(i) || !device_class(i - 1)) sink.join();
@@ -775,6 +823,17 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
       drop_pending(&c);
       return rc;
     }
+  }
+  if (replays) {
+    if (c.pending) {
+      drop_pending(&c);
+      return fail(FMX_ERR_INVALID_ARG, "captured sequence ends with a deferred gather");
+    }
+    sink.join();  // the fence node depends on every leaf of the graph
+    if (replay_fence && plan_fence(&c, sink)) return FMX_ERR_INVALID_ARG;
+    if (rep == 0)
+      for (int k = 0; k < kNumCounters; ++k) delta[k] = *c.counter(k) - c0[k];
+  }
   }
   if (c.pending) {  // an unflushed deferred gather: the sequence must end with a flush
     drop_pending(&c);

@@ -316,6 +316,8 @@ int plan_broadcast(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
                    int root);
 // enqueue the pending deferred gather, if any (every plan does this first)
 int plan_flush(fmx_comm* c, Sink& k);
+// fmx_comm_fence: flush, signal FENCE, wait for every peer's FENCE (lane 1)
+int plan_fence(fmx_comm* c, Sink& k);
 void drop_pending(fmx_comm* c);
 
 }  // namespace fmx

@@ -586,3 +586,63 @@ def test_deferred_gather_must_be_flushed(monkeypatch):
     monkeypatch.setenv("FMX_TRACE_DEFER", "1")
     with pytest.raises(ValueError):
         _lib.trace_plan(2, 0, [("allreduce", 30_000, 0)], 4096, "ce")
+
+
+# ---- captured CUDA graphs (fmx_graph_*): replays of one captured schedule ------
+
+REPLAY_SEQUENCES = {
+    "dp-step": [("allreduce", 30_001, 0), ("allreduce", 200_003, 0), ("allreduce", 77_777, 0),
+                ("allreduce", 5, 0), ("allreduce", 20_000, 0), ("flush", 0, 0)],
+    "mixed": [("allreduce", 20_000, 0), ("reduce_scatter", 9_001, 0), ("broadcast", 5_000, 0, 1),
+              ("allreduce", 123_457, 1), ("allgather", 3, 0), ("allreduce", 300, 0),
+              ("flush", 0, 0)],
+}
+
+
+@pytest.mark.parametrize("n", [2, 3, 7])
+@pytest.mark.parametrize("seq", sorted(REPLAY_SEQUENCES))
+@pytest.mark.parametrize("lanes,transport,defer", [("1", "ce", "1"), ("3", "ce", "1"),
+                                                   ("3", "zc", "0"), ("3", "auto", "1"),
+                                                   ("1", "auto", "0")])
+def test_graph_replays(monkeypatch, n, seq, lanes, transport, defer):
+    """A captured step replayed 3 times: every replay runs the captured slots
+    and rounds with flag values re-based by the counters' advance, drops waits
+    on events of other replays, and ends with the appended fence - race-,
+    stale-read- and deadlock-free on the lanes and as one FIFO."""
+    monkeypatch.setenv("FMX_TRACE_REPLAYS", "3")
+    monkeypatch.setenv("FMX_TRACE_OVERLAP", "1")
+    monkeypatch.setenv("FMX_TRACE_DEFER", defer)
+    monkeypatch.setenv("FMX_LANES", lanes)
+    monkeypatch.setenv("FMX_ZC_MAX", "100000")
+    progs = programs(n, REPLAY_SEQUENCES[seq], 4096, transport)
+    for seed in range(8):
+        simulate(progs, seed, burst=4)
+    merged = programs(n, REPLAY_SEQUENCES[seq], 4096, transport, merged=True)
+    for seed in range(4):
+        simulate(merged, seed)
+
+
+def test_graph_replays_need_the_fence(monkeypatch):
+    """Without the end-of-replay fence, a replay's baked slots are reused while
+    a slow peer still reads the previous replay's: the checker must object.
+    (Pipelined allreduces alone would be safe - every rank's first stage of
+    replay r+1 follows its complete replay r, whose gathers waited for every
+    owner's REDUCED - but a one-shot publish or a broadcast root does not wait
+    for its readers: their slot alternation / reuse wait is decided on the
+    captured round, so a replay writes the slot a slow peer still reads.)"""
+    monkeypatch.setenv("FMX_TRACE_REPLAYS", "3")
+    monkeypatch.setenv("FMX_TRACE_OVERLAP", "1")
+    for ops in ([("allreduce", 5, 0)], [("broadcast", 3000, 0, 0)]):
+        monkeypatch.setenv("FMX_TRACE_REPLAY_FENCE", "0")
+        progs = programs(3, ops, 4096, "auto")
+        failures = 0
+        for seed in range(80):
+            try:
+                simulate(progs, seed, burst=4)
+            except AssertionError:
+                failures += 1
+        assert failures > 0, ops
+        monkeypatch.setenv("FMX_TRACE_REPLAY_FENCE", "1")
+        progs = programs(3, ops, 4096, "auto")
+        for seed in range(80):
+            simulate(progs, seed, burst=4)
