@@ -630,12 +630,15 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
     inst = inst_mod.bind(gpu_id, inst_id, cfg["profiles"][rank], mode=inst_mode, device=gpu_local)
     comm = init_process_group(None, rank, job_key, instance=inst, nranks=n,
                               transport=cfg["transport"], timeout_s=300)
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(cfg["port"])
-    pg = dist.new_group(backend="gloo") if dist.is_initialized() else None
-    if pg is None:
-        dist.init_process_group("gloo", rank=rank, world_size=n)
-        pg = dist.group.WORLD
+    pg, own_pg = None, False
+    if cfg.get("engine", "graph") != "graph":
+        # torch DDP's control plane (parameter-shape checks) on gloo over the same ranks
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(cfg["port"])
+        pg = dist.new_group(backend="gloo") if dist.is_initialized() else None
+        if pg is None:
+            dist.init_process_group("gloo", rank=rank, world_size=n)
+            pg, own_pg = dist.group.WORLD, True
     stream = inst.stream
     torch.manual_seed(0)
     name = cfg.get("model", "resnet50")
@@ -668,7 +671,8 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
             net = model
         else:
             net = fddp.ShmDataParallel(model, comm, bucket_cap_mb=cfg.get("bucket_mb", 8.0),
-                                       first_bucket_mb=cfg.get("first_bucket_mb", 1.0))
+                                       first_bucket_mb=cfg.get("first_bucket_mb", 1.0),
+                                       compress=cfg.get("compress"))
         if name == "bert":
             opt = torch.optim.AdamW(net.parameters(), lr=2e-5, capturable=graph)
         else:
@@ -755,7 +759,8 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
            "stamps": stamps,
            "launches": comm.kernel_launches() - l0,
            "param_digest": float(sum(p.detach().double().sum().item() for p in model.parameters()))}
-    dist.destroy_process_group()
+    if own_pg:
+        dist.destroy_process_group()
     comm.destroy()
     return out
 
@@ -846,49 +851,101 @@ TRAIN_MODELS = {
 }
 
 
-def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) -> dict:
-    """Data-parallel training throughput on the same instances (single-GPU
-    layout only); DDP buckets allreduced by ddp.flexshm_hook."""
+def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) -> dict | None:
+    """Data-parallel training throughput on the instances of `d`: one
+    communicator over all of them; under torchrun (N > 1) each process runs its
+    GPU's instance ranks, the time is the max over every rank of every process
+    and rank 0 returns the line (the others None).  Graph engine:
+    ddp.ShmDataParallel, the step as one CUDA graph; ddp engine: torch DDP +
+    ddp.flexshm_hook (gloo control group, single-process layouts only)."""
+    import torch
+
+    grank, world, local = dist_env()
     n = len(d.instances)
+    engine = args.train_engine if args.train_engine != "auto" else \
+        ("ddp" if model == "bert" else "graph")
+    if world > 1 and engine == "ddp":
+        raise ValueError("the eager DDP engine's gloo control group is single-process: "
+                         "use --train-engine graph under torchrun")
     cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
            "batch": args.batch, "train_steps": args.train_steps, "train_warmup": args.train_warmup,
            "port": 29000 + os.getpid() % 1000, "model": model, "no_sync": no_sync,
            "bucket_mb": args.bucket_mb, "first_bucket_mb": args.first_bucket_mb,
-           "stamps": bool(args.stamps) and not no_sync,
-           # the bf16-compressed exchange exists as a DDP comm hook only
-           "engine": "ddp" if args.compress else args.train_engine if args.train_engine != "auto"
-           else ("ddp" if model == "bert" else "graph"),
+           "stamps": bool(args.stamps) and not no_sync, "engine": engine,
            "compress": args.compress}
-    res = run_ranks(train_body, _spawned_train, list(range(n)), job_key + "-t", n, cfg,
-                    args.train_mode, 0)
-    t = max(r["ms_total"] for r in res.values()) / 1e3
-    digests = {round(r["param_digest"], 3) for r in res.values()}
+    mine, gpu_local = list(range(n)), 0
+    if world > 1:
+        import torch.distributed as dist
+        obj = [job_key if grank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)     # one job key for every process
+        job_key = obj[0]
+        mine = [r for r, (g, _) in enumerate(d.instances) if g == grank]
+        gpu_local = local if not os.environ.get("FMX_ONE_GPU_VISIBLE") else 0
+        if os.environ.get("FMX_DEVICE_MAP"):
+            gpu_local = int(os.environ["FMX_DEVICE_MAP"].split(",")[local])
+    res, err = {}, None
+    try:
+        res = run_ranks(train_body, _spawned_train, mine, job_key + "-t", n, cfg,
+                        args.train_mode, gpu_local)
+    except Exception as exc:  # noqa: BLE001 - every process must reach the reductions below
+        err = exc
+    t_local = max((r["ms_total"] for r in res.values()), default=-1.0) if err is None else -1.0
+    launches = sum(r["launches"] for r in res.values())
+    digests = {r: round(r_["param_digest"], 3) for r, r_ in res.items()}
+    if world > 1:
+        import torch.distributed as dist
+        v = torch.tensor([t_local, -t_local, float(launches)], dtype=torch.float64)
+        mx = v.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        every = [None] * world
+        dist.all_gather_object(every, digests)
+        digests = {k: x for part in every for k, x in part.items()}
+        sm = torch.tensor([float(launches)], dtype=torch.float64)
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        launches = int(sm.item())
+        if err is None and -mx[1].item() < 0:
+            err = RuntimeError("a training rank of another process failed")
+        t_local = mx[0].item()
+    if err is not None:
+        raise err
+    if grank != 0:
+        return None
+    t = t_local / 1e3
     desc, precision, unit = TRAIN_MODELS[model]
     if cfg["stamps"]:
         path = args.stamps if args.train_only else os.path.splitext(args.stamps)[0] + "_train.json"
         with open(path, "w") as f:
             json.dump({"n": n, "model": model, "train": {r: v["stamps"] for r, v in res.items()}}, f)
-    return {unit: n * args.batch * args.train_steps / t, "instances": n, "batch_per_instance":
-            args.batch, "ms_per_step": t * 1e3 / args.train_steps, "steps": args.train_steps,
-            "warmup": args.train_warmup, "instance_mode": args.train_mode,
-            "precision": (precision.replace("(fp32 SHM allreduce)",
-                                            "(bf16 SHM allreduce of the fp32 buckets)")
-                          if args.compress else precision),
-            "replicas_agree": len(digests) == 1, "loss": res[0]["loss"],
-            "host": {"enqueue_ms_per_step": max(r["host_enqueue_ms"] for r in res.values())
-                     / args.train_steps,
-                     "hook_ms_per_step": max(r["hook_host_ms"] for r in res.values())
-                     / args.train_steps,
-                     "hooks_per_step": res[0]["hook_calls"] / args.train_steps,
-                     "phase_ms_per_step_rank0": {k: v / args.train_steps for k, v in
-                                                 res[0]["host_phase_ms"].items()},
-                     "what": "host time to enqueue the timed steps (max over ranks; loss.item() "
-                             "syncs once per step only in the last one) and the part spent "
-                             "inside flexshm_hook's collective calls"},
-            "gpu_launches": sum(r["launches"] for r in res.values()), "model": desc,
-            "engine": ("ddp.ShmDataParallel: whole step (fwd, bwd with bucket allreduces, "
-                       "optimizer) replayed as one CUDA graph" if cfg["engine"] == "graph" else
-                       "torch DDP + ddp.flexshm_hook, eager")}
+    r0 = res[min(res)]
+    out = {unit: n * args.batch * args.train_steps / t, "instances": n, "batch_per_instance":
+           args.batch, "ms_per_step": t * 1e3 / args.train_steps, "steps": args.train_steps,
+           "warmup": args.train_warmup, "instance_mode": args.train_mode,
+           "precision": (precision.replace("(fp32 SHM allreduce)",
+                                           "(bf16 SHM allreduce of the fp32 buckets)")
+                         if args.compress else precision),
+           "replicas_agree": len(set(digests.values())) == 1, "loss": r0["loss"],
+           "host": {"enqueue_ms_per_step": max(r["host_enqueue_ms"] for r in res.values())
+                    / args.train_steps,
+                    "hook_ms_per_step": max(r["hook_host_ms"] for r in res.values())
+                    / args.train_steps,
+                    "hooks_per_step": r0["hook_calls"] / args.train_steps,
+                    "phase_ms_per_step_rank0": {k: v / args.train_steps for k, v in
+                                                r0["host_phase_ms"].items()},
+                    "what": "host time to enqueue the timed steps (max over this process's "
+                            "ranks; loss.item() syncs once per step only in the last one) and "
+                            "the part spent inside flexshm_hook's collective calls"},
+           "gpu_launches": launches, "model": desc,
+           "engine": ("ddp.ShmDataParallel: whole step (fwd, bwd with bucket allreduces, "
+                      "optimizer) replayed as one CUDA graph" if engine == "graph" else
+                      "torch DDP + ddp.flexshm_hook, eager")}
+    if world > 1:
+        out["n_gpus"] = world
+        out["scaling"] = "weak"
+        if os.environ.get("FMX_DEVICE_MAP"):
+            out["logical_gpus"] = (f"{world} LOGICAL GPUs (FMX_DEVICE_MAP="
+                                   f"{os.environ['FMX_DEVICE_MAP']}): all instances share the "
+                                   "physical devices listed - not a scaling number")
+    return out
 
 
 def dry_exchange(d, mine: list[int], job_key: str, m: int = 4099) -> dict[int, int]:
@@ -1329,12 +1386,17 @@ def _main(args, world, n, unit):
                 f.writelines(json.dumps(ln) + "\n" for ln in lines)
         return 0
     if args.train_only:
-        d = decision_for(args.gpus, args.ranks_per_gpu)
-        line = {args.train_model: run_train(args, d, f"train-{os.getpid()}", args.train_model)}
+        d = decision_for(args.gpus if world == 1 else world, args.ranks_per_gpu)
+        tr = run_train(args, d, f"train-{os.getpid()}", args.train_model)
+        ns = None
         if args.train_no_sync:
             # same instances, same step, gradients NOT synchronised: the compute-only bound
-            line[args.train_model]["no_sync"] = run_train(args, d, f"train-ns-{os.getpid()}",
-                                                          args.train_model, no_sync=True)
+            ns = run_train(args, d, f"train-ns-{os.getpid()}", args.train_model, no_sync=True)
+        if tr is None:       # torchrun rank != 0
+            return 0
+        line = {args.train_model: tr}
+        if ns is not None:
+            line[args.train_model]["no_sync"] = ns
         print(json.dumps(line))
         if args.out:
             with open(args.out, "w") as f:
@@ -1346,14 +1408,18 @@ def _main(args, world, n, unit):
         nccl = run_nccl_point(args, tr)      # collective: every torchrun rank takes part
         if line is not None:
             line[f"nccl_{tr}"] = nccl
+    train = None
+    if not args.no_train and not args.dry_run and (world > 1 or args.gpus == 1):
+        # every torchrun process takes part (its GPU's instance ranks); rank 0 reports
+        d = decision_for(world if world > 1 else 1, args.ranks_per_gpu)
+        try:
+            train = run_train(args, d, f"train-{os.getpid()}")
+        except Exception as exc:  # noqa: BLE001 - report, keep the allreduce line
+            train = {"error": repr(exc)[:300]}
     if line is None:
         return 0
-    if not args.no_train and args.gpus == 1 and world == 1:
-        d = decision_for(1, args.ranks_per_gpu)
-        try:
-            line["resnet50"] = run_train(args, d, f"train-{os.getpid()}")
-        except Exception as exc:  # noqa: BLE001 - report, keep the allreduce line
-            line["resnet50"] = {"error": repr(exc)[:300]}
+    if train is not None:
+        line["resnet50"] = train
     if not args.no_cpu_baseline:
         r = run_cpu_reference(args.count, n, args.dtype, 3, 1, seconds=args.cpu_seconds)
         line["cpu_baseline"] = {"value": r["value"], "unit": line["unit"], "cores": r["cores"],

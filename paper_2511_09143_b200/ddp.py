@@ -305,11 +305,16 @@ class ShmDataParallel(torch.nn.Module):
 
     Call `zero_grad()` (in-place zeroing of the buckets) instead of the
     optimizer's set_to_none; gradients that arrive detached from their bucket
-    view are copied into it.
+    view are copied into it.  compress="bf16": each fp32 bucket is rounded to a
+    bf16 shadow, averaged over SHM with the bf16 contract (fp32 rank-order
+    accumulation, one RNE rounding) and widened back after the backward pass -
+    half the host-link bytes, torch's bf16_compress_hook idea; within the
+    north_star's bf16 tolerance, not the fp32 bit-exact path.
     """
 
     def __init__(self, module: torch.nn.Module, comm: ShmCommunicator, bucket_cap_mb: float = 8.0,
-                 first_bucket_mb: float = 1.0, stream=None, defer_gather: bool | None = None):
+                 first_bucket_mb: float = 1.0, stream=None, defer_gather: bool | None = None,
+                 compress: str | None = None):
         super().__init__()
         self.module = module
         self.comm = comm
@@ -320,6 +325,10 @@ class ShmDataParallel(torch.nn.Module):
         # each bucket's last gather is enqueued after the next bucket's stage
         # (fmx_comm_set_defer) while the backward pass runs; flushed at its end
         self.defer = os.environ.get("FMX_DEFER", "1") != "0" if defer_gather is None else defer_gather
+        if compress not in (None, "bf16"):
+            raise ValueError(f"unknown gradient compression {compress!r}")
+        self.compress = compress
+        self._shadow = []
         self.hook_state = HookState(comm, stream)
         self.stream = self.hook_state.stream
         self.buckets = None          # [(flat tensor, [param index])]
@@ -371,6 +380,11 @@ class ShmDataParallel(torch.nn.Module):
                 self.bucket_of[i] = b
                 self._views[i] = view
             self.buckets.append((flat, idx))
+            if self.compress == "bf16" and flat.dtype == torch.float32:
+                self._shadow.append(torch.empty(flat.numel(), dtype=torch.bfloat16,
+                                                device=flat.device))
+            else:
+                self._shadow.append(None)
 
     def zero_grad(self, set_to_none: bool = False):  # noqa: ARG002 - buckets are persistent
         if self.buckets is None:
@@ -413,11 +427,15 @@ class ShmDataParallel(torch.nn.Module):
         cur = torch.cuda.current_stream(flat.device)
         if _MEASURE["stamp"]:     # timeline probe: when this bucket is ready on the GPU
             self.comm.stamp(100 + b, stream=cur)
+        buf = flat
+        if self._shadow[b] is not None:   # round to bf16 after the bucket's producers
+            buf = self._shadow[b]
+            buf.copy_(flat)
         self.comm.set_join_stream(self.stream)
         try:
             if self.defer:
                 self.comm.set_defer(True)
-            self.comm.allreduce(flat, op="avg", stream=cur)
+            self.comm.allreduce(buf, op="avg", stream=cur)
         finally:
             self.comm.set_join_stream(None)
 
@@ -438,6 +456,11 @@ class ShmDataParallel(torch.nn.Module):
             finally:
                 self.comm.set_join_stream(None)
                 self.comm.set_defer(False)
+        if any(sh is not None for sh in self._shadow):
+            with torch.cuda.stream(self.stream):    # widen the averaged bf16 buckets
+                for (flat, _), sh in zip(self.buckets, self._shadow):
+                    if sh is not None:
+                        flat.copy_(sh)
         cur.wait_stream(self.stream)
 
     # -- CUDA graph ----------------------------------------------------------

@@ -328,7 +328,7 @@ def zero_worker(rank: int, job_key: str, n: int, mode: str = "green"):
 
 
 def graph_dp_worker(rank: int, job_key: str, n: int, mode: str = "mps", defer: bool = True,
-                    steps: int = 5, warmup: int = 2):
+                    compress: str | None = None, steps: int = 5, warmup: int = 2):
     """ddp.ShmDataParallel on a small MLP: (1) the first step's averaged
     gradient next to this rank's local gradient (oracle check in the test);
     (2) `steps` eager training steps; (3) the same from the same start as a
@@ -366,7 +366,7 @@ def graph_dp_worker(rank: int, job_key: str, n: int, mode: str = "mps", defer: b
         for kind in ("eager", "graph"):
             model = build()
             net = fddp.ShmDataParallel(model, comm, bucket_cap_mb=0.05, first_bucket_mb=0.01,
-                                       defer_gather=defer)
+                                       defer_gather=defer, compress=compress)
             opt = torch.optim.SGD(net.parameters(), lr=0.05, momentum=0.9)
 
             def step():

@@ -18,19 +18,27 @@ from tests import _workers
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n,mode,defer", [(2, "mps", True), (3, "mps", True), (3, "green", True),
-                                          (3, "mps", False)])
-def test_graphed_dp_matches_eager_and_oracle(n, mode, defer):
+@pytest.mark.parametrize("n,mode,defer,compress", [
+    (2, "mps", True, None), (3, "mps", True, None), (3, "green", True, None),
+    (3, "mps", False, None), (3, "mps", True, "bf16")])
+def test_graphed_dp_matches_eager_and_oracle(n, mode, defer, compress):
     from paper_2511_09143_b200.launcher import launch, new_job_key
     from paper_2511_09143_b200.scheduler import fm_select, make_cluster
     from paper_2511_09143_b200.workload import Job
 
     d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
     key = new_job_key("gdp")
-    res = launch(_workers.graph_dp_worker, d, args=(key, n, mode, defer), job_key=key, timeout_s=300,
+    res = launch(_workers.graph_dp_worker, d, args=(key, n, mode, defer, compress), job_key=key,
+                 timeout_s=300,
                  mode=mode)
     assert res[0]["buckets"] >= 3
-    want = orc.allreduce_c([r["local"] for r in res], orc.F32, *orc.ddp_mean(n))
+    if compress == "bf16":   # bf16 contract on the bf16-rounded local gradients, widened
+        import torch
+        loc = [torch.from_numpy(r["local"]).to(torch.bfloat16).view(torch.int16).numpy()
+               .view(np.uint16) for r in res]
+        want = orc.bf16_to_f32(orc.allreduce_c(loc, orc.BF16, *orc.ddp_mean(n)))
+    else:
+        want = orc.allreduce_c([r["local"] for r in res], orc.F32, *orc.ddp_mean(n))
     extra = [np.arange(1000, dtype=np.float32) * (r + 1) for r in range(n)]
     want_extra = orc.allreduce_c(extra, orc.F32, orc.OP_SUM)
     for rank, r in enumerate(res):
