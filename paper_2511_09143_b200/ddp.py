@@ -431,6 +431,20 @@ class ShmDataParallel(torch.nn.Module):
         if self._shadow[b] is not None:   # round to bf16 after the bucket's producers
             buf = self._shadow[b]
             buf.copy_(flat)
+        if _MEASURE["noop"] == "3":
+            # measurement only, no exchange: the exchange's copy-engine traffic alone
+            # (bucket D2H to pinned host memory, twice H2D back) on the side stream
+            self.stream.wait_stream(cur)
+            with torch.cuda.stream(self.stream):
+                key = (buf.numel(), buf.dtype)
+                if key not in _SCRATCH:
+                    _SCRATCH[key] = (torch.empty(buf.numel(), dtype=buf.dtype).pin_memory(),
+                                     torch.empty_like(buf))
+                host, dev = _SCRATCH[key]
+                host.copy_(buf, non_blocking=True)
+                dev.copy_(host, non_blocking=True)
+                dev.copy_(host, non_blocking=True)
+            return
         self.comm.set_join_stream(self.stream)
         try:
             if self.defer:
