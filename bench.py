@@ -95,12 +95,12 @@ def parse_args(argv=None):
                    default="resnet50", help="model of the --train-only leg")
     p.add_argument("--train-engine", choices=["auto", "graph", "ddp"], default="auto",
                    help="graph: ddp.ShmDataParallel, whole step captured as one CUDA graph; "
-                        "ddp: torch DDP + flexshm_hook, eager; auto (default): graph for the "
-                        "conv nets, ddp for bert (link-bound; graph 2465 vs eager 2658 seq/s, "
-                        "r02/r2v)")
+                        "ddp: torch DDP + flexshm_hook, eager; auto (default): graph")
     p.add_argument("--train-no-sync", action="store_true",
                    help="--train-only: also time the step without gradient sync (compute bound)")
-    p.add_argument("--bucket-mb", type=float, default=8.0, help="DDP bucket_cap_mb of the DP legs")
+    p.add_argument("--bucket-mb", type=float, default=None,
+                   help="bucket cap (MiB) of the DP legs; default 8 for the conv nets, 25 for "
+                        "BERT-base (graph engine: 2917-2958 seq/s at 25 vs 2284 at 8, r02/r3c-r3d)")
     p.add_argument("--first-bucket-mb", type=float, default=1.0,
                    help="first bucket cap of the graph engine (DDP's first_bucket_bytes)")
     p.add_argument("--compress", choices=["bf16"], default=None,
@@ -674,7 +674,9 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
                                        first_bucket_mb=cfg.get("first_bucket_mb", 1.0),
                                        compress=cfg.get("compress"))
         if name == "bert":
-            opt = torch.optim.AdamW(net.parameters(), lr=2e-5, capturable=graph)
+            # in a graph: the fused multi-tensor AdamW (capturable), one kernel per step
+            opt = torch.optim.AdamW(net.parameters(), lr=2e-5, capturable=graph,
+                                    fused=True if graph else None)
         else:
             opt = torch.optim.SGD(net.parameters(), lr=0.01, momentum=0.9)
 
@@ -862,15 +864,16 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
 
     grank, world, local = dist_env()
     n = len(d.instances)
-    engine = args.train_engine if args.train_engine != "auto" else \
-        ("ddp" if model == "bert" else "graph")
+    engine = args.train_engine if args.train_engine != "auto" else "graph"
     if world > 1 and engine == "ddp":
         raise ValueError("the eager DDP engine's gloo control group is single-process: "
                          "use --train-engine graph under torchrun")
     cfg = {"instances": d.instances, "profiles": d.profiles, "transport": args.transport,
            "batch": args.batch, "train_steps": args.train_steps, "train_warmup": args.train_warmup,
            "port": 29000 + os.getpid() % 1000, "model": model, "no_sync": no_sync,
-           "bucket_mb": args.bucket_mb, "first_bucket_mb": args.first_bucket_mb,
+           "bucket_mb": args.bucket_mb if args.bucket_mb is not None else
+           (25.0 if model == "bert" else 8.0),
+           "first_bucket_mb": args.first_bucket_mb,
            "stamps": bool(args.stamps) and not no_sync, "engine": engine,
            "compress": args.compress}
     mine, gpu_local = list(range(n)), 0
@@ -934,7 +937,7 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
                     "what": "host time to enqueue the timed steps (max over this process's "
                             "ranks; loss.item() syncs once per step only in the last one) and "
                             "the part spent inside flexshm_hook's collective calls"},
-           "gpu_launches": launches, "model": desc,
+           "gpu_launches": launches, "model": desc, "bucket_mb": cfg["bucket_mb"],
            "engine": ("ddp.ShmDataParallel: whole step (fwd, bwd with bucket allreduces, "
                       "optimizer) replayed as one CUDA graph" if engine == "graph" else
                       "torch DDP + ddp.flexshm_hook, eager")}
