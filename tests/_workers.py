@@ -396,3 +396,117 @@ def graph_dp_worker(rank: int, job_key: str, n: int, mode: str = "mps", defer: b
     out.update(params_eager=runs["eager"], params_graph=runs["graph"])
     comm.destroy()
     return out
+
+
+GRAPH_API_SEED = {"big": 1000, "small": 2000, "rs": 3000, "bc": 4000}
+
+
+def graph_api_worker(rank: int, job_key: str, n: int, mode: str = "mps"):
+    """The raw fmx_graph_* / deferred-gather API on one rank.
+
+    (1) Deferred gathers in join-stream mode: three allreduces (multi-round,
+        one-shot size, one-round) forked from the compute stream, then a flush;
+        set_defer(False) with a gather pending must raise.
+    (2) Two captured graphs - G1: copy inputs in, allreduce (avg) of a
+        multi-round buffer, broadcast from the last rank; G2: allreduce of a
+        one-shot-sized buffer, reduce-scatter - replayed G1, G2, G1 (on another
+        stream), eager allreduce (third stream), G2, G1 with fresh inputs
+        before every replay.  Returns every result (flattened fp32)."""
+    import torch
+
+    from oracle import oracle as orc
+    from paper_2511_09143_b200 import instance as inst_mod
+    from paper_2511_09143_b200.comm import init_process_group
+
+    inst = inst_mod.bind(0, rank + 1, mode=mode)
+    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n, timeout_s=120)
+    out = {}
+    s0 = inst.stream
+    dev = torch.device("cuda")
+    t = lambda a: torch.from_numpy(a).to(dev)
+    with torch.cuda.stream(s0):
+        # (1) deferred gathers
+        sizes = [300_001, 1000, 40_000]
+        bufs = [t(orc.synthetic_gradient(rank, c, orc.F32, seed=50 + i)) for i, c in enumerate(sizes)]
+        side = torch.cuda.Stream()
+        comm.set_join_stream(side)
+        comm.set_defer(True)
+        for b in bufs:
+            comm.allreduce(b, op="sum", stream=s0)
+        raised = False
+        try:
+            comm.set_defer(False)
+        except ValueError:
+            raised = True
+        comm.flush(stream=s0)
+        comm.set_join_stream(None)
+        comm.set_defer(False)
+        s0.wait_stream(side)
+        out["defer_raised"] = raised
+        out["defer"] = [b.cpu().numpy() for b in bufs]
+
+        # (2) two captured graphs
+        c_big, c_small, c_rs, c_bc = 200_003, 5, 999, 3000
+        inp = {k: torch.empty(c, device=dev) for k, c in
+               (("big", c_big), ("small", c_small), ("rs", n * c_rs), ("bc", c_bc))}
+        work = {k: torch.empty_like(v) for k, v in inp.items()}
+        rs_out = torch.empty(c_rs, device=dev)
+        torch.cuda.synchronize()
+
+        def capture(body):
+            g = torch.cuda.CUDAGraph(keep_graph=True)
+            comm.capture_begin()
+            with torch.cuda.graph(g, stream=s0):
+                body()
+            h = comm.capture_end(g.raw_cuda_graph())
+            g.instantiate()
+            return g, h, g.raw_cuda_graph_exec()
+
+        def g1_body():
+            cur = torch.cuda.current_stream()
+            work["big"].copy_(inp["big"])
+            work["bc"].copy_(inp["bc"])
+            comm.allreduce(work["big"], op="avg", stream=cur)
+            comm.broadcast(work["bc"], root=n - 1, stream=cur)
+
+        def g2_body():
+            cur = torch.cuda.current_stream()
+            work["small"].copy_(inp["small"])
+            work["rs"].copy_(inp["rs"])
+            comm.allreduce(work["small"], op="sum", stream=cur)
+            comm.reduce_scatter(work["rs"], rs_out, op="sum", stream=cur)
+
+        G1, G2 = capture(g1_body), capture(g2_body)
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        plan = [("G1", s0), ("G2", s0), ("G1", s1), ("eager", s2), ("G2", s1), ("G1", s0)]
+        results = []
+        for k, (what, st) in enumerate(plan):
+            seed = 100 + k
+            with torch.cuda.stream(st):
+                st.wait_stream(s0)   # the fresh inputs are written on s0 below
+            if what == "eager":
+                x = t(orc.synthetic_gradient(rank, 77_777, orc.F32, seed=seed))
+                torch.cuda.synchronize()
+                with torch.cuda.stream(st):
+                    comm.allreduce(x, op="sum", stream=st)
+                st.synchronize()
+                results.append(("eager", seed, x.cpu().numpy()))
+                continue
+            torch.cuda.synchronize()
+            for key in inp:
+                inp[key].copy_(t(orc.synthetic_gradient(rank, inp[key].numel(), orc.F32,
+                                                        seed=seed + GRAPH_API_SEED[key])))
+            torch.cuda.synchronize()
+            g, h, ex = G1 if what == "G1" else G2
+            with torch.cuda.stream(st):
+                comm.launch_prepare(h, ex, st)
+                g.replay()
+            st.synchronize()
+            if what == "G1":
+                results.append(("G1", seed, work["big"].cpu().numpy(), work["bc"].cpu().numpy()))
+            else:
+                results.append(("G2", seed, work["small"].cpu().numpy(), rs_out.cpu().numpy()))
+        out["graphs"] = results
+    torch.cuda.synchronize()
+    comm.destroy()
+    return out

@@ -48,3 +48,52 @@ def test_graphed_dp_matches_eager_and_oracle(n, mode, defer, compress):
         assert np.array_equal(r["params_graph"].view(np.uint32),
                               res[0]["params_graph"].view(np.uint32)), rank
         assert np.array_equal(r["extra"].view(np.uint32), want_extra.view(np.uint32)), rank
+
+
+@pytest.mark.parametrize("n,mode", [(3, "mps"), (2, "green")])
+def test_graph_api_and_deferred_gathers(n, mode):
+    """The raw API: deferred gathers + flush (bit-exact, pending-gather guard);
+    two captured graphs replayed on different streams with an eager collective
+    on a third stream in between, fresh inputs each replay - every result
+    bit-exact against the oracle."""
+    from paper_2511_09143_b200.launcher import launch, new_job_key
+    from paper_2511_09143_b200.scheduler import fm_select, make_cluster
+    from paper_2511_09143_b200.workload import Job
+
+    d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
+    key = new_job_key("gapi")
+    res = launch(_workers.graph_api_worker, d, args=(key, n, mode), job_key=key, timeout_s=300,
+                 mode=mode)
+    bits = lambda a: a.view(np.uint32)
+    sizes = [300_001, 1000, 40_000]
+    for i, c in enumerate(sizes):
+        want = orc.allreduce_c([orc.synthetic_gradient(r, c, orc.F32, seed=50 + i)
+                                for r in range(n)], orc.F32, orc.OP_SUM)
+        for r in res:
+            assert np.array_equal(bits(r["defer"][i]), bits(want)), (i, c)
+    assert all(r["defer_raised"] for r in res)
+    def gen(r, c, seed, key):
+        return orc.synthetic_gradient(r, c, orc.F32, seed=seed + _workers.GRAPH_API_SEED[key])
+    for step in range(len(res[0]["graphs"])):
+        what, seed = res[0]["graphs"][step][:2]
+        if what == "eager":
+            want = orc.allreduce_c([orc.synthetic_gradient(r, 77_777, orc.F32, seed=seed)
+                                    for r in range(n)], orc.F32, orc.OP_SUM)
+            for r in res:
+                assert np.array_equal(bits(r["graphs"][step][2]), bits(want)), step
+        elif what == "G1":
+            want = orc.allreduce_c([gen(r, 200_003, seed, "big") for r in range(n)], orc.F32,
+                                   *orc.ddp_mean(n))
+            want_bc = gen(n - 1, 3000, seed, "bc")
+            for r in res:
+                assert np.array_equal(bits(r["graphs"][step][2]), bits(want)), step
+                assert np.array_equal(bits(r["graphs"][step][3]), bits(want_bc)), step
+        else:
+            want = orc.allreduce_c([gen(r, 5, seed, "small") for r in range(n)], orc.F32,
+                                   orc.OP_SUM)
+            full = orc.allreduce_c([gen(r, n * 999, seed, "rs") for r in range(n)], orc.F32,
+                                   orc.OP_SUM)
+            for rank, r in enumerate(res):
+                assert np.array_equal(bits(r["graphs"][step][2]), bits(want)), step
+                assert np.array_equal(bits(r["graphs"][step][3]),
+                                      bits(full[rank * 999:(rank + 1) * 999])), step
