@@ -335,6 +335,30 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- rank body
 
 
+def graphed(comm, stream, step):
+    """`step` (collectives enqueued on `stream`) captured once as a CUDA graph;
+    returns the replay function (fmx_graph_* re-bases its flags per launch)."""
+    import torch
+    g = torch.cuda.CUDAGraph(keep_graph=True)
+    comm.capture_begin()
+    try:
+        with torch.cuda.graph(g, stream=stream):
+            step()
+    except BaseException:
+        comm.capture_end(0)
+        raise
+    h = comm.capture_end(g.raw_cuda_graph())
+    g.instantiate()
+    ex = g.raw_cuda_graph_exec()
+
+    def replay():
+        comm.launch_prepare(h, ex, stream)
+        with torch.cuda.stream(stream):
+            g.replay()
+    replay.graph = g
+    return replay
+
+
 def rank_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_local: int):
     """One instance rank: bind, join, warm up, then time K allreduces three
     ways - (1) device-resident gradient (`value`), (2) host-resident
@@ -406,6 +430,12 @@ def rank_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_lo
     for _ in range(cfg["warmup"]):
         device_step()
     torch.cuda.synchronize()
+    if os.environ.get("FMX_BENCH_GRAPH") == "1":
+        # experiment: the allreduce captured once, replayed per step (fmx_graph_*)
+        device_step = graphed(comm, stream, device_step)
+        for _ in range(cfg["warmup"]):
+            device_step()
+        torch.cuda.synchronize()
     if cfg.get("load"):
         # interference probe: keep this instance's SMs busy with bf16 GEMMs on
         # another stream while the allreduces run (what DP training does)
@@ -483,6 +513,11 @@ def rank_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_lo
         for _ in range(cfg["warmup"]):
             host_step()
         torch.cuda.synchronize()
+        if os.environ.get("FMX_BENCH_GRAPH") == "1":
+            host_step = graphed(comm, stream, host_step)
+            for _ in range(cfg["warmup"]):
+                host_step()
+            torch.cuda.synchronize()
         out["ms_total_e2e"], out["launches_e2e"] = timed(cfg["steps"], host_step)
         out["e2e_digest"] = int(region.view(torch.int32 if esz == 4 else torch.int16)
                                 .to(torch.int64).sum().item())
