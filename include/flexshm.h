@@ -294,9 +294,10 @@ int fmx_comm_flush(fmx_comm_t comm, void* stream);
  *                  leaf and records the graph's flag operations -> *handle
  *                  (graph NULL: abandon a failed capture);
  *   launch_prepare before EVERY launch of an instance (cudaGraphExec_t) of
- *                  that graph on `stream`: re-bases the instance's flag values
- *                  to the communicator's round counters (and fences first if
- *                  collectives ran since the last replay).
+ *                  that graph on `stream`, followed by exactly one launch:
+ *                  re-bases the instance's flag values to the communicator's
+ *                  round counters (and fences first if collectives ran since
+ *                  the last replay).
  * Replays of one communicator's graphs and its eager calls are ordered by the
  * streams they are issued on (a replay on another stream than the previous
  * one waits for it).  Every rank must capture and replay the same sequence. */

@@ -23,6 +23,7 @@ PAPER.md:264-271), so here:
   blocks and re-assembles it with a single in-place all-gather.
 """
 
+import contextlib
 import os
 import time
 
@@ -337,12 +338,24 @@ class ShmDataParallel(torch.nn.Module):
         self._pending = []
         self._next = 0
         self._armed = False
+        self._sync = True            # no_sync(): gradients accumulate locally
         index = {id(p): i for i, p in enumerate(self.params)}
         self._hooks = [p.register_post_accumulate_grad_hook(
             lambda p, i=index[id(p)]: self._on_grad(i)) for p in self.params]
 
     def forward(self, *args, **kwargs):
         return self.module(*args, **kwargs)
+
+    @contextlib.contextmanager
+    def no_sync(self):
+        """DDP.no_sync: backward passes inside accumulate gradients in the
+        buckets without exchanging them; the next backward outside exchanges
+        the accumulated sum."""
+        prev, self._sync = self._sync, False
+        try:
+            yield
+        finally:
+            self._sync = prev
 
     # -- buckets -------------------------------------------------------------
     def _build(self):
@@ -416,6 +429,8 @@ class ShmDataParallel(torch.nn.Module):
             else:
                 view.copy_(p.grad)
             p.grad = view
+        if not self._sync:
+            return
         b = self.bucket_of[i]
         self._pending[b] -= 1
         while self._next < len(self.buckets) and self._pending[self._next] == 0:
@@ -459,6 +474,8 @@ class ShmDataParallel(torch.nn.Module):
             self._build()          # first backward: buckets in gradient-ready order
             self._pending = [0] * len(self.buckets)
             self._next = 0
+        if not self._sync:
+            return
         while self._next < len(self.buckets):
             self._launch(self._next)
             self._next += 1

@@ -392,6 +392,22 @@ def graph_dp_worker(rank: int, job_key: str, n: int, mode: str = "mps", defer: b
                 out["extra"] = extra.cpu().numpy()
                 out["launches_per_replay"] = comm.kernel_launches()
             runs[kind] = flat(model.parameters())
+        # gradient accumulation: one backward under no_sync, one outside - the
+        # exchanged gradient is the DDP mean of the ranks' accumulated gradients
+        x2 = torch.randn(32, 64, generator=g).cuda()
+        y2 = torch.randint(0, 10, (32,), generator=g).cuda()
+        ref2 = build()
+        fddp.broadcast_parameters(ref2, comm)
+        F.cross_entropy(ref2(x), y).backward()
+        F.cross_entropy(ref2(x2), y2).backward()
+        out["local_acc"] = flat([p.grad for p in ref2.parameters()])
+        model3 = build()
+        net3 = fddp.ShmDataParallel(model3, comm, bucket_cap_mb=0.05, first_bucket_mb=0.01,
+                                    defer_gather=defer, compress=compress)
+        with net3.no_sync():
+            F.cross_entropy(net3(x), y).backward()
+        F.cross_entropy(net3(x2), y2).backward()
+        out["synced_acc"] = flat([p.grad for p in model3.parameters()])
     stream.synchronize()
     out.update(params_eager=runs["eager"], params_graph=runs["graph"])
     comm.destroy()

@@ -5,7 +5,9 @@ replayed, flag values re-based per replay by the library.
 Checked: the first step's averaged gradient is the oracle's rank-order
 DDP mean of the ranks' local gradients (bit-exact); the graph-replayed
 training ends bit-identical to the same steps run eagerly, on every rank;
-an eager allreduce between two replays (fence + counter continuity) is exact."""
+an eager allreduce between two replays (fence + counter continuity) is exact;
+gradient accumulation under no_sync exchanges the DDP mean of the
+accumulated local gradients."""
 
 from __future__ import annotations
 
@@ -41,8 +43,15 @@ def test_graphed_dp_matches_eager_and_oracle(n, mode, defer, compress):
         want = orc.allreduce_c([r["local"] for r in res], orc.F32, *orc.ddp_mean(n))
     extra = [np.arange(1000, dtype=np.float32) * (r + 1) for r in range(n)]
     want_extra = orc.allreduce_c(extra, orc.F32, orc.OP_SUM)
+    if compress == "bf16":
+        loc = [torch.from_numpy(r["local_acc"]).to(torch.bfloat16).view(torch.int16).numpy()
+               .view(np.uint16) for r in res]
+        want_acc = orc.bf16_to_f32(orc.allreduce_c(loc, orc.BF16, *orc.ddp_mean(n)))
+    else:
+        want_acc = orc.allreduce_c([r["local_acc"] for r in res], orc.F32, *orc.ddp_mean(n))
     for rank, r in enumerate(res):
         assert np.array_equal(r["synced"].view(np.uint32), want.view(np.uint32)), rank
+        assert np.array_equal(r["synced_acc"].view(np.uint32), want_acc.view(np.uint32)), rank
         assert np.array_equal(r["params_graph"].view(np.uint32),
                               r["params_eager"].view(np.uint32)), rank
         assert np.array_equal(r["params_graph"].view(np.uint32),
