@@ -273,6 +273,7 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t c
 // With FMX_LANES=2 the gather runs on lane 1 and the W/G waits are implied by
 // stream order (the schedule of the first B200 runs).
 enum { kEvSlotFree = 0, kEvGathered = FMX_MAX_SLOTS };  // + R % K: W(R) and G(R) above
+constexpr int kEvReduceDone = 2 * FMX_MAX_SLOTS + 7;   // stage_after_reduce: reduce(R) done
 
 // The all-gather of one round: wait for the owners' REDUCED, record W(R), copy
 // their results out of the out-slots, record G(R).  Built per round; with
@@ -416,14 +417,16 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
   // a deferred gather of the previous allreduce goes after this call's first
   // stage(s) (allreduce) or first of all (reduce-scatter / all-gather)
   if (!ar && (rc = plan_flush(c, k))) return rc;
-  // lane 0 stages K-1 rounds ahead of the reduction
+  // lane 0 stages K-1 rounds ahead of the reduction (stage_after_reduce: stage
+  // j+K-1 is enqueued after reduce(j) and waits for it on the GPU)
   const uint32_t ahead = (uint32_t)K - 1;
+  const bool sar = c->stage_after_reduce && !ag;
   for (uint32_t j = 0; j < ahead && j < g.rounds; ++j)
     if ((rc = stage(j))) return rc;
   if ((rc = plan_flush(c, k))) return rc;
   for (uint32_t j = 0; j < g.rounds; ++j) {
     const uint32_t R = R0 + j;
-    if (j + ahead < g.rounds && (rc = stage(j + ahead))) return rc;
+    if (!sar && j + ahead < g.rounds && (rc = stage(j + ahead))) return rc;
     // lane 1: fetch, then reduce-scatter my chunk in ascending rank order
     const size_t mylen = g.len(me, j);
     if (mylen && ag) {
@@ -503,6 +506,7 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
       if (split && R + 1 >= (uint32_t)K && (rc = k.wait_event(kLaneMain, kEvSlotFree + (R + 1 - K) % K)))
         return rc;
       if ((rc = k.reduce(kLaneMain, pr))) return rc;
+      if (sar && j + ahead < g.rounds && (rc = k.record(kLaneMain, kEvReduceDone))) return rc;
       if (via_ce) {  // result slot written by the copy engine from HBM
         segs.clear();
         segs.push_back({my_out(j), c->at(false, out_off), mylen * g.esz,
@@ -510,6 +514,10 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
                         ubuf(g.lo(me, j) * g.esz, mylen * g.esz)});
         if ((rc = k.copy(kLaneMain, segs, false, false))) return rc;
       }
+    }
+    if (sar && j + ahead < g.rounds) {
+      if (mylen && (rc = k.wait_event(kLaneStage, kEvReduceDone))) return rc;
+      if ((rc = stage(j + ahead))) return rc;
     }
     // REDUCED(R) also says "my gather(R-1) is done": G(R-1)
     if (split && R >= 1 && (rc = k.wait_event(kLaneMain, kEvGathered + (R - 1) % K))) return rc;
@@ -764,6 +772,7 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   apply_proto(&c, proto_from_env());
   // FMX_TRACE_DEFER=1: fmx_comm_set_defer (an allreduce's last gather deferred)
   c.defer_gather = getenv("FMX_TRACE_DEFER") && atoi(getenv("FMX_TRACE_DEFER"));
+  c.stage_after_reduce = getenv("FMX_STAGE_AFTER_REDUCE") && atoi(getenv("FMX_STAGE_AFTER_REDUCE"));
   c.slice_bytes = slice_bytes;
   size_t max_bytes = 0;
   for (int i = 0; i < nops; ++i) max_bytes = std::max(max_bytes, counts[i] * (dtypes[i] ? 2 : 4));

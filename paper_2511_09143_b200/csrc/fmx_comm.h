@@ -14,7 +14,8 @@
 #include "fmx_internal.h"
 
 namespace fmx {
-constexpr int kNumEvents = 2 * FMX_MAX_SLOTS + 7;  // W[K], G[K]; host path F[2], C[2], inputs, P[2]
+constexpr int kNumEvents = 2 * FMX_MAX_SLOTS + 8;  // W[K], G[K]; host path F[2], C[2], inputs,
+                                                   // P[2]; reduce done (stage_after_reduce)
 
 // Round counters a flag's values follow (fmx_graph_*: baked flag values of a
 // captured graph are re-based per replay by their counter's advance).
@@ -107,6 +108,10 @@ struct fmx_comm {
   // single in-order stream stages bucket b+1 while peers finish reducing b
   bool defer_gather = false;
   fmx::PendingGather* pending = nullptr;
+  // FMX_STAGE_AFTER_REDUCE=1 (local knob: an intra-rank order only): stage(R+1)
+  // waits for this rank's reduce(R), so the reduction's result store does not
+  // share the D2H direction with this rank's next stage
+  bool stage_after_reduce = false;
   int nlanes = 3;              // FMX_LANES=1: one stream; 2: gather on the reduce lane
   int join_lanes = 1;          // join-stream mode: 1 every lane on the join stream; 2 stage on
                                // its own stream; 3 stage and gather on their own (FMX_JOIN_LANES,

@@ -646,3 +646,28 @@ def test_graph_replays_need_the_fence(monkeypatch):
         progs = programs(3, ops, 4096, "auto")
         for seed in range(80):
             simulate(progs, seed, burst=4)
+
+
+@pytest.mark.parametrize("n", [2, 3, 7])
+@pytest.mark.parametrize("lanes,slots,transport", [("3", "2", "ce"), ("3", "3", "ce"),
+                                                   ("2", "2", "ce"), ("1", "2", "ce"),
+                                                   ("3", "2", "zc")])
+def test_stage_after_reduce(monkeypatch, n, lanes, slots, transport):
+    """FMX_STAGE_AFTER_REDUCE: stage(R+K-1) enqueued after reduce(R) and
+    waiting for it - still race- and deadlock-free, on the lanes, as one FIFO,
+    and in join-stream / deferred-gather mode."""
+    monkeypatch.setenv("FMX_STAGE_AFTER_REDUCE", "1")
+    monkeypatch.setenv("FMX_LANES", lanes)
+    monkeypatch.setenv("FMX_SLOTS", slots)
+    seq = SEQUENCES["mixed"] + [("allreduce", 200_003, 0), ("reduce_scatter", 40_000, 1)]
+    progs = programs(n, seq, 4096, transport)
+    for seed in range(6):
+        simulate(progs, seed)
+    merged = programs(n, seq, 4096, transport, merged=True)
+    for seed in range(4):
+        simulate(merged, seed)
+    monkeypatch.setenv("FMX_TRACE_OVERLAP", "1")
+    monkeypatch.setenv("FMX_TRACE_DEFER", "1")
+    progs = programs(n, DEFER_SEQUENCES["buckets"], 4096, transport)
+    for seed in range(4):
+        simulate(progs, seed, burst=4)
