@@ -230,7 +230,9 @@ int main(int argc, char** argv) {
   constexpr int kStages = 4;
   const int grids[] = {1, 2, 4, 8, 16, 32, 64, 148};
   const uint32_t chunks[] = {16384, 32768, 49152};
+  const bool load_only = getenv("PROBE_LOAD_ONLY") != nullptr;
   for (uint32_t chunk : chunks) {
+    if (load_only) break;
     const size_t smem = (size_t)chunk * kStages;
     CK(cudaFuncSetAttribute(tma_load_kernel<kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaFuncSetAttribute(tma_store_kernel<kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -251,11 +253,60 @@ int main(int argc, char** argv) {
     }
   }
   for (int g : grids) {
+    if (load_only) break;
     float ms = time_ms([&] { ldg_kernel<<<g * 4, 512>>>((const uint4*)dv_src, total / 16, sink); }, iters);
     printf("{\"probe\": \"ldg_load\", \"ctas\": %d, \"threads\": 512, \"gbs\": %.2f}\n", g * 4, total / ms / 1e6);
     ms = time_ms([&] { stg_kernel<<<g * 4, 512>>>((uint4*)dv_dst, total / 16); }, iters);
     printf("{\"probe\": \"stg_store\", \"ctas\": %d, \"threads\": 512, \"gbs\": %.2f}\n", g * 4, total / ms / 1e6);
     fflush(stdout);
+  }
+  // under load: copy engines stream H2D and D2H on two other streams while
+  // the SM / TMA store (or load) runs - the pipeline's live condition
+  {
+    const size_t big = 256ull << 20;
+    char *h_a, *h_b, *d_a, *d_b;
+    CK(cudaHostAlloc(&h_a, big, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&h_b, big, cudaHostAllocDefault));
+    CK(cudaMalloc(&d_a, big));
+    CK(cudaMalloc(&d_b, big));
+    cudaStream_t sh, sd, sk;
+    CK(cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&sk, cudaStreamNonBlocking));
+    const size_t part = 64ull << 20;  // kernel-side bytes per measurement
+    auto under = [&](const char* name, int ctas, auto&& launch) {
+      for (const char* load : {"none", "both"}) {
+        CK(cudaDeviceSynchronize());
+        if (load[0] == 'b')
+          for (int i = 0; i < 12; ++i) {
+            CK(cudaMemcpyAsync(d_a, h_a, big, cudaMemcpyHostToDevice, sh));
+            CK(cudaMemcpyAsync(h_b, d_b, big, cudaMemcpyDeviceToHost, sd));
+          }
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        launch(sk);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(a, sk));
+        for (int i = 0; i < 5; ++i) launch(sk);
+        CK(cudaEventRecord(b, sk));
+        CK(cudaEventSynchronize(b));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        printf("{\"probe\": \"%s_under_load\", \"ctas\": %d, \"load\": \"%s\", \"gbs\": %.2f}\n", name,
+               ctas, load, 5 * part / ms / 1e6);
+        fflush(stdout);
+        CK(cudaDeviceSynchronize());
+      }
+    };
+    for (int g : {16, 64, 256}) under("stg_store", g, [&](cudaStream_t st) { stg_kernel<<<g, 512, 0, st>>>((uint4*)dv_dst, part / 16); });
+    for (int g : {16, 64, 256}) under("ldg_load", g, [&](cudaStream_t st) { ldg_kernel<<<g, 512, 0, st>>>((const uint4*)dv_src, part / 16, sink); });
+    const uint32_t chunk = 32768;
+    const size_t smem = (size_t)chunk * kStages;
+    CK(cudaFuncSetAttribute(tma_load_kernel<kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(tma_store_kernel<kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    for (int g : {1, 4, 16}) under("tma_store", g, [&](cudaStream_t st) { tma_store_kernel<kStages><<<g, 32, smem, st>>>(dv_dst, part, chunk); });
+    for (int g : {1, 4, 16}) under("tma_load", g, [&](cudaStream_t st) { tma_load_kernel<kStages><<<g, 32, smem, st>>>(dv_src, part, chunk, sink); });
   }
   float ms = time_ms([&] { CK(cudaMemcpyAsync(d_buf, h_src, total, cudaMemcpyHostToDevice)); }, iters);
   printf("{\"probe\": \"ce_h2d\", \"gbs\": %.2f}\n", total / ms / 1e6);
