@@ -1370,6 +1370,7 @@ int fmx_graph_capture_begin(fmx_comm_t c) {
   }
   for (int k = 0; k < kNumCounters; ++k) c->cap_c0[k] = *c->counter(k);
   c->cap_launches0 = c->launches;
+  c->cap_fenced = c->fenced;
   c->cap_active = ++c->cap_next;
   return FMX_OK;
 }
@@ -1378,16 +1379,18 @@ int fmx_graph_capture_end(fmx_comm_t c, void* graph, int* handle) {
   if (!c || !c->hdr || (graph && !handle)) return fail(FMX_ERR_INVALID_ARG, "null argument");
   if (!c->cap_active) return fail(FMX_ERR_INVALID_ARG, "no capture is active");
   c->cap_active = 0;
+  c->fenced = c->cap_fenced;  // the captured calls did not run
+  if (!graph) {  // the capture failed: abandon it (nothing was enqueued that will run)
+    drop_pending(c);
+    for (int k = 0; k < kNumCounters; ++k) *c->counter(k) = c->cap_c0[k];
+    c->launches = c->cap_launches0;
+    return FMX_OK;
+  }
   if (c->pending) {  // a gather deferred inside the capture would never run
     drop_pending(c);
     for (int k = 0; k < kNumCounters; ++k) *c->counter(k) = c->cap_c0[k];
     c->launches = c->cap_launches0;
     return fail(FMX_ERR_INVALID_ARG, "the capture ended with a deferred gather: flush inside it");
-  }
-  if (!graph) {  // the capture failed: abandon it (nothing was enqueued that will run)
-    for (int k = 0; k < kNumCounters; ++k) *c->counter(k) = c->cap_c0[k];
-    c->launches = c->cap_launches0;
-    return FMX_OK;
   }
   CUgraph g = (CUgraph)graph;
   GraphRec rec;

@@ -143,6 +143,7 @@ struct fmx_comm {
   int ev_cap[fmx::kNumEvents] = {};
   int done_cap = 0;
   bool fenced = true;                    // no collective since the last fence / replay
+  bool cap_fenced = true;                // `fenced` when the capture began (nothing captured runs)
   cudaStream_t graph_stream = nullptr;   // stream of the last replay (ordering of the next call)
   cudaEvent_t graph_ev = nullptr;
   std::vector<fmx::GraphRec> graphs;

@@ -521,6 +521,9 @@ class ShmDataParallel(torch.nn.Module):
                 out = step_fn()
         except BaseException:
             self.comm.capture_end(0)       # abandon the capture (counters roll back)
+            self.comm.set_join_stream(None)
+            self.comm.set_defer(False)
+            self._armed = False
             raise
         handle = self.comm.capture_end(g.raw_cuda_graph())
         g.instantiate()
