@@ -99,8 +99,9 @@ def parse_args(argv=None):
     p.add_argument("--train-no-sync", action="store_true",
                    help="--train-only: also time the step without gradient sync (compute bound)")
     p.add_argument("--bucket-mb", type=float, default=None,
-                   help="bucket cap (MiB) of the DP legs; default 8 for the conv nets, 25 for "
-                        "BERT-base (graph engine: 2917-2958 seq/s at 25 vs 2284 at 8, r02/r3c-r3d)")
+                   help="bucket cap (MiB) of the DP legs; default 14 for ResNet-50 (graph "
+                        "engine 4027-4037 img/s vs 3947-3949 at 8, r02/r3n), 25 for BERT-base "
+                        "(2917-2958 seq/s vs 2284 at 8, r02/r3c-r3d), 8 otherwise")
     p.add_argument("--first-bucket-mb", type=float, default=1.0,
                    help="first bucket cap of the graph engine (DDP's first_bucket_bytes)")
     p.add_argument("--compress", choices=["bf16"], default=None,
@@ -907,7 +908,7 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
            "batch": args.batch, "train_steps": args.train_steps, "train_warmup": args.train_warmup,
            "port": 29000 + os.getpid() % 1000, "model": model, "no_sync": no_sync,
            "bucket_mb": args.bucket_mb if args.bucket_mb is not None else
-           (25.0 if model == "bert" else 8.0),
+           {"bert": 25.0, "resnet50": 14.0}.get(model, 8.0),
            "first_bucket_mb": args.first_bucket_mb,
            "stamps": bool(args.stamps) and not no_sync, "engine": engine,
            "compress": args.compress}
