@@ -837,6 +837,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   // local-only knobs (how this rank issues its copies; the protocol is unchanged)
   if (const char* v = getenv("FMX_COPY2D")) c->copy2d = atoi(v) != 0;
   if (const char* v = getenv("FMX_STAGE_AFTER_REDUCE")) c->stage_after_reduce = atoi(v) != 0;
+  if (const char* v = getenv("FMX_STAGE_ZC")) c->stage_zc = atoi(v) != 0;
   if (const char* v = getenv("FMX_COPY_FENCE")) c->copy_fence = atoi(v) != 0;
   if (const char* v = getenv("FMX_JOIN_LANES")) c->join_lanes = std::max(1, std::min(3, atoi(v)));
   if (const char* v = getenv("FMX_FUSE_SIGNAL")) c->fuse_signal = atoi(v) != 0;

@@ -381,6 +381,9 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
   // soon as their first contributors staged (a shorter pipeline fill)
   auto coarse_round = [&](uint32_t j) { return c->coarse && !(c->fine_first && j == 0); };
 
+  // FMX_STAGE_ZC=1 (local knob): the stage's D2H by the SM copy kernel even on
+  // the copy-engine transport, so the D2H direction carries SM stores only
+  const bool szc = zc || c->stage_zc;
   auto stage = [&](uint32_t j) -> int {
     const uint32_t R = R0 + j;
     if (ag) return FMX_OK;  // nothing to reduce: no contributions to stage
@@ -392,11 +395,11 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
         const size_t len = o == me ? 0 : g.len(o, j);
         if (!len) continue;
         const size_t off = c->in_off(R, o, me);
-        segs.push_back({src + g.lo(o, j) * g.esz, c->at(zc, off), len * g.esz,
+        segs.push_back({src + g.lo(o, j) * g.esz, c->at(szc, off), len * g.esz,
                         Annot{(int64_t)off, len * g.esz, me, R}, true,
                         ubuf(g.lo(o, j) * g.esz, len * g.esz)});
       }
-      return k.copy_signal(kLaneStage, segs, false, zc, kStaged, R + 1);
+      return k.copy_signal(kLaneStage, segs, false, szc, kStaged, R + 1);
     }
     for (int i = 0; i < n - 1; ++i) {
       const int o = rot(i);
@@ -404,10 +407,10 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
       segs.clear();
       if (len) {
         const size_t off = c->in_off(R, o, me);
-        segs.push_back({src + g.lo(o, j) * g.esz, c->at(zc, off), len * g.esz,
+        segs.push_back({src + g.lo(o, j) * g.esz, c->at(szc, off), len * g.esz,
                         Annot{(int64_t)off, len * g.esz, me, R}, true,
                         ubuf(g.lo(o, j) * g.esz, len * g.esz)});
-        if ((rc = k.copy(kLaneStage, segs, false, zc))) return rc;
+        if ((rc = k.copy(kLaneStage, segs, false, szc))) return rc;
       }
       if ((rc = k.signal(kLaneStage, kStagedTo + o, R + 1))) return rc;
     }

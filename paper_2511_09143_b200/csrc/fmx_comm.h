@@ -112,6 +112,7 @@ struct fmx_comm {
   // waits for this rank's reduce(R), so the reduction's result store does not
   // share the D2H direction with this rank's next stage
   bool stage_after_reduce = false;
+  bool stage_zc = false;       // FMX_STAGE_ZC=1 (local knob): stage by the SM copy kernel on CE
   int nlanes = 3;              // FMX_LANES=1: one stream; 2: gather on the reduce lane
   int join_lanes = 1;          // join-stream mode: 1 every lane on the join stream; 2 stage on
                                // its own stream; 3 stage and gather on their own (FMX_JOIN_LANES,
