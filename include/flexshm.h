@@ -27,6 +27,11 @@
  *   fmx_allgather       <- ncclAllGather (inference jobs, PAPER.md:485;
  *                          nccl.h:425)
  *   fmx_comm_destroy / fmx_comm_abort <- ncclCommDestroy / ncclCommAbort
+ *   fmx_comm_fence, fmx_comm_set_defer / fmx_comm_flush, fmx_graph_*
+ *                       <- no reference interface: what makes the collectives
+ *                          usable inside a CUDA-graph-captured DP step (NCCL's
+ *                          analog is capturing ncclAllReduce under
+ *                          cudaStreamBeginCapture); DESIGN.md §3.3-3.4
  *
  * Status codes map 1:1 to Python exceptions (paper_2511_09143_b200/_lib.py):
  * DUPLICATE_DEVICE -> DuplicateDeviceError(rank_a, rank_b) with the same
