@@ -910,7 +910,9 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
            "bucket_mb": args.bucket_mb if args.bucket_mb is not None else
            {"bert": 25.0, "resnet50": 14.0}.get(model, 8.0),
            "first_bucket_mb": args.first_bucket_mb,
-           "stamps": bool(args.stamps) and not no_sync, "engine": engine,
+           # (the default run's --stamps is for the allreduce; a training timeline
+           # is asked for with --train-only --stamps: stamp kernels slow the step)
+           "stamps": bool(args.stamps) and args.train_only and not no_sync, "engine": engine,
            "compress": args.compress}
     mine, gpu_local = list(range(n)), 0
     if world > 1:
