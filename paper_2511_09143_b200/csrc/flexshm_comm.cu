@@ -838,6 +838,19 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (const char* v = getenv("FMX_COPY2D")) c->copy2d = atoi(v) != 0;
   if (const char* v = getenv("FMX_STAGE_AFTER_REDUCE")) c->stage_after_reduce = atoi(v) != 0;
   if (const char* v = getenv("FMX_STAGE_ZC")) c->stage_zc = atoi(v) != 0;
+  // The next round's fetch on the gather lane pays off with few ranks per GPU,
+  // where each round's reduction stores as much as the fetch moves (two ranks:
+  // 1 GiB 53.6-54.5 vs 60.1-60.7 ms), not with seven (the extra stream per MPS
+  // client costs more: 290 vs 281 ms, r02/r3r).  Ranks on my GPU = peers with
+  // my bus id.
+  {
+    int same = 0;
+    for (const fmx_peer_info& p : c->peers)
+      if (strncmp(p.pcie_bus_id, c->peers[rank].pcie_bus_id, FMX_BUS_ID_LEN) == 0) ++same;
+    c->fetch_lane = same <= 2;
+  }
+  if (const char* v = getenv("FMX_FETCH_LANE")) c->fetch_lane = atoi(v) != 0;
+  if (const char* v = getenv("FMX_RCE_ROUNDS")) c->rce_rounds = std::max(1, atoi(v));
   if (const char* v = getenv("FMX_COPY_FENCE")) c->copy_fence = atoi(v) != 0;
   if (const char* v = getenv("FMX_JOIN_LANES")) c->join_lanes = std::max(1, std::min(3, atoi(v)));
   if (const char* v = getenv("FMX_FUSE_SIGNAL")) c->fuse_signal = atoi(v) != 0;

@@ -274,6 +274,9 @@ Geometry allreduce_geometry(const fmx_comm* c, size_t count, int dtype, size_t c
 // stream order (the schedule of the first B200 runs).
 enum { kEvSlotFree = 0, kEvGathered = FMX_MAX_SLOTS };  // + R % K: W(R) and G(R) above
 constexpr int kEvReduceDone = 2 * FMX_MAX_SLOTS + 7;   // stage_after_reduce: reduce(R) done
+// fetch lane (FMX_FETCH_LANE): F(R) fetch of round R landed in scratch slot R%2,
+// S(R) reduce(R) done reading it
+constexpr int kEvFetchedDev = 2 * FMX_MAX_SLOTS + 8, kEvScratchFree = kEvFetchedDev + 2;
 
 // The all-gather of one round: wait for the owners' REDUCED, record W(R), copy
 // their results out of the out-slots, record G(R).  Built per round; with
@@ -384,6 +387,48 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
   // FMX_STAGE_ZC=1 (local knob): the stage's D2H by the SM copy kernel even on
   // the copy-engine transport, so the D2H direction carries SM stores only
   const bool szc = zc || c->stage_zc;
+  // FMX_FETCH_LANE=1: the copy-engine fetch of round R+1 runs on the gather lane
+  // into the other half of a double-buffered scratch while lane 1 still reduces
+  // round R (with the fetch on lane 1, the fetch of R+1 queued behind reduce(R)
+  // and left the H2D direction idle for the reduction's duration: two ranks per
+  // GPU, r02/r3q).  Copy-engine transport, three lanes.
+  const bool fl = c->fetch_lane && !zc && !ag && LG != kLaneMain;
+  auto scratch_slot = [&](uint32_t R, int q) -> size_t {
+    return ((fl ? (size_t)(R % 2) * n : 0) + (size_t)q) * c->slice_bytes;
+  };
+  // fetch(j): every contributor's piece of my chunk into HBM scratch, each as
+  // soon as its contributor staged it (lane `L`)
+  auto fetch = [&](uint32_t j, int L) -> int {
+    const uint32_t R = R0 + j;
+    const size_t mylen = g.len(me, j);
+    if (fl && R >= 2 && (rc = k.wait_event(L, kEvScratchFree + R % 2))) return rc;  // S(R-2)
+    if (coarse_round(j)) {
+      if ((rc = k.wait_peers(L, kStaged, R + 1, me))) return rc;
+      segs.clear();
+      for (int q = 0; q < n && mylen; ++q) {
+        if (q == me) continue;
+        const size_t off = c->in_off(R, me, q);
+        segs.push_back({c->at(false, off), c->scratch + scratch_slot(R, q), mylen * g.esz,
+                        Annot{(int64_t)off, mylen * g.esz, q, R}, false,
+                        sbuf(scratch_slot(R, q), mylen * g.esz)});
+      }
+      if ((rc = k.copy(L, segs, true, false))) return rc;
+    } else {
+      for (int i = 0; i < n - 1; ++i) {
+        const int q = rot(i);
+        if ((rc = k.wait_rank(L, q, kStagedTo + me, R + 1))) return rc;
+        if (!mylen) continue;
+        const size_t off = c->in_off(R, me, q);
+        segs.clear();
+        segs.push_back({c->at(false, off), c->scratch + scratch_slot(R, q), mylen * g.esz,
+                        Annot{(int64_t)off, mylen * g.esz, q, R}, false,
+                        sbuf(scratch_slot(R, q), mylen * g.esz)});
+        if ((rc = k.copy(L, segs, true, false))) return rc;
+      }
+    }
+    if (fl && (rc = k.record(L, kEvFetchedDev + R % 2))) return rc;  // F(R)
+    return FMX_OK;
+  };
   auto stage = [&](uint32_t j) -> int {
     const uint32_t R = R0 + j;
     if (ag) return FMX_OK;  // nothing to reduce: no contributions to stage
@@ -427,9 +472,11 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
   for (uint32_t j = 0; j < ahead && j < g.rounds; ++j)
     if ((rc = stage(j))) return rc;
   if ((rc = plan_flush(c, k))) return rc;
+  if (fl && (rc = fetch(0, LG))) return rc;
   for (uint32_t j = 0; j < g.rounds; ++j) {
     const uint32_t R = R0 + j;
     if (!sar && j + ahead < g.rounds && (rc = stage(j + ahead))) return rc;
+    if (fl && j + 1 < g.rounds && (rc = fetch(j + 1, LG))) return rc;
     // lane 1: fetch, then reduce-scatter my chunk in ascending rank order
     const size_t mylen = g.len(me, j);
     if (mylen && ag) {
@@ -460,37 +507,27 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
       a.out_dev = my_out(j);
       const size_t out_off = c->out_off(R, me);
       pr.user_rw = ubuf(g.lo(me, j) * g.esz, mylen * g.esz);
-      const bool via_ce = ar && !zc && c->result_via_ce;
+      // result slot by the copy engine: FMX_RESULT_VIA_CE, or with the fetch lane on
+      // long pipelines (two ranks per GPU, >= rce_rounds rounds: the SM result store
+      // starves under the copy engines' D2H, a copy-engine write does not - 1 GiB
+      // 48.2-49.4 vs 53.7-54.5 ms; at 2 rounds the extra copy costs more, r02/r3t).
+      // A local choice: peers only see REDUCED.
+      const bool via_ce = ar && !zc && (c->result_via_ce || (fl && g.rounds >= (uint32_t)c->rce_rounds));
       if (ar && !via_ce) {
         a.out_sys = c->at(true, out_off);
         pr.write = Annot{(int64_t)out_off, mylen * g.esz, me, R};
       }
       // each contribution is fetched as soon as its contributor staged it
-      if (coarse_round(j)) {
+      // (fetch lane: already enqueued on lane LG; wait for it here)
+      if (fl) {
+        if ((rc = k.wait_event(kLaneMain, kEvFetchedDev + R % 2))) return rc;  // F(R)
+      } else if (!zc) {
+        if ((rc = fetch(j, kLaneMain))) return rc;
+      } else if (coarse_round(j)) {   // zero-copy: the reduction reads the slots itself
         if ((rc = k.wait_peers(kLaneMain, kStaged, R + 1, me))) return rc;
-        if (!zc) {
-          segs.clear();
-          for (int q = 0; q < n; ++q) {
-            if (q == me) continue;
-            const size_t off = c->in_off(R, me, q);
-            segs.push_back({c->at(false, off), c->scratch + (size_t)q * c->slice_bytes,
-                            mylen * g.esz, Annot{(int64_t)off, mylen * g.esz, q, R}, false,
-                            sbuf((size_t)q * c->slice_bytes, mylen * g.esz)});
-          }
-          if ((rc = k.copy(kLaneMain, segs, true, false))) return rc;
-        }
-      }
-      for (int i = 0; i < n - 1 && !coarse_round(j); ++i) {
-        const int q = rot(i);
-        if ((rc = k.wait_rank(kLaneMain, q, kStagedTo + me, R + 1))) return rc;
-        if (!zc) {
-          const size_t off = c->in_off(R, me, q);
-          segs.clear();
-          segs.push_back({c->at(false, off), c->scratch + (size_t)q * c->slice_bytes,
-                          mylen * g.esz, Annot{(int64_t)off, mylen * g.esz, q, R}, false,
-                          sbuf((size_t)q * c->slice_bytes, mylen * g.esz)});
-          if ((rc = k.copy(kLaneMain, segs, true, false))) return rc;
-        }
+      } else {
+        for (int i = 0; i < n - 1; ++i)
+          if ((rc = k.wait_rank(kLaneMain, rot(i), kStagedTo + me, R + 1))) return rc;
       }
       for (int q = 0; q < n; ++q) {
         if (q == me) {
@@ -501,14 +538,15 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
           a.sys_mask |= 1ull << q;
           pr.reads.push_back(Annot{(int64_t)off, mylen * g.esz, q, R});
         } else {
-          a.src[q] = c->scratch + (size_t)q * c->slice_bytes;
-          pr.scratch_reads.push_back(sbuf((size_t)q * c->slice_bytes, mylen * g.esz));
+          a.src[q] = c->scratch + scratch_slot(R, q);
+          pr.scratch_reads.push_back(sbuf(scratch_slot(R, q), mylen * g.esz));
         }
       }
       // out[R%K][me] is free once every peer gathered round R-K: W(R-K+1)
       if (split && R + 1 >= (uint32_t)K && (rc = k.wait_event(kLaneMain, kEvSlotFree + (R + 1 - K) % K)))
         return rc;
       if ((rc = k.reduce(kLaneMain, pr))) return rc;
+      if (fl && (rc = k.record(kLaneMain, kEvScratchFree + R % 2))) return rc;  // S(R)
       if (sar && j + ahead < g.rounds && (rc = k.record(kLaneMain, kEvReduceDone))) return rc;
       if (via_ce) {  // result slot written by the copy engine from HBM
         segs.clear();
@@ -776,6 +814,8 @@ int fmx_trace_plan(int nranks, int rank, int transport, size_t slice_bytes, int 
   // FMX_TRACE_DEFER=1: fmx_comm_set_defer (an allreduce's last gather deferred)
   c.defer_gather = getenv("FMX_TRACE_DEFER") && atoi(getenv("FMX_TRACE_DEFER"));
   c.stage_after_reduce = getenv("FMX_STAGE_AFTER_REDUCE") && atoi(getenv("FMX_STAGE_AFTER_REDUCE"));
+  if (const char* v = getenv("FMX_FETCH_LANE")) c.fetch_lane = atoi(v) != 0;
+  if (const char* v = getenv("FMX_RCE_ROUNDS")) c.rce_rounds = std::max(1, atoi(v));
   c.slice_bytes = slice_bytes;
   size_t max_bytes = 0;
   for (int i = 0; i < nops; ++i) max_bytes = std::max(max_bytes, counts[i] * (dtypes[i] ? 2 : 4));

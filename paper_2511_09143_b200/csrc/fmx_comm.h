@@ -14,8 +14,9 @@
 #include "fmx_internal.h"
 
 namespace fmx {
-constexpr int kNumEvents = 2 * FMX_MAX_SLOTS + 8;  // W[K], G[K]; host path F[2], C[2], inputs,
-                                                   // P[2]; reduce done (stage_after_reduce)
+constexpr int kNumEvents = 2 * FMX_MAX_SLOTS + 12;  // W[K], G[K]; host path F[2], C[2],
+                                                    // inputs, P[2]; reduce done (stage after
+                                                    // reduce); fetch lane F[2], S[2]
 
 // Round counters a flag's values follow (fmx_graph_*: baked flag values of a
 // captured graph are re-based per replay by their counter's advance).
@@ -113,6 +114,10 @@ struct fmx_comm {
   // share the D2H direction with this rank's next stage
   bool stage_after_reduce = false;
   bool stage_zc = false;       // FMX_STAGE_ZC=1 (local knob): stage by the SM copy kernel on CE
+  bool fetch_lane = false;     // FMX_FETCH_LANE=1 (local knob): fetch on the gather lane into a
+                               // double-buffered scratch (plan_allreduce)
+  int rce_rounds = 8;          // with the fetch lane: result slot by copy engine from this many
+                               // rounds (FMX_RCE_ROUNDS, local knob)
   int nlanes = 3;              // FMX_LANES=1: one stream; 2: gather on the reduce lane
   int join_lanes = 1;          // join-stream mode: 1 every lane on the join stream; 2 stage on
                                // its own stream; 3 stage and gather on their own (FMX_JOIN_LANES,

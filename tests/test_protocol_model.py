@@ -671,3 +671,55 @@ def test_stage_after_reduce(monkeypatch, n, lanes, slots, transport):
     progs = programs(n, DEFER_SEQUENCES["buckets"], 4096, transport)
     for seed in range(4):
         simulate(progs, seed, burst=4)
+
+
+@pytest.mark.parametrize("n", [2, 3, 7])
+@pytest.mark.parametrize("slots,transport,grain", [("2", "ce", "coarse"), ("3", "ce", "coarse"),
+                                                   ("2", "ce", "fine"), ("4", "auto", "coarse"),
+                                                   ("2", "zc", "coarse")])
+def test_fetch_lane(monkeypatch, n, slots, transport, grain):
+    """FMX_FETCH_LANE: the fetch of round R+1 on the gather lane into a
+    double-buffered HBM scratch while lane 1 reduces round R - race-free on
+    the scratch (S(R-2) before fetch(R)), deadlock-free on the lanes and as
+    one FIFO, across calls in join-stream / deferred-gather mode."""
+    monkeypatch.setenv("FMX_FETCH_LANE", "1")
+    monkeypatch.setenv("FMX_RCE_ROUNDS", "3")      # result slot by copy engine on long pipelines
+    monkeypatch.setenv("FMX_SLOTS", slots)
+    monkeypatch.setenv("FMX_GRAIN", grain)
+    monkeypatch.setenv("FMX_ZC_MAX", "100000")
+    seq = SEQUENCES["mixed"] + [("allreduce", 200_003, 0), ("reduce_scatter", 40_000, 1),
+                                ("allreduce", 77_777, 1)]
+    progs = programs(n, seq, 4096, transport)
+    for seed in range(6):
+        simulate(progs, seed)
+    merged = programs(n, seq, 4096, transport, merged=True)
+    for seed in range(4):
+        simulate(merged, seed)
+    monkeypatch.setenv("FMX_TRACE_OVERLAP", "1")
+    monkeypatch.setenv("FMX_TRACE_DEFER", "1")
+    progs = programs(n, DEFER_SEQUENCES["mixed"], 4096, transport)
+    for seed in range(4):
+        simulate(progs, seed, burst=4)
+
+
+def test_fetch_lane_needs_the_scratch_wait(monkeypatch):
+    """Drop lane 2's waits on S (reduce(R-2) done reading scratch slot R%2)
+    and the checker must see fetch(R) overwrite scratch a reduction still
+    reads.  (With K = 2 slots the wait is implied - peers stage R only after
+    seeing my REDUCED(R-2) - so the check runs at K = 3.)"""
+    monkeypatch.setenv("FMX_FETCH_LANE", "1")
+    monkeypatch.setenv("FMX_SLOTS", "3")
+    ops = [("allreduce", 3 * 8 * 1024, 0)]        # 8 rounds of 1 KiB pieces at n=3
+    progs = programs(3, ops, 4096, "ce")
+    lanes = progs[1]
+    s_events = {2 * 4 + 10, 2 * 4 + 11}            # kEvScratchFree + 0/1 (FMX_MAX_SLOTS = 4)
+    broken2 = [op for op in lanes[2] if not (op[0] == "X" and op[1] in s_events)]
+    assert broken2 != lanes[2]
+    broken = [[lanes[0], lanes[1], broken2] if r == 1 else p for r, p in enumerate(progs)]
+    failures = 0
+    for seed in range(80):
+        try:
+            simulate(broken, seed, burst=4)
+        except AssertionError:
+            failures += 1
+    assert failures > 0
