@@ -723,3 +723,23 @@ def test_fetch_lane_needs_the_scratch_wait(monkeypatch):
         except AssertionError:
             failures += 1
     assert failures > 0
+
+
+@pytest.mark.parametrize("n,ops,slots", [
+    # C1: the ResNet-50 gradient over two ranks of one GPU (16 MiB slices, K = 4)
+    (2, [("allreduce", 25_557_032, 0), ("allreduce", 268_435_456, 0)], "4"),
+    # C3: MobileNetV2 over 4 ranks, two per GPU
+    (4, [("allreduce", 3_504_872, 0), ("broadcast", 3_504_872, 0, 3)], "2"),
+])
+def test_two_ranks_per_gpu_defaults_at_config_shapes(monkeypatch, n, ops, slots):
+    """The <= 2-ranks-per-GPU defaults (fetch lane, copy-engine result from 8
+    rounds) at the BASELINE configs' own shapes and default slice geometry."""
+    monkeypatch.setenv("FMX_FETCH_LANE", "1")
+    monkeypatch.setenv("FMX_RCE_ROUNDS", "8")
+    monkeypatch.setenv("FMX_SLOTS", slots)
+    sb = (16 << 20) if n <= 2 else default_slice(n)
+    progs = programs(n, ops, sb, "auto")
+    for seed in range(2):
+        simulate(progs, seed, burst=8)
+    merged = programs(n, ops, sb, "auto", merged=True)
+    simulate(merged, 0)
