@@ -168,3 +168,37 @@ def test_multiprocess_bootstrap_refuses_cross_host_peers():
         status, msg = out[r]
         assert status == "net", out[r]
         assert "rank 2" in msg and "NET" in msg
+
+
+def test_graph_and_defer_api_argument_checks():
+    """The fence / defer / graph entry points on a single-rank host-transport
+    communicator (no CUDA): a host-only communicator has no device path, so
+    capture, fence and flush are refused with a clear error; capture_end and
+    launch_prepare validate their state and handles."""
+    import ctypes
+
+    from paper_2511_09143_b200 import _lib
+    from paper_2511_09143_b200.comm import init_process_group
+    from paper_2511_09143_b200.commsim import PeerInfo
+    from paper_2511_09143_b200.errors import FlexShmError
+
+    key = f"cpu-{uuid.uuid4().hex[:10]}"
+    comm = init_process_group(None, 0, key, peer=PeerInfo(0, "00:C0:00.0", "MIG-x", 7, 100),
+                              nranks=1, transport="host", timeout_s=30)
+    L = _lib.lib()
+    try:
+        with pytest.raises(FlexShmError):          # host-only: no device path
+            comm.capture_begin()
+        with pytest.raises(FlexShmError):
+            comm.fence(stream=0)
+        with pytest.raises(ValueError):            # no capture is active
+            comm.capture_end(0)
+        with pytest.raises(FlexShmError):          # host-only, before the handle check
+            _lib.check(L.fmx_graph_launch_prepare(comm._h, 3, ctypes.c_void_p(1), None))
+        with pytest.raises(ValueError):            # bad handle
+            _lib.check(L.fmx_graph_release(comm._h, 0))
+        comm.set_defer(True)                       # no pending gather: toggles freely
+        comm.set_defer(False)
+        assert L.fmx_comm_flush(None, None) == _lib.FMX_ERR_INVALID_ARG
+    finally:
+        comm.destroy()
