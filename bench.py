@@ -96,6 +96,10 @@ def parse_args(argv=None):
     p.add_argument("--train-engine", choices=["auto", "graph", "ddp"], default="auto",
                    help="graph: ddp.ShmDataParallel, whole step captured as one CUDA graph; "
                         "ddp: torch DDP + flexshm_hook, eager; auto (default): graph")
+    p.add_argument("--fused-sgd", action="store_true",
+                   help="graph engine, conv nets: the SGD step fused into the collective "
+                        "(ShmDataParallel fused_sgd / fmx_allreduce_sgd) instead of torch's "
+                        "optimizer after it")
     p.add_argument("--train-no-sync", action="store_true",
                    help="--train-only: also time the step without gradient sync (compute bound)")
     p.add_argument("--bucket-mb", type=float, default=None,
@@ -706,13 +710,16 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
             fddp.broadcast_parameters(model, comm)   # same start, no exchange in the step
             net = model
         else:
+            fused = dict(lr=0.01, momentum=0.9) if cfg.get("fused_sgd") else None
             net = fddp.ShmDataParallel(model, comm, bucket_cap_mb=cfg.get("bucket_mb", 8.0),
                                        first_bucket_mb=cfg.get("first_bucket_mb", 1.0),
-                                       compress=cfg.get("compress"))
+                                       compress=cfg.get("compress"), fused_sgd=fused)
         if name == "bert":
             # in a graph: the fused multi-tensor AdamW (capturable), one kernel per step
             opt = torch.optim.AdamW(net.parameters(), lr=2e-5, capturable=graph,
                                     fused=True if graph else None)
+        elif cfg.get("fused_sgd") and graph and not cfg.get("no_sync"):
+            opt = None   # the same SGD step runs inside the collective (fmx_allreduce_sgd)
         else:
             opt = torch.optim.SGD(net.parameters(), lr=0.01, momentum=0.9)
 
@@ -739,7 +746,8 @@ def train_body(rank: int, job_key: str, n: int, cfg: dict, inst_mode: str, gpu_l
         t1 = time.perf_counter()
         loss.backward()
         t2 = time.perf_counter()
-        opt.step()
+        if opt is not None:
+            opt.step()
         t3 = time.perf_counter()
         host_phase["fwd"] += t1 - t0
         host_phase["bwd"] += t2 - t1
@@ -913,7 +921,7 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
            # (the default run's --stamps is for the allreduce; a training timeline
            # is asked for with --train-only --stamps: stamp kernels slow the step)
            "stamps": bool(args.stamps) and args.train_only and not no_sync, "engine": engine,
-           "compress": args.compress}
+           "compress": args.compress, "fused_sgd": args.fused_sgd}
     mine, gpu_local = list(range(n)), 0
     if world > 1:
         import torch.distributed as dist
@@ -976,6 +984,10 @@ def run_train(args, d, job_key, model: str = "resnet50", no_sync: bool = False) 
                             "ranks; loss.item() syncs once per step only in the last one) and "
                             "the part spent inside flexshm_hook's collective calls"},
            "gpu_launches": launches, "model": desc, "bucket_mb": cfg["bucket_mb"],
+           "optimizer": ("AdamW" if model == "bert" else
+                         "SGD(momentum 0.9) fused into the allreduce (fmx_allreduce_sgd)"
+                         if args.fused_sgd and engine == "graph" and not no_sync else
+                         "torch.optim.SGD(momentum 0.9) after the exchange"),
            "engine": ("ddp.ShmDataParallel: whole step (fwd, bwd with bucket allreduces, "
                       "optimizer) replayed as one CUDA graph" if engine == "graph" else
                       "torch DDP + ddp.flexshm_hook, eager")}

@@ -170,6 +170,26 @@ int fmx_comm_init(fmx_comm_t* comm, const char* job_key, int nranks, int rank,
 int fmx_allreduce(fmx_comm_t comm, const void* send, void* recv, size_t count, int dtype,
                   int op, float factor, void* stream);
 
+/* Fused optimizer step (fp32): allreduce of `grad` (op SUM or PREMUL_SUM, as
+ * fmx_allreduce) in which each OWNER applies torch's SGD step (torch/optim/
+ * sgd.py _multi_tensor_sgd: weight decay, momentum with dampening, Nesterov)
+ * to its chunk of `param` with the reduced gradient, and the all-gather then
+ * distributes the updated parameters into every rank's `param` - the
+ * optimizer fused into the collective's reduction, each element stepped once
+ * instead of on every rank (ZeRO-1 style: `momentum` holds only this rank's
+ * shard, fmx_allreduce_shard's len elements, fp32, 16-byte aligned).  `grad`
+ * is left as it was.  Bit-identical to every rank running torch's SGD on the
+ * averaged gradient (tests/test_graph_dp_gpu.py). */
+typedef struct fmx_sgd {
+  float lr, momentum, dampening, weight_decay;
+  int nesterov;
+  int first_step; /* 1: the momentum shard is initialised to the gradient (torch's first step) */
+} fmx_sgd;
+int fmx_allreduce_sgd(fmx_comm_t comm, const void* grad, void* param, void* momentum, size_t count,
+                      int op, float factor, const fmx_sgd* sgd, void* stream);
+/* This rank's owner chunk of an allreduce of `count` elements: [*offset, *offset + *len). */
+int fmx_allreduce_shard(fmx_comm_t comm, size_t count, int dtype, size_t* offset, size_t* len);
+
 /* Root's send buffer -> every rank's recv buffer (bit copy). */
 int fmx_broadcast(fmx_comm_t comm, const void* send, void* recv, size_t count, int dtype,
                   int root, void* stream);

@@ -46,7 +46,7 @@ MAX_RANKS = 64
 # Every symbol include/flexshm.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "fmx_check_peer", "fmx_validate_peers", "fmx_topology", "fmx_restore_bus_id",
-    "fmx_comm_init", "fmx_allreduce", "fmx_broadcast", "fmx_reduce_scatter", "fmx_allgather",
+    "fmx_comm_init", "fmx_allreduce", "fmx_allreduce_sgd", "fmx_allreduce_shard", "fmx_broadcast", "fmx_reduce_scatter", "fmx_allgather",
     "fmx_host_buffer", "fmx_allreduce_host",
     "fmx_reduce_local", "fmx_barrier", "fmx_comm_destroy",
     "fmx_comm_abort", "fmx_comm_rank", "fmx_comm_count", "fmx_comm_peer", "fmx_comm_config",
@@ -58,6 +58,13 @@ EXPORTS = (
     "fmx_trace_plan", "fmx_last_error", "fmx_dup_ranks",
     "fmx_abi_version",
 )
+
+
+class SgdC(ctypes.Structure):
+    """struct fmx_sgd (include/flexshm.h)."""
+    _fields_ = [("lr", ctypes.c_float), ("momentum", ctypes.c_float),
+                ("dampening", ctypes.c_float), ("weight_decay", ctypes.c_float),
+                ("nesterov", ctypes.c_int), ("first_step", ctypes.c_int)]
 
 
 class PeerInfoC(ctypes.Structure):
@@ -112,6 +119,9 @@ def lib() -> ctypes.CDLL:
         "fmx_reduce_local": [P(c_void), c_int, ctypes.c_uint64, c_void, c_void, c_size, c_int,
                              c_int, c_float, c_void],
         "fmx_allreduce": [c_void, c_void, c_void, c_size, c_int, c_int, c_float, c_void],
+        "fmx_allreduce_sgd": [c_void, c_void, c_void, c_void, c_size, c_int, c_float, P(SgdC),
+                              c_void],
+        "fmx_allreduce_shard": [c_void, c_size, c_int, P(c_size), P(c_size)],
         "fmx_broadcast": [c_void, c_void, c_void, c_size, c_int, c_int, c_void],
         "fmx_reduce_scatter": [c_void, c_void, c_void, c_size, c_int, c_int, c_float, c_void],
         "fmx_allgather": [c_void, c_void, c_void, c_size, c_int, c_void],

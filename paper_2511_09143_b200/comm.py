@@ -149,6 +149,37 @@ class ShmCommunicator:
         _lib.check(rc, "fmx_allreduce")
         return dst
 
+    def shard(self, count: int, dtype=None) -> tuple[int, int]:
+        """(offset, len) of this rank's owner chunk of an allreduce of `count`
+        elements (fmx_allreduce_shard)."""
+        import torch
+        code = _dtype_code(torch.empty(0, dtype=dtype or torch.float32))
+        off, ln = ctypes.c_size_t(), ctypes.c_size_t()
+        _lib.check(_lib.lib().fmx_allreduce_shard(self._h, int(count), code, ctypes.byref(off),
+                                                  ctypes.byref(ln)), "fmx_allreduce_shard")
+        return off.value, ln.value
+
+    def allreduce_sgd(self, grad, param, momentum, lr: float, momentum_coef: float = 0.0,
+                      dampening: float = 0.0, weight_decay: float = 0.0, nesterov: bool = False,
+                      first_step: bool = False, op: str = "avg", stream=None):
+        """Fused optimizer step (fmx_allreduce_sgd): `param` <- torch's SGD step
+        with the `op`-reduced `grad`, computed once by each chunk's owner and
+        all-gathered.  `momentum`: this rank's shard (self.shard(numel)), fp32."""
+        self._alive()
+        _check_tensor(grad, "grad")
+        _check_tensor(param, "param")
+        if grad.dtype != param.dtype or grad.numel() != param.numel():
+            raise ValueError("grad and param must match in dtype and size")
+        op, factor = resolve_op(op, None, self.size)
+        sgd = _lib.SgdC(lr, momentum_coef, dampening, weight_decay, int(bool(nesterov)),
+                        int(bool(first_step)))
+        mom = momentum.data_ptr() if momentum is not None else None
+        rc = _lib.lib().fmx_allreduce_sgd(self._h, grad.data_ptr(), param.data_ptr(), mom,
+                                          grad.numel(), OPS[op], ctypes.c_float(factor),
+                                          ctypes.byref(sgd), self._stream(stream))
+        _lib.check(rc, "fmx_allreduce_sgd")
+        return param
+
     def broadcast(self, tensor, root: int = 0, stream=None):
         self._alive()
         _check_tensor(tensor, "tensor")

@@ -938,6 +938,69 @@ int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int 
   });
 }
 
+int fmx_allreduce_shard(fmx_comm_t c, size_t count, int dtype, size_t* offset, size_t* len) {
+  if (!c || !offset || !len) return fail(FMX_ERR_INVALID_ARG, "null argument");
+  if (dtype != FMX_FLOAT32 && dtype != FMX_BFLOAT16)
+    return fail(FMX_ERR_INVALID_ARG, "bad dtype %d", dtype);
+  if (c->nranks == 1 || count == 0) {
+    *offset = 0;
+    *len = count;
+    return FMX_OK;
+  }
+  const Geometry g = allreduce_geometry(c, count, dtype);
+  const size_t lo = std::min(count, (size_t)c->rank * g.chunk);
+  *offset = lo;
+  *len = std::min(g.chunk, count - lo);
+  return FMX_OK;
+}
+
+int fmx_allreduce_sgd(fmx_comm_t c, const void* grad, void* param, void* momentum, size_t count,
+                      int op, float factor, const fmx_sgd* sgd, void* stream) {
+  int rc = check_comm(c);
+  if (rc) return rc;
+  if (!sgd || !grad || !param) return fail(FMX_ERR_INVALID_ARG, "null argument");
+  if (op != FMX_OP_SUM && op != FMX_OP_PREMUL_SUM)
+    return fail(FMX_ERR_INVALID_ARG, "fused SGD takes op SUM or PREMUL_SUM");
+  if (op != FMX_OP_SUM && !std::isfinite(factor)) return fail(FMX_ERR_INVALID_ARG, "factor must be finite");
+  if (grad == param) return fail(FMX_ERR_INVALID_ARG, "gradient and parameter buffers must differ");
+  if (sgd->momentum != 0.f && !momentum) return fail(FMX_ERR_INVALID_ARG, "momentum buffer required");
+  if (count == 0) return FMX_OK;
+  SgdEpi e{(char*)(sgd->momentum != 0.f ? momentum : nullptr), sgd->lr, sgd->momentum,
+           sgd->dampening, sgd->weight_decay, sgd->nesterov, sgd->first_step};
+  const bool aligned = (((uintptr_t)grad | (uintptr_t)param | (uintptr_t)e.mom) & 15) == 0;
+  CudaSink sink(c);
+  if (c->nranks == 1) {  // my shard is the whole buffer: the step alone
+    return on_lanes(c, (cudaStream_t)stream, 0, [&]() -> int {
+      PlanReduce pr;
+      memset(&pr.args, 0, sizeof pr.args);
+      pr.args.src[0] = (const char*)grad;
+      pr.args.nsrc = 1;
+      pr.args.out_dev = (char*)param;
+      pr.args.len = count;
+      pr.args.op = op;
+      pr.args.factor = factor;
+      pr.args.sgd = 1;
+      pr.args.mom = e.mom;
+      pr.args.lr = e.lr;
+      pr.args.mu = e.mu;
+      pr.args.damp = e.damp;
+      pr.args.wd = e.wd;
+      pr.args.nesterov = e.nesterov;
+      pr.args.init = e.init;
+      pr.dtype = FMX_FLOAT32;
+      pr.aligned = aligned;
+      return sink.reduce(kLaneMain, pr);
+    });
+  }
+  c->sgd = &e;  // the pipelined schedule (never the one-shot: the step runs on owners)
+  rc = on_lanes(c, (cudaStream_t)stream, 0, [&]() {
+    return plan_allreduce(c, sink, (const char*)grad, (char*)param, count, FMX_FLOAT32, op,
+                          factor, aligned);
+  });
+  c->sgd = nullptr;
+  return rc;
+}
+
 // Shared argument checks of the dtype / op / factor triple.
 static int check_reduction_args(int dtype, int op, float factor) {
   if (dtype != FMX_FLOAT32 && dtype != FMX_BFLOAT16)

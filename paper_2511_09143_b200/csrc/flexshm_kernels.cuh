@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "../../include/flexshm.h"
 #include "fmx_args.h"
 
@@ -242,8 +244,23 @@ __device__ __forceinline__ void reduce_vec(const ReduceArgs& a, size_t off, floa
   for (int k = 0; k < V; ++k) acc[k] = scale_out<OP>(acc[k], a.factor);
 }
 
+// The fused SGD step of one element (ReduceArgs::sgd): torch's multi-tensor SGD
+// (torch/optim/sgd.py _multi_tensor_sgd) op by op - _foreach_add with alpha is
+// `a + alpha * b` contracted to one FMA, _foreach_mul one rounded product - so
+// the owner's update is bit-identical to every rank updating its replica.
+// `p` is the old parameter; returns the new one and updates *m.
+__device__ __forceinline__ float sgd_step(const ReduceArgs& a, float g, float p, float* m) {
+  if (a.wd != 0.f) g = __fmaf_rn(a.wd, p, g);
+  float d = g;
+  if (a.mu != 0.f) {
+    *m = a.init ? g : __fmaf_rn(1.f - a.damp, g, __fmul_rn(*m, a.mu));
+    d = a.nesterov ? __fmaf_rn(a.mu, *m, g) : *m;
+  }
+  return __fmaf_rn(-a.lr, d, p);
+}
+
 // One element (tails and the unaligned path).
-template <typename T, int OP>
+template <typename T, int OP, bool SGD = false>
 __device__ __forceinline__ void reduce_elem(const ReduceArgs& a, size_t e) {
   using E = Elem<T>;
   const size_t esz = sizeof(T);
@@ -253,12 +270,17 @@ __device__ __forceinline__ void reduce_elem(const ReduceArgs& a, size_t e) {
     acc = q == 0 ? c : __fadd_rn(acc, c);
   }
   acc = scale_out<OP>(acc, a.factor);
+  if constexpr (SGD) {
+    float m = a.mom ? ((const float*)a.mom)[e] : 0.f;
+    acc = sgd_step(a, acc, E::load1(a.out_dev + e * esz), &m);
+    if (a.mom) ((float*)a.mom)[e] = m;
+  }
   E::store1(a.out_dev + e * esz, acc);
   for (int k = 1; k < a.n_rep; ++k) E::store1(a.out_dev + k * a.rep_stride + e * esz, acc);
   if (a.out_sys) E::store1(a.out_sys + e * esz, acc);
 }
 
-template <typename T, int U, int OP>
+template <typename T, int U, int OP, bool SGD = false>
 __global__ void __launch_bounds__(256, 2) fmx_reduce_kernel(const __grid_constant__ ReduceArgs a) {
   using E = Elem<T>;
   constexpr int V = E::kVec;
@@ -271,6 +293,19 @@ __global__ void __launch_bounds__(256, 2) fmx_reduce_kernel(const __grid_constan
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (i + u * stride < nvec) reduce_vec<T, OP>(a, (i + u * stride) * 16, acc[u]);
+    if constexpr (SGD) {   // fp32 only: V = 4 parameters and momenta per vector
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i + u * stride >= nvec) continue;
+        const size_t off = (i + u * stride) * 16;
+        float p[V], m[V] = {};
+        E::widen(ld_v4(a.out_dev + off), p);
+        if (a.mom) E::widen(ld_v4(a.mom + off), m);
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[u][k] = sgd_step(a, acc[u][k], p[k], &m[k]);
+        if (a.mom) st_v4(a.mom + off, E::narrow(m));
+      }
+    }
     uint4 o[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -288,23 +323,23 @@ __global__ void __launch_bounds__(256, 2) fmx_reduce_kernel(const __grid_constan
     }
   }
   // element tail (len not a multiple of the vector width)
-  for (size_t e = nvec * V + tid; e < a.len; e += stride) reduce_elem<T, OP>(a, e);
+  for (size_t e = nvec * V + tid; e < a.len; e += stride) reduce_elem<T, OP, SGD>(a, e);
 }
 
 // Unaligned fallback: one element per thread iteration.
-template <typename T, int OP>
+template <typename T, int OP, bool SGD = false>
 __global__ void __launch_bounds__(256) fmx_reduce_scalar_kernel(const __grid_constant__ ReduceArgs a) {
   if (a.wait_flags) wait_flags_cta(a.wait_flags, a.wait_stride, a.nsrc, a.wait_skip, a.wait_value);
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.len; e += stride)
-    reduce_elem<T, OP>(a, e);
+    reduce_elem<T, OP, SGD>(a, e);
 }
 
 // Host-side dispatch over (dtype, op, alignment): grid capped at 8 x 148 CTAs
 // of 256 threads, 2 vectors per thread in flight.
 constexpr int kReduceThreads = 256, kReduceU = 2, kReduceGridCap = 1184;
 
-template <typename T, int OP>
+template <typename T, int OP, bool SGD = false>
 inline void launch_reduce_t(const ReduceArgs& a, bool aligned, cudaStream_t s, int cap) {
   constexpr int V = Elem<T>::kVec;
   auto grid = [cap](size_t items) {
@@ -312,14 +347,20 @@ inline void launch_reduce_t(const ReduceArgs& a, bool aligned, cudaStream_t s, i
     return (int)(g < 1 ? 1 : g > (size_t)cap ? cap : g);
   };
   if (aligned)
-    fmx_reduce_kernel<T, kReduceU, OP>
+    fmx_reduce_kernel<T, kReduceU, OP, SGD>
         <<<grid((a.len / V + kReduceU - 1) / kReduceU + 1), kReduceThreads, 0, s>>>(a);
   else
-    fmx_reduce_scalar_kernel<T, OP><<<grid(a.len), kReduceThreads, 0, s>>>(a);
+    fmx_reduce_scalar_kernel<T, OP, SGD><<<grid(a.len), kReduceThreads, 0, s>>>(a);
 }
 
 template <typename T>
 inline void launch_reduce_op(const ReduceArgs& a, bool aligned, cudaStream_t s, int cap) {
+  if constexpr (std::is_same<T, float>::value) {
+    if (a.sgd) {   // fused SGD step: DDP's mean (PREMUL) or a plain sum
+      if (a.op == FMX_OP_PREMUL_SUM) return launch_reduce_t<T, FMX_OP_PREMUL_SUM, true>(a, aligned, s, cap);
+      return launch_reduce_t<T, FMX_OP_SUM, true>(a, aligned, s, cap);
+    }
+  }
   switch (a.op) {
     case FMX_OP_SUM_POSTSCALE: return launch_reduce_t<T, FMX_OP_SUM_POSTSCALE>(a, aligned, s, cap);
     case FMX_OP_PREDIV_SUM: return launch_reduce_t<T, FMX_OP_PREDIV_SUM>(a, aligned, s, cap);

@@ -505,6 +505,17 @@ int plan_allreduce(fmx_comm* c, Sink& k, const char* src, char* dst, size_t coun
       a.op = op;
       a.factor = factor;
       a.out_dev = my_out(j);
+      if (ar && c->sgd) {   // fused SGD step on my piece of the parameters (fp32)
+        const SgdEpi& e = *c->sgd;
+        a.sgd = 1;
+        a.mom = e.mom ? e.mom + g.start[j] * g.esz : nullptr;
+        a.lr = e.lr;
+        a.mu = e.mu;
+        a.damp = e.damp;
+        a.wd = e.wd;
+        a.nesterov = e.nesterov;
+        a.init = e.init;
+      }
       const size_t out_off = c->out_off(R, me);
       pr.user_rw = ubuf(g.lo(me, j) * g.esz, mylen * g.esz);
       // result slot by the copy engine: FMX_RESULT_VIA_CE, or with the fetch lane on

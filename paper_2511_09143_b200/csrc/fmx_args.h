@@ -27,6 +27,16 @@ struct ReduceArgs {
   size_t wait_stride;
   uint32_t wait_value;
   int wait_skip;
+  // fused SGD epilogue (fmx_allreduce_sgd; fp32): the reduced gradient g of
+  // element e updates the parameter p = out_dev[e] in place and its momentum
+  // mom[e], torch's multi-tensor SGD step op by op, and p (not g) is what
+  // goes to out_sys and the all-gather:
+  //   g = wd ? g + wd*p : g;  m = init ? g : m*mu + (1-damp)*g;
+  //   d = nesterov ? g + mu*m : m;  p = p + (-lr)*d     (x + a*y as one FMA)
+  int sgd;        // 1: apply the epilogue
+  char* mom;      // momentum of the elements of out_dev (null: momentum 0)
+  float lr, mu, damp, wd;
+  int nesterov, init;
 };
 
 // Pipeline timeline probe entry (fmx_comm_set_stamps).

@@ -24,6 +24,14 @@ enum Counter { kCtrAr = 0, kCtrOs = 1, kCtrBc = 2, kCtrFence = 3, kNumCounters =
 
 struct PendingGather;  // an allreduce's deferred last gather (flexshm_plan.cpp)
 
+// The fused SGD epilogue of the allreduce being planned (fmx_allreduce_sgd):
+// the owner's reduction updates its parameter piece and momentum shard.
+struct SgdEpi {
+  char* mom;  // momentum shard of this rank's owner chunk (null: momentum 0)
+  float lr, mu, damp, wd;
+  int nesterov, init;
+};
+
 // One batch-memop node of a captured graph that signals / waits on this
 // communicator's flags, with its parameters as captured.
 struct GraphMemop {
@@ -109,6 +117,7 @@ struct fmx_comm {
   // single in-order stream stages bucket b+1 while peers finish reducing b
   bool defer_gather = false;
   fmx::PendingGather* pending = nullptr;
+  const fmx::SgdEpi* sgd = nullptr;  // set for the duration of one fmx_allreduce_sgd
   // FMX_STAGE_AFTER_REDUCE=1 (local knob: an intra-rank order only): stage(R+1)
   // waits for this rank's reduce(R), so the reduction's result store does not
   // share the D2H direction with this rank's next stage

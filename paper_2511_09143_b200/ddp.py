@@ -311,11 +311,20 @@ class ShmDataParallel(torch.nn.Module):
     accumulation, one RNE rounding) and widened back after the backward pass -
     half the host-link bytes, torch's bf16_compress_hook idea; within the
     north_star's bf16 tolerance, not the fp32 bit-exact path.
+
+    fused_sgd=dict(lr=..., momentum=0., dampening=0., weight_decay=0.,
+    nesterov=False): the optimizer runs inside the collective
+    (fmx_allreduce_sgd) - each bucket's owner applies torch's SGD step to its
+    chunk of the parameters with the averaged gradient, and the all-gather
+    distributes parameters instead of gradients; the momentum lives only for
+    the owner's shard (ZeRO-1).  Bit-identical to torch.optim.SGD (foreach) on
+    every rank; no optimizer.step() then, and .grad keeps the LOCAL gradient.
+    fp32 parameters; a fixed lr (it is baked into a captured graph).
     """
 
     def __init__(self, module: torch.nn.Module, comm: ShmCommunicator, bucket_cap_mb: float = 8.0,
                  first_bucket_mb: float = 1.0, stream=None, defer_gather: bool | None = None,
-                 compress: str | None = None):
+                 compress: str | None = None, fused_sgd: dict | None = None):
         super().__init__()
         self.module = module
         self.comm = comm
@@ -330,6 +339,15 @@ class ShmDataParallel(torch.nn.Module):
             raise ValueError(f"unknown gradient compression {compress!r}")
         self.compress = compress
         self._shadow = []
+        if fused_sgd is not None:
+            if compress is not None:
+                raise ValueError("fused_sgd exchanges fp32 gradients: no compression")
+            unknown = set(fused_sgd) - {"lr", "momentum", "dampening", "weight_decay", "nesterov"}
+            if unknown or "lr" not in fused_sgd:
+                raise ValueError(f"fused_sgd needs lr (and optionally momentum, dampening, "
+                                 f"weight_decay, nesterov); got {sorted(fused_sgd)}")
+        self.fused_sgd = fused_sgd
+        self._pflat, self._mom, self._first = [], [], []
         self.hook_state = HookState(comm, stream)
         self.stream = self.hook_state.stream
         self.buckets = None          # [(flat tensor, [param index])]
@@ -393,6 +411,25 @@ class ShmDataParallel(torch.nn.Module):
                 self.bucket_of[i] = b
                 self._views[i] = view
             self.buckets.append((flat, idx))
+            if self.fused_sgd is not None:
+                # parameters move into a flat buffer laid out like the gradient bucket
+                if flat.dtype != torch.float32:
+                    raise TypeError("fused_sgd needs fp32 parameters")
+                pflat = torch.empty_like(flat)
+                off = 0
+                for i in idx:
+                    p = self.params[i]
+                    pv = pflat.as_strided(p.size(), p.stride(), off) if _dense(p) else \
+                        pflat[off:off + p.numel()].view_as(p)
+                    with torch.no_grad():
+                        pv.copy_(p.data)
+                    p.data = pv
+                    off += p.numel()
+                _, ln = self.comm.shard(flat.numel(), flat.dtype)
+                self._pflat.append(pflat)
+                self._mom.append(torch.zeros(max(1, ln), dtype=torch.float32, device=flat.device)
+                                 if self.fused_sgd.get("momentum", 0.0) else None)
+                self._first.append(True)
             if self.compress == "bf16" and flat.dtype == torch.float32:
                 self._shadow.append(torch.empty(flat.numel(), dtype=torch.bfloat16,
                                                 device=flat.device))
@@ -464,7 +501,17 @@ class ShmDataParallel(torch.nn.Module):
         try:
             if self.defer:
                 self.comm.set_defer(True)
-            self.comm.allreduce(buf, op="avg", stream=cur)
+            if self.fused_sgd is not None:
+                f = self.fused_sgd
+                self.comm.allreduce_sgd(buf, self._pflat[b], self._mom[b], lr=f["lr"],
+                                        momentum_coef=f.get("momentum", 0.0),
+                                        dampening=f.get("dampening", 0.0),
+                                        weight_decay=f.get("weight_decay", 0.0),
+                                        nesterov=f.get("nesterov", False),
+                                        first_step=self._first[b], op="avg", stream=cur)
+                self._first[b] = False
+            else:
+                self.comm.allreduce(buf, op="avg", stream=cur)
         finally:
             self.comm.set_join_stream(None)
 

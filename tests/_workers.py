@@ -392,6 +392,38 @@ def graph_dp_worker(rank: int, job_key: str, n: int, mode: str = "mps", defer: b
                 out["extra"] = extra.cpu().numpy()
                 out["launches_per_replay"] = comm.kernel_launches()
             runs[kind] = flat(model.parameters())
+        # the optimizer fused into the collective (fmx_allreduce_sgd): eager steps then
+        # graph replays, against torch.optim.SGD on every rank (the eager run above)
+        model4 = build()
+        net4 = fddp.ShmDataParallel(model4, comm, bucket_cap_mb=0.05, first_bucket_mb=0.01,
+                                    defer_gather=defer, fused_sgd=dict(lr=0.05, momentum=0.9))
+
+        def step4():
+            net4.zero_grad()
+            loss = F.cross_entropy(net4(x), y)
+            loss.backward()
+            return loss
+
+        replay4 = net4.graphed_step(step4, warmup=warmup)
+        for _ in range(steps - warmup):
+            replay4()
+        out["params_fused"] = flat(model4.parameters())
+        # weight decay + Nesterov, eager, against torch's SGD with the same settings
+        cfg = dict(lr=0.03, momentum=0.8, weight_decay=1e-3, nesterov=True)
+        for kind in ("torch", "fused"):
+            m = build()
+            if kind == "torch":
+                nt = fddp.ShmDataParallel(m, comm, bucket_cap_mb=0.05, first_bucket_mb=0.01)
+                o = torch.optim.SGD(nt.parameters(), **cfg)
+            else:
+                nt = fddp.ShmDataParallel(m, comm, bucket_cap_mb=0.05, first_bucket_mb=0.01,
+                                          fused_sgd=cfg)
+            for _ in range(4):
+                nt.zero_grad()
+                F.cross_entropy(nt(x), y).backward()
+                if kind == "torch":
+                    o.step()
+            out[f"params_wd_{kind}"] = flat(m.parameters())
         # gradient accumulation: one backward under no_sync, one outside - the
         # exchanged gradient is the DDP mean of the ranks' accumulated gradients
         x2 = torch.randn(32, 64, generator=g).cuda()

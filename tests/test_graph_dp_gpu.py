@@ -7,7 +7,10 @@ DDP mean of the ranks' local gradients (bit-exact); the graph-replayed
 training ends bit-identical to the same steps run eagerly, on every rank;
 an eager allreduce between two replays (fence + counter continuity) is exact;
 gradient accumulation under no_sync exchanges the DDP mean of the
-accumulated local gradients."""
+accumulated local gradients; the SGD step fused into the collective
+(fused_sgd / fmx_allreduce_sgd: owners step their chunk, the all-gather moves
+parameters) ends bit-identical to torch.optim.SGD on every rank - momentum,
+and weight decay + Nesterov - eager and replayed as a graph."""
 
 from __future__ import annotations
 
@@ -52,6 +55,11 @@ def test_graphed_dp_matches_eager_and_oracle(n, mode, defer, compress):
     for rank, r in enumerate(res):
         assert np.array_equal(r["synced"].view(np.uint32), want.view(np.uint32)), rank
         assert np.array_equal(r["synced_acc"].view(np.uint32), want_acc.view(np.uint32)), rank
+        if compress is None:   # the optimizer fused into the collective == torch SGD per rank
+            assert np.array_equal(r["params_fused"].view(np.uint32),
+                                  r["params_eager"].view(np.uint32)), rank
+            assert np.array_equal(r["params_wd_fused"].view(np.uint32),
+                                  r["params_wd_torch"].view(np.uint32)), rank
         assert np.array_equal(r["params_graph"].view(np.uint32),
                               r["params_eager"].view(np.uint32)), rank
         assert np.array_equal(r["params_graph"].view(np.uint32),
