@@ -558,3 +558,43 @@ def graph_api_worker(rank: int, job_key: str, n: int, mode: str = "mps"):
     torch.cuda.synchronize()
     comm.destroy()
     return out
+
+
+def fused_sgd_worker(rank: int, job_key: str, n: int, count: int, transport: str,
+                     slice_bytes: int, mode: str = "mps", steps: int = 3):
+    """fmx_allreduce_sgd on a flat buffer against the same steps done the
+    unfused way on this rank: comm.allreduce(op="avg") of the gradient, then
+    torch.optim.SGD (foreach) on a Parameter.  Returns both parameter vectors."""
+    import torch
+
+    from oracle import oracle as orc
+    from paper_2511_09143_b200 import instance as inst_mod
+    from paper_2511_09143_b200.comm import init_process_group
+
+    inst = inst_mod.bind(0, rank + 1, mode=mode)
+    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n, transport=transport,
+                              slice_bytes=slice_bytes, timeout_s=120)
+    s = inst.stream
+    cfg = dict(lr=0.02, momentum=0.9, weight_decay=1e-3, nesterov=False, dampening=0.1)
+    with torch.cuda.stream(s):
+        p0 = torch.from_numpy(orc.synthetic_gradient(0, count, orc.F32, seed=77)).cuda() * 100
+        ref = torch.nn.Parameter(p0.clone())
+        opt = torch.optim.SGD([ref], lr=cfg["lr"], momentum=cfg["momentum"],
+                              weight_decay=cfg["weight_decay"], dampening=cfg["dampening"],
+                              foreach=True)
+        fused = p0.clone()
+        _, ln = comm.shard(count)
+        mom = torch.zeros(max(1, ln), device="cuda")
+        for k in range(steps):
+            g = torch.from_numpy(orc.synthetic_gradient(rank, count, orc.F32, seed=500 + k)).cuda()
+            comm.allreduce_sgd(g, fused, mom, lr=cfg["lr"], momentum_coef=cfg["momentum"],
+                               dampening=cfg["dampening"], weight_decay=cfg["weight_decay"],
+                               first_step=k == 0, op="avg", stream=s)
+            gr = g.clone()
+            comm.allreduce(gr, op="avg", stream=s)
+            ref.grad = gr
+            opt.step()
+    s.synchronize()
+    out = {"fused": fused.cpu().numpy(), "torch": ref.detach().cpu().numpy()}
+    comm.destroy()
+    return out

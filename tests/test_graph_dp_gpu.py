@@ -114,3 +114,24 @@ def test_graph_api_and_deferred_gathers(n, mode):
                 assert np.array_equal(bits(r["graphs"][step][2]), bits(want)), step
                 assert np.array_equal(bits(r["graphs"][step][3]),
                                       bits(full[rank * 999:(rank + 1) * 999])), step
+
+
+@pytest.mark.parametrize("n,count,transport,slice_bytes", [
+    (2, 3_000_001, "ce", 64 << 10),   # two ranks: fetch lane + copy-engine result (>= 8 rounds)
+    (3, 1_000_003, "ce", 64 << 10),   # multi-round copy-engine pipeline
+    (3, 100_003, "zc", 0),            # zero-copy: the reduction reads the slots itself
+    (1, 10_007, "auto", 0)])          # one rank: the step alone
+def test_fused_sgd_flat_buffer_matches_torch_sgd(n, count, transport, slice_bytes):
+    """fmx_allreduce_sgd (weight decay, dampened momentum) over three steps on
+    every transport / schedule: bit-identical to allreduce(avg) + torch SGD."""
+    from paper_2511_09143_b200.launcher import launch, new_job_key
+    from paper_2511_09143_b200.scheduler import fm_select, make_cluster
+    from paper_2511_09143_b200.workload import Job
+
+    d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
+    key = new_job_key("fsgd")
+    res = launch(_workers.fused_sgd_worker, d, args=(key, n, count, transport, slice_bytes),
+                 job_key=key, timeout_s=300, mode="mps")
+    for rank, r in enumerate(res):
+        assert np.array_equal(r["fused"].view(np.uint32), r["torch"].view(np.uint32)), rank
+        assert np.array_equal(r["fused"].view(np.uint32), res[0]["fused"].view(np.uint32)), rank
