@@ -449,7 +449,8 @@ def graph_dp_worker(rank: int, job_key: str, n: int, mode: str = "mps", defer: b
 GRAPH_API_SEED = {"big": 1000, "small": 2000, "rs": 3000, "bc": 4000}
 
 
-def graph_api_worker(rank: int, job_key: str, n: int, mode: str = "mps"):
+def graph_api_worker(rank: int, job_key: str, n: int, mode: str = "mps", transport: str = "auto",
+                     slice_bytes: int = 0):
     """The raw fmx_graph_* / deferred-gather API on one rank.
 
     (1) Deferred gathers in join-stream mode: three allreduces (multi-round,
@@ -467,7 +468,8 @@ def graph_api_worker(rank: int, job_key: str, n: int, mode: str = "mps"):
     from paper_2511_09143_b200.comm import init_process_group
 
     inst = inst_mod.bind(0, rank + 1, mode=mode)
-    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n, timeout_s=120)
+    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n, timeout_s=120,
+                              transport=transport, slice_bytes=slice_bytes)
     out = {}
     s0 = inst.stream
     dev = torch.device("cuda")

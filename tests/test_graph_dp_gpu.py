@@ -67,8 +67,12 @@ def test_graphed_dp_matches_eager_and_oracle(n, mode, defer, compress):
         assert np.array_equal(r["extra"].view(np.uint32), want_extra.view(np.uint32)), rank
 
 
-@pytest.mark.parametrize("n,mode", [(3, "mps"), (2, "green")])
-def test_graph_api_and_deferred_gathers(n, mode):
+@pytest.mark.parametrize("n,mode,transport,slice_bytes", [
+    (3, "mps", "auto", 0), (2, "green", "auto", 0),
+    # copy engines in many small rounds: the two-rank fetch lane + copy-engine result
+    # slot, and the three-rank pipeline, inside captured graphs
+    (2, "mps", "ce", 64 << 10), (3, "mps", "ce", 64 << 10)])
+def test_graph_api_and_deferred_gathers(n, mode, transport, slice_bytes):
     """The raw API: deferred gathers + flush (bit-exact, pending-gather guard);
     two captured graphs replayed on different streams with an eager collective
     on a third stream in between, fresh inputs each replay - every result
@@ -79,8 +83,8 @@ def test_graph_api_and_deferred_gathers(n, mode):
 
     d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
     key = new_job_key("gapi")
-    res = launch(_workers.graph_api_worker, d, args=(key, n, mode), job_key=key, timeout_s=300,
-                 mode=mode)
+    res = launch(_workers.graph_api_worker, d, args=(key, n, mode, transport, slice_bytes),
+                 job_key=key, timeout_s=300, mode=mode)
     bits = lambda a: a.view(np.uint32)
     sizes = [300_001, 1000, 40_000]
     for i, c in enumerate(sizes):
