@@ -60,7 +60,9 @@ typedef CUresult (*PFN_batchMemOp)(CUstream, unsigned int, CUstreamBatchMemOpPar
 typedef CUresult (*PFN_streamGetCtx)(CUstream, CUcontext*);
 typedef CUresult (*PFN_ctxPush)(CUcontext);
 typedef CUresult (*PFN_ctxPop)(CUcontext*);
+typedef CUresult (*PFN_ctxGetCurrent)(CUcontext*);
 PFN_batchMemOp g_batch = nullptr;
+PFN_ctxGetCurrent g_ctx_current = nullptr;
 PFN_streamGetCtx g_stream_ctx = nullptr;
 PFN_ctxPush g_ctx_push = nullptr;
 PFN_ctxPop g_ctx_pop = nullptr;
@@ -79,6 +81,7 @@ int load_driver() {
     get("cuStreamGetCtx", (void**)&g_stream_ctx);
     get("cuCtxPushCurrent", (void**)&g_ctx_push);
     get("cuCtxPopCurrent", (void**)&g_ctx_pop);
+    get("cuCtxGetCurrent", (void**)&g_ctx_current);
   });
   if (g_driver_status != FMX_OK)
     return fail(FMX_ERR_UNSUPPORTED, "driver entry points (stream mem ops / contexts) unavailable");
@@ -927,8 +930,10 @@ int fmx_allreduce(fmx_comm_t c, const void* send, void* recv, size_t count, int 
       return sink.reduce(kLaneMain, pr);
     });
   }
+  // (a deferred gather still pending runs on the gather lane first: then the
+  // one-shot forks and joins the extra lanes like any pipelined call)
   if (c->use_oneshot(count * esz))
-    return on_lanes(c, s, 2, [&]() {
+    return on_lanes(c, s, c->pending ? 0 : 2, [&]() {
       return plan_allreduce_oneshot(c, sink, (const char*)send, (char*)recv, count, dtype, op,
                                     factor, aligned);
     });
@@ -1444,6 +1449,15 @@ int fmx_graph_capture_begin(fmx_comm_t c) {
     // on eager events, and a replay is ordered after it by launch_prepare
     CtxPush push(c->lane_ctx);
     FMX_CUDA(cudaEventSynchronize(c->done));
+  }
+  if (!c->lane_ctx) {
+    // no collective yet: the lane streams / events are created now, in the
+    // current context (creating them inside the capture is not allowed); a
+    // capture on a stream of another context is refused by on_lanes
+    CUcontext ctx = nullptr;
+    if (g_ctx_current(&ctx) != CUDA_SUCCESS || !ctx)
+      return fail(FMX_ERR_CUDA, "no current CUDA context to create the lane objects in");
+    if ((rc = make_lane_objects(c, ctx))) return rc;
   }
   for (int k = 0; k < kNumCounters; ++k) c->cap_c0[k] = *c->counter(k);
   c->cap_launches0 = c->launches;

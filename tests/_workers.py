@@ -600,3 +600,124 @@ def fused_sgd_worker(rank: int, job_key: str, n: int, count: int, transport: str
     out = {"fused": fused.cpu().numpy(), "torch": ref.detach().cpu().numpy()}
     comm.destroy()
     return out
+
+
+def graph_stress_worker(rank: int, job_key: str, n: int, seed: int, nops: int, replays: int = 3,
+                        mode: str = "mps", slice_bytes: int = 0, sticky_defer: bool = False):
+    """The random program of stress_ops captured ONCE as a CUDA graph (join-stream
+    ops with deferred gathers included) and replayed `replays` times with fresh
+    inputs written before each replay (seed + 100000 * replay); returns a
+    sha256 per replay per op."""
+    import torch
+
+    from paper_2511_09143_b200 import instance as inst_mod
+    from paper_2511_09143_b200.comm import init_process_group
+
+    inst = inst_mod.bind(0, rank + 1, mode=mode)
+    comm = init_process_group(None, rank, job_key, instance=inst, nranks=n, timeout_s=300,
+                              slice_bytes=slice_bytes)
+    s = inst.stream
+    side = torch.cuda.Stream()
+    ops = stress_ops(n, seed, nops)
+    dev = torch.device("cuda")
+
+    def as_tensor(x, dtype):
+        host = torch.from_numpy(x.view(np.float32) if dtype == "f32" else x.view(np.int16))
+        t = host.to(dev)
+        return t if dtype == "f32" else t.view(torch.bfloat16)
+
+    inp, work, res = [], [], []
+    for o in ops:
+        t = as_tensor(stress_input(rank, o, n), o["dtype"])
+        inp.append(t)
+        work.append(torch.empty_like(t))
+        c = o["size"]
+        k = o["kind"]
+        if k == "reduce_scatter" and not o["inplace"]:
+            res.append(torch.empty(c, dtype=t.dtype, device=dev))
+        elif k == "allgather":
+            res.append(torch.empty(n * c, dtype=t.dtype, device=dev))
+        elif k == "allreduce" and not o["inplace"]:
+            res.append(torch.empty_like(t))
+        else:
+            res.append(None)
+    torch.cuda.synchronize()
+
+    def is_join(o):
+        return o["join"] and o["kind"] == "allreduce"
+
+    def program():
+        used_side = False
+        for i, o in enumerate(ops):
+            k, c = o["kind"], o["size"]
+            factor = 0.25 if o["op"] == "postscale" else None
+            join = is_join(o)
+            if join:   # a run of join-stream allreduces with deferred gathers
+                comm.set_join_stream(side)
+                comm.set_defer(True)
+                used_side = True
+            if k == "allreduce":
+                if o["inplace"]:
+                    work[i].copy_(inp[i])
+                    comm.allreduce(work[i], op=o["op"], factor=factor, stream=s)
+                else:
+                    comm.allreduce(inp[i], op=o["op"], factor=factor, out=res[i], stream=s)
+            elif k == "reduce_scatter":
+                work[i].copy_(inp[i])
+                out = work[i][rank * c:(rank + 1) * c] if o["inplace"] else res[i]
+                comm.reduce_scatter(work[i], out, op=o["op"], factor=factor, stream=s)
+            elif k == "allgather":
+                if o["inplace"]:
+                    res[i][rank * c:(rank + 1) * c].copy_(inp[i])
+                    comm.allgather(res[i][rank * c:(rank + 1) * c], res[i], stream=s)
+                else:
+                    comm.allgather(inp[i], res[i], stream=s)
+            else:
+                work[i].copy_(inp[i])
+                comm.broadcast(work[i], root=o["root"], stream=s)
+            if join and not sticky_defer and (i + 1 == len(ops) or not is_join(ops[i + 1])):
+                comm.flush(stream=s)          # the run's last gather, on the join stream
+                comm.set_defer(False)
+            if join:
+                comm.set_join_stream(None)
+        if sticky_defer:   # deferral stayed on across every later call: flush at the end
+            comm.flush(stream=s)
+            comm.set_defer(False)
+        if used_side:   # the join stream rejoins the capture
+            s.wait_stream(side)
+
+    g = torch.cuda.CUDAGraph(keep_graph=True)
+    comm.capture_begin()
+    with torch.cuda.graph(g, stream=s):
+        program()
+    h = comm.capture_end(g.raw_cuda_graph())
+    g.instantiate()
+    ex = g.raw_cuda_graph_exec()
+    digests = []
+    for rep in range(replays):
+        for i, o in enumerate(ops):
+            x = stress_input(rank, dict(o, seed=o["seed"] + 100_000 * rep), n)
+            inp[i].copy_(as_tensor(x, o["dtype"]))
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s):
+            comm.launch_prepare(h, ex, s)
+            g.replay()
+        s.synchronize()
+        row = []
+        for i, o in enumerate(ops):
+            k, c = o["kind"], o["size"]
+            if k == "allreduce":
+                t = work[i] if o["inplace"] else res[i]
+            elif k == "reduce_scatter":
+                t = work[i][rank * c:(rank + 1) * c] if o["inplace"] else res[i]
+            elif k == "allgather":
+                t = res[i]
+            else:
+                t = work[i]
+            r = t.cpu()
+            arr = r.numpy() if o["dtype"] == "f32" else r.view(torch.int16).numpy().view(np.uint16)
+            row.append(digest(arr))
+        digests.append(row)
+    comm.barrier(120)
+    comm.destroy()
+    return {"digests": digests}

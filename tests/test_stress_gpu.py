@@ -74,3 +74,30 @@ def test_wide_communicators_on_logical_gpus(monkeypatch, n, gpus):
     for i, o in enumerate(ops):
         for r in range(n):
             assert res[r]["digests"][i] == expected_digest(o, n, r), (i, o, r)
+
+
+@pytest.mark.parametrize("n,mode,seed,slice_bytes,sticky", [
+    (3, "mps", 5, 0, False), (2, "mps", 6, 64 << 10, False), (7, "mps", 7, 0, False),
+    # deferral switched on at the first join-stream call and left on for every
+    # later call, whatever its kind (one-shots, broadcasts, ... flush it)
+    (3, "mps", 5, 0, True)])
+def test_random_program_as_a_captured_graph(n, mode, seed, slice_bytes, sticky):
+    """The random program (every collective, dtype and op; join-stream allreduces
+    with deferred gathers) captured once as a CUDA graph and replayed three times
+    with fresh inputs: every replay's every result bit-exact against the oracle."""
+    from paper_2511_09143_b200.launcher import launch, new_job_key
+    from paper_2511_09143_b200.scheduler import fm_select, make_cluster
+    from paper_2511_09143_b200.workload import Job
+
+    nops, replays = 24, 3
+    d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
+    key = new_job_key("gstress")
+    res = launch(_workers.graph_stress_worker, d,
+                 args=(key, n, seed, nops, replays, mode, slice_bytes, sticky), job_key=key,
+                 timeout_s=600, mode=mode)
+    ops = _workers.stress_ops(n, seed, nops)
+    for rep in range(replays):
+        for i, o in enumerate(ops):
+            o_r = dict(o, seed=o["seed"] + 100_000 * rep)
+            for r in range(n):
+                assert res[r]["digests"][rep][i] == expected_digest(o_r, n, r), (rep, i, o, r)
