@@ -89,7 +89,7 @@ def test_random_program_as_a_captured_graph(n, mode, seed, slice_bytes, sticky):
     from paper_2511_09143_b200.scheduler import fm_select, make_cluster
     from paper_2511_09143_b200.workload import Job
 
-    nops, replays = 24, 3
+    nops, replays = (16, 2) if n >= 7 else (24, 3)   # (the suite's runtime budget)
     d = fm_select(Job(0, "train", n, 0.0, 0.0), make_cluster("FM", 1))
     key = new_job_key("gstress")
     res = launch(_workers.graph_stress_worker, d,
