@@ -603,7 +603,8 @@ def fused_sgd_worker(rank: int, job_key: str, n: int, count: int, transport: str
 
 
 def graph_stress_worker(rank: int, job_key: str, n: int, seed: int, nops: int, replays: int = 3,
-                        mode: str = "mps", slice_bytes: int = 0, sticky_defer: bool = False):
+                        mode: str = "mps", slice_bytes: int = 0, sticky_defer: bool = False,
+                        check_every: int = 1):
     """The random program of stress_ops captured ONCE as a CUDA graph (join-stream
     ops with deferred gathers included) and replayed `replays` times with fresh
     inputs written before each replay (seed + 100000 * replay); returns a
@@ -695,13 +696,18 @@ def graph_stress_worker(rank: int, job_key: str, n: int, seed: int, nops: int, r
     ex = g.raw_cuda_graph_exec()
     digests = []
     for rep in range(replays):
-        for i, o in enumerate(ops):
-            x = stress_input(rank, dict(o, seed=o["seed"] + 100_000 * rep), n)
-            inp[i].copy_(as_tensor(x, o["dtype"]))
-        torch.cuda.synchronize()
+        check = rep % check_every == 0   # (soaks: fresh inputs and digests every k-th replay)
+        if check:
+            for i, o in enumerate(ops):
+                x = stress_input(rank, dict(o, seed=o["seed"] + 100_000 * rep), n)
+                inp[i].copy_(as_tensor(x, o["dtype"]))
+            torch.cuda.synchronize()
         with torch.cuda.stream(s):
             comm.launch_prepare(h, ex, s)
             g.replay()
+        if not check:
+            digests.append(None)
+            continue
         s.synchronize()
         row = []
         for i, o in enumerate(ops):
