@@ -136,6 +136,29 @@ __global__ void ldg_kernel(const uint4* __restrict__ src, size_t n16, unsigned l
   if (acc == 0x12345) *sink = acc;
 }
 
+// 256-bit stores / loads (sm_100: STG.E.ENL2.256 / LDG.E.ENL2.256), 32 B per thread
+__global__ void stg256_kernel(float* __restrict__ dst, size_t n32) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n32;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const float v = (float)i;
+    asm volatile("st.global.v8.f32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(dst + i * 8), "f"(v)
+                 : "memory");
+  }
+}
+
+__global__ void ldg256_kernel(const float* __restrict__ src, size_t n32, unsigned long long* sink) {
+  float acc = 0.f;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n32;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float a0, a1, a2, a3, a4, a5, a6, a7;
+    asm volatile("ld.global.volatile.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3), "=f"(a4), "=f"(a5), "=f"(a6), "=f"(a7)
+                 : "l"(src + i * 8));
+    acc += a0 + a7;
+  }
+  if (acc == 12345.f) *sink = 1;
+}
+
 __global__ void stg_kernel(uint4* __restrict__ dst, size_t n16) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16;
        i += (size_t)gridDim.x * blockDim.x)
@@ -301,6 +324,8 @@ int main(int argc, char** argv) {
     };
     for (int g : {16, 64, 256}) under("stg_store", g, [&](cudaStream_t st) { stg_kernel<<<g, 512, 0, st>>>((uint4*)dv_dst, part / 16); });
     for (int g : {16, 64, 256}) under("ldg_load", g, [&](cudaStream_t st) { ldg_kernel<<<g, 512, 0, st>>>((const uint4*)dv_src, part / 16, sink); });
+    for (int g : {16, 64, 256}) under("stg256_store", g, [&](cudaStream_t st) { stg256_kernel<<<g, 512, 0, st>>>((float*)dv_dst, part / 32); });
+    for (int g : {16, 64, 256}) under("ldg256_load", g, [&](cudaStream_t st) { ldg256_kernel<<<g, 512, 0, st>>>((const float*)dv_src, part / 32, sink); });
     const uint32_t chunk = 32768;
     const size_t smem = (size_t)chunk * kStages;
     CK(cudaFuncSetAttribute(tma_load_kernel<kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
