@@ -35,7 +35,8 @@ def expected_digest(o: dict, n: int, rank: int) -> str:
     return _workers.digest(full)
 
 
-@pytest.mark.parametrize("n,mode,seed", [(7, "mps", 1), (3, "green", 2)])
+@pytest.mark.parametrize("n,mode,seed", [(7, "mps", 1), (3, "green", 2),
+                                         (2, "mps", 4)])   # two ranks: the fetch-lane schedule
 def test_random_collective_program_is_bit_exact(n, mode, seed):
     from paper_2511_09143_b200.launcher import launch, new_job_key
     from paper_2511_09143_b200.scheduler import fm_select, make_cluster
