@@ -212,36 +212,54 @@ __device__ __forceinline__ float scale_out(float acc, float f) {
   else return acc;
 }
 
-// Sum of one 16-byte vector position across all sources, rank order.
-template <typename T, int OP>
-__device__ __forceinline__ void reduce_vec(const ReduceArgs& a, size_t off, float* acc) {
+// Sum of U 16-byte vector positions (i, i + stride, ...) across all sources,
+// rank order.  The loads of all U positions of a source batch are issued
+// before any is consumed, so a thread keeps U x B independent 128-bit loads in
+// flight: inside a 1g-sized partition (~20 SMs) the kernel is latency bound,
+// and one round trip per U vectors instead of per vector halves the HBM-only
+// launch (result slot by copy engine).  The per-element arithmetic and its
+// order are unchanged.
+template <typename T, int OP, int U>
+__device__ __forceinline__ void reduce_vecs(const ReduceArgs& a, size_t i, size_t stride, size_t nvec,
+                                            float (&acc)[U][Elem<T>::kVec]) {
   using E = Elem<T>;
   constexpr int V = E::kVec;
-  constexpr int B = 8;  // sources loaded per batch (independent loads in flight)
+  constexpr int B = 8;  // sources loaded per batch
   for (int q0 = 0; q0 < a.nsrc; q0 += B) {
-    uint4 raw[B];
+    uint4 raw[U][B];
 #pragma unroll
-    for (int b = 0; b < B; ++b) {
-      const int q = q0 + b;
-      if (q < a.nsrc)
-        raw[b] = ((a.sys_mask >> q) & 1) ? ld_cv_v4(a.src[q] + off) : ld_v4(a.src[q] + off);
+    for (int u = 0; u < U; ++u) {
+      if (i + u * stride >= nvec) continue;
+      const size_t off = (i + u * stride) * 16;
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const int q = q0 + b;
+        if (q < a.nsrc)
+          raw[u][b] = ((a.sys_mask >> q) & 1) ? ld_cv_v4(a.src[q] + off) : ld_v4(a.src[q] + off);
+      }
     }
 #pragma unroll
-    for (int b = 0; b < B; ++b) {
-      const int q = q0 + b;
-      if (q < a.nsrc) {
-        float x[V];
-        E::widen(raw[b], x);
+    for (int u = 0; u < U; ++u) {
+      if (i + u * stride >= nvec) continue;
 #pragma unroll
-        for (int k = 0; k < V; ++k) {
-          const float c = scale_in<T, OP>(x[k], a.factor);
-          acc[k] = q == 0 ? c : __fadd_rn(acc[k], c);
+      for (int b = 0; b < B; ++b) {
+        const int q = q0 + b;
+        if (q < a.nsrc) {
+          float x[V];
+          E::widen(raw[u][b], x);
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+            const float c = scale_in<T, OP>(x[k], a.factor);
+            acc[u][k] = q == 0 ? c : __fadd_rn(acc[u][k], c);
+          }
         }
       }
     }
   }
 #pragma unroll
-  for (int k = 0; k < V; ++k) acc[k] = scale_out<OP>(acc[k], a.factor);
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[u][k] = scale_out<OP>(acc[u][k], a.factor);
 }
 
 // The fused SGD step of one element (ReduceArgs::sgd): torch's multi-tensor SGD
@@ -290,9 +308,7 @@ __global__ void __launch_bounds__(256, 2) fmx_reduce_kernel(const __grid_constan
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (size_t i = tid; i < nvec; i += U * stride) {
     float acc[U][V];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (i + u * stride < nvec) reduce_vec<T, OP>(a, (i + u * stride) * 16, acc[u]);
+    reduce_vecs<T, OP, U>(a, i, stride, nvec, acc);
     if constexpr (SGD) {   // fp32 only: V = 4 parameters and momenta per vector
 #pragma unroll
       for (int u = 0; u < U; ++u) {
