@@ -260,7 +260,7 @@ class CudaSink final : public Sink {
         maxb = std::max(maxb, a.seg[k].bytes);
       }
       constexpr int kThreads = 512, kU = 4;
-      int gx = grid_for((maxb / 16 + kU - 1) / kU, kThreads, std::max(1, 1184 / a.nseg));
+      int gx = grid_for((maxb / 16 + kU - 1) / kU, kThreads, std::max(1, c_->copy_ctas / a.nseg));
       dim3 grid(gx, a.nseg);
       fmx_copy_kernel<kU><<<grid, kThreads, 0, s>>>(a);
       FMX_CUDA(cudaGetLastError());
@@ -857,6 +857,7 @@ int fmx_comm_init(fmx_comm_t* out, const char* job_key, int nranks, int rank,
   if (const char* v = getenv("FMX_COPY_FENCE")) c->copy_fence = atoi(v) != 0;
   if (const char* v = getenv("FMX_JOIN_LANES")) c->join_lanes = std::max(1, std::min(3, atoi(v)));
   if (const char* v = getenv("FMX_FUSE_SIGNAL")) c->fuse_signal = atoi(v) != 0;
+  if (const char* v = getenv("FMX_COPY_CTAS")) c->copy_ctas = std::max(1, std::min(atoi(v), 1184));
   if (const char* v = getenv("FMX_REDUCE_CTAS")) c->reduce_ctas = std::max(1, std::min(atoi(v), kReduceGridCap));
   c->serialize = profiler_injected();
   // The one-shot may fuse its flag wait into the reduction (spinning CTAs) only

@@ -78,6 +78,8 @@ struct fmx_comm {
   bool spin_wait = false;              // one-shot: OS_READY wait fused into the reduce kernel
                                        //   (MPS-concurrent ranks only; FMX_SPIN_WAIT=0/1 overrides)
   int reduce_ctas = 1184;              // grid cap of the reduce kernel (FMX_REDUCE_CTAS; local knob)
+  int copy_ctas = 1184;                // CTA cap of one copy-kernel launch over all its segments
+                                       // (FMX_COPY_CTAS; local knob: paces SM-side host stores)
   bool copy_fence = true;              // no-op kernel after every copy-engine batch (CudaSink::copy)
   bool fuse_signal = true;             // FMX_FUSE_SIGNAL=0: zero-copy stage + STAGED as two ops
   bool serialize = false;              // drain this rank's lanes before every kernel launch
