@@ -212,41 +212,39 @@ __device__ __forceinline__ float scale_out(float acc, float f) {
   else return acc;
 }
 
-// Sum of U 16-byte vector positions (i, i + stride, ...) across all sources,
-// rank order.  The loads of all U positions of a source batch are issued
-// before any is consumed, so a thread keeps U x B independent 128-bit loads in
-// flight: inside a 1g-sized partition (~20 SMs) the kernel is latency bound,
-// and one round trip per U vectors instead of per vector halves the HBM-only
-// launch (result slot by copy engine).  The per-element arithmetic and its
-// order are unchanged.
-template <typename T, int OP, int U>
-__device__ __forceinline__ void reduce_vecs(const ReduceArgs& a, size_t i, size_t stride, size_t nvec,
-                                            float (&acc)[U][Elem<T>::kVec]) {
+// Sum of the vector positions i + u * stride, u in [U0, U0 + G), across all
+// sources, rank order; the loads of all G positions of a source batch are
+// issued before any is consumed (G x B independent 128-bit loads in flight).
+template <typename T, int OP, int U, int U0, int G>
+__device__ __forceinline__ void reduce_group(const ReduceArgs& a, size_t i, size_t stride, size_t nvec,
+                                             float (&acc)[U][Elem<T>::kVec]) {
   using E = Elem<T>;
   constexpr int V = E::kVec;
   constexpr int B = 8;  // sources loaded per batch
   for (int q0 = 0; q0 < a.nsrc; q0 += B) {
-    uint4 raw[U][B];
+    uint4 raw[G][B];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int g = 0; g < G; ++g) {
+      const int u = U0 + g;
       if (i + u * stride >= nvec) continue;
       const size_t off = (i + u * stride) * 16;
 #pragma unroll
       for (int b = 0; b < B; ++b) {
         const int q = q0 + b;
         if (q < a.nsrc)
-          raw[u][b] = ((a.sys_mask >> q) & 1) ? ld_cv_v4(a.src[q] + off) : ld_v4(a.src[q] + off);
+          raw[g][b] = ((a.sys_mask >> q) & 1) ? ld_cv_v4(a.src[q] + off) : ld_v4(a.src[q] + off);
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int g = 0; g < G; ++g) {
+      const int u = U0 + g;
       if (i + u * stride >= nvec) continue;
 #pragma unroll
       for (int b = 0; b < B; ++b) {
         const int q = q0 + b;
         if (q < a.nsrc) {
           float x[V];
-          E::widen(raw[u][b], x);
+          E::widen(raw[g][b], x);
 #pragma unroll
           for (int k = 0; k < V; ++k) {
             const float c = scale_in<T, OP>(x[k], a.factor);
@@ -256,10 +254,37 @@ __device__ __forceinline__ void reduce_vecs(const ReduceArgs& a, size_t i, size_
       }
     }
   }
+}
+
+template <typename T, int OP, int U, int U0 = 0>
+__device__ __forceinline__ void reduce_each(const ReduceArgs& a, size_t i, size_t stride, size_t nvec,
+                                            float (&acc)[U][Elem<T>::kVec]) {
+  if constexpr (U0 < U) {
+    reduce_group<T, OP, U, U0, 1>(a, i, stride, nvec, acc);
+    reduce_each<T, OP, U, U0 + 1>(a, i, stride, nvec, acc);
+  }
+}
+
+// Sum of U vector positions (i, i + stride, ...) across all sources, rank
+// order.  HBM sources (the copy-engine transport): the loads of all U
+// positions are in flight together - inside a 1g-sized partition the kernel
+// is latency bound, and one round trip per U vectors instead of per vector
+// cuts the HBM-only launch (result slot by copy engine) 78.5 -> 62-67 us
+// (r02/r5b).  Host sources (zero-copy transport, one-shot): one position's
+// sources at a time, as before - U x 7 concurrent host reads per thread made
+// the 64 KiB one-shot at 7 ranks 11 % slower (r02/r5e).  The per-element
+// arithmetic and its order are the same either way.
+template <typename T, int OP, int U, bool HOST_SRC>
+__device__ __forceinline__ void reduce_vecs(const ReduceArgs& a, size_t i, size_t stride, size_t nvec,
+                                            float (&acc)[U][Elem<T>::kVec]) {
+  if constexpr (HOST_SRC)
+    reduce_each<T, OP, U>(a, i, stride, nvec, acc);
+  else
+    reduce_group<T, OP, U, 0, U>(a, i, stride, nvec, acc);
 #pragma unroll
   for (int u = 0; u < U; ++u)
 #pragma unroll
-    for (int k = 0; k < V; ++k) acc[u][k] = scale_out<OP>(acc[u][k], a.factor);
+    for (int k = 0; k < Elem<T>::kVec; ++k) acc[u][k] = scale_out<OP>(acc[u][k], a.factor);
 }
 
 // The fused SGD step of one element (ReduceArgs::sgd): torch's multi-tensor SGD
@@ -298,7 +323,7 @@ __device__ __forceinline__ void reduce_elem(const ReduceArgs& a, size_t e) {
   if (a.out_sys) E::store1(a.out_sys + e * esz, acc);
 }
 
-template <typename T, int U, int OP, bool SGD = false>
+template <typename T, int U, int OP, bool SGD = false, bool HOST_SRC = false>
 __global__ void __launch_bounds__(256, 2) fmx_reduce_kernel(const __grid_constant__ ReduceArgs a) {
   using E = Elem<T>;
   constexpr int V = E::kVec;
@@ -308,7 +333,7 @@ __global__ void __launch_bounds__(256, 2) fmx_reduce_kernel(const __grid_constan
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (size_t i = tid; i < nvec; i += U * stride) {
     float acc[U][V];
-    reduce_vecs<T, OP, U>(a, i, stride, nvec, acc);
+    reduce_vecs<T, OP, U, HOST_SRC>(a, i, stride, nvec, acc);
     if constexpr (SGD) {   // fp32 only: V = 4 parameters and momenta per vector
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -362,9 +387,11 @@ inline void launch_reduce_t(const ReduceArgs& a, bool aligned, cudaStream_t s, i
     size_t g = (items + kReduceThreads - 1) / kReduceThreads;
     return (int)(g < 1 ? 1 : g > (size_t)cap ? cap : g);
   };
-  if (aligned)
-    fmx_reduce_kernel<T, kReduceU, OP, SGD>
-        <<<grid((a.len / V + kReduceU - 1) / kReduceU + 1), kReduceThreads, 0, s>>>(a);
+  const int g = grid((a.len / V + kReduceU - 1) / kReduceU + 1);
+  if (aligned && a.sys_mask)   // sources in mapped host memory (zero-copy, one-shot)
+    fmx_reduce_kernel<T, kReduceU, OP, SGD, true><<<g, kReduceThreads, 0, s>>>(a);
+  else if (aligned)
+    fmx_reduce_kernel<T, kReduceU, OP, SGD, false><<<g, kReduceThreads, 0, s>>>(a);
   else
     fmx_reduce_scalar_kernel<T, OP, SGD><<<grid(a.len), kReduceThreads, 0, s>>>(a);
 }
