@@ -256,12 +256,34 @@ __device__ __forceinline__ void reduce_group(const ReduceArgs& a, size_t i, size
   }
 }
 
-template <typename T, int OP, int U, int U0 = 0>
-__device__ __forceinline__ void reduce_each(const ReduceArgs& a, size_t i, size_t stride, size_t nvec,
-                                            float (&acc)[U][Elem<T>::kVec]) {
-  if constexpr (U0 < U) {
-    reduce_group<T, OP, U, U0, 1>(a, i, stride, nvec, acc);
-    reduce_each<T, OP, U, U0 + 1>(a, i, stride, nvec, acc);
+// One vector position's sources, rank order (host sources: one vector's
+// sources in flight at a time).
+template <typename T, int OP>
+__device__ __forceinline__ void reduce_one(const ReduceArgs& a, size_t off, float* acc) {
+  using E = Elem<T>;
+  constexpr int V = E::kVec;
+  constexpr int B = 8;  // sources loaded per batch
+  for (int q0 = 0; q0 < a.nsrc; q0 += B) {
+    uint4 raw[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int q = q0 + b;
+      if (q < a.nsrc)
+        raw[b] = ((a.sys_mask >> q) & 1) ? ld_cv_v4(a.src[q] + off) : ld_v4(a.src[q] + off);
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int q = q0 + b;
+      if (q < a.nsrc) {
+        float x[V];
+        E::widen(raw[b], x);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          const float c = scale_in<T, OP>(x[k], a.factor);
+          acc[k] = q == 0 ? c : __fadd_rn(acc[k], c);
+        }
+      }
+    }
   }
 }
 
@@ -271,15 +293,17 @@ __device__ __forceinline__ void reduce_each(const ReduceArgs& a, size_t i, size_
 // is latency bound, and one round trip per U vectors instead of per vector
 // cuts the HBM-only launch (result slot by copy engine) 78.5 -> 62-67 us
 // (r02/r5b).  Host sources (zero-copy transport, one-shot): one position's
-// sources at a time, as before - U x 7 concurrent host reads per thread made
-// the 64 KiB one-shot at 7 ranks 11 % slower (r02/r5e).  The per-element
-// arithmetic and its order are the same either way.
+// sources at a time, the round-1 form and register count (70) - 14 concurrent
+// host reads per thread made the 64 KiB one-shot at 7 ranks 5-11 % slower
+// (r02/r5e, r5f).  The per-element arithmetic and its order are the same.
 template <typename T, int OP, int U, bool HOST_SRC>
 __device__ __forceinline__ void reduce_vecs(const ReduceArgs& a, size_t i, size_t stride, size_t nvec,
                                             float (&acc)[U][Elem<T>::kVec]) {
-  if constexpr (HOST_SRC)
-    reduce_each<T, OP, U>(a, i, stride, nvec, acc);
-  else
+  if constexpr (HOST_SRC) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i + u * stride < nvec) reduce_one<T, OP>(a, (i + u * stride) * 16, acc[u]);
+  } else
     reduce_group<T, OP, U, 0, U>(a, i, stride, nvec, acc);
 #pragma unroll
   for (int u = 0; u < U; ++u)
